@@ -1,0 +1,92 @@
+/*
+ * windvox_b200.h -- C ABI of the B200 winding-number hot path.
+ *
+ * One shared library (paper_2407_11272_b200/_lib/libwindvox_b200.so, built for
+ * sm_100a) exports the functions below.  Conventions, mirroring the
+ * reference kernel ABI (/root/reference/pkg/src/windvox/_kernels.py:1-19,
+ * _parallel.py:1-10):
+ *   * plain pointers and sizes only; every buffer is caller-owned DEVICE
+ *     memory (the caller pre-allocates outputs, exactly as the reference
+ *     callers pre-allocate `out`/`flags`/`grad`, winding.py:288-289,
+ *     grad.py:64,115);
+ *   * kernels never raise: they return a status code (WV_OK == 0) and report
+ *     on-surface query points through `flags`, like the reference kernels;
+ *   * stream-ordered: `stream` is a cudaStream_t (NULL = legacy default);
+ *     nothing synchronizes the host;
+ *   * stateless and re-entrant, so one process per GPU or one host thread
+ *     per device both work (_parallel.py:39-53);
+ *   * a node range [n0, n0+count) of a lattice, or an explicit point list,
+ *     plays the role of the reference's per-chunk slice `points[s:e]`.
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef WINDVOX_B200_H
+#define WINDVOX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define WV_OK 0
+#define WV_ERR_ARG 1       /* invalid argument (null pointer, bad kind, ...) */
+#define WV_ERR_WORKSPACE 2 /* workspace missing or smaller than required    */
+#define WV_ERR_LAUNCH 3    /* kernel launch failed                           */
+#define WV_ERR_CUDA 4      /* CUDA runtime error                             */
+
+/* packed face-array kinds (wv_pack_faces) */
+#define WV_PACK_EXACT_F32 1
+#define WV_PACK_SOFT_F32 2
+#define WV_PACK_EXACT_F64 3
+#define WV_PACK_SOFT_F64 4
+
+/* stored value for on-surface (flagged) nodes */
+#define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
+#define WV_POLICY_HALF 1 /* exactly 0.5: voxelize, winding.py:358                          */
+
+/* GridSpec (winding.py:69-140): node (i,j,k) at lo + (hi-lo)*(i/(R-1)),
+ * midpoint when R == 1; flat index ((i*Ry)+j)*Rz+k (k fastest). */
+typedef struct wv_grid {
+  double lo[3];
+  double hi[3];
+  int64_t res[3];
+} wv_grid_t;
+
+const char *wv_version(void);
+const char *wv_status_string(int status);
+/* CUDA device ordinal the calls on this thread use (cudaSetDevice). */
+int wv_set_device(int device);
+
+/* ---- per-mesh staging -------------------------------------------------
+ * Replaces surface_epsilon (winding.py:193-197), _prepare_exact
+ * (winding.py:258-268) and TriangleMesh.triangle_corners (mesh_io.py:90-92).
+ * vertices: (V,3) f32 (vert_f64=0) or f64 (vert_f64=1); faces: (F,3) int32
+ * (faces_i64=0) or int64.  `packed` must hold wv_packed_bytes(kind, F).
+ * Exact kinds keep degenerate faces in place, marked dead (the reference
+ * drops them; results are identical). */
+size_t wv_packed_bytes(int kind, int64_t n_faces);
+int wv_pack_faces(int kind, const void *vertices, int vert_f64, int64_t n_verts,
+                  const void *faces, int faces_i64, int64_t n_faces, void *packed,
+                  void *stream);
+
+/* ---- exact forward -----------------------------------------------------
+ * Replaces _kernels.exact_batch_f32 (_kernels.py:235-309; FP32 compute with
+ * fp64 tile-partial accumulation) and, for the f64 variants,
+ * _kernels.exact_batch (_kernels.py:34-116).  Writes out[0..count) (W) and
+ * flags[0..count) (1 = on-surface).  `workspace` may be NULL when
+ * wv_fwd_workspace_bytes(...) returns 0. */
+size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count);
+int wv_exact_fwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, int policy, float *out, uint8_t *flags,
+                          void *workspace, size_t workspace_bytes, void *stream);
+int wv_exact_fwd_points_f32(const void *packed, int64_t n_faces, const float *points,
+                            int64_t count, int policy, float *out, uint8_t *flags,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WINDVOX_B200_H */

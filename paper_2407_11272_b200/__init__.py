@@ -1,0 +1,24 @@
+"""paper_2407_11272_b200 -- B200-native winding-number voxelization hot path.
+
+Drop-in for the hot path of the reference package ``windvox``
+(/root/reference/pkg/src/windvox): same API names and semantics, backed by
+hand-written sm_100a CUDA kernels behind the C ABI of
+``include/windvox_b200.h``.  There is no CPU fallback.
+"""
+
+from .errors import DegenerateError, DivergedError, OnSurfaceError, ParseError
+from .types import (GridSpec, LossReport, QueryBatchConfig, ScalarField, TriangleMesh,
+                    VertexGradients, surface_epsilon)
+from .winding import (binarize, solid_angle_triangle, voxelize, winding_number_batch,
+                      winding_number_exact, winding_number_soft)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DegenerateError", "DivergedError", "OnSurfaceError", "ParseError",
+    "TriangleMesh", "GridSpec", "ScalarField", "QueryBatchConfig", "VertexGradients",
+    "LossReport", "surface_epsilon",
+    "solid_angle_triangle", "winding_number_exact", "winding_number_soft",
+    "winding_number_batch", "voxelize", "binarize",
+    "__version__",
+]

@@ -1,0 +1,105 @@
+"""ctypes binding of the C ABI in ``include/windvox_b200.h``.
+
+The library is the in-tree ``_lib/libwindvox_b200.so`` built for sm_100a
+(``python -m paper_2407_11272_b200._build``).  There is no CPU fallback: if
+the library is missing or no CUDA device is visible, every entry point raises
+``WindvoxCudaUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libwindvox_b200.so"
+
+WV_OK = 0
+PACK_EXACT_F32 = 1
+PACK_SOFT_F32 = 2
+PACK_EXACT_F64 = 3
+PACK_SOFT_F64 = 4
+POLICY_RAW = 0
+POLICY_HALF = 1
+
+# every symbol the public header declares (checked by tests/test_capi_symbols.py)
+EXPORTED = (
+    "wv_version", "wv_status_string", "wv_set_device", "wv_packed_bytes", "wv_pack_faces",
+    "wv_fwd_workspace_bytes", "wv_exact_fwd_grid_f32", "wv_exact_fwd_points_f32",
+)
+
+
+class WindvoxCudaUnavailable(RuntimeError):
+    """The sm_100a CUDA library or a CUDA device is not available."""
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+                ("res", ctypes.c_int64 * 3)]
+
+
+_lib = None
+
+
+def _declare(lib):
+    P = ctypes.c_void_p
+    I64 = ctypes.c_int64
+    I = ctypes.c_int
+    SZ = ctypes.c_size_t
+    sig = {
+        "wv_version": ([], ctypes.c_char_p),
+        "wv_status_string": ([I], ctypes.c_char_p),
+        "wv_set_device": ([I], I),
+        "wv_packed_bytes": ([I, I64], SZ),
+        "wv_pack_faces": ([I, P, I, I64, P, I, I64, P, P], I),
+        "wv_fwd_workspace_bytes": ([I, I64, I64], SZ),
+        "wv_exact_fwd_grid_f32": ([P, I64, Grid, I64, I64, I, P, P, P, SZ, P], I),
+        "wv_exact_fwd_points_f32": ([P, I64, P, I64, I, P, P, P, SZ, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+def load_library(path: Path | None = None):
+    """Load (without requiring a GPU) the shared library; raises if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise WindvoxCudaUnavailable(
+            f"{p} is missing: build it with `python -m paper_2407_11272_b200._build` "
+            "(nvcc, sm_100a). There is no CPU fallback.")
+    lib = _declare(ctypes.CDLL(str(p)))
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def lib():
+    """The loaded library, after checking a CUDA device is present."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise WindvoxCudaUnavailable(
+            "no CUDA device visible: windvox_b200 runs only on B200 (sm_100a); "
+            "there is no CPU fallback")
+    return load_library()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != WV_OK:
+        msg = load_library().wv_status_string(int(rc)).decode()
+        raise RuntimeError(f"{what} failed: status {rc} ({msg})")
+
+
+def make_grid(bounds_min, bounds_max, resolution) -> Grid:
+    g = Grid()
+    for i in range(3):
+        g.lo[i] = float(bounds_min[i])
+        g.hi[i] = float(bounds_max[i])
+        g.res[i] = int(resolution[i])
+    return g

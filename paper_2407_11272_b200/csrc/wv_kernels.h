@@ -1,0 +1,116 @@
+// wv_kernels.h -- internal launch interface shared by the .cu files and the
+// C-ABI layer (wv_capi.cu).  Not part of the public header.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "wv_common.cuh"
+
+namespace wv {
+
+// status codes (mirrored in include/windvox_b200.h)
+constexpr int kOk = 0;
+constexpr int kErrArg = 1;
+constexpr int kErrWorkspace = 2;
+constexpr int kErrLaunch = 3;
+constexpr int kErrCuda = 4;
+
+// on-surface policy for stored values
+constexpr int kPolicyRaw = 0;   // winding_number_batch: flagged keeps its partial sum
+constexpr int kPolicyHalf = 1;  // voxelize: flagged -> exactly 0.5 (winding.py:358)
+
+struct PointSource {
+  enum Kind { kGrid = 0, kList = 1 };
+  int kind;
+  GridDesc grid;        // kGrid: nodes n0 .. n0+count-1 of the lattice
+  int64_t n0;
+  const float* points;  // kList f32 (count,3)
+  const double* points64;  // kList f64 (count,3)
+};
+
+struct GridSrc {
+  GridDesc g;
+  int64_t n0;
+  __device__ __forceinline__ void point(int64_t l, float& x, float& y, float& z) const {
+    double dx, dy, dz;
+    grid_node(g, n0 + l, dx, dy, dz);
+    x = (float)dx;  // winding.py:363: f64 node coordinates cast to f32
+    y = (float)dy;
+    z = (float)dz;
+  }
+  __device__ __forceinline__ void point(int64_t l, double& x, double& y, double& z) const {
+    grid_node(g, n0 + l, x, y, z);
+  }
+};
+
+struct ListSrc {
+  const float* pts;
+  __device__ __forceinline__ void point(int64_t l, float& x, float& y, float& z) const {
+    x = pts[3 * l + 0];
+    y = pts[3 * l + 1];
+    z = pts[3 * l + 2];
+  }
+};
+
+struct ListSrc64 {
+  const double* pts;
+  __device__ __forceinline__ void point(int64_t l, double& x, double& y, double& z) const {
+    x = pts[3 * l + 0];
+    y = pts[3 * l + 1];
+    z = pts[3 * l + 2];
+  }
+};
+
+// Forward output sink: final values (single split) or per-split partials.
+struct OutF32 {
+  float* out = nullptr;
+  uint8_t* flags = nullptr;
+  double* part = nullptr;
+  uint8_t* part_flags = nullptr;
+  int64_t n_count = 0;
+  int policy = kPolicyRaw;
+  double scale = 1.0;
+  __device__ __forceinline__ void store(int split, int64_t l, double acc, uint32_t hit) const {
+    if (part != nullptr) {
+      part[(int64_t)split * n_count + l] = acc;
+      part_flags[(int64_t)split * n_count + l] = (uint8_t)hit;
+      return;
+    }
+    double w = acc * scale;
+    if (hit && policy == kPolicyHalf) w = 0.5;
+    out[l] = (float)w;
+    if (flags) flags[l] = (uint8_t)hit;
+  }
+};
+
+// Face splits: when the node blocks alone cannot fill the chip, split the
+// face range so that >= ~2 waves of CTAs exist; partials are summed in fixed
+// split order by a finalize kernel (deterministic).  Depends only on the
+// problem shape, never on timing.
+inline int choose_splits(int64_t blocks_x, int64_t n_tiles, int num_sms, int ctas_per_sm) {
+  if (n_tiles <= 1) return 1;
+  const int64_t want = (int64_t)num_sms * ctas_per_sm * 2;
+  if (blocks_x >= want) return 1;
+  int64_t s = (want + blocks_x - 1) / blocks_x;
+  if (s > n_tiles) s = n_tiles;
+  if (s > 64) s = 64;
+  return (int)(s < 1 ? 1 : s);
+}
+
+// packing (wv_pack.cu)
+int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                const void* faces, int faces_i64, int64_t n_faces, const double* eps_dev,
+                void* packed, cudaStream_t stream);
+int launch_surface_eps(const void* vertices, int vert_f64, int64_t n_verts, double* eps_dev,
+                       cudaStream_t stream);
+size_t packed_bytes(int kind, int64_t n_faces);
+
+// forward (wv_exact_fwd.cu, wv_soft_fwd.cu, wv_f64.cu)
+int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, int policy, float* out, uint8_t* flags,
+                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream);
+size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+
+}  // namespace wv

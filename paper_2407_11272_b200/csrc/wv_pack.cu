@@ -1,0 +1,197 @@
+// wv_pack.cu -- per-mesh staging on the device (compiled with -fmad=false so
+// every f64 expression is the same IEEE sequence as the numpy reference).
+//
+//  * surface_eps_kernel : eps = 1e-9 * |bbox max - bbox min|
+//                         (winding.py:193-197, mesh_io.py:80-88)
+//  * pack_kernel        : the reference's per-face staging
+//                         (_prepare_exact, winding.py:258-268, and the soft
+//                         path's triangle_corners, winding.py:301) folded into
+//                         one record per face.  Exact-mode degenerate faces
+//                         (|N| == 0) are kept in place but marked dead, so
+//                         face order is preserved without a compaction pass.
+#include "wv_kernels.h"
+
+namespace wv {
+
+template <typename V>
+__device__ __forceinline__ void load_vertex(const V* v, int64_t i, double* out) {
+  out[0] = (double)v[3 * i + 0];
+  out[1] = (double)v[3 * i + 1];
+  out[2] = (double)v[3 * i + 2];
+}
+
+template <typename V>
+__global__ void surface_eps_kernel(const V* __restrict__ verts, int64_t n_verts,
+                                   PackHeader* __restrict__ hdr) {
+  __shared__ double smin[3][1024];
+  __shared__ double smax[3][1024];
+  double lo[3] = {INFINITY, INFINITY, INFINITY};
+  double hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = threadIdx.x; i < n_verts; i += blockDim.x) {
+    double p[3];
+    load_vertex(verts, i, p);
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fmin(lo[d], p[d]);
+      hi[d] = fmax(hi[d], p[d]);
+    }
+  }
+  for (int d = 0; d < 3; ++d) {
+    smin[d][threadIdx.x] = lo[d];
+    smax[d][threadIdx.x] = hi[d];
+  }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int d = 0; d < 3; ++d) {
+        smin[d][threadIdx.x] = fmin(smin[d][threadIdx.x], smin[d][threadIdx.x + s]);
+        smax[d][threadIdx.x] = fmax(smax[d][threadIdx.x], smax[d][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double eps = 0.0;
+    if (n_verts > 0) {
+      const double dx = smax[0][0] - smin[0][0];
+      const double dy = smax[1][0] - smin[1][0];
+      const double dz = smax[2][0] - smin[2][0];
+      eps = 1e-9 * sqrt(dx * dx + dy * dy + dz * dz);
+    }
+    hdr->eps = eps;
+    hdr->eps_f32 = (float)eps;
+  }
+}
+
+template <typename V, typename I>
+__global__ void pack_kernel(int kind, const V* __restrict__ verts,
+                            const I* __restrict__ faces, int64_t n_faces,
+                            PackHeader* __restrict__ hdr, void* __restrict__ recs) {
+  const double eps = hdr->eps;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_faces;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    double v0[3], v1[3], v2[3];
+    load_vertex(verts, (int64_t)faces[3 * f + 0], v0);
+    load_vertex(verts, (int64_t)faces[3 * f + 1], v1);
+    load_vertex(verts, (int64_t)faces[3 * f + 2], v2);
+    const double ux = v1[0] - v0[0], uy = v1[1] - v0[1], uz = v1[2] - v0[2];
+    const double wx = v2[0] - v0[0], wy = v2[1] - v0[1], wz = v2[2] - v0[2];
+    // np.cross(u, w) component order (winding.py:262)
+    const double nx = uy * wz - uz * wy;
+    const double ny = uz * wx - ux * wz;
+    const double nz = ux * wy - uy * wx;
+    if (kind == 1 || kind == 3) {
+      const double norm = sqrt(nx * nx + ny * ny + nz * nz);  // np.linalg.norm
+      const bool dead = !(norm > 0.0);
+      if (kind == 1) {
+        ExactRecF32* r = static_cast<ExactRecF32*>(recs) + f;
+        const float epsN = dead ? __int_as_float(0x7f800000) : (float)(eps * norm);
+        r->v0e = make_float4((float)v0[0], (float)v0[1], (float)v0[2], epsN);
+        r->v1 = make_float4((float)v1[0], (float)v1[1], (float)v1[2], 0.0f);
+        r->v2 = make_float4((float)v2[0], (float)v2[1], (float)v2[2], 0.0f);
+        r->n = make_float4((float)nx, (float)ny, (float)nz, 0.0f);
+      } else {
+        ExactRecF64* r = static_cast<ExactRecF64*>(recs) + f;
+        for (int d = 0; d < 3; ++d) {
+          r->v[d] = v0[d];
+          r->v[3 + d] = v1[d];
+          r->v[6 + d] = v2[d];
+        }
+        double hx = 0.0, hy = 0.0, hz = 0.0, pld = 0.0;
+        if (!dead) {
+          hx = nx / norm;
+          hy = ny / norm;
+          hz = nz / norm;
+          pld = hx * v0[0] + hy * v0[1] + hz * v0[2];  // (nhat*tri[:,0]).sum(1)
+        }
+        r->nhat[0] = hx;
+        r->nhat[1] = hy;
+        r->nhat[2] = hz;
+        r->pld = pld;
+        r->dead = dead ? 1.0 : 0.0;
+        r->pad[0] = r->pad[1] = 0.0;
+      }
+    } else {
+      // centroid exactly as _kernels.py:145-147 minus the (-q) term
+      const double cx = v0[0] + (ux + wx) / 3.0;
+      const double cy = v0[1] + (uy + wy) / 3.0;
+      const double cz = v0[2] + (uz + wz) / 3.0;
+      if (kind == 2) {
+        SoftRecF32* r = static_cast<SoftRecF32*>(recs) + f;
+        r->c = make_float4((float)cx, (float)cy, (float)cz, (float)nx);
+        r->n = make_float4((float)ny, (float)nz, 0.0f, 0.0f);
+      } else {
+        SoftRecF64* r = static_cast<SoftRecF64*>(recs) + f;
+        r->c[0] = cx;
+        r->c[1] = cy;
+        r->c[2] = cz;
+        r->n[0] = nx;
+        r->n[1] = ny;
+        r->n[2] = nz;
+        r->pad[0] = r->pad[1] = 0.0;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hdr->kind = kind;
+    hdr->n_faces = n_faces;
+    hdr->n_live = n_faces;
+  }
+}
+
+size_t packed_bytes(int kind, int64_t n_faces) {
+  size_t rec = 0;
+  switch (kind) {
+    case 1: rec = sizeof(ExactRecF32); break;
+    case 2: rec = sizeof(SoftRecF32); break;
+    case 3: rec = sizeof(ExactRecF64); break;
+    case 4: rec = sizeof(SoftRecF64); break;
+    default: return 0;
+  }
+  return sizeof(PackHeader) + rec * (size_t)(n_faces > 0 ? n_faces : 0);
+}
+
+int launch_surface_eps(const void* vertices, int vert_f64, int64_t n_verts, double* eps_dev,
+                       cudaStream_t stream) {
+  PackHeader* hdr = reinterpret_cast<PackHeader*>(eps_dev);
+  if (vert_f64)
+    surface_eps_kernel<double><<<1, 1024, 0, stream>>>(static_cast<const double*>(vertices),
+                                                       n_verts, hdr);
+  else
+    surface_eps_kernel<float><<<1, 1024, 0, stream>>>(static_cast<const float*>(vertices),
+                                                      n_verts, hdr);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                const void* faces, int faces_i64, int64_t n_faces, const double* /*eps_dev*/,
+                void* packed, cudaStream_t stream) {
+  if (kind < 1 || kind > 4) return kErrArg;
+  PackHeader* hdr = static_cast<PackHeader*>(packed);
+  int rc = launch_surface_eps(vertices, vert_f64, n_verts, reinterpret_cast<double*>(hdr),
+                              stream);
+  if (rc != kOk) return rc;
+  void* recs = hdr + 1;
+  const int threads = 256;
+  int64_t blocks = (n_faces + threads - 1) / threads;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 4096) blocks = 4096;
+  if (vert_f64) {
+    const double* v = static_cast<const double*>(vertices);
+    if (faces_i64)
+      pack_kernel<double, int64_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs);
+    else
+      pack_kernel<double, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs);
+  } else {
+    const float* v = static_cast<const float*>(vertices);
+    if (faces_i64)
+      pack_kernel<float, int64_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs);
+    else
+      pack_kernel<float, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs);
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+}  // namespace wv
