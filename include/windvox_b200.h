@@ -42,6 +42,8 @@ extern "C" {
 #define WV_PACK_SOFT_F32 2
 #define WV_PACK_EXACT_F64 3
 #define WV_PACK_SOFT_F64 4
+#define WV_PACK_SOFTGRAD_F32 5
+#define WV_PACK_SOFTGRAD_F64 6
 
 /* stored value for on-surface (flagged) nodes */
 #define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
@@ -72,12 +74,18 @@ int wv_pack_faces(int kind, const void *vertices, int vert_f64, int64_t n_verts,
                   const void *faces, int faces_i64, int64_t n_faces, void *packed,
                   void *stream);
 
-/* ---- exact forward -----------------------------------------------------
- * Replaces _kernels.exact_batch_f32 (_kernels.py:235-309; FP32 compute with
- * fp64 tile-partial accumulation) and, for the f64 variants,
- * _kernels.exact_batch (_kernels.py:34-116).  Writes out[0..count) (W) and
- * flags[0..count) (1 = on-surface).  `workspace` may be NULL when
- * wv_fwd_workspace_bytes(...) returns 0. */
+/* ---- forward: winding numbers at lattice nodes or explicit points -------
+ * exact f32: replaces _kernels.exact_batch_f32 (_kernels.py:235-309); FP32
+ *   compute with fp64 tile-partial accumulation, within 1e-5 of the f64
+ *   reference.  packed kind WV_PACK_EXACT_F32.
+ * soft f32: replaces _kernels.soft_batch_f32 (_kernels.py:312-349).
+ *   packed kind WV_PACK_SOFT_F32.
+ * exact f64 / soft f64: replace _kernels.exact_batch / soft_batch
+ *   (_kernels.py:34-116, 119-158) in the reference's operation order; kinds
+ *   WV_PACK_EXACT_F64 / WV_PACK_SOFT_F64.  use_atan2=0 selects the
+ *   single-argument arctan regression branch (_kernels.py:106-114).
+ * Writes out[0..count) and flags[0..count) (1 = on-surface, may be NULL).
+ * `workspace` may be NULL when wv_fwd_workspace_bytes(...) returns 0. */
 size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count);
 int wv_exact_fwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                           int64_t count, int policy, float *out, uint8_t *flags,
@@ -85,6 +93,90 @@ int wv_exact_fwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, i
 int wv_exact_fwd_points_f32(const void *packed, int64_t n_faces, const float *points,
                             int64_t count, int policy, float *out, uint8_t *flags,
                             void *workspace, size_t workspace_bytes, void *stream);
+int wv_soft_fwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, int policy, float *out, uint8_t *flags, void *workspace,
+                         size_t workspace_bytes, void *stream);
+int wv_soft_fwd_points_f32(const void *packed, int64_t n_faces, const float *points,
+                           int64_t count, int policy, float *out, uint8_t *flags,
+                           void *workspace, size_t workspace_bytes, void *stream);
+int wv_exact_fwd_grid_f64(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, int use_atan2, int policy, double *out, uint8_t *flags,
+                          void *stream);
+int wv_exact_fwd_points_f64(const void *packed, int64_t n_faces, const double *points,
+                            int64_t count, int use_atan2, int policy, double *out,
+                            uint8_t *flags, void *stream);
+int wv_soft_fwd_grid_f64(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, int policy, double *out, uint8_t *flags, void *stream);
+int wv_soft_fwd_points_f64(const void *packed, int64_t n_faces, const double *points,
+                           int64_t count, int policy, double *out, uint8_t *flags,
+                           void *stream);
+
+/* ---- backward: per-face corner gradients reduced over query points ------
+ * face_grad (F,3,3) f64 is OVERWRITTEN with
+ *   sum_p coef_scale * coefs[p] * dW(q_p)/dv_{f,k}
+ * over the node range / point list; points with coefs[p] == 0 are skipped
+ * and pairs the forward skipped (on-surface) contribute nothing.
+ * soft: replaces _kernels.soft_grad_accum (_kernels.py:161-232); packed kind
+ *   WV_PACK_SOFTGRAD_F32 / _F64.
+ * exact: NEW (no reference kernel, grad.py:9-12): closed-form d(Omega)/dv of
+ *   the VOS solid angle; packed kind WV_PACK_EXACT_F32 / _F64.
+ * Corner sums become vertex gradients with wv_face_to_vertex. */
+size_t wv_bwd_workspace_bytes(int kind, int64_t n_faces, int64_t count);
+int wv_exact_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, const float *coefs, double coef_scale,
+                          double *face_grad, void *workspace, size_t workspace_bytes,
+                          void *stream);
+int wv_exact_bwd_points_f32(const void *packed, int64_t n_faces, const float *points,
+                            int64_t count, const float *coefs, double coef_scale,
+                            double *face_grad, void *workspace, size_t workspace_bytes,
+                            void *stream);
+int wv_soft_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, const float *coefs, double coef_scale,
+                         double *face_grad, void *workspace, size_t workspace_bytes,
+                         void *stream);
+int wv_soft_bwd_points_f32(const void *packed, int64_t n_faces, const float *points,
+                           int64_t count, const float *coefs, double coef_scale,
+                           double *face_grad, void *workspace, size_t workspace_bytes,
+                           void *stream);
+int wv_exact_bwd_grid_f64(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, const double *coefs, double coef_scale,
+                          double *face_grad, void *workspace, size_t workspace_bytes,
+                          void *stream);
+int wv_exact_bwd_points_f64(const void *packed, int64_t n_faces, const double *points,
+                            int64_t count, const double *coefs, double coef_scale,
+                            double *face_grad, void *workspace, size_t workspace_bytes,
+                            void *stream);
+int wv_soft_bwd_grid_f64(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, const double *coefs, double coef_scale,
+                         double *face_grad, void *workspace, size_t workspace_bytes,
+                         void *stream);
+int wv_soft_bwd_points_f64(const void *packed, int64_t n_faces, const double *points,
+                           int64_t count, const double *coefs, double coef_scale,
+                           double *face_grad, void *workspace, size_t workspace_bytes,
+                           void *stream);
+
+/* Vertex gradients from face-corner sums, in CSR order (deterministic):
+ *   out[v] (+)= scale * sum_{e in [off[v], off[v+1])} face_grad[slots[e]]
+ * slots[e] = 3*f + k for every corner k of face f incident to v, sorted by v
+ * (stable).  `scale` is a DEVICE pointer (NULL = 1).  out64 / out32 may each
+ * be NULL.  Replaces the chunk-ordered buffer merge of grad.py:113-127. */
+int wv_face_to_vertex(const double *face_grad, const int64_t *csr_offsets,
+                      const int64_t *csr_slots, int64_t n_verts, const double *scale,
+                      int accumulate, double *out64, float *out32, void *stream);
+
+/* ---- occupancy loss terms (grad.py:101-110), fused on the device ---------
+ * coefs[n] = 2 w r (0 on flagged nodes); sums (8 doubles, device) =
+ * {sum w r^2, sum w, n_flagged, 1/sum w, loss, 0, 0, 0}.  weights may be NULL
+ * (all ones).  wv_loss_finalize recomputes sums[3..4] after sums[0..2] were
+ * all-reduced across ranks. */
+size_t wv_loss_workspace_bytes(int64_t count);
+int wv_loss_terms_f32(const float *values, const uint8_t *flags, const float *targets,
+                      const float *weights, int64_t count, float *coefs, double *sums,
+                      void *workspace, size_t workspace_bytes, void *stream);
+int wv_loss_terms_f64(const double *values, const uint8_t *flags, const double *targets,
+                      const double *weights, int64_t count, double *coefs, double *sums,
+                      void *workspace, size_t workspace_bytes, void *stream);
+int wv_loss_finalize(double *sums, void *stream);
 
 #ifdef __cplusplus
 }

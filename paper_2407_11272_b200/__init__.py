@@ -11,6 +11,8 @@ from .types import (GridSpec, LossReport, QueryBatchConfig, ScalarField, Triangl
                     VertexGradients, surface_epsilon)
 from .winding import (binarize, solid_angle_triangle, voxelize, winding_number_batch,
                       winding_number_exact, winding_number_soft)
+from .grad import exact_loss_grad, occupancy_loss_grad, soft_winding_vertex_jacobian
+from .autograd import WindingNumber, winding_number
 
 __version__ = "0.1.0"
 
@@ -20,5 +22,7 @@ __all__ = [
     "LossReport", "surface_epsilon",
     "solid_angle_triangle", "winding_number_exact", "winding_number_soft",
     "winding_number_batch", "voxelize", "binarize",
+    "soft_winding_vertex_jacobian", "occupancy_loss_grad", "exact_loss_grad",
+    "WindingNumber", "winding_number",
     "__version__",
 ]

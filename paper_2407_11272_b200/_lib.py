@@ -19,6 +19,8 @@ PACK_EXACT_F32 = 1
 PACK_SOFT_F32 = 2
 PACK_EXACT_F64 = 3
 PACK_SOFT_F64 = 4
+PACK_SOFTGRAD_F32 = 5
+PACK_SOFTGRAD_F64 = 6
 POLICY_RAW = 0
 POLICY_HALF = 1
 
@@ -26,6 +28,13 @@ POLICY_HALF = 1
 EXPORTED = (
     "wv_version", "wv_status_string", "wv_set_device", "wv_packed_bytes", "wv_pack_faces",
     "wv_fwd_workspace_bytes", "wv_exact_fwd_grid_f32", "wv_exact_fwd_points_f32",
+    "wv_soft_fwd_grid_f32", "wv_soft_fwd_points_f32", "wv_exact_fwd_grid_f64",
+    "wv_exact_fwd_points_f64", "wv_soft_fwd_grid_f64", "wv_soft_fwd_points_f64",
+    "wv_bwd_workspace_bytes", "wv_exact_bwd_grid_f32", "wv_exact_bwd_points_f32",
+    "wv_soft_bwd_grid_f32", "wv_soft_bwd_points_f32", "wv_exact_bwd_grid_f64",
+    "wv_exact_bwd_points_f64", "wv_soft_bwd_grid_f64", "wv_soft_bwd_points_f64",
+    "wv_face_to_vertex", "wv_loss_workspace_bytes", "wv_loss_terms_f32", "wv_loss_terms_f64",
+    "wv_loss_finalize",
 )
 
 
@@ -46,6 +55,12 @@ def _declare(lib):
     I64 = ctypes.c_int64
     I = ctypes.c_int
     SZ = ctypes.c_size_t
+    D = ctypes.c_double
+    fwd32_grid = [P, I64, Grid, I64, I64, I, P, P, P, SZ, P]
+    fwd32_pts = [P, I64, P, I64, I, P, P, P, SZ, P]
+    bwd_grid = [P, I64, Grid, I64, I64, P, D, P, P, SZ, P]
+    bwd_pts = [P, I64, P, I64, P, D, P, P, SZ, P]
+    loss = [P, P, P, P, I64, P, P, P, SZ, P]
     sig = {
         "wv_version": ([], ctypes.c_char_p),
         "wv_status_string": ([I], ctypes.c_char_p),
@@ -53,8 +68,28 @@ def _declare(lib):
         "wv_packed_bytes": ([I, I64], SZ),
         "wv_pack_faces": ([I, P, I, I64, P, I, I64, P, P], I),
         "wv_fwd_workspace_bytes": ([I, I64, I64], SZ),
-        "wv_exact_fwd_grid_f32": ([P, I64, Grid, I64, I64, I, P, P, P, SZ, P], I),
-        "wv_exact_fwd_points_f32": ([P, I64, P, I64, I, P, P, P, SZ, P], I),
+        "wv_exact_fwd_grid_f32": (fwd32_grid, I),
+        "wv_exact_fwd_points_f32": (fwd32_pts, I),
+        "wv_soft_fwd_grid_f32": (fwd32_grid, I),
+        "wv_soft_fwd_points_f32": (fwd32_pts, I),
+        "wv_exact_fwd_grid_f64": ([P, I64, Grid, I64, I64, I, I, P, P, P], I),
+        "wv_exact_fwd_points_f64": ([P, I64, P, I64, I, I, P, P, P], I),
+        "wv_soft_fwd_grid_f64": ([P, I64, Grid, I64, I64, I, P, P, P], I),
+        "wv_soft_fwd_points_f64": ([P, I64, P, I64, I, P, P, P], I),
+        "wv_bwd_workspace_bytes": ([I, I64, I64], SZ),
+        "wv_exact_bwd_grid_f32": (bwd_grid, I),
+        "wv_exact_bwd_points_f32": (bwd_pts, I),
+        "wv_soft_bwd_grid_f32": (bwd_grid, I),
+        "wv_soft_bwd_points_f32": (bwd_pts, I),
+        "wv_exact_bwd_grid_f64": (bwd_grid, I),
+        "wv_exact_bwd_points_f64": (bwd_pts, I),
+        "wv_soft_bwd_grid_f64": (bwd_grid, I),
+        "wv_soft_bwd_points_f64": (bwd_pts, I),
+        "wv_face_to_vertex": ([P, P, P, I64, P, I, P, P, P], I),
+        "wv_loss_workspace_bytes": ([I64], SZ),
+        "wv_loss_terms_f32": (loss, I),
+        "wv_loss_terms_f64": (loss, I),
+        "wv_loss_finalize": ([P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

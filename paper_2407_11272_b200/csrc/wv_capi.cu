@@ -1,8 +1,6 @@
 // wv_capi.cu -- extern "C" boundary (include/windvox_b200.h).  Argument
 // validation, device-attribute caching, launch dispatch.  No exceptions cross
 // the ABI; every entry point returns a status code.
-#include <cstdio>
-
 #include "../../include/windvox_b200.h"
 #include "wv_kernels.h"
 
@@ -22,21 +20,43 @@ int sm_count() {
   return cached;
 }
 
-wv::GridDesc to_desc(const wv_grid_t& g) {
-  wv::GridDesc d;
-  for (int i = 0; i < 3; ++i) {
-    d.lo[i] = g.lo[i];
-    d.hi[i] = g.hi[i];
-    d.res[i] = g.res[i];
-  }
-  return d;
-}
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 bool grid_ok(const wv_grid_t& g, int64_t n0, int64_t count) {
   for (int i = 0; i < 3; ++i)
     if (g.res[i] < 1) return false;
   const int64_t n = g.res[0] * g.res[1] * g.res[2];
   return n0 >= 0 && count >= 0 && n0 + count <= n;
+}
+
+wv::PointSource grid_src(const wv_grid_t& g, int64_t n0) {
+  wv::PointSource ps{};
+  ps.kind = wv::PointSource::kGrid;
+  for (int i = 0; i < 3; ++i) {
+    ps.grid.lo[i] = g.lo[i];
+    ps.grid.hi[i] = g.hi[i];
+    ps.grid.res[i] = g.res[i];
+  }
+  ps.n0 = n0;
+  return ps;
+}
+
+wv::PointSource list_src(const float* p32, const double* p64) {
+  wv::PointSource ps{};
+  ps.kind = wv::PointSource::kList;
+  ps.points = p32;
+  ps.points64 = p64;
+  return ps;
+}
+
+bool fwd_args_ok(const void* packed, const void* out, int64_t n_faces, int64_t count) {
+  return packed != nullptr && n_faces >= 0 && count >= 0 && (count == 0 || out != nullptr);
+}
+
+bool bwd_args_ok(const void* packed, const void* coefs, const double* face_grad,
+                 int64_t n_faces, int64_t count) {
+  return packed != nullptr && n_faces >= 0 && count >= 0 &&
+         (n_faces == 0 || face_grad != nullptr) && (count == 0 || coefs != nullptr);
 }
 
 }  // namespace
@@ -68,13 +88,15 @@ int wv_pack_faces(int kind, const void* vertices, int vert_f64, int64_t n_verts,
   if (packed == nullptr || n_verts < 0 || n_faces < 0) return WV_ERR_ARG;
   if ((n_verts > 0 && vertices == nullptr) || (n_faces > 0 && faces == nullptr))
     return WV_ERR_ARG;
-  return wv::launch_pack(kind, vertices, vert_f64, n_verts, faces, faces_i64, n_faces,
-                         nullptr, packed, static_cast<cudaStream_t>(stream));
+  return wv::launch_pack(kind, vertices, vert_f64, n_verts, faces, faces_i64, n_faces, nullptr,
+                         packed, as_stream(stream));
 }
 
+// ---- forward ---------------------------------------------------------------
 size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {
     case WV_PACK_EXACT_F32: return wv::exact_fwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_SOFT_F32: return wv::soft_fwd_workspace_bytes(n_faces, count, sm_count());
     default: return 0;
   }
 }
@@ -82,28 +104,207 @@ size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
 int wv_exact_fwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                           int64_t count, int policy, float* out, uint8_t* flags,
                           void* workspace, size_t workspace_bytes, void* stream) {
-  if (packed == nullptr || out == nullptr || n_faces < 0) return WV_ERR_ARG;
-  if (!grid_ok(grid, n0, count)) return WV_ERR_ARG;
-  wv::PointSource ps{};
-  ps.kind = wv::PointSource::kGrid;
-  ps.grid = to_desc(grid);
-  ps.n0 = n0;
-  return wv::launch_exact_fwd_f32(packed, n_faces, ps, count, policy, out, flags, workspace,
-                                  workspace_bytes, sm_count(),
-                                  static_cast<cudaStream_t>(stream));
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count)) return WV_ERR_ARG;
+  return wv::launch_exact_fwd_f32(packed, n_faces, grid_src(grid, n0), count, policy, out, flags,
+                                  workspace, workspace_bytes, sm_count(), as_stream(stream));
 }
 
 int wv_exact_fwd_points_f32(const void* packed, int64_t n_faces, const float* points,
                             int64_t count, int policy, float* out, uint8_t* flags,
                             void* workspace, size_t workspace_bytes, void* stream) {
-  if (packed == nullptr || out == nullptr || n_faces < 0 || count < 0) return WV_ERR_ARG;
-  if (count > 0 && points == nullptr) return WV_ERR_ARG;
-  wv::PointSource ps{};
-  ps.kind = wv::PointSource::kList;
-  ps.points = points;
-  return wv::launch_exact_fwd_f32(packed, n_faces, ps, count, policy, out, flags, workspace,
-                                  workspace_bytes, sm_count(),
-                                  static_cast<cudaStream_t>(stream));
+  if (!fwd_args_ok(packed, out, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_fwd_f32(packed, n_faces, list_src(points, nullptr), count, policy, out,
+                                  flags, workspace, workspace_bytes, sm_count(),
+                                  as_stream(stream));
+}
+
+int wv_soft_fwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, int policy, float* out, uint8_t* flags, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count)) return WV_ERR_ARG;
+  return wv::launch_soft_fwd_f32(packed, n_faces, grid_src(grid, n0), count, policy, out, flags,
+                                 workspace, workspace_bytes, sm_count(), as_stream(stream));
+}
+
+int wv_soft_fwd_points_f32(const void* packed, int64_t n_faces, const float* points,
+                           int64_t count, int policy, float* out, uint8_t* flags,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_soft_fwd_f32(packed, n_faces, list_src(points, nullptr), count, policy, out,
+                                 flags, workspace, workspace_bytes, sm_count(),
+                                 as_stream(stream));
+}
+
+int wv_exact_fwd_grid_f64(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, int use_atan2, int policy, double* out, uint8_t* flags,
+                          void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count)) return WV_ERR_ARG;
+  return wv::launch_exact_fwd_f64(packed, n_faces, grid_src(grid, n0), count, use_atan2, policy,
+                                  out, flags, as_stream(stream));
+}
+
+int wv_exact_fwd_points_f64(const void* packed, int64_t n_faces, const double* points,
+                            int64_t count, int use_atan2, int policy, double* out,
+                            uint8_t* flags, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_fwd_f64(packed, n_faces, list_src(nullptr, points), count, use_atan2,
+                                  policy, out, flags, as_stream(stream));
+}
+
+int wv_soft_fwd_grid_f64(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, int policy, double* out, uint8_t* flags, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count)) return WV_ERR_ARG;
+  return wv::launch_soft_fwd_f64(packed, n_faces, grid_src(grid, n0), count, policy, out, flags,
+                                 as_stream(stream));
+}
+
+int wv_soft_fwd_points_f64(const void* packed, int64_t n_faces, const double* points,
+                           int64_t count, int policy, double* out, uint8_t* flags,
+                           void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_soft_fwd_f64(packed, n_faces, list_src(nullptr, points), count, policy, out,
+                                 flags, as_stream(stream));
+}
+
+// ---- backward --------------------------------------------------------------
+size_t wv_bwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
+  switch (kind) {
+    case WV_PACK_EXACT_F32:
+    case WV_PACK_SOFTGRAD_F32: return wv::bwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_EXACT_F64:
+    case WV_PACK_SOFTGRAD_F64: return wv::bwd64_workspace_bytes(n_faces, count, sm_count());
+    default: return 0;
+  }
+}
+
+int wv_exact_bwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, const float* coefs, double coef_scale,
+                          double* face_grad, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || !grid_ok(grid, n0, count))
+    return WV_ERR_ARG;
+  return wv::launch_exact_bwd_f32(packed, n_faces, grid_src(grid, n0), count, coefs, coef_scale,
+                                  face_grad, workspace, workspace_bytes, sm_count(),
+                                  as_stream(stream));
+}
+
+int wv_exact_bwd_points_f32(const void* packed, int64_t n_faces, const float* points,
+                            int64_t count, const float* coefs, double coef_scale,
+                            double* face_grad, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_bwd_f32(packed, n_faces, list_src(points, nullptr), count, coefs,
+                                  coef_scale, face_grad, workspace, workspace_bytes, sm_count(),
+                                  as_stream(stream));
+}
+
+int wv_soft_bwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, const float* coefs, double coef_scale,
+                         double* face_grad, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || !grid_ok(grid, n0, count))
+    return WV_ERR_ARG;
+  return wv::launch_soft_bwd_f32(packed, n_faces, grid_src(grid, n0), count, coefs, coef_scale,
+                                 face_grad, workspace, workspace_bytes, sm_count(),
+                                 as_stream(stream));
+}
+
+int wv_soft_bwd_points_f32(const void* packed, int64_t n_faces, const float* points,
+                           int64_t count, const float* coefs, double coef_scale,
+                           double* face_grad, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_soft_bwd_f32(packed, n_faces, list_src(points, nullptr), count, coefs,
+                                 coef_scale, face_grad, workspace, workspace_bytes, sm_count(),
+                                 as_stream(stream));
+}
+
+int wv_exact_bwd_grid_f64(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                          int64_t count, const double* coefs, double coef_scale,
+                          double* face_grad, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || !grid_ok(grid, n0, count))
+    return WV_ERR_ARG;
+  return wv::launch_exact_bwd_f64(packed, n_faces, grid_src(grid, n0), count, coefs, coef_scale,
+                                  face_grad, workspace, workspace_bytes, sm_count(),
+                                  as_stream(stream));
+}
+
+int wv_exact_bwd_points_f64(const void* packed, int64_t n_faces, const double* points,
+                            int64_t count, const double* coefs, double coef_scale,
+                            double* face_grad, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_bwd_f64(packed, n_faces, list_src(nullptr, points), count, coefs,
+                                  coef_scale, face_grad, workspace, workspace_bytes, sm_count(),
+                                  as_stream(stream));
+}
+
+int wv_soft_bwd_grid_f64(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                         int64_t count, const double* coefs, double coef_scale,
+                         double* face_grad, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || !grid_ok(grid, n0, count))
+    return WV_ERR_ARG;
+  return wv::launch_soft_bwd_f64(packed, n_faces, grid_src(grid, n0), count, coefs, coef_scale,
+                                 face_grad, workspace, workspace_bytes, sm_count(),
+                                 as_stream(stream));
+}
+
+int wv_soft_bwd_points_f64(const void* packed, int64_t n_faces, const double* points,
+                           int64_t count, const double* coefs, double coef_scale,
+                           double* face_grad, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_soft_bwd_f64(packed, n_faces, list_src(nullptr, points), count, coefs,
+                                 coef_scale, face_grad, workspace, workspace_bytes, sm_count(),
+                                 as_stream(stream));
+}
+
+int wv_face_to_vertex(const double* face_grad, const int64_t* csr_offsets,
+                      const int64_t* csr_slots, int64_t n_verts, const double* scale,
+                      int accumulate, double* out64, float* out32, void* stream) {
+  if (n_verts < 0) return WV_ERR_ARG;
+  if (n_verts > 0 && (csr_offsets == nullptr || (out64 == nullptr && out32 == nullptr)))
+    return WV_ERR_ARG;
+  return wv::launch_face_to_vertex(face_grad, csr_offsets, csr_slots, n_verts, scale, accumulate,
+                                   out64, out32, sm_count(), as_stream(stream));
+}
+
+// ---- loss --------------------------------------------------------------------
+size_t wv_loss_workspace_bytes(int64_t count) { return wv::loss_workspace_bytes(count); }
+
+int wv_loss_terms_f32(const float* values, const uint8_t* flags, const float* targets,
+                      const float* weights, int64_t count, float* coefs, double* sums,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  if (count < 0 || sums == nullptr) return WV_ERR_ARG;
+  if (count > 0 && (values == nullptr || flags == nullptr || targets == nullptr || coefs == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_loss_f32(values, flags, targets, weights, count, coefs, sums, workspace,
+                             workspace_bytes, as_stream(stream));
+}
+
+int wv_loss_terms_f64(const double* values, const uint8_t* flags, const double* targets,
+                      const double* weights, int64_t count, double* coefs, double* sums,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  if (count < 0 || sums == nullptr) return WV_ERR_ARG;
+  if (count > 0 && (values == nullptr || flags == nullptr || targets == nullptr || coefs == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_loss_f64(values, flags, targets, weights, count, coefs, sums, workspace,
+                             workspace_bytes, as_stream(stream));
+}
+
+int wv_loss_finalize(double* sums, void* stream) {
+  if (sums == nullptr) return WV_ERR_ARG;
+  return wv::launch_loss_finalize(sums, as_stream(stream));
 }
 
 }  // extern "C"

@@ -39,6 +39,26 @@ struct __align__(16) SoftRecF32 {
 };
 static_assert(sizeof(SoftRecF32) == 32, "record size");
 
+// SoftGradRecF32 (64 B): what the soft backward needs per face -- centroid,
+//   N = u x w, u = v1-v0, w = v2-v0 (all from f64, then rounded).
+struct __align__(16) SoftGradRecF32 {
+  float4 c;  // c.xyz, 0
+  float4 n;  // N.xyz, 0
+  float4 u;  // u.xyz, 0
+  float4 w;  // w.xyz, 0
+};
+static_assert(sizeof(SoftGradRecF32) == 64, "record size");
+
+// SoftGradRecF64 (128 B): f64 twin for the parity backward.
+struct __align__(16) SoftGradRecF64 {
+  double c[3];
+  double n[3];
+  double u[3];
+  double w[3];
+  double pad[4];
+};
+static_assert(sizeof(SoftGradRecF64) == 128, "record size");
+
 // ExactRecF64 (128 B): the reference's own per-face arrays (tri, nhat, pld,
 //   winding.py:258-268) plus a dead flag for degenerate faces.
 struct __align__(16) ExactRecF64 {
@@ -64,7 +84,8 @@ static_assert(sizeof(SoftRecF64) == 64, "record size");
 struct __align__(16) PackHeader {
   double eps;       // 1e-9 * bbox diagonal (winding.py:193-197)
   float eps_f32;    // float32(eps)  (winding.py:367)
-  int32_t kind;     // 1 exact f32, 2 soft f32, 3 exact f64, 4 soft f64
+  int32_t kind;     // 1 exact f32, 2 soft f32, 3 exact f64, 4 soft f64,
+                    // 5 soft-grad f32, 6 soft-grad f64
   int64_t n_faces;
   int64_t n_live;   // non-degenerate faces (exact kinds)
   double pad[4];
@@ -198,6 +219,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Producer-side wait: the slot frees only after every consumer warp has
+// finished a whole tile (tens of microseconds), so poll with a sleep instead
+// of spinning -- a spinning producer steals issue slots from the consumers.
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(2000);
+  }
+}
 __device__ __forceinline__ void tma_bulk_g2s(void* smem_dst, const void* gmem_src,
                                              uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -240,7 +280,7 @@ __device__ __forceinline__ void ring_produce(FaceRing<Rec, TILE, STAGES>& r,
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int64_t it = t - t_begin;
     const int s = (int)(it % STAGES);
-    if (it >= STAGES) mbar_wait(&r.empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+    if (it >= STAGES) mbar_wait_sleepy(&r.empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
     const int64_t first = t * TILE;
     const int64_t cnt = (n_recs - first) < TILE ? (n_recs - first) : TILE;
     const uint32_t bytes = (uint32_t)(cnt * (int64_t)sizeof(Rec));

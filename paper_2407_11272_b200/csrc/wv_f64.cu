@@ -1,0 +1,394 @@
+// wv_f64.cu -- FP64 parity kernels (compiled with -fmad=false).
+//
+// These are the GPU twins of the reference's default-precision kernels,
+// written in the reference's exact operation order so that the
+// `precision="f64"` API path reproduces the reference to the last bit where
+// the math library allows:
+//   exact_fwd_f64  <- _kernels.exact_batch  (_kernels.py:34-116); identical
+//                     except CUDA's atan2 vs libm's (<= 1-2 ulp per term)
+//   soft_fwd_f64   <- _kernels.soft_batch   (_kernels.py:119-158); bit-exact
+// Faces are streamed through the same TMA bulk-copy ring as the FP32 path and
+// accumulated sequentially in face index order per point (no face splits), as
+// the reference does.
+#include "wv_kernels.h"
+
+namespace wv {
+
+constexpr int kF64Tile = 64;
+constexpr int kF64Stages = 4;
+constexpr int kF64ConsumerWarps = 4;
+constexpr int kF64NC = kF64ConsumerWarps * 32;
+constexpr int kF64Threads = kF64NC + 32;
+constexpr int kF64P = 4;
+constexpr double kBaryTol = 1e-12;  // _kernels.py:31
+
+struct ExactF64Pol {
+  using Rec = ExactRecF64;
+  static constexpr double kDiv = 4.0 * kPi;  // out = acc / _FOUR_PI
+  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
+                                              double eps, int use_atan2, double& acc,
+                                              bool& hit) {
+    if (R.dead != 0.0) return;  // dropped by _prepare_exact
+    const double* t = R.v;
+    const double ax = t[0] - qx, ay = t[1] - qy, az = t[2] - qz;
+    const double bx = t[3] - qx, by = t[4] - qy, bz = t[5] - qz;
+    const double cx = t[6] - qx, cy = t[7] - qy, cz = t[8] - qz;
+    const double na = sqrt(ax * ax + ay * ay + az * az);
+    const double nb = sqrt(bx * bx + by * by + bz * bz);
+    const double nc = sqrt(cx * cx + cy * cy + cz * cz);
+    if (na < eps || nb < eps || nc < eps) {
+      hit = true;
+      return;
+    }
+    const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
+    if (-eps < pd && pd < eps) {
+      const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+      const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
+      const double d00 = ux * ux + uy * uy + uz * uz;
+      const double d01 = ux * wx + uy * wy + uz * wz;
+      const double d11 = wx * wx + wy * wy + wz * wz;
+      const double denom = d00 * d11 - d01 * d01;
+      const double ru = -(ax * ux + ay * uy + az * uz);
+      const double rw = -(ax * wx + ay * wy + az * wz);
+      const double b1 = (d11 * ru - d01 * rw) / denom;
+      const double b2 = (d00 * rw - d01 * ru) / denom;
+      if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) {
+        hit = true;
+        return;
+      }
+    }
+    const double alpha = (ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz)) +
+                         az * (bx * cy - by * cx);
+    const double beta = (na * (nb * nc) + (bx * cx + by * cy + bz * cz) * na) +
+                        ((ax * bx + ay * by + az * bz) * nc + (cx * ax + cy * ay + cz * az) * nb);
+    if (use_atan2) {
+      acc += 2.0 * atan2(alpha, beta);
+    } else {  // regression-demonstration branch, _kernels.py:106-114
+      if (beta != 0.0)
+        acc += 2.0 * atan(alpha / beta);
+      else if (alpha > 0.0)
+        acc += kPi;
+      else if (alpha < 0.0)
+        acc -= kPi;
+    }
+  }
+};
+
+struct SoftF64Pol {
+  using Rec = SoftRecF64;
+  static constexpr double kDiv = 8.0 * kPi;  // out = acc / _EIGHT_PI
+  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
+                                              double eps, int, double& acc, bool& hit) {
+    const double dx = R.c[0] - qx, dy = R.c[1] - qy, dz = R.c[2] - qz;
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    const double r = sqrt(r2);
+    if (r < eps) {
+      hit = true;
+      return;
+    }
+    acc += (R.n[0] * dx + R.n[1] * dy + R.n[2] * dz) / (r2 * r);
+  }
+};
+
+template <class Pol, class Src>
+__global__ void __launch_bounds__(kF64Threads, 2)
+fwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
+               int64_t n_faces, Src src, int64_t n_count, int use_atan2, int policy,
+               double* __restrict__ out, uint8_t* __restrict__ flags) {
+  using Rec = typename Pol::Rec;
+  __shared__ FaceRing<Rec, kF64Tile, kF64Stages> ring;
+  ring_init(ring, kF64ConsumerWarps);
+  const int64_t n_tiles = (n_faces + kF64Tile - 1) / kF64Tile;
+  if ((threadIdx.x >> 5) == kF64ConsumerWarps) {
+    if ((threadIdx.x & 31) == 0 && n_tiles > 0) ring_produce(ring, recs, n_faces, 0, n_tiles);
+    return;
+  }
+  const double eps = hdr->eps;
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * (kF64NC * kF64P);
+  double qx[kF64P], qy[kF64P], qz[kF64P], acc[kF64P];
+  bool hit[kF64P];
+#pragma unroll
+  for (int p = 0; p < kF64P; ++p) {
+    int64_t l = base + p * kF64NC + tid;
+    if (l >= n_count) l = n_count - 1;
+    src.point(l, qx[p], qy[p], qz[p]);
+    acc[p] = 0.0;
+    hit[p] = false;
+  }
+  for (int64_t t = 0; t < n_tiles; ++t) {
+    const int s = (int)(t % kF64Stages);
+    mbar_wait(&ring.full[s], (uint32_t)((t / kF64Stages) & 1));
+    const int64_t first = t * kF64Tile;
+    const int cnt = (int)((n_faces - first) < kF64Tile ? (n_faces - first) : kF64Tile);
+    const Rec* tile = ring.tiles[s];
+#pragma unroll 1
+    for (int f = 0; f < cnt; ++f) {
+      const Rec R = tile[f];
+#pragma unroll
+      for (int p = 0; p < kF64P; ++p) Pol::pair(R, qx[p], qy[p], qz[p], eps, use_atan2, acc[p], hit[p]);
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&ring.empty[s]);
+  }
+#pragma unroll
+  for (int p = 0; p < kF64P; ++p) {
+    const int64_t l = base + p * kF64NC + tid;
+    if (l < n_count) {
+      double w = acc[p] / Pol::kDiv;
+      if (hit[p] && policy == kPolicyHalf) w = 0.5;
+      out[l] = w;
+      if (flags) flags[l] = hit[p] ? 1 : 0;
+    }
+  }
+}
+
+template <class Pol>
+static int launch_f64(const void* packed, int64_t n_faces, const PointSource& ps, int64_t n_count,
+                      int use_atan2, int policy, double* out, uint8_t* flags,
+                      cudaStream_t stream) {
+  if (n_count <= 0) return kOk;
+  const PackHeader* hdr = static_cast<const PackHeader*>(packed);
+  const auto* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
+  const int64_t per_block = (int64_t)kF64NC * kF64P;
+  const unsigned blocks = (unsigned)((n_count + per_block - 1) / per_block);
+  if (ps.kind == PointSource::kGrid) {
+    GridSrc src{ps.grid, ps.n0};
+    fwd_f64_kernel<Pol, GridSrc><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+  } else {
+    ListSrc64 src{ps.points64};
+    fwd_f64_kernel<Pol, ListSrc64><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+int launch_exact_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, int use_atan2, int policy, double* out, uint8_t* flags,
+                         cudaStream_t stream) {
+  return launch_f64<ExactF64Pol>(packed, n_faces, ps, n_count, use_atan2, policy, out, flags,
+                                 stream);
+}
+
+int launch_soft_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, int policy, double* out, uint8_t* flags,
+                        cudaStream_t stream) {
+  return launch_f64<SoftF64Pol>(packed, n_faces, ps, n_count, 1, policy, out, flags, stream);
+}
+
+
+// ---------------------------------------------------------------------------
+// FP64 backward (parity path): same face-per-thread / point-broadcast mapping
+// as wv_bwd_f32.cu, per-pair arithmetic in the reference's operation order.
+constexpr int kBwd64Threads = 128;
+constexpr int kBwd64Chunk = 256;
+constexpr double kEightPi = 8.0 * kPi;
+
+struct ExactBwd64 {
+  using Rec = ExactRecF64;
+  // closed-form d(theta)/dv of the exact forward (oracle wvo_exact_grad_accum)
+  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
+                                              double coef, double eps, double* g) {
+    if (R.dead != 0.0) return;
+    const double* t = R.v;
+    const double a[3] = {t[0] - qx, t[1] - qy, t[2] - qz};
+    const double b[3] = {t[3] - qx, t[4] - qy, t[5] - qz};
+    const double c[3] = {t[6] - qx, t[7] - qy, t[8] - qz};
+    const double na = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    const double nb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    const double nc = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    if (na < eps || nb < eps || nc < eps) return;
+    const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
+    if (-eps < pd && pd < eps) {
+      const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+      const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
+      const double d00 = ux * ux + uy * uy + uz * uz;
+      const double d01 = ux * wx + uy * wy + uz * wz;
+      const double d11 = wx * wx + wy * wy + wz * wz;
+      const double denom = d00 * d11 - d01 * d01;
+      const double ru = -(a[0] * ux + a[1] * uy + a[2] * uz);
+      const double rw = -(a[0] * wx + a[1] * wy + a[2] * wz);
+      const double b1 = (d11 * ru - d01 * rw) / denom;
+      const double b2 = (d00 * rw - d01 * ru) / denom;
+      if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) return;
+    }
+    const double bxc[3] = {b[1] * c[2] - b[2] * c[1], b[2] * c[0] - b[0] * c[2],
+                           b[0] * c[1] - b[1] * c[0]};
+    const double cxa[3] = {c[1] * a[2] - c[2] * a[1], c[2] * a[0] - c[0] * a[2],
+                           c[0] * a[1] - c[1] * a[0]};
+    const double axb[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
+                           a[0] * b[1] - a[1] * b[0]};
+    const double alpha = a[0] * bxc[0] + a[1] * bxc[1] + a[2] * bxc[2];
+    const double ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+    const double bc = b[0] * c[0] + b[1] * c[1] + b[2] * c[2];
+    const double ca = c[0] * a[0] + c[1] * a[1] + c[2] * a[2];
+    const double beta = na * nb * nc + bc * na + ab * nc + ca * nb;
+    const double den = alpha * alpha + beta * beta;
+    if (den == 0.0) return;
+    const double s = coef / (2.0 * kPi * den);
+    const double ga = s * beta, gb = -s * alpha;
+    const double ka = (nb * nc + bc) / na, kb = (na * nc + ca) / nb, kc = (na * nb + ab) / nc;
+    for (int d = 0; d < 3; ++d) {
+      g[d] += ga * bxc[d] + gb * (ka * a[d] + nc * b[d] + nb * c[d]);
+      g[3 + d] += ga * cxa[d] + gb * (kb * b[d] + nc * a[d] + na * c[d]);
+      g[6 + d] += ga * axb[d] + gb * (kc * c[d] + nb * a[d] + na * b[d]);
+    }
+  }
+};
+
+struct SoftBwd64 {
+  using Rec = SoftGradRecF64;
+  // _kernels.py:198-232, same expression order per pair
+  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
+                                              double coef, double eps, double* g) {
+    const double dx = R.c[0] - qx, dy = R.c[1] - qy, dz = R.c[2] - qz;
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    const double r = sqrt(r2);
+    if (r < eps) return;
+    const double nx = R.n[0], ny = R.n[1], nz = R.n[2];
+    const double s = nx * dx + ny * dy + nz * dz;
+    const double inv3 = coef / (kEightPi * r2 * r);
+    const double inv5 = coef * s / (kEightPi * r2 * r2 * r);
+    const double ux = R.u[0], uy = R.u[1], uz = R.u[2];
+    const double wx = R.w[0], wy = R.w[1], wz = R.w[2];
+    const double g1x = wy * dz - wz * dy, g1y = wz * dx - wx * dz, g1z = wx * dy - wy * dx;
+    const double g2x = dy * uz - dz * uy, g2y = dz * ux - dx * uz, g2z = dx * uy - dy * ux;
+    const double n3x = nx / 3.0, n3y = ny / 3.0, n3z = nz / 3.0;
+    g[0] += (-g1x - g2x + n3x) * inv3 - dx * inv5;
+    g[1] += (-g1y - g2y + n3y) * inv3 - dy * inv5;
+    g[2] += (-g1z - g2z + n3z) * inv3 - dz * inv5;
+    g[3] += (g1x + n3x) * inv3 - dx * inv5;
+    g[4] += (g1y + n3y) * inv3 - dy * inv5;
+    g[5] += (g1z + n3z) * inv3 - dz * inv5;
+    g[6] += (g2x + n3x) * inv3 - dx * inv5;
+    g[7] += (g2y + n3y) * inv3 - dy * inv5;
+    g[8] += (g2z + n3z) * inv3 - dz * inv5;
+  }
+};
+
+template <class Pol, class Src>
+__global__ void __launch_bounds__(kBwd64Threads, 2)
+bwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
+               int64_t n_faces, Src src, const double* __restrict__ coefs, int64_t n_count,
+               int64_t pts_per_split, double coef_scale, double* __restrict__ out) {
+  __shared__ double4 chunk[kBwd64Chunk];
+  const int64_t f = (int64_t)blockIdx.x * kBwd64Threads + threadIdx.x;
+  const bool live = f < n_faces;
+  const typename Pol::Rec R = recs[live ? f : 0];
+  const double eps = hdr->eps;
+  const int64_t p_begin = (int64_t)blockIdx.y * pts_per_split;
+  int64_t p_end = p_begin + pts_per_split;
+  if (p_end > n_count) p_end = n_count;
+  double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t c0 = p_begin; c0 < p_end; c0 += kBwd64Chunk) {
+    const int n = (int)((p_end - c0) < kBwd64Chunk ? (p_end - c0) : kBwd64Chunk);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kBwd64Threads) {
+      double x, y, z;
+      src.point(c0 + i, x, y, z);
+      chunk[i] = make_double4(x, y, z, coefs[c0 + i] * coef_scale);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) {
+      const double4 q = chunk[i];
+      if (q.w == 0.0) continue;  // _kernels.py:182-184
+      Pol::pair(R, q.x, q.y, q.z, q.w, eps, g);
+    }
+  }
+  if (live) {
+    double* dst = out + ((int64_t)blockIdx.y * n_faces + f) * 9;
+    for (int j = 0; j < 9; ++j) dst[j] = g[j];
+  }
+}
+
+__global__ void reduce_splits64_kernel(const double* __restrict__ part, int splits, int64_t n,
+                                       double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int s = 0; s < splits; ++s) a += part[(int64_t)s * n + i];
+    out[i] = a;
+  }
+}
+
+static void bwd64_plan(int64_t n_faces, int64_t n_count, int num_sms, int64_t* bx, int* splits,
+                       int64_t* pps) {
+  *bx = (n_faces + kBwd64Threads - 1) / kBwd64Threads;
+  if (*bx < 1) *bx = 1;
+  const int64_t want = (int64_t)num_sms * 8;
+  int64_t s = (want + *bx - 1) / *bx;
+  const int64_t max_s = (n_count + kBwd64Chunk - 1) / kBwd64Chunk;
+  if (s > max_s) s = max_s;
+  if (s > 4096) s = 4096;
+  if (s < 1) s = 1;
+  *pps = ((n_count + s - 1) / s + kBwd64Chunk - 1) / kBwd64Chunk * kBwd64Chunk;
+  *splits = (int)((n_count + *pps - 1) / *pps);
+  if (*splits < 1) *splits = 1;
+}
+
+size_t bwd64_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+  int64_t bx, pps;
+  int s;
+  bwd64_plan(n_faces, n_count, num_sms, &bx, &s, &pps);
+  return s > 1 ? (size_t)s * n_faces * 9 * sizeof(double) : 0;
+}
+
+template <class Pol>
+static int launch_bwd64(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, const double* coefs, double coef_scale,
+                        double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                        cudaStream_t stream) {
+  if (n_faces <= 0) return kOk;
+  if (n_count <= 0)
+    return cudaMemsetAsync(face_grad, 0, (size_t)n_faces * 9 * sizeof(double), stream) ==
+                   cudaSuccess ? kOk : kErrCuda;
+  const PackHeader* hdr = static_cast<const PackHeader*>(packed);
+  const auto* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
+  int64_t bx, pps;
+  int splits;
+  bwd64_plan(n_faces, n_count, num_sms, &bx, &splits, &pps);
+  double* dst = face_grad;
+  if (splits > 1) {
+    if (ws == nullptr || ws_bytes < (size_t)splits * n_faces * 9 * sizeof(double))
+      return kErrWorkspace;
+    dst = static_cast<double*>(ws);
+  }
+  dim3 grid((unsigned)bx, (unsigned)splits);
+  if (ps.kind == PointSource::kGrid) {
+    GridSrc src{ps.grid, ps.n0};
+    bwd_f64_kernel<Pol, GridSrc><<<grid, kBwd64Threads, 0, stream>>>(hdr, recs, n_faces, src,
+                                                                     coefs, n_count, pps,
+                                                                     coef_scale, dst);
+  } else {
+    ListSrc64 src{ps.points64};
+    bwd_f64_kernel<Pol, ListSrc64><<<grid, kBwd64Threads, 0, stream>>>(hdr, recs, n_faces, src,
+                                                                       coefs, n_count, pps,
+                                                                       coef_scale, dst);
+  }
+  if (splits > 1) {
+    const int64_t n = n_faces * 9;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > num_sms * 8) blocks = num_sms * 8;
+    reduce_splits64_kernel<<<blocks, 256, 0, stream>>>(dst, splits, n, face_grad);
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+int launch_exact_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, const double* coefs, double coef_scale,
+                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                         cudaStream_t stream) {
+  return launch_bwd64<ExactBwd64>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad,
+                                  ws, ws_bytes, num_sms, stream);
+}
+int launch_soft_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, const double* coefs, double coef_scale,
+                        double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                        cudaStream_t stream) {
+  return launch_bwd64<SoftBwd64>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad,
+                                 ws, ws_bytes, num_sms, stream);
+}
+
+}  // namespace wv

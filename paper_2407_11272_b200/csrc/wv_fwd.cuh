@@ -1,0 +1,165 @@
+// wv_fwd.cuh -- generic FP32 all-pairs forward (point per thread, faces
+// streamed through a TMA ring).  Instantiated by wv_fwd_f32.cu with the exact
+// (Van Oosterom-Strackee) and soft (dipole) pair policies.
+//
+//  * one producer warp streams TILE-record tiles of the packed face array into
+//    a STAGES-deep shared-memory ring with cp.async.bulk (TMA, SASS UBLKCP);
+//  * each consumer thread holds P query points in registers and walks the
+//    tiles in face order; per face it evaluates the common path for all P
+//    points branch-free and defers the few "rare" pairs (near-plane /
+//    wide-angle / on-surface candidates) to an out-of-line handler;
+//  * per tile the terms are summed in fp32, tile partials in fp64.
+#pragma once
+
+#include "wv_kernels.h"
+
+namespace wv {
+
+template <class Pol, class Src>
+__global__ void __launch_bounds__(Pol::kThreads, Pol::kMinBlocks)
+fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
+               int64_t n_faces, Src src, int64_t n_count, int64_t tiles_per_split, OutF32 o) {
+  using Rec = typename Pol::Rec;
+  constexpr int TILE = Pol::kTile;
+  constexpr int STAGES = Pol::kStages;
+  constexpr int CW = Pol::kConsumerWarps;
+  constexpr int NC = CW * 32;
+  constexpr int P = Pol::kP;
+  __shared__ FaceRing<Rec, TILE, STAGES> ring;
+  ring_init(ring, CW);
+
+  const int64_t n_tiles = (n_faces + TILE - 1) / TILE;
+  const int64_t t_begin = (int64_t)blockIdx.y * tiles_per_split;
+  int64_t t_end = t_begin + tiles_per_split;
+  if (t_end > n_tiles) t_end = n_tiles;
+
+  if ((threadIdx.x >> 5) == CW) {  // producer warp
+    if ((threadIdx.x & 31) == 0 && t_begin < t_end)
+      ring_produce(ring, recs, n_faces, t_begin, t_end);
+    return;
+  }
+
+  const float eps = hdr->eps_f32;
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * (NC * P);
+  float qx[P], qy[P], qz[P];
+  double accd[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    int64_t l = base + p * NC + tid;
+    if (l >= n_count) l = n_count - 1;  // padded lanes recompute a valid node
+    src.point(l, qx[p], qy[p], qz[p]);
+    accd[p] = 0.0;
+  }
+  typename Pol::Ctx ctx = Pol::make_ctx(eps);
+  uint32_t hits = 0;
+
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int64_t it = t - t_begin;
+    const int s = (int)(it % STAGES);
+    mbar_wait(&ring.full[s], (uint32_t)((it / STAGES) & 1));
+    const int64_t first = t * TILE;
+    const int cnt = (int)((n_faces - first) < TILE ? (n_faces - first) : TILE);
+    const Rec* tile = ring.tiles[s];
+    float tacc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) tacc[p] = 0.0f;
+
+#pragma unroll 1
+    for (int f = 0; f < cnt; ++f) {
+      const Rec R = tile[f];
+      uint32_t rare = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (Pol::common(R, qx[p], qy[p], qz[p], ctx, tacc[p])) rare |= 1u << p;
+      }
+      if (rare != 0u) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          if (rare & (1u << p)) {
+            const float th = Pol::rare(R, qx[p], qy[p], qz[p], eps);
+            if (th != th) hits |= 1u << p;  // NaN marks an on-surface pair
+            else tacc[p] += th;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) accd[p] += (double)tacc[p];
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&ring.empty[s]);
+  }
+
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int64_t l = base + p * NC + tid;
+    if (l < n_count) o.store(blockIdx.y, l, accd[p], (hits >> p) & 1u);
+  }
+}
+
+template <class Pol>
+struct FwdPlan {
+  int64_t blocks_x = 0;
+  int splits = 1;
+  int64_t tiles_per_split = 0;
+  static FwdPlan make(int64_t n_faces, int64_t n_count, int num_sms) {
+    FwdPlan pl;
+    const int64_t per_block = (int64_t)Pol::kConsumerWarps * 32 * Pol::kP;
+    pl.blocks_x = (n_count + per_block - 1) / per_block;
+    const int64_t n_tiles = (n_faces + Pol::kTile - 1) / Pol::kTile;
+    const int s = choose_splits(pl.blocks_x, n_tiles, num_sms, Pol::kMinBlocks);
+    pl.tiles_per_split = n_tiles > 0 ? (n_tiles + s - 1) / s : 0;
+    pl.splits = pl.tiles_per_split > 0 ? (int)((n_tiles + pl.tiles_per_split - 1) / pl.tiles_per_split) : 1;
+    return pl;
+  }
+  size_t workspace(int64_t n_count) const {
+    return splits > 1 ? (size_t)splits * (size_t)n_count * (sizeof(double) + 1) + 256 : 0;
+  }
+};
+
+__global__ void finalize_theta_kernel(const double* __restrict__ part,
+                                      const uint8_t* __restrict__ pflags, int splits,
+                                      int64_t n_count, int policy, float* __restrict__ out_f32,
+                                      uint8_t* __restrict__ flags, double scale);
+
+template <class Pol>
+int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, int64_t n_count,
+                   int policy, float* out, uint8_t* flags, void* workspace, size_t ws_bytes,
+                   int num_sms, cudaStream_t stream) {
+  if (n_count <= 0) return kOk;
+  const PackHeader* hdr = static_cast<const PackHeader*>(packed);
+  const typename Pol::Rec* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
+  const FwdPlan<Pol> pl = FwdPlan<Pol>::make(n_faces, n_count, num_sms);
+  OutF32 o;
+  o.out = out;
+  o.flags = flags;
+  o.policy = policy;
+  o.scale = Pol::kScale;
+  if (pl.splits > 1) {
+    if (workspace == nullptr || ws_bytes < pl.workspace(n_count)) return kErrWorkspace;
+    o.part = static_cast<double*>(workspace);
+    o.part_flags = reinterpret_cast<uint8_t*>(o.part + (size_t)pl.splits * n_count);
+    o.n_count = n_count;
+  }
+  dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits);
+  const unsigned threads = Pol::kThreads;
+  if (ps.kind == PointSource::kGrid) {
+    GridSrc src{ps.grid, ps.n0};
+    fwd_f32_kernel<Pol, GridSrc><<<grid, threads, 0, stream>>>(hdr, recs, n_faces, src, n_count,
+                                                                 pl.tiles_per_split, o);
+  } else {
+    ListSrc src{ps.points};
+    fwd_f32_kernel<Pol, ListSrc><<<grid, threads, 0, stream>>>(hdr, recs, n_faces, src, n_count,
+                                                                 pl.tiles_per_split, o);
+  }
+  if (pl.splits > 1) {
+    const int t = 256;
+    int blocks = (int)((n_count + t - 1) / t);
+    if (blocks > num_sms * 8) blocks = num_sms * 8;
+    finalize_theta_kernel<<<blocks, t, 0, stream>>>(o.part, o.part_flags, pl.splits, n_count,
+                                                    policy, out, flags, o.scale);
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+}  // namespace wv

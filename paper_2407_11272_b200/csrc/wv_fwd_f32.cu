@@ -1,0 +1,167 @@
+// wv_fwd_f32.cu -- FP32 forward kernels (sm_100a): exact generalized winding
+// number and the soft (dipole) winding number, both on the generic TMA-tiled
+// all-pairs skeleton of wv_fwd.cuh.
+//
+// Exact (replaces _kernels.exact_batch_f32, _kernels.py:235-309, and the f64
+// exact_batch hot loop, :34-116, under the 1e-5 tolerance of north_star):
+//   theta = atan2(alpha, beta),  Omega = 2 theta,  W = sum(theta) / (2 pi)
+//   alpha = N.(v0-q) (= det(a,b,c)), beta grouped as _kernels.py:98-103.
+//   Common pairs (beta >= |alpha|, |alpha| >= eps|N|) need one MUFU.RCP and an
+//   8-term minimax polynomial; the rest go to exact_rare().
+// Soft (replaces _kernels.soft_batch_f32, :312-349, and soft_batch, :119-158):
+//   term = N.(c-q) / |c-q|^3 with one MUFU.RSQ,  W = sum(term) / (8 pi);
+//   |c-q| < eps flags the point and skips the face.
+#include "wv_fwd.cuh"
+
+namespace wv {
+
+// Rare exact pairs: on-surface candidates (plane distance < eps,
+// _kernels.py:65-88) and wide angles (|theta| > pi/4, incl. beta < 0).
+// Recomputes the pair; returns theta, or NaN for an on-surface pair.
+__device__ __noinline__ float exact_rare(float4 A, float4 B, float4 C, float4 N, float qx,
+                                         float qy, float qz, float eps) {
+  const float ax = A.x - qx, ay = A.y - qy, az = A.z - qz;
+  const float bx = B.x - qx, by = B.y - qy, bz = B.z - qz;
+  const float cx = C.x - qx, cy = C.y - qy, cz = C.z - qz;
+  const float alpha = fmaf(N.z, az, fmaf(N.y, ay, N.x * ax));
+  const float la = sqrt_approx(fmaf(az, az, fmaf(ay, ay, ax * ax)));
+  const float lb = sqrt_approx(fmaf(bz, bz, fmaf(by, by, bx * bx)));
+  const float lc = sqrt_approx(fmaf(cz, cz, fmaf(cy, cy, cx * cx)));
+  const float ab = fmaf(az, bz, fmaf(ay, by, ax * bx));
+  const float bc = fmaf(bz, cz, fmaf(by, cy, bx * cx));
+  const float ca = fmaf(az, cz, fmaf(ay, cy, ax * cx));
+  const float g1 = fmaf(bc, la, la * (lb * lc));
+  const float g2 = __fadd_rn(__fmul_rn(ab, lc), __fmul_rn(ca, lb));
+  const float beta = g1 + g2;
+  const float epsN = A.w;
+  if (fabsf(alpha) < epsN) {
+    if (epsN == __int_as_float(0x7f800000)) return 0.0f;  // degenerate face
+    // _kernels.py:65-67 vertex test, then :70-88 plane + barycentric test
+    if (la < eps || lb < eps || lc < eps) return __int_as_float(0x7fc00000);
+    const float ux = B.x - A.x, uy = B.y - A.y, uz = B.z - A.z;
+    const float wx = C.x - A.x, wy = C.y - A.y, wz = C.z - A.z;
+    const float d00 = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
+    const float d01 = fmaf(uz, wz, fmaf(uy, wy, ux * wx));
+    const float d11 = fmaf(wz, wz, fmaf(wy, wy, wx * wx));
+    const float denom = __fsub_rn(__fmul_rn(d00, d11), __fmul_rn(d01, d01));
+    const float ru = -fmaf(az, uz, fmaf(ay, uy, ax * ux));
+    const float rw = -fmaf(az, wz, fmaf(ay, wy, ax * wx));
+    const float b1 = __fdiv_rn(__fsub_rn(__fmul_rn(d11, ru), __fmul_rn(d01, rw)), denom);
+    const float b2 = __fdiv_rn(__fsub_rn(__fmul_rn(d00, rw), __fmul_rn(d01, ru)), denom);
+    const float btol = 1e-12f;
+    if (b1 >= -btol && b2 >= -btol && b1 + b2 <= 1.0f + btol)
+      return __int_as_float(0x7fc00000);
+  }
+  return atan2_full(alpha, beta);
+}
+
+struct ExactPol {
+  using Rec = ExactRecF32;
+  static constexpr int kTile = 128;
+  static constexpr int kStages = 4;
+  static constexpr int kConsumerWarps = 4;
+  static constexpr int kThreads = kConsumerWarps * 32 + 32;
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kP = 8;
+  static constexpr double kScale = 1.0 / (2.0 * kPi);
+  struct Ctx {};
+  __device__ static Ctx make_ctx(float) { return Ctx{}; }
+  // returns true when the pair must go to the rare path (contributes 0 here)
+  __device__ __forceinline__ static bool common(const Rec& R, float qx, float qy, float qz,
+                                                const Ctx&, float& tacc) {
+    const float ax = R.v0e.x - qx, ay = R.v0e.y - qy, az = R.v0e.z - qz;
+    const float bx = R.v1.x - qx, by = R.v1.y - qy, bz = R.v1.z - qz;
+    const float cx = R.v2.x - qx, cy = R.v2.y - qy, cz = R.v2.z - qz;
+    const float alpha = fmaf(R.n.z, az, fmaf(R.n.y, ay, R.n.x * ax));
+    const float la = sqrt_approx(fmaf(az, az, fmaf(ay, ay, ax * ax)));
+    const float lb = sqrt_approx(fmaf(bz, bz, fmaf(by, by, bx * bx)));
+    const float lc = sqrt_approx(fmaf(cz, cz, fmaf(cy, cy, cx * cx)));
+    const float ab = fmaf(az, bz, fmaf(ay, by, ax * bx));
+    const float bc = fmaf(bz, cz, fmaf(by, cy, bx * cx));
+    const float ca = fmaf(az, cz, fmaf(ay, cy, ax * cx));
+    // beta grouped as _kernels.py:98-103: swapping v1<->v2 leaves it
+    // bit-identical, so orientation flips negate W exactly.
+    const float g1 = fmaf(bc, la, la * (lb * lc));
+    const float g2 = __fadd_rn(__fmul_rn(ab, lc), __fmul_rn(ca, lb));
+    const float beta = g1 + g2;
+    const float aa = fabsf(alpha);
+    const bool r = (aa > beta) || (aa < R.v0e.w);
+    const float tt = r ? 0.0f : alpha * rcp_approx(beta);
+    tacc = fmaf(tt, atan_poly_coef(tt * tt), tacc);
+    return r;
+  }
+  __device__ __forceinline__ static float rare(const Rec& R, float qx, float qy, float qz,
+                                               float eps) {
+    return exact_rare(R.v0e, R.v1, R.v2, R.n, qx, qy, qz, eps);
+  }
+};
+
+struct SoftPol {
+  using Rec = SoftRecF32;
+  static constexpr int kTile = 256;
+  static constexpr int kStages = 4;
+  static constexpr int kConsumerWarps = 4;
+  static constexpr int kThreads = kConsumerWarps * 32 + 32;
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kP = 8;
+  static constexpr double kScale = 1.0 / (8.0 * kPi);
+  struct Ctx {
+    float eps2;
+  };
+  __device__ static Ctx make_ctx(float eps) { return Ctx{eps * eps}; }
+  __device__ __forceinline__ static bool common(const Rec& R, float qx, float qy, float qz,
+                                                const Ctx& ctx, float& tacc) {
+    const float dx = R.c.x - qx, dy = R.c.y - qy, dz = R.c.z - qz;
+    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    const float rs = rsqrt_approx(r2);
+    const float s = fmaf(R.n.y, dz, fmaf(R.n.x, dy, R.c.w * dx));
+    const bool h = r2 < ctx.eps2;  // |c - q| < eps: on a centroid (_kernels.py:150)
+    const float rs3 = h ? 0.0f : rs * rs * rs;
+    tacc = fmaf(s, rs3, tacc);
+    return h;
+  }
+  __device__ __forceinline__ static float rare(const Rec&, float, float, float, float) {
+    return __int_as_float(0x7fc00000);  // always an on-surface (flagged) pair
+  }
+};
+
+// Sum split partials in split order (deterministic), then W = sum * scale.
+__global__ void finalize_theta_kernel(const double* __restrict__ part,
+                                      const uint8_t* __restrict__ pflags, int splits,
+                                      int64_t n_count, int policy, float* __restrict__ out_f32,
+                                      uint8_t* __restrict__ flags, double scale) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n_count;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    uint8_t h = 0;
+    for (int s = 0; s < splits; ++s) {
+      acc += part[(int64_t)s * n_count + l];
+      h |= pflags[(int64_t)s * n_count + l];
+    }
+    double w = acc * scale;
+    if (h && policy == kPolicyHalf) w = 0.5;
+    out_f32[l] = (float)w;
+    if (flags) flags[l] = h;
+  }
+}
+
+int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, int policy, float* out, uint8_t* flags,
+                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream) {
+  return launch_fwd_f32<ExactPol>(packed, n_faces, ps, n_count, policy, out, flags, workspace,
+                                  ws_bytes, num_sms, stream);
+}
+size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+  return FwdPlan<ExactPol>::make(n_faces, n_count, num_sms).workspace(n_count);
+}
+int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, int policy, float* out, uint8_t* flags,
+                        void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream) {
+  return launch_fwd_f32<SoftPol>(packed, n_faces, ps, n_count, policy, out, flags, workspace,
+                                 ws_bytes, num_sms, stream);
+}
+size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+  return FwdPlan<SoftPol>::make(n_faces, n_count, num_sms).workspace(n_count);
+}
+
+}  // namespace wv

@@ -112,5 +112,48 @@ int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource&
                          int64_t n_count, int policy, float* out, uint8_t* flags,
                          void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream);
 size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, int policy, float* out, uint8_t* flags,
+                        void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream);
+size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+int launch_exact_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, int use_atan2, int policy, double* out, uint8_t* flags,
+                         cudaStream_t stream);
+int launch_soft_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, int policy, double* out, uint8_t* flags,
+                        cudaStream_t stream);
+
+// backward (wv_bwd_f32.cu, wv_f64.cu)
+int launch_exact_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, const float* coefs, double coef_scale,
+                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                         cudaStream_t stream);
+int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, const float* coefs, double coef_scale,
+                        double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                        cudaStream_t stream);
+size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+int launch_exact_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                         int64_t n_count, const double* coefs, double coef_scale,
+                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                         cudaStream_t stream);
+int launch_soft_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                        int64_t n_count, const double* coefs, double coef_scale,
+                        double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                        cudaStream_t stream);
+size_t bwd64_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+int launch_face_to_vertex(const double* face_grad, const int64_t* off, const int64_t* slots,
+                          int64_t n_verts, const double* scale, int accumulate, double* out64,
+                          float* out32, int num_sms, cudaStream_t stream);
+
+// loss (wv_loss.cu)
+size_t loss_workspace_bytes(int64_t n);
+int launch_loss_f32(const float* values, const uint8_t* flags, const float* targets,
+                    const float* weights, int64_t n, float* coefs, double* sums, void* ws,
+                    size_t ws_bytes, cudaStream_t stream);
+int launch_loss_f64(const double* values, const uint8_t* flags, const double* targets,
+                    const double* weights, int64_t n, double* coefs, double* sums, void* ws,
+                    size_t ws_bytes, cudaStream_t stream);
+int launch_loss_finalize(double* sums, cudaStream_t stream);
 
 }  // namespace wv

@@ -118,6 +118,19 @@ __global__ void pack_kernel(int kind, const V* __restrict__ verts,
         SoftRecF32* r = static_cast<SoftRecF32*>(recs) + f;
         r->c = make_float4((float)cx, (float)cy, (float)cz, (float)nx);
         r->n = make_float4((float)ny, (float)nz, 0.0f, 0.0f);
+      } else if (kind == 5) {
+        SoftGradRecF32* r = static_cast<SoftGradRecF32*>(recs) + f;
+        r->c = make_float4((float)cx, (float)cy, (float)cz, 0.0f);
+        r->n = make_float4((float)nx, (float)ny, (float)nz, 0.0f);
+        r->u = make_float4((float)ux, (float)uy, (float)uz, 0.0f);
+        r->w = make_float4((float)wx, (float)wy, (float)wz, 0.0f);
+      } else if (kind == 6) {
+        SoftGradRecF64* r = static_cast<SoftGradRecF64*>(recs) + f;
+        r->c[0] = cx; r->c[1] = cy; r->c[2] = cz;
+        r->n[0] = nx; r->n[1] = ny; r->n[2] = nz;
+        r->u[0] = ux; r->u[1] = uy; r->u[2] = uz;
+        r->w[0] = wx; r->w[1] = wy; r->w[2] = wz;
+        r->pad[0] = r->pad[1] = r->pad[2] = r->pad[3] = 0.0;
       } else {
         SoftRecF64* r = static_cast<SoftRecF64*>(recs) + f;
         r->c[0] = cx;
@@ -144,6 +157,8 @@ size_t packed_bytes(int kind, int64_t n_faces) {
     case 2: rec = sizeof(SoftRecF32); break;
     case 3: rec = sizeof(ExactRecF64); break;
     case 4: rec = sizeof(SoftRecF64); break;
+    case 5: rec = sizeof(SoftGradRecF32); break;
+    case 6: rec = sizeof(SoftGradRecF64); break;
     default: return 0;
   }
   return sizeof(PackHeader) + rec * (size_t)(n_faces > 0 ? n_faces : 0);
@@ -164,7 +179,7 @@ int launch_surface_eps(const void* vertices, int vert_f64, int64_t n_verts, doub
 int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
                 const void* faces, int faces_i64, int64_t n_faces, const double* /*eps_dev*/,
                 void* packed, cudaStream_t stream) {
-  if (kind < 1 || kind > 4) return kErrArg;
+  if (kind < 1 || kind > 6) return kErrArg;
   PackHeader* hdr = static_cast<PackHeader*>(packed);
   int rc = launch_surface_eps(vertices, vert_f64, n_verts, reinterpret_cast<double*>(hdr),
                               stream);

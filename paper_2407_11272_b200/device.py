@@ -1,10 +1,14 @@
 """Device-side staging and kernel launches (torch tensors for memory and
 streams, the C ABI for every computation).
 
-``DeviceMesh`` holds a mesh resident in HBM and lazily packs the per-kind
-face records (``wv_pack_faces``), so a morph loop or a multi-call voxelize
-re-packs only when the vertices change.  Every launch is stream-ordered on
-torch's current stream; nothing here synchronises the host.
+``DeviceMesh`` holds a mesh resident in HBM, lazily packs the per-kind face
+records (``wv_pack_faces``) and keeps the vertex CSR used by the gradient
+gather, so a morph loop or repeated voxelize re-packs only when the vertices
+change.  Every launch is stream-ordered on torch's current stream; nothing
+here synchronises the host.
+
+Precision: ``"f32"`` is the FP32 hot path (north_star), ``"f64"`` the parity
+path that mirrors the reference's default f64 kernels.
 """
 
 from __future__ import annotations
@@ -15,6 +19,11 @@ import numpy as np
 import torch
 
 from . import _lib as L
+
+_EXACT = {"f32": L.PACK_EXACT_F32, "f64": L.PACK_EXACT_F64}
+_SOFT = {"f32": L.PACK_SOFT_F32, "f64": L.PACK_SOFT_F64}
+_SOFTGRAD = {"f32": L.PACK_SOFTGRAD_F32, "f64": L.PACK_SOFTGRAD_F64}
+_DT = {"f32": torch.float32, "f64": torch.float64}
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -30,26 +39,46 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def _check_precision(precision: str) -> None:
+    if precision not in _DT:
+        raise ValueError(f"precision must be 'f64' or 'f32', got {precision!r}")
+
+
+def vertex_csr(faces: np.ndarray, n_verts: int) -> tuple[np.ndarray, np.ndarray]:
+    """(offsets (V+1,), slots (3F,)) with slot = 3*f + corner, grouped by
+    vertex in stable (face, corner) order -- the fixed summation order of
+    the face->vertex gather."""
+    flat = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1)
+    slots = np.argsort(flat, kind="stable").astype(np.int64)
+    counts = np.bincount(flat, minlength=n_verts) if flat.size else np.zeros(n_verts, np.int64)
+    off = np.zeros(n_verts + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    return off, slots
+
+
 @dataclass
 class DeviceMesh:
-    """Mesh resident on the GPU.  ``vertices`` (V,3) f32/f64, ``faces``
-    (F,3) int32/int64, both contiguous CUDA tensors."""
+    """Mesh resident on the GPU.  ``vertices`` (V,3) f32/f64 and ``faces``
+    (F,3) int32/int64, contiguous CUDA tensors."""
 
     vertices: torch.Tensor
     faces: torch.Tensor
     _packs: dict = field(default_factory=dict, repr=False)
     _version: int = field(default=-1, repr=False)
+    _csr: tuple | None = field(default=None, repr=False)
 
     @classmethod
     def from_numpy(cls, vertices: np.ndarray, faces: np.ndarray, dev=None,
                    dtype=torch.float64) -> "DeviceMesh":
         dev = dev or device()
-        v = torch.as_tensor(np.ascontiguousarray(vertices), dtype=dtype).reshape(-1, 3)
-        f = torch.as_tensor(np.ascontiguousarray(faces, dtype=np.int64)).reshape(-1, 3)
-        if dev.type == "cuda":
-            v = v.pin_memory().to(dev, non_blocking=True)
-            f = f.pin_memory().to(dev, non_blocking=True)
-        return cls(v.contiguous(), f.contiguous())
+        v = torch.from_numpy(np.ascontiguousarray(np.asarray(vertices), dtype=np.float64)
+                             ).reshape(-1, 3).to(dtype)
+        f = torch.from_numpy(np.ascontiguousarray(np.asarray(faces), dtype=np.int64)).reshape(-1, 3)
+        v = v.pin_memory().to(dev, non_blocking=True)
+        f = f.pin_memory().to(dev, non_blocking=True)
+        m = cls(v.contiguous(), f.contiguous())
+        m._faces_np = np.ascontiguousarray(np.asarray(faces), dtype=np.int64).reshape(-1, 3)
+        return m
 
     @property
     def num_vertices(self) -> int:
@@ -62,8 +91,13 @@ class DeviceMesh:
     def invalidate(self) -> None:
         self._packs.clear()
 
+    def set_vertices(self, vertices: torch.Tensor) -> None:
+        """Replace the vertex positions (same connectivity); re-packs lazily."""
+        self.vertices = vertices.contiguous()
+        self._packs.clear()
+
     def packed(self, kind: int) -> torch.Tensor:
-        ver = self.vertices._version
+        ver = (id(self.vertices), self.vertices._version)
         if ver != self._version:
             self._packs.clear()
             self._version = ver
@@ -71,14 +105,15 @@ class DeviceMesh:
         if buf is not None:
             return buf
         lib = L.lib()
-        if not (self.vertices.is_cuda and self.faces.is_cuda):
+        v, f = self.vertices, self.faces
+        if not (v.is_cuda and f.is_cuda):
             raise ValueError("DeviceMesh tensors must live on a CUDA device")
-        v = self.vertices.contiguous()
-        f = self.faces.contiguous()
         if v.dtype not in (torch.float32, torch.float64):
             raise TypeError("vertices must be float32 or float64")
         if f.dtype not in (torch.int32, torch.int64):
             raise TypeError("faces must be int32 or int64")
+        v = v.contiguous()
+        f = f.contiguous()
         nbytes = int(lib.wv_packed_bytes(kind, self.num_faces))
         buf = torch.empty(nbytes, dtype=torch.uint8, device=v.device)
         L.check(lib.wv_pack_faces(kind, _ptr(v), int(v.dtype == torch.float64),
@@ -87,42 +122,164 @@ class DeviceMesh:
         self._packs[kind] = buf
         return buf
 
+    def csr(self) -> tuple[torch.Tensor, torch.Tensor]:
+        if self._csr is None:
+            faces_np = getattr(self, "_faces_np", None)
+            if faces_np is None:
+                faces_np = self.faces.detach().cpu().numpy()  # connectivity is static
+            off, slots = vertex_csr(faces_np, self.num_vertices)
+            dev = self.vertices.device
+            self._csr = (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev))
+        return self._csr
 
-def _workspace(kind: int, n_faces: int, count: int, dev) -> tuple[torch.Tensor | None, int]:
-    nbytes = int(L.lib().wv_fwd_workspace_bytes(kind, n_faces, count))
-    if nbytes == 0:
-        return None, 0
-    return torch.empty(nbytes, dtype=torch.uint8, device=dev), nbytes
+
+def _points_arg(points, dev, dtype):
+    pts = torch.as_tensor(points).to(device=dev, dtype=dtype).contiguous().reshape(-1, 3)
+    return pts, int(pts.shape[0])
 
 
-def exact_forward_f32(mesh: DeviceMesh, *, grid=None, n0: int = 0, count: int | None = None,
-                      points: torch.Tensor | None = None, policy: int = L.POLICY_RAW,
-                      out: torch.Tensor | None = None, flags: torch.Tensor | None = None):
-    """FP32 exact winding numbers.  Either ``grid=(lo, hi, res)`` with the
-    node range [n0, n0+count), or ``points`` (n,3) float32 on the device.
-    Returns (values f32, flags u8) device tensors."""
+def _grid_count(grid, n0, count):
+    lo, hi, res = grid
+    total = int(res[0]) * int(res[1]) * int(res[2])
+    return total - int(n0) if count is None else int(count)
+
+
+def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int = 0,
+            count: int | None = None, points=None, policy: int = L.POLICY_RAW,
+            use_atan2: bool = True, out: torch.Tensor | None = None,
+            flags: torch.Tensor | None = None):
+    """Winding numbers on the device.  ``grid=(lo, hi, res)`` with the node
+    range [n0, n0+count), or ``points`` (n,3).  Returns (values, flags u8)."""
+    _check_precision(precision)
+    if mode not in ("exact", "soft"):
+        raise ValueError(f"mode must be 'exact' or 'soft', got {mode!r}")
     lib = L.lib()
     dev = mesh.vertices.device
-    packed = mesh.packed(L.PACK_EXACT_F32)
+    dt = _DT[precision]
+    kind = (_EXACT if mode == "exact" else _SOFT)[precision]
+    packed = mesh.packed(kind)
     if points is not None:
-        pts = points.to(device=dev, dtype=torch.float32).contiguous().reshape(-1, 3)
-        count = int(pts.shape[0])
+        pts, count = _points_arg(points, dev, dt)
     else:
-        lo, hi, res = grid
-        if count is None:
-            count = int(res[0]) * int(res[1]) * int(res[2]) - n0
-    out = torch.empty(count, dtype=torch.float32, device=dev) if out is None else out
+        count = _grid_count(grid, n0, count)
+    out = torch.empty(count, dtype=dt, device=dev) if out is None else out
     flags = torch.empty(count, dtype=torch.uint8, device=dev) if flags is None else flags
     if count == 0:
         return out, flags
-    ws, wsb = _workspace(L.PACK_EXACT_F32, mesh.num_faces, count, dev)
-    if points is not None:
-        rc = lib.wv_exact_fwd_points_f32(_ptr(packed), mesh.num_faces, _ptr(pts), count,
-                                         policy, _ptr(out), _ptr(flags), _ptr(ws), wsb,
-                                         _stream())
+    F = mesh.num_faces
+    st = _stream()
+    if precision == "f32":
+        if not use_atan2:
+            raise ValueError("the single-argument arctan branch exists only at precision='f64'")
+        wsb = int(lib.wv_fwd_workspace_bytes(kind, F, count))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
+        if points is not None:
+            fn = lib.wv_exact_fwd_points_f32 if mode == "exact" else lib.wv_soft_fwd_points_f32
+            rc = fn(_ptr(packed), F, _ptr(pts), count, policy, _ptr(out), _ptr(flags), _ptr(ws),
+                    wsb, st)
+        else:
+            fn = lib.wv_exact_fwd_grid_f32 if mode == "exact" else lib.wv_soft_fwd_grid_f32
+            rc = fn(_ptr(packed), F, L.make_grid(*grid), int(n0), count, policy, _ptr(out),
+                    _ptr(flags), _ptr(ws), wsb, st)
     else:
-        rc = lib.wv_exact_fwd_grid_f32(_ptr(packed), mesh.num_faces, L.make_grid(lo, hi, res),
-                                       int(n0), count, policy, _ptr(out), _ptr(flags),
-                                       _ptr(ws), wsb, _stream())
-    L.check(rc, "wv_exact_fwd")
+        if mode == "exact":
+            if points is not None:
+                rc = lib.wv_exact_fwd_points_f64(_ptr(packed), F, _ptr(pts), count,
+                                                 int(bool(use_atan2)), policy, _ptr(out),
+                                                 _ptr(flags), st)
+            else:
+                rc = lib.wv_exact_fwd_grid_f64(_ptr(packed), F, L.make_grid(*grid), int(n0),
+                                               count, int(bool(use_atan2)), policy, _ptr(out),
+                                               _ptr(flags), st)
+        else:
+            if points is not None:
+                rc = lib.wv_soft_fwd_points_f64(_ptr(packed), F, _ptr(pts), count, policy,
+                                                _ptr(out), _ptr(flags), st)
+            else:
+                rc = lib.wv_soft_fwd_grid_f64(_ptr(packed), F, L.make_grid(*grid), int(n0), count,
+                                              policy, _ptr(out), _ptr(flags), st)
+    L.check(rc, f"{mode} forward ({precision})")
     return out, flags
+
+
+def exact_forward_f32(mesh: DeviceMesh, **kw):
+    return forward(mesh, "exact", "f32", **kw)
+
+
+def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, *, grid=None,
+              n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-face corner gradients (F,3,3) f64 = sum_p coef_scale*coefs[p]*dW_p/dv."""
+    _check_precision(precision)
+    lib = L.lib()
+    dev = mesh.vertices.device
+    dt = _DT[precision]
+    kind = (_EXACT if mode == "exact" else _SOFTGRAD)[precision]
+    packed = mesh.packed(kind)
+    F = mesh.num_faces
+    if points is not None:
+        pts, count = _points_arg(points, dev, dt)
+    else:
+        count = _grid_count(grid, n0, count)
+    cf = coefs.to(device=dev, dtype=dt).contiguous().reshape(-1)
+    if cf.numel() != count:
+        raise ValueError(f"coefs has {cf.numel()} entries for {count} query points")
+    out = torch.empty((F, 3, 3), dtype=torch.float64, device=dev) if out is None else out
+    if F == 0:
+        return out
+    wsb = int(lib.wv_bwd_workspace_bytes(kind, F, count))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
+    st = _stream()
+    suffix = "f32" if precision == "f32" else "f64"
+    name = f"wv_{mode}_bwd_{'points' if points is not None else 'grid'}_{suffix}"
+    fn = getattr(lib, name)
+    if points is not None:
+        rc = fn(_ptr(packed), F, _ptr(pts), count, _ptr(cf), float(coef_scale), _ptr(out),
+                _ptr(ws), wsb, st)
+    else:
+        rc = fn(_ptr(packed), F, L.make_grid(*grid), int(n0), count, _ptr(cf), float(coef_scale),
+                _ptr(out), _ptr(ws), wsb, st)
+    L.check(rc, name)
+    return out
+
+
+def vertex_grad(mesh: DeviceMesh, fgrad: torch.Tensor, *, scale: torch.Tensor | None = None,
+                dtype=torch.float64, out: torch.Tensor | None = None,
+                accumulate: bool = False) -> torch.Tensor:
+    """(V,3) vertex gradients from (F,3,3) corner sums (CSR gather)."""
+    lib = L.lib()
+    dev = mesh.vertices.device
+    off, slots = mesh.csr()
+    V = mesh.num_vertices
+    if out is None:
+        out = torch.zeros((V, 3), dtype=dtype, device=dev)
+    o64 = out if out.dtype == torch.float64 else None
+    o32 = out if out.dtype == torch.float32 else None
+    L.check(lib.wv_face_to_vertex(_ptr(fgrad), _ptr(off), _ptr(slots), V, _ptr(scale),
+                                  int(accumulate), _ptr(o64), _ptr(o32), _stream()),
+            "wv_face_to_vertex")
+    return out
+
+
+def loss_terms(values: torch.Tensor, flags: torch.Tensor, targets: torch.Tensor,
+               weights: torch.Tensor | None = None):
+    """(coefs = 2 w r, sums[8]) on the device (see include/windvox_b200.h)."""
+    lib = L.lib()
+    dev = values.device
+    n = int(values.numel())
+    dt = values.dtype
+    tg = targets.to(device=dev, dtype=dt).contiguous()
+    wt = None if weights is None else weights.to(device=dev, dtype=dt).contiguous()
+    coefs = torch.empty_like(values)
+    sums = torch.zeros(8, dtype=torch.float64, device=dev)
+    wsb = int(lib.wv_loss_workspace_bytes(n))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    fn = lib.wv_loss_terms_f32 if dt == torch.float32 else lib.wv_loss_terms_f64
+    L.check(fn(_ptr(values), _ptr(flags), _ptr(tg), _ptr(wt), n, _ptr(coefs), _ptr(sums),
+               _ptr(ws), wsb, _stream()), "wv_loss_terms")
+    return coefs, sums
+
+
+def loss_finalize(sums: torch.Tensor) -> torch.Tensor:
+    L.check(L.lib().wv_loss_finalize(_ptr(sums), _stream()), "wv_loss_finalize")
+    return sums

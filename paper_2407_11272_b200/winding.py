@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .device import DeviceMesh, exact_forward_f32
+from .device import DeviceMesh, forward
 from .errors import OnSurfaceError
 from .types import (SURFACE_EPS_FACTOR, GridSpec, QueryBatchConfig, ScalarField, TriangleMesh,
                     surface_epsilon)
@@ -41,9 +41,11 @@ def _check_precision(precision: str) -> None:
 
 def _dispatch(dmesh: DeviceMesh, mode: str, precision: str, use_atan2: bool, *, grid=None,
               points=None, policy=L.POLICY_RAW):
-    if mode == "exact" and precision == "f32" and use_atan2:
-        return exact_forward_f32(dmesh, grid=grid, points=points, policy=policy)
-    raise NotImplementedError(f"mode={mode} precision={precision} use_atan2={use_atan2}")
+    if not use_atan2 and precision == "f32":
+        # the regression-demonstration branch is an f64 reference path only
+        precision = "f64"
+    return forward(dmesh, mode, precision, grid=grid, points=points, policy=policy,
+                   use_atan2=use_atan2)
 
 
 def winding_number_batch(mesh: TriangleMesh, points, mode: str = "exact",
