@@ -44,6 +44,8 @@ extern "C" {
 #define WV_PACK_SOFT_F64 4
 #define WV_PACK_SOFTGRAD_F32 5
 #define WV_PACK_SOFTGRAD_F64 6
+#define WV_PACK_EXACTGRAD_F32 7 /* wv_pack_exact_grad: active faces of the exact backward */
+#define WV_PACK_EXACTGRAD_F64 8
 
 /* stored value for on-surface (flagged) nodes */
 #define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
@@ -73,6 +75,16 @@ size_t wv_packed_bytes(int kind, int64_t n_faces);
 int wv_pack_faces(int kind, const void *vertices, int vert_f64, int64_t n_verts,
                   const void *faces, int faces_i64, int64_t n_faces, void *packed,
                   void *stream);
+/* Staging for the exact backward (kinds 7/8): only the `active` faces
+ * (A,) int64 -- those with a non-cancelling directed edge -- with the net
+ * weights (A,3) f32 of their edges v0->v1, v1->v2, v2->v0.  Interior edges of
+ * a consistently oriented mesh cancel exactly in d(Omega)/dv, so a closed
+ * manifold packs no face (its exact gradient vanishes, test_grad.py:231-246).
+ * Degenerate faces (dropped by the reference forward) must be excluded from
+ * the edge count by the caller.  `packed` holds wv_packed_bytes(kind, A). */
+int wv_pack_exact_grad(int kind, const void *vertices, int vert_f64, int64_t n_verts,
+                       const void *faces, int faces_i64, const int64_t *active,
+                       const float *weights, int64_t n_active, void *packed, void *stream);
 
 /* ---- forward: winding numbers at lattice nodes or explicit points -------
  * exact f32: replaces _kernels.exact_batch_f32 (_kernels.py:235-309); FP32
@@ -118,8 +130,11 @@ int wv_soft_fwd_points_f64(const void *packed, int64_t n_faces, const double *po
  * and pairs the forward skipped (on-surface) contribute nothing.
  * soft: replaces _kernels.soft_grad_accum (_kernels.py:161-232); packed kind
  *   WV_PACK_SOFTGRAD_F32 / _F64.
- * exact: NEW (no reference kernel, grad.py:9-12): closed-form d(Omega)/dv of
- *   the VOS solid angle; packed kind WV_PACK_EXACT_F32 / _F64.
+ * exact: NEW (no reference kernel, grad.py:9-12): d(Omega)/dv of the VOS
+ *   solid angle in its per-edge (Biot-Savart) form; packed kind
+ *   WV_PACK_EXACTGRAD_F32 / _F64 and n_faces = number of ACTIVE faces.
+ *   Callers pass coefs == 0 at on-surface (flagged) points, where W is
+ *   discontinuous and has no derivative.
  * Corner sums become vertex gradients with wv_face_to_vertex. */
 size_t wv_bwd_workspace_bytes(int kind, int64_t n_faces, int64_t count);
 int wv_exact_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,

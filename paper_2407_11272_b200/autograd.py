@@ -55,8 +55,9 @@ class _WindingNumberFn(torch.autograd.Function):
         points, flags = ctx.saved_tensors
         layer = ctx.layer
         coefs = grad_W.contiguous()
-        if layer.policy == L.POLICY_HALF:
-            # voxelize policy: flagged nodes hold the constant 0.5 -> no gradient
+        if layer.policy == L.POLICY_HALF or layer.mode == "exact":
+            # voxelize policy: flagged nodes hold the constant 0.5; exact mode:
+            # W jumps across the surface, so on-surface nodes have no derivative
             coefs = torch.where(flags.bool(), torch.zeros_like(coefs), coefs)
         if ctx.has_points:
             fg = face_grad(ctx.mesh, layer.mode, ctx.prec, coefs, points=points)
@@ -99,7 +100,13 @@ class WindingNumber(torch.nn.Module):
             faces = self.faces.to(vertices.device).contiguous()
             self._mesh = DeviceMesh(vertices.contiguous(), faces)
             self._mesh.csr()
-        return DeviceMesh(vertices.contiguous(), self._mesh.faces, _csr=self._mesh._csr)
+            if self.mode == "exact":
+                self._mesh.exact_grad_setup()
+        m = DeviceMesh(vertices.contiguous(), self._mesh.faces, _csr=self._mesh._csr)
+        m._faces_np = self._mesh._faces_np
+        if self.mode == "exact":
+            m._exact_grad = self._mesh._exact_grad
+        return m
 
     def forward(self, vertices: torch.Tensor, points: torch.Tensor | None = None):
         if points is None and self.grid is None:

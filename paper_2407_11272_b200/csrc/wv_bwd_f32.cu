@@ -11,8 +11,9 @@
 // (wv_face_to_vertex) sums face corners into vertices -- bit-reproducible
 // run to run, as the reference's chunk-ordered merge is (grad.py:113-127).
 //
-// Exact  (NEW, no reference kernel; closed form SURVEY.md A.4):
-//   dW/dv_k = 1/(2 pi) (beta dalpha/dv_k - alpha dbeta/dv_k) / (alpha^2+beta^2)
+// Exact  (NEW, no reference kernel): d(Omega)/dv in its edge (Biot-Savart)
+//   form, equal to the face-wise closed form of SURVEY.md A.4; only faces
+//   with a non-cancelling edge are launched (see ExactEdgeBwd).
 // Soft   (replaces _kernels.soft_grad_accum, _kernels.py:161-232):
 //   dW/dv_k = [(G_k + N/3) / r^3 - S d / r^5] / (8 pi),  G_1 = w x d,
 //   G_2 = d x u, G_0 = -G_1 - G_2; the N/3 and d terms are shared by the three
@@ -25,84 +26,59 @@ namespace wv {
 constexpr int kBwdThreads = 128;   // faces per CTA
 constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
 
-// Rare exact pair: plane distance below eps.  Returns 1 to keep the pair, 0
-// when the forward skipped it (on-surface, _kernels.py:65-88, or a dead face).
-__device__ __noinline__ float exact_keep(float4 A, float4 B, float4 C, float qx, float qy,
-                                         float qz, float eps) {
-  if (A.w == __int_as_float(0x7f800000)) return 0.0f;
-  const float ax = A.x - qx, ay = A.y - qy, az = A.z - qz;
-  const float bx = B.x - qx, by = B.y - qy, bz = B.z - qz;
-  const float cx = C.x - qx, cy = C.y - qy, cz = C.z - qz;
-  const float la = sqrt_approx(fmaf(az, az, fmaf(ay, ay, ax * ax)));
-  const float lb = sqrt_approx(fmaf(bz, bz, fmaf(by, by, bx * bx)));
-  const float lc = sqrt_approx(fmaf(cz, cz, fmaf(cy, cy, cx * cx)));
-  if (la < eps || lb < eps || lc < eps) return 0.0f;
-  const float ux = B.x - A.x, uy = B.y - A.y, uz = B.z - A.z;
-  const float wx = C.x - A.x, wy = C.y - A.y, wz = C.z - A.z;
-  const float d00 = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
-  const float d01 = fmaf(uz, wz, fmaf(uy, wy, ux * wx));
-  const float d11 = fmaf(wz, wz, fmaf(wy, wy, wx * wx));
-  const float denom = __fsub_rn(__fmul_rn(d00, d11), __fmul_rn(d01, d01));
-  const float ru = -fmaf(az, uz, fmaf(ay, uy, ax * ux));
-  const float rw = -fmaf(az, wz, fmaf(ay, wy, ax * wx));
-  const float b1 = __fdiv_rn(__fsub_rn(__fmul_rn(d11, ru), __fmul_rn(d01, rw)), denom);
-  const float b2 = __fdiv_rn(__fsub_rn(__fmul_rn(d00, rw), __fmul_rn(d01, ru)), denom);
-  const float btol = 1e-12f;
-  return (b1 >= -btol && b2 >= -btol && b1 + b2 <= 1.0f + btol) ? 0.0f : 1.0f;
-}
-
-struct ExactBwd {
-  using Rec = ExactRecF32;
+// Exact backward, edge form.  For a triangle seen from q, the variation of
+// its solid angle is a boundary integral (the integrand (x-q)/|x-q|^3 is
+// divergence-free), so d(Omega)/dv is a sum of per-edge Biot-Savart terms.
+// For the directed edge P->Q with a = P-q, b = Q-q, m = a x b:
+//   dW/dP = -m / (4 pi |a| (|a||b| + a.b)),  dW/dQ = -m / (4 pi |b| (|a||b| + a.b))
+// (identical to the face-wise closed form of SURVEY.md A.4, oracle
+// wvo_exact_grad_accum; stable: no differences of large terms).  Terms of an
+// interior edge cancel exactly between its two faces, so each face carries
+// the NET weight of its edges (0 for cancelled ones) and faces whose three
+// weights vanish are not packed at all.  The sign and 1/(4 pi) are folded
+// into coef_scale by the launcher.
+struct ExactEdgeBwd {
+  using Rec = ExactGradRecF32;
   static constexpr int kMinBlocks = 4;
-  static constexpr double kCoefScale = 1.0 / (2.0 * kPi);
+  static constexpr double kCoefScale = -1.0 / (4.0 * kPi);
   static constexpr int kAcc = 9;
   __device__ __forceinline__ static void pair(const Rec& R, float qx, float qy, float qz,
-                                              float coef, float eps, float eps2, float* g) {
-    const float ax = R.v0e.x - qx, ay = R.v0e.y - qy, az = R.v0e.z - qz;
-    const float bx = R.v1.x - qx, by = R.v1.y - qy, bz = R.v1.z - qz;
-    const float cx = R.v2.x - qx, cy = R.v2.y - qy, cz = R.v2.z - qz;
-    const float la2 = fmaf(az, az, fmaf(ay, ay, ax * ax));
-    const float lb2 = fmaf(bz, bz, fmaf(by, by, bx * bx));
-    const float lc2 = fmaf(cz, cz, fmaf(cy, cy, cx * cx));
-    const float ia = rsqrt_approx(la2), ib = rsqrt_approx(lb2), ic = rsqrt_approx(lc2);
-    const float la = la2 * ia, lb = lb2 * ib, lc = lc2 * ic;
-    const float alpha = fmaf(R.n.z, az, fmaf(R.n.y, ay, R.n.x * ax));
+                                              float coef, float, float, float* g) {
+    const float ax = R.a.x - qx, ay = R.a.y - qy, az = R.a.z - qz;
+    const float bx = R.b.x - qx, by = R.b.y - qy, bz = R.b.z - qz;
+    const float cx = R.c.x - qx, cy = R.c.y - qy, cz = R.c.z - qz;
+    const float a2 = fmaf(az, az, fmaf(ay, ay, ax * ax));
+    const float b2 = fmaf(bz, bz, fmaf(by, by, bx * bx));
+    const float c2 = fmaf(cz, cz, fmaf(cy, cy, cx * cx));
+    const float ia = rsqrt_approx(a2), ib = rsqrt_approx(b2), ic = rsqrt_approx(c2);
+    const float la = a2 * ia, lb = b2 * ib, lc = c2 * ic;
     const float ab = fmaf(az, bz, fmaf(ay, by, ax * bx));
     const float bc = fmaf(bz, cz, fmaf(by, cy, bx * cx));
     const float ca = fmaf(az, cz, fmaf(ay, cy, ax * cx));
-    const float lblc = lb * lc;
-    const float beta = fmaf(ca, lb, fmaf(ab, lc, fmaf(bc, la, la * lblc)));
-    float s = coef * rcp_approx(fmaf(alpha, alpha, beta * beta));
-    if (fabsf(alpha) < R.v0e.w && exact_keep(R.v0e, R.v1, R.v2, qx, qy, qz, eps) == 0.0f)
-      s = 0.0f;  // pair skipped by the forward's on-surface policy
-    const float ga = s * beta;   // d theta / d alpha
-    const float gb = -s * alpha; // d theta / d beta
-    const float ka = (lblc + bc) * ia;
-    const float kb = fmaf(la, lc, ca) * ib;
-    const float kc = fmaf(la, lb, ab) * ic;
-    // d alpha / d v0 = b x c, / d v1 = c x a, / d v2 = a x b
-    const float x0 = by * cz - bz * cy, y0 = bz * cx - bx * cz, z0 = bx * cy - by * cx;
-    const float x1 = cy * az - cz * ay, y1 = cz * ax - cx * az, z1 = cx * ay - cy * ax;
-    const float x2 = ay * bz - az * by, y2 = az * bx - ax * bz, z2 = ax * by - ay * bx;
-    // d beta / d a = ka a + lc b + lb c ; / d b = lc a + kb b + la c ;
-    // d beta / d c = lb a + la b + kc c
-    const float A0 = gb * ka, Bc = gb * lc, Cb = gb * lb, A1 = gb * kb, Da = gb * la,
-                A2 = gb * kc;
-    g[0] = fmaf(ga, x0, fmaf(Cb, cx, fmaf(Bc, bx, fmaf(A0, ax, g[0]))));
-    g[1] = fmaf(ga, y0, fmaf(Cb, cy, fmaf(Bc, by, fmaf(A0, ay, g[1]))));
-    g[2] = fmaf(ga, z0, fmaf(Cb, cz, fmaf(Bc, bz, fmaf(A0, az, g[2]))));
-    g[3] = fmaf(ga, x1, fmaf(Da, cx, fmaf(A1, bx, fmaf(Bc, ax, g[3]))));
-    g[4] = fmaf(ga, y1, fmaf(Da, cy, fmaf(A1, by, fmaf(Bc, ay, g[4]))));
-    g[5] = fmaf(ga, z1, fmaf(Da, cz, fmaf(A1, bz, fmaf(Bc, az, g[5]))));
-    g[6] = fmaf(ga, x2, fmaf(A2, cx, fmaf(Da, bx, fmaf(Cb, ax, g[6]))));
-    g[7] = fmaf(ga, y2, fmaf(A2, cy, fmaf(Da, by, fmaf(Cb, ay, g[7]))));
-    g[8] = fmaf(ga, z2, fmaf(A2, cz, fmaf(Da, bz, fmaf(Cb, az, g[8]))));
+    const float t01 = (coef * R.a.w) * rcp_approx(fmaf(la, lb, ab));
+    const float t12 = (coef * R.b.w) * rcp_approx(fmaf(lb, lc, bc));
+    const float t20 = (coef * R.c.w) * rcp_approx(fmaf(lc, la, ca));
+    // m01 = a x b, m12 = b x c, m20 = c x a
+    const float m01x = ay * bz - az * by, m01y = az * bx - ax * bz, m01z = ax * by - ay * bx;
+    const float m12x = by * cz - bz * cy, m12y = bz * cx - bx * cz, m12z = bx * cy - by * cx;
+    const float m20x = cy * az - cz * ay, m20y = cz * ax - cx * az, m20z = cx * ay - cy * ax;
+    const float s01a = t01 * ia, s20a = t20 * ia;  // v0 is P of 01, Q of 20
+    const float s01b = t01 * ib, s12b = t12 * ib;  // v1 is Q of 01, P of 12
+    const float s12c = t12 * ic, s20c = t20 * ic;  // v2 is Q of 12, P of 20
+    g[0] = fmaf(m20x, s20a, fmaf(m01x, s01a, g[0]));
+    g[1] = fmaf(m20y, s20a, fmaf(m01y, s01a, g[1]));
+    g[2] = fmaf(m20z, s20a, fmaf(m01z, s01a, g[2]));
+    g[3] = fmaf(m12x, s12b, fmaf(m01x, s01b, g[3]));
+    g[4] = fmaf(m12y, s12b, fmaf(m01y, s01b, g[4]));
+    g[5] = fmaf(m12z, s12b, fmaf(m01z, s01b, g[5]));
+    g[6] = fmaf(m20x, s20c, fmaf(m12x, s12c, g[6]));
+    g[7] = fmaf(m20y, s20c, fmaf(m12y, s12c, g[7]));
+    g[8] = fmaf(m20z, s20c, fmaf(m12z, s12c, g[8]));
   }
   __device__ __forceinline__ static void finish(const Rec&, const double* acc, double* out9) {
     for (int j = 0; j < 9; ++j) out9[j] = acc[j];
   }
 };
-
 struct SoftBwd {
   using Rec = SoftGradRecF32;
   static constexpr int kMinBlocks = 4;
@@ -274,7 +250,7 @@ int launch_exact_bwd_f32(const void* packed, int64_t n_faces, const PointSource&
                          int64_t n_count, const float* coefs, double coef_scale,
                          double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                          cudaStream_t stream) {
-  return launch_bwd<ExactBwd>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad, ws,
+  return launch_bwd<ExactEdgeBwd>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad, ws,
                               ws_bytes, num_sms, stream);
 }
 int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,

@@ -92,6 +92,17 @@ int wv_pack_faces(int kind, const void* vertices, int vert_f64, int64_t n_verts,
                          packed, as_stream(stream));
 }
 
+int wv_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                       const void* faces, int faces_i64, const int64_t* active,
+                       const float* weights, int64_t n_active, void* packed, void* stream) {
+  if (packed == nullptr || n_verts < 0 || n_active < 0) return WV_ERR_ARG;
+  if (n_active > 0 && (vertices == nullptr || faces == nullptr || active == nullptr ||
+                       weights == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_pack_exact_grad(kind, vertices, vert_f64, n_verts, faces, faces_i64, active,
+                                    weights, n_active, packed, as_stream(stream));
+}
+
 // ---- forward ---------------------------------------------------------------
 size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {
@@ -173,9 +184,9 @@ int wv_soft_fwd_points_f64(const void* packed, int64_t n_faces, const double* po
 // ---- backward --------------------------------------------------------------
 size_t wv_bwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {
-    case WV_PACK_EXACT_F32:
+    case WV_PACK_EXACTGRAD_F32:
     case WV_PACK_SOFTGRAD_F32: return wv::bwd_workspace_bytes(n_faces, count, sm_count());
-    case WV_PACK_EXACT_F64:
+    case WV_PACK_EXACTGRAD_F64:
     case WV_PACK_SOFTGRAD_F64: return wv::bwd64_workspace_bytes(n_faces, count, sm_count());
     default: return 0;
   }

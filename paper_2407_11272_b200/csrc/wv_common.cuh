@@ -49,6 +49,25 @@ struct __align__(16) SoftGradRecF32 {
 };
 static_assert(sizeof(SoftGradRecF32) == 64, "record size");
 
+// ExactGradRecF32 (48 B): one ACTIVE face of the exact backward -- corners
+//   plus the net weights of its three directed edges (v0->v1, v1->v2,
+//   v2->v0).  The exact d(Omega)/dv of a triangle is a sum of per-edge
+//   Biot-Savart terms that cancel exactly between the two faces sharing an
+//   interior edge, so only faces with a non-cancelling edge are packed.
+struct __align__(16) ExactGradRecF32 {
+  float4 a;  // v0.xyz, w01
+  float4 b;  // v1.xyz, w12
+  float4 c;  // v2.xyz, w20
+};
+static_assert(sizeof(ExactGradRecF32) == 48, "record size");
+
+struct __align__(16) ExactGradRecF64 {
+  double v[9];
+  double w[3];
+  double pad[4];
+};
+static_assert(sizeof(ExactGradRecF64) == 128, "record size");
+
 // SoftGradRecF64 (128 B): f64 twin for the parity backward.
 struct __align__(16) SoftGradRecF64 {
   double c[3];

@@ -186,57 +186,35 @@ constexpr int kBwd64Chunk = 256;
 constexpr double kEightPi = 8.0 * kPi;
 
 struct ExactBwd64 {
-  using Rec = ExactRecF64;
-  // closed-form d(theta)/dv of the exact forward (oracle wvo_exact_grad_accum)
-  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
-                                              double coef, double eps, double* g) {
-    if (R.dead != 0.0) return;
-    const double* t = R.v;
-    const double a[3] = {t[0] - qx, t[1] - qy, t[2] - qz};
-    const double b[3] = {t[3] - qx, t[4] - qy, t[5] - qz};
-    const double c[3] = {t[6] - qx, t[7] - qy, t[8] - qz};
-    const double na = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-    const double nb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
-    const double nc = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
-    if (na < eps || nb < eps || nc < eps) return;
-    const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
-    if (-eps < pd && pd < eps) {
-      const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
-      const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
-      const double d00 = ux * ux + uy * uy + uz * uz;
-      const double d01 = ux * wx + uy * wy + uz * wz;
-      const double d11 = wx * wx + wy * wy + wz * wz;
-      const double denom = d00 * d11 - d01 * d01;
-      const double ru = -(a[0] * ux + a[1] * uy + a[2] * uz);
-      const double rw = -(a[0] * wx + a[1] * wy + a[2] * wz);
-      const double b1 = (d11 * ru - d01 * rw) / denom;
-      const double b2 = (d00 * rw - d01 * ru) / denom;
-      if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) return;
-    }
-    const double bxc[3] = {b[1] * c[2] - b[2] * c[1], b[2] * c[0] - b[0] * c[2],
-                           b[0] * c[1] - b[1] * c[0]};
-    const double cxa[3] = {c[1] * a[2] - c[2] * a[1], c[2] * a[0] - c[0] * a[2],
-                           c[0] * a[1] - c[1] * a[0]};
-    const double axb[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
-                           a[0] * b[1] - a[1] * b[0]};
-    const double alpha = a[0] * bxc[0] + a[1] * bxc[1] + a[2] * bxc[2];
-    const double ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
-    const double bc = b[0] * c[0] + b[1] * c[1] + b[2] * c[2];
-    const double ca = c[0] * a[0] + c[1] * a[1] + c[2] * a[2];
-    const double beta = na * nb * nc + bc * na + ab * nc + ca * nb;
-    const double den = alpha * alpha + beta * beta;
-    if (den == 0.0) return;
-    const double s = coef / (2.0 * kPi * den);
-    const double ga = s * beta, gb = -s * alpha;
-    const double ka = (nb * nc + bc) / na, kb = (na * nc + ca) / nb, kc = (na * nb + ab) / nc;
+  using Rec = ExactGradRecF64;
+  // edge (Biot-Savart) form of d(Omega)/dv, see ExactEdgeBwd in wv_bwd_f32.cu;
+  // coef carries the -1/(4 pi) factor
+  __device__ __forceinline__ static void edge(const double* P, const double* Q, double qx,
+                                              double qy, double qz, double cw, double* gP,
+                                              double* gQ) {
+    if (cw == 0.0) return;
+    const double a[3] = {P[0] - qx, P[1] - qy, P[2] - qz};
+    const double b[3] = {Q[0] - qx, Q[1] - qy, Q[2] - qz};
+    const double la = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    const double lb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    const double den = la * lb + (a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
+    if (!(den > 0.0)) return;  // q on the segment: an on-surface point
+    const double t = cw / den;
+    const double m[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
+                         a[0] * b[1] - a[1] * b[0]};
+    const double sp = t / la, sq = t / lb;
     for (int d = 0; d < 3; ++d) {
-      g[d] += ga * bxc[d] + gb * (ka * a[d] + nc * b[d] + nb * c[d]);
-      g[3 + d] += ga * cxa[d] + gb * (kb * b[d] + nc * a[d] + na * c[d]);
-      g[6 + d] += ga * axb[d] + gb * (kc * c[d] + nb * a[d] + na * b[d]);
+      gP[d] += m[d] * sp;
+      gQ[d] += m[d] * sq;
     }
   }
+  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
+                                              double coef, double, double* g) {
+    edge(R.v + 0, R.v + 3, qx, qy, qz, coef * R.w[0], g + 0, g + 3);
+    edge(R.v + 3, R.v + 6, qx, qy, qz, coef * R.w[1], g + 3, g + 6);
+    edge(R.v + 6, R.v + 0, qx, qy, qz, coef * R.w[2], g + 6, g + 0);
+  }
 };
-
 struct SoftBwd64 {
   using Rec = SoftGradRecF64;
   // _kernels.py:198-232, same expression order per pair
@@ -380,7 +358,8 @@ int launch_exact_bwd_f64(const void* packed, int64_t n_faces, const PointSource&
                          int64_t n_count, const double* coefs, double coef_scale,
                          double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                          cudaStream_t stream) {
-  return launch_bwd64<ExactBwd64>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad,
+  return launch_bwd64<ExactBwd64>(packed, n_faces, ps, n_count, coefs,
+                                  coef_scale * (-1.0 / (4.0 * kPi)), face_grad,
                                   ws, ws_bytes, num_sms, stream);
 }
 int launch_soft_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,

@@ -106,6 +106,10 @@ int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
 int launch_surface_eps(const void* vertices, int vert_f64, int64_t n_verts, double* eps_dev,
                        cudaStream_t stream);
 size_t packed_bytes(int kind, int64_t n_faces);
+int launch_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                           const void* faces, int faces_i64, const int64_t* active,
+                           const float* weights, int64_t n_active, void* packed,
+                           cudaStream_t stream);
 
 // forward (wv_exact_fwd.cu, wv_soft_fwd.cu, wv_f64.cu)
 int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,

@@ -150,6 +150,67 @@ __global__ void pack_kernel(int kind, const V* __restrict__ verts,
   }
 }
 
+// Active faces of the exact backward (kind 7 f32, 8 f64): corners + the net
+// weights of the three directed edges, computed on the host from the
+// connectivity (paper_2407_11272_b200/device.py:exact_edge_weights).
+template <typename V, typename I>
+__global__ void pack_exact_grad_kernel(int kind, const V* __restrict__ verts,
+                                       const I* __restrict__ faces,
+                                       const int64_t* __restrict__ active,
+                                       const float* __restrict__ weights, int64_t n_active,
+                                       void* __restrict__ recs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = active[i];
+    double v0[3], v1[3], v2[3];
+    load_vertex(verts, (int64_t)faces[3 * f + 0], v0);
+    load_vertex(verts, (int64_t)faces[3 * f + 1], v1);
+    load_vertex(verts, (int64_t)faces[3 * f + 2], v2);
+    if (kind == 7) {
+      ExactGradRecF32* r = static_cast<ExactGradRecF32*>(recs) + i;
+      r->a = make_float4((float)v0[0], (float)v0[1], (float)v0[2], weights[3 * i + 0]);
+      r->b = make_float4((float)v1[0], (float)v1[1], (float)v1[2], weights[3 * i + 1]);
+      r->c = make_float4((float)v2[0], (float)v2[1], (float)v2[2], weights[3 * i + 2]);
+    } else {
+      ExactGradRecF64* r = static_cast<ExactGradRecF64*>(recs) + i;
+      for (int d = 0; d < 3; ++d) {
+        r->v[d] = v0[d];
+        r->v[3 + d] = v1[d];
+        r->v[6 + d] = v2[d];
+        r->w[d] = (double)weights[3 * i + d];
+      }
+      r->pad[0] = r->pad[1] = r->pad[2] = r->pad[3] = 0.0;
+    }
+  }
+}
+
+int launch_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                           const void* faces, int faces_i64, const int64_t* active,
+                           const float* weights, int64_t n_active, void* packed,
+                           cudaStream_t stream) {
+  if (kind != 7 && kind != 8) return kErrArg;
+  PackHeader* hdr = static_cast<PackHeader*>(packed);
+  int rc = launch_surface_eps(vertices, vert_f64, n_verts, reinterpret_cast<double*>(hdr), stream);
+  if (rc != kOk) return rc;
+  if (n_active <= 0) return kOk;
+  void* recs = hdr + 1;
+  int64_t blocks = (n_active + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+#define WV_PACK_EG(VT, IT)                                                                    \
+  pack_exact_grad_kernel<VT, IT><<<(unsigned)blocks, 256, 0, stream>>>(                       \
+      kind, static_cast<const VT*>(vertices), static_cast<const IT*>(faces), active, weights, \
+      n_active, recs)
+  if (vert_f64) {
+    if (faces_i64) WV_PACK_EG(double, int64_t);
+    else WV_PACK_EG(double, int32_t);
+  } else {
+    if (faces_i64) WV_PACK_EG(float, int64_t);
+    else WV_PACK_EG(float, int32_t);
+  }
+#undef WV_PACK_EG
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
 size_t packed_bytes(int kind, int64_t n_faces) {
   size_t rec = 0;
   switch (kind) {
@@ -159,6 +220,8 @@ size_t packed_bytes(int kind, int64_t n_faces) {
     case 4: rec = sizeof(SoftRecF64); break;
     case 5: rec = sizeof(SoftGradRecF32); break;
     case 6: rec = sizeof(SoftGradRecF64); break;
+    case 7: rec = sizeof(ExactGradRecF32); break;
+    case 8: rec = sizeof(ExactGradRecF64); break;
     default: return 0;
   }
   return sizeof(PackHeader) + rec * (size_t)(n_faces > 0 ? n_faces : 0);

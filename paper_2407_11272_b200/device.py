@@ -23,6 +23,7 @@ from . import _lib as L
 _EXACT = {"f32": L.PACK_EXACT_F32, "f64": L.PACK_EXACT_F64}
 _SOFT = {"f32": L.PACK_SOFT_F32, "f64": L.PACK_SOFT_F64}
 _SOFTGRAD = {"f32": L.PACK_SOFTGRAD_F32, "f64": L.PACK_SOFTGRAD_F64}
+_EXACTGRAD = {"f32": L.PACK_EXACTGRAD_F32, "f64": L.PACK_EXACTGRAD_F64}
 _DT = {"f32": torch.float32, "f64": torch.float64}
 
 
@@ -56,6 +57,54 @@ def vertex_csr(faces: np.ndarray, n_verts: int) -> tuple[np.ndarray, np.ndarray]
     return off, slots
 
 
+def exact_edge_weights(faces: np.ndarray, dead: np.ndarray | None = None):
+    """Active faces and net directed-edge weights for the exact backward.
+
+    d(Omega_f)/dv is a sum of per-edge terms T(P->Q) with T(Q->P) = -T(P->Q),
+    so over the whole mesh only the NET multiplicity of each undirected edge
+    matters: k = #(min->max) - #(max->min).  The first occurrence (face order)
+    of each edge carries weight k*dir (dir = +1 if it runs min->max), every
+    other occurrence 0; faces whose three weights vanish are inactive.
+    Degenerate faces (dropped by the reference forward, winding.py:264) are
+    excluded.  Returns (active (A,) int64, weights (A,3) float32)."""
+    f = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
+    nf = len(f)
+    if nf == 0:
+        return np.zeros(0, np.int64), np.zeros((0, 3), np.float32)
+    live = np.ones(nf, bool) if dead is None else ~np.asarray(dead, bool)
+    u = f.reshape(-1)                        # corner k of face i -> edge (k, k+1)
+    v = f[:, [1, 2, 0]].reshape(-1)
+    lo = np.minimum(u, v)
+    hi = np.maximum(u, v)
+    sgn = np.where(u < v, 1, -1)
+    sgn[u == v] = 0                          # self-loop edges carry nothing
+    sgn = sgn * np.repeat(live, 3)
+    key = lo * (int(f.max()) + 1) + hi
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    start = np.ones(len(ks), bool)
+    start[1:] = ks[1:] != ks[:-1]
+    grp = np.cumsum(start) - 1
+    net = np.zeros(int(grp[-1]) + 1, np.int64)
+    np.add.at(net, grp, sgn[order])
+    first = order[start]                     # first occurrence of each edge
+    w = np.zeros(len(u), np.float32)
+    w[first] = (net * sgn[first]).astype(np.float32)   # sgn[first] in {+1,-1,0}
+    w = w.reshape(nf, 3)
+    active = np.flatnonzero(np.any(w != 0, axis=1)).astype(np.int64)
+    return active, np.ascontiguousarray(w[active])
+
+
+def dead_faces(vertices: np.ndarray, faces: np.ndarray) -> np.ndarray:
+    """|N| == 0 in f64, the reference's degenerate-face test (winding.py:262-264)."""
+    v = np.asarray(vertices, dtype=np.float64).reshape(-1, 3)
+    f = np.asarray(faces, dtype=np.int64).reshape(-1, 3)
+    if len(f) == 0:
+        return np.zeros(0, bool)
+    t = v[f]
+    return ~(np.linalg.norm(np.cross(t[:, 1] - t[:, 0], t[:, 2] - t[:, 0]), axis=1) > 0.0)
+
+
 @dataclass
 class DeviceMesh:
     """Mesh resident on the GPU.  ``vertices`` (V,3) f32/f64 and ``faces``
@@ -78,6 +127,7 @@ class DeviceMesh:
         f = f.pin_memory().to(dev, non_blocking=True)
         m = cls(v.contiguous(), f.contiguous())
         m._faces_np = np.ascontiguousarray(np.asarray(faces), dtype=np.int64).reshape(-1, 3)
+        m._verts_np = np.ascontiguousarray(np.asarray(vertices), dtype=np.float64).reshape(-1, 3)
         return m
 
     @property
@@ -122,15 +172,59 @@ class DeviceMesh:
         self._packs[kind] = buf
         return buf
 
+    def faces_np(self) -> np.ndarray:
+        fn = getattr(self, "_faces_np", None)
+        if fn is None:
+            fn = self.faces.detach().cpu().numpy().astype(np.int64)  # connectivity is static
+            self._faces_np = fn
+        return fn
+
     def csr(self) -> tuple[torch.Tensor, torch.Tensor]:
         if self._csr is None:
-            faces_np = getattr(self, "_faces_np", None)
-            if faces_np is None:
-                faces_np = self.faces.detach().cpu().numpy()  # connectivity is static
-            off, slots = vertex_csr(faces_np, self.num_vertices)
+            off, slots = vertex_csr(self.faces_np(), self.num_vertices)
             dev = self.vertices.device
             self._csr = (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev))
         return self._csr
+
+    def exact_grad_setup(self):
+        """(active (A,) int64 dev, weights (A,3) f32 dev, CSR over active
+        corners).  Connectivity-only, computed once (dead faces from the
+        vertex positions at setup time)."""
+        eg = getattr(self, "_exact_grad", None)
+        if eg is None:
+            vnp = getattr(self, "_verts_np", None)
+            if vnp is None:
+                vnp = self.vertices.detach().double().cpu().numpy()
+            fnp = self.faces_np()
+            active, w = exact_edge_weights(fnp, dead_faces(vnp, fnp))
+            off, slots = vertex_csr(fnp[active], self.num_vertices)
+            dev = self.vertices.device
+            eg = (torch.from_numpy(active).to(dev), torch.from_numpy(w).to(dev),
+                  (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev)))
+            self._exact_grad = eg
+        return eg
+
+    def packed_exact_grad(self, precision: str) -> torch.Tensor:
+        kind = _EXACTGRAD[precision]
+        ver = (id(self.vertices), self.vertices._version)
+        if ver != self._version:
+            self._packs.clear()
+            self._version = ver
+        buf = self._packs.get(kind)
+        if buf is not None:
+            return buf
+        active, w, _ = self.exact_grad_setup()
+        lib = L.lib()
+        v = self.vertices.contiguous()
+        f = self.faces.contiguous()
+        A = int(active.shape[0])
+        buf = torch.empty(int(lib.wv_packed_bytes(kind, A)), dtype=torch.uint8, device=v.device)
+        L.check(lib.wv_pack_exact_grad(kind, _ptr(v), int(v.dtype == torch.float64),
+                                       self.num_vertices, _ptr(f), int(f.dtype == torch.int64),
+                                       _ptr(active), _ptr(w), A, _ptr(buf), _stream()),
+                "wv_pack_exact_grad")
+        self._packs[kind] = buf
+        return buf
 
 
 def _points_arg(points, dev, dtype):
@@ -207,16 +301,27 @@ def exact_forward_f32(mesh: DeviceMesh, **kw):
 
 
 def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, *, grid=None,
-              n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0,
-              out: torch.Tensor | None = None) -> torch.Tensor:
-    """Per-face corner gradients (F,3,3) f64 = sum_p coef_scale*coefs[p]*dW_p/dv."""
+              n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0):
+    """Per-face corner gradients sum_p coef_scale*coefs[p]*dW_p/dv, f64.
+    Returns (corner_grad (A,3,3), csr) where the rows are all faces (soft) or
+    the active faces of the exact edge form (exact); feed both to
+    ``vertex_grad``.  Exact mode expects coefs == 0 at flagged points."""
     _check_precision(precision)
     lib = L.lib()
     dev = mesh.vertices.device
     dt = _DT[precision]
-    kind = (_EXACT if mode == "exact" else _SOFTGRAD)[precision]
-    packed = mesh.packed(kind)
-    F = mesh.num_faces
+    if mode == "exact":
+        kind = _EXACTGRAD[precision]
+        packed = mesh.packed_exact_grad(precision)
+        active, _, csr = mesh.exact_grad_setup()
+        F = int(active.shape[0])
+    elif mode == "soft":
+        kind = _SOFTGRAD[precision]
+        packed = mesh.packed(kind)
+        csr = mesh.csr()
+        F = mesh.num_faces
+    else:
+        raise ValueError(f"mode must be 'exact' or 'soft', got {mode!r}")
     if points is not None:
         pts, count = _points_arg(points, dev, dt)
     else:
@@ -224,14 +329,13 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     cf = coefs.to(device=dev, dtype=dt).contiguous().reshape(-1)
     if cf.numel() != count:
         raise ValueError(f"coefs has {cf.numel()} entries for {count} query points")
-    out = torch.empty((F, 3, 3), dtype=torch.float64, device=dev) if out is None else out
+    out = torch.empty((F, 3, 3), dtype=torch.float64, device=dev)
     if F == 0:
-        return out
+        return out, csr
     wsb = int(lib.wv_bwd_workspace_bytes(kind, F, count))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     st = _stream()
-    suffix = "f32" if precision == "f32" else "f64"
-    name = f"wv_{mode}_bwd_{'points' if points is not None else 'grid'}_{suffix}"
+    name = f"wv_{mode}_bwd_{'points' if points is not None else 'grid'}_{precision}"
     fn = getattr(lib, name)
     if points is not None:
         rc = fn(_ptr(packed), F, _ptr(pts), count, _ptr(cf), float(coef_scale), _ptr(out),
@@ -240,22 +344,22 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
         rc = fn(_ptr(packed), F, L.make_grid(*grid), int(n0), count, _ptr(cf), float(coef_scale),
                 _ptr(out), _ptr(ws), wsb, st)
     L.check(rc, name)
-    return out
+    return out, csr
 
 
-def vertex_grad(mesh: DeviceMesh, fgrad: torch.Tensor, *, scale: torch.Tensor | None = None,
+def vertex_grad(mesh: DeviceMesh, fgrad, *, scale: torch.Tensor | None = None,
                 dtype=torch.float64, out: torch.Tensor | None = None,
                 accumulate: bool = False) -> torch.Tensor:
-    """(V,3) vertex gradients from (F,3,3) corner sums (CSR gather)."""
+    """(V,3) vertex gradients from ``face_grad``'s (corner_grad, csr)."""
     lib = L.lib()
     dev = mesh.vertices.device
-    off, slots = mesh.csr()
+    fg, (off, slots) = fgrad
     V = mesh.num_vertices
     if out is None:
         out = torch.zeros((V, 3), dtype=dtype, device=dev)
     o64 = out if out.dtype == torch.float64 else None
     o32 = out if out.dtype == torch.float32 else None
-    L.check(lib.wv_face_to_vertex(_ptr(fgrad), _ptr(off), _ptr(slots), V, _ptr(scale),
+    L.check(lib.wv_face_to_vertex(_ptr(fg), _ptr(off), _ptr(slots), V, _ptr(scale),
                                   int(accumulate), _ptr(o64), _ptr(o32), _stream()),
             "wv_face_to_vertex")
     return out
