@@ -80,7 +80,9 @@ def exact_edge_weights(faces: np.ndarray, dead: np.ndarray | None = None):
     sgn[u == v] = 0                          # self-loop edges carry nothing
     sgn = sgn * np.repeat(live, 3)
     key = lo * (int(f.max()) + 1) + hi
-    order = np.argsort(key, kind="stable")
+    # group by edge; within a group live (sgn != 0) occurrences first, so the
+    # weight lands on a face that actually contributes
+    order = np.lexsort(((sgn == 0).astype(np.int8), key))
     ks = key[order]
     start = np.ones(len(ks), bool)
     start[1:] = ks[1:] != ks[:-1]

@@ -1,0 +1,135 @@
+"""CPU-only tests: the C-ABI library loads and exports every symbol the
+public header declares (no compute calls -- there is no GPU here), plus the
+host-side logic of the package (types, CSR, exact-gradient edge weights)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "windvox_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(wv_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2407_11272_b200 import _lib
+    lib = _lib.load_library()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(_lib.EXPORTED) == syms
+    assert lib.wv_version().startswith(b"windvox_b200")
+    assert lib.wv_status_string(2) == b"workspace missing or too small"
+
+
+def test_packed_sizes():
+    from paper_2407_11272_b200 import _lib
+    lib = _lib.load_library()
+    assert lib.wv_packed_bytes(1, 10) == 64 + 10 * 64
+    assert lib.wv_packed_bytes(2, 10) == 64 + 10 * 32
+    assert lib.wv_packed_bytes(3, 10) == 64 + 10 * 128
+    assert lib.wv_packed_bytes(7, 10) == 64 + 10 * 48
+    assert lib.wv_packed_bytes(99, 10) == 0
+
+
+def test_no_cpu_fallback():
+    """The product path refuses to run without a CUDA device."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2407_11272_b200 as wv
+    from paper_2407_11272_b200._lib import WindvoxCudaUnavailable
+    mesh = wv.TriangleMesh(np.eye(3), [[0, 1, 2]])
+    with pytest.raises(WindvoxCudaUnavailable):
+        wv.voxelize(mesh, wv.GridSpec((-1.0,) * 3, (1.0,) * 3, 4))
+
+
+def test_types_mirror_reference_validation():
+    import paper_2407_11272_b200 as wv
+    with pytest.raises(ValueError):
+        wv.GridSpec((0.0,) * 3, (0.0, 1.0, 1.0), 4)
+    with pytest.raises(ValueError):
+        wv.GridSpec((0.0,) * 3, (1.0,) * 3, (4, 0, 4))
+    with pytest.raises(ValueError):
+        wv.ScalarField(wv.GridSpec((0.0,) * 3, (1.0,) * 3, 2), np.zeros(9))
+    with pytest.raises(IndexError):
+        wv.TriangleMesh(np.zeros((3, 3)), [[0, 1, 3]])
+    with pytest.raises(ValueError):
+        wv.QueryBatchConfig(chunk_size=0)
+    spec = wv.GridSpec((-1.0, 0.0, 2.0), (1.0, 3.0, 2.5), (3, 4, 2))
+    from oracle import oracle as orc
+    assert np.array_equal(spec.node_coordinates(),
+                          orc.node_coordinates((-1.0, 0.0, 2.0), (1.0, 3.0, 2.5), (3, 4, 2)))
+    one = wv.GridSpec((0.0,) * 3, (2.0,) * 3, (1, 1, 3))
+    assert np.allclose(one.node_coordinates()[:, :2], 1.0)
+    f = wv.binarize(wv.ScalarField(wv.GridSpec((0.0,) * 3, (1.0,) * 3, (1, 1, 3)),
+                                   np.array([0.9, 0.1, 0.5])))
+    assert f.values.tolist() == [1.0, 0.0, 0.0]
+
+
+def test_solid_angle_triangle_known_answers():
+    import paper_2407_11272_b200 as wv
+    assert abs(wv.solid_angle_triangle([1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, 0]) - np.pi / 2) < 1e-12
+    assert wv.solid_angle_triangle([1, 0, 0], [1, 0, 0], [0, 1, 0], [0.3, 0.1, -2.0]) == 0.0
+    assert wv.solid_angle_triangle([0, 0, 0], [1, 0, 0], [0, 1, 0], [3.0, 3.0, 0.0]) == 0.0
+    with pytest.raises(wv.OnSurfaceError):
+        wv.solid_angle_triangle([0, 0, 0], [1, 0, 0], [0, 1, 0], [0.2, 0.2, 0.0])
+
+
+def test_vertex_csr_order():
+    from paper_2407_11272_b200.device import vertex_csr
+    faces = np.array([[0, 1, 2], [2, 1, 3], [3, 0, 2]])
+    off, slots = vertex_csr(faces, 5)
+    assert off.tolist() == [0, 2, 4, 7, 9, 9]
+    for v in range(4):
+        s = slots[off[v]:off[v + 1]]
+        assert (faces.reshape(-1)[s] == v).all() and (np.diff(s) > 0).all()
+
+
+def _edge_form_grad(v, faces, pts, coefs, active, w):
+    """numpy restatement of the kernels' edge form (test-side)."""
+    g = np.zeros_like(v)
+    for fi, ww in zip(active, w):
+        tri = faces[fi]
+        for k in range(3):
+            i, j = tri[k], tri[(k + 1) % 3]
+            if ww[k] == 0:
+                continue
+            for q, c in zip(pts, coefs):
+                a, b = v[i] - q, v[j] - q
+                la, lb = np.linalg.norm(a), np.linalg.norm(b)
+                t = -c * ww[k] / (4 * np.pi * (la * lb + a @ b))
+                m = np.cross(a, b)
+                g[i] += m * t / la
+                g[j] += m * t / lb
+    return g
+
+
+@pytest.mark.parametrize("case", ["holes", "soup", "random"])
+def test_exact_edge_weights_reproduce_face_closed_form(case):
+    from oracle import oracle as orc
+    from paper_2407_11272_b200 import configs
+    from paper_2407_11272_b200.device import dead_faces, exact_edge_weights
+    rng = np.random.default_rng(3)
+    if case == "holes":
+        v, f = configs.torus_with_holes(nu=16, nv=12, holes=2, patch=2, seed=1)
+    elif case == "soup":
+        v, f = configs.soup(*configs.torus(0.7, 0.3, 8, 6))
+    else:
+        v = rng.normal(size=(12, 3))
+        f = rng.integers(0, 12, size=(20, 3))
+        f[0] = [4, 4, 5]  # degenerate (dropped by the reference forward)
+    pts = rng.normal(size=(6, 3)) * 1.3
+    coefs = rng.normal(size=6)
+    active, w = exact_edge_weights(f, dead_faces(v, f))
+    got = _edge_form_grad(v, f, pts, coefs, active, w)
+    ref = orc.exact_grad(v, f, pts, coefs)
+    assert np.abs(got - ref).max() <= 1e-10 * max(np.abs(ref).max(), 1e-12)
+    if case == "holes":
+        assert len(active) < len(f) // 2
