@@ -2,18 +2,23 @@
 point-triangle solid-angle evaluations/s, forward and forward+backward, plus
 256^3 voxelize ms).
 
-Workload (N=1 default): config C3 -- a 100k-face triangle soup (torus
-(0.7,0.3,250,200) un-welded and shuffled, seeded) voxelized on [-1,1]^3 at
-256^3.  A step = one pass of the hot path over the node slab this rank owns
-(contiguous i-slabs).  Inputs are synthetic (no network).
+Workload (default, N=1): config C3 -- a 100k-face triangle soup (torus
+(0.7,0.3,250,200) un-welded and shuffled with a fixed seed) on [-1,1]^3 at
+256^3 = 16.8M lattice nodes, 1.68e12 point-triangle pairs per pass.  A step
+is one forward+backward training pass of the occupancy loss in exact mode on
+the FP32 path: pack the (moved) mesh, exact forward over the rank's i-slab,
+fused loss terms against a fixed target occupancy, exact backward, vertex
+gather, and (N>1) one all-reduce of [grad numerator | loss sums].  Synthetic
+inputs (no network); the target is the binarized exact occupancy of the same
+soup scaled by 1.03, computed once before timing.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N>1) every rank times its slab on its own GPU; the reported
-time is the max over ranks and ``value`` is the whole-job pair rate.
-``--impl reference`` times the reference's CPU algorithm (the bit-exact C
-port in oracle/, all host threads) on a bounded node sample of the same
-workload; rank 0 only.
+Under torchrun each rank owns 1/N of the grid (weak scaling in pairs per
+GPU is NOT what this is: total work is fixed, so scaling is "strong"); time
+is the max over ranks.  ``--impl reference`` times the reference's CPU
+algorithm (the bit-exact C port in oracle/, all host threads) on a bounded
+node sample of the same workload, rank 0 only.
 """
 
 from __future__ import annotations
@@ -22,7 +27,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -33,9 +37,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-EXACT_FWD_FLOPS = 63      # SURVEY.md 8d / Appendix A.1 (VOS formula as written)
-EXACT_BWD_FLOPS = 170     # Appendix A.4
-FP32_PEAK_NOMINAL = None  # computed from MEASURED_PEAKS sm_max_mhz below
+# algorithmic work per point-triangle pair
+EXACT_FWD_FLOPS = 63
+EXACT_BWD_FLOPS = 170
 
 
 def parse():
@@ -48,55 +52,49 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target duration of the CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
-    sm_mhz = 1965.0
-    out = {"source": "nominal"}
+    sm_mhz, src = 1965.0, "nominal 1965 MHz"
     if p.exists():
         d = json.loads(p.read_text())
         sm_mhz = float(d.get("sm_max_mhz", sm_mhz))
-        out.update(d)
-        out["source"] = "MEASURED_PEAKS.json sm_max_mhz"
-    # FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 FLOP/FMA x clock
-    out["fp32_tflops_nominal"] = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-    return out
+        src = "MEASURED_PEAKS.json sm_max_mhz"
+    # FP32 CUDA-core peak: 148 SMs x 128 FP32 lanes x 2 FLOP/FMA x clock
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, src
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clock / throttle reasons sampled (NVML) DURING the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index: int, period: float = 0.25):
+        self.index, self.period = index, period
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                    timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.samples.append((sm, mx, r, pw))
+                self._stop.wait(self.period)
+        except Exception as e:  # pragma: no cover - reported in the JSON line
+            self.error = repr(e)
 
     def __enter__(self):
         self._t.start()
@@ -108,53 +106,57 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
-        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "power_w_median": statistics.median(pw) if pw else None,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["unsampled: " + getattr(self, "error", "no samples")]}
+        import pynvml as N
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({k for s in self.samples for k, b in bits.items() if s[2] & b})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "power_w_median": statistics.median(s[3] for s in self.samples),
+                "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------
-# reference arm / CPU baseline (oracle = bit-exact C port of the reference)
-
-def cpu_sample_rate(w, seconds: float, threads: int, seed: int = 0):
-    """Exact f64 forward of the reference algorithm on a seeded node sample
-    sized to take about `seconds` on `threads` host threads."""
-    from oracle import oracle as orc
-
-    nodes_all = int(np.prod(w.res))
-    rng = np.random.default_rng(seed)
-    probe = max(threads * 2, 16)
-    idx = rng.choice(nodes_all, size=probe, replace=False)
-    pts = _nodes(w, idx)
-    t0 = time.perf_counter()
-    orc.winding_number_batch(w.vertices, w.faces, pts, chunk=1, threads=threads)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    rate = probe * w.n_faces / dt
-    n = int(min(nodes_all, max(threads * 8, rate * seconds / w.n_faces)))
-    idx = np.sort(rng.choice(nodes_all, size=n, replace=False))
-    pts = _nodes(w, idx)
-    chunk = max(1, min(2000, n // (threads * 4) or 1))
-    t0 = time.perf_counter()
-    orc.winding_number_batch(w.vertices, w.faces, pts, chunk=chunk, threads=threads)
-    dt = time.perf_counter() - t0
-    return n * w.n_faces / dt, n, dt
-
+# CPU side: the reference algorithm (bit-exact C port, oracle/) on a sample
 
 def _nodes(w, idx):
     from oracle import oracle as orc
-    rx, ry, rz = w.res
-    i, rem = np.divmod(idx, ry * rz)
-    j, k = np.divmod(rem, rz)
+    i, rem = np.divmod(idx, w.res[1] * w.res[2])
+    j, k = np.divmod(rem, w.res[2])
     ax = [orc.axis_nodes(w.lo[a], w.hi[a], w.res[a]) for a in range(3)]
     return np.stack([ax[0][i], ax[1][j], ax[2][k]], axis=1)
+
+
+def cpu_fwd_bwd_rate(w, seconds: float, threads: int, seed: int = 0):
+    """Exact f64 forward (reference exact_batch, bit-exact port) + exact f64
+    gradient (closed-form oracle; the reference has no exact-gradient kernel)
+    on a seeded node sample sized for ~`seconds` on `threads` threads.
+    Returns (fwd+bwd pairs/s, fwd pairs/s, nodes, wall s)."""
+    from oracle import oracle as orc
+    rng = np.random.default_rng(seed)
+    probe = max(threads * 32, 64)  # large enough that per-call staging does not dominate
+    pts = _nodes(w, rng.choice(w.n_nodes, size=probe, replace=False))
+    t0 = time.perf_counter()
+    orc.winding_number_batch(w.vertices, w.faces, pts, chunk=1, threads=threads)
+    orc.exact_grad(w.vertices, w.faces, pts, np.ones(probe), chunk=1, threads=threads)
+    rate = probe * w.n_faces / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(w.n_nodes, max(threads * 4, rate * seconds / w.n_faces)))
+    pts = _nodes(w, np.sort(rng.choice(w.n_nodes, size=n, replace=False)))
+    chunk = max(1, n // (threads * 4))
+    t0 = time.perf_counter()
+    vals, flags = orc.winding_number_batch(w.vertices, w.faces, pts, chunk=chunk, threads=threads)
+    t_f = time.perf_counter() - t0
+    coefs = np.where(flags, 0.0, 2.0 * (vals - (vals > 0.5)))
+    # one (V,3) buffer per chunk in the reference's merge (grad.py:113-127)
+    gchunk = max(chunk, n // threads)
+    t1 = time.perf_counter()
+    orc.exact_grad(w.vertices, w.faces, pts, coefs, chunk=gchunk, threads=threads)
+    t_b = time.perf_counter() - t1
+    return n * w.n_faces / (t_f + t_b), n * w.n_faces / t_f, n, t_f + t_b
 
 
 def run_reference(args):
@@ -163,34 +165,39 @@ def run_reference(args):
         return 0
     from oracle import oracle as orc
     from paper_2407_11272_b200 import configs
-
     w = configs.make(args.config)
     threads = orc.default_threads()
-    per = max(2.0, args.cpu_seconds / max(1, args.steps))
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_sample_rate(w, 0.5, threads, seed=99)
-    rates, samples = [], []
+    per = max(3.0, args.cpu_seconds / max(1, args.steps))
+    for _ in range(min(1, args.warmup)):
+        cpu_fwd_bwd_rate(w, 0.5, threads, seed=99)
+    rates, fwd, samples = [], [], []
     t_all = time.perf_counter()
     for k in range(args.steps):
-        r, n, dt = cpu_sample_rate(w, per, threads, seed=k)
+        r, rf, n, _ = cpu_fwd_bwd_rate(w, per, threads, seed=k)
         rates.append(r)
+        fwd.append(rf)
         samples.append(n)
     wall = time.perf_counter() - t_all
     rate = statistics.median(rates)
     line = {
-        "impl": "reference", "metric": "point-triangle solid-angle evals/sec (exact fwd, f64 CPU reference)",
+        "impl": "reference",
+        "metric": "point-triangle solid-angle evals/sec, exact fwd+bwd (256^3 voxelize ms in "
+                  "extrapolated_voxelize_ms)",
         "value": rate, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": w.name, "faces": w.n_faces,
-                                        "grid": list(w.res), "mode": "exact"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": w.name, "faces": w.n_faces, "grid": list(w.res), "mode": "exact",
+                   "step": "bounded node sample: exact forward + exact gradient"},
+        "fwd_pairs_per_s": statistics.median(fwd),
+        "extrapolated_voxelize_ms": w.pairs / statistics.median(fwd) * 1e3,
         "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "sample": f"{samples} seeded random nodes of the {w.res[0]}^3 grid x "
-                                   f"{w.n_faces} faces per step (bit-exact C port of "
-                                   "_kernels.exact_batch, oracle/windvox_oracle.c)"},
+                                   f"{w.n_faces} faces per step; forward = bit-exact C port of "
+                                   "_kernels.exact_batch, backward = closed-form oracle "
+                                   "(no reference exact-gradient kernel exists)"},
         "e2e": {"value": rate, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "extrapolated_full_forward_s": w.pairs / rate,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -207,29 +214,51 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import paper_2407_11272_b200 as wvb
     from paper_2407_11272_b200 import configs, device
+    from paper_2407_11272_b200 import _lib as L
+    from paper_2407_11272_b200.distributed import SlabDriver, slab_range
 
     dev = torch.device("cuda", local)
     w = configs.make(args.config)
-    n_total = w.n_nodes
-    per_rank = (n_total + world - 1) // world
-    n0 = rank * per_rank
-    cnt = max(0, min(n_total, n0 + per_rank) - n0)
+    n0, cnt = slab_range(w.n_nodes, rank, world)
     grid = (w.lo, w.hi, w.res)
 
+    # fixed target: binarized exact occupancy of the soup scaled by 1.03 (untimed)
+    tmesh = device.DeviceMesh.from_numpy(w.vertices * 1.03, w.faces, dev)
+    tv, _ = device.forward(tmesh, "exact", "f32", grid=grid, n0=n0, count=cnt)
+    targets = (tv > 0.5).to(torch.float32)
+    del tmesh, tv
+
     dmesh = device.DeviceMesh.from_numpy(w.vertices, w.faces, dev)
-    out = torch.empty(cnt, dtype=torch.float32, device=dev)
-    flags = torch.empty(cnt, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    ev = {k: [] for k in ("f0", "f1", "b0", "b1")}
 
-    def step():
-        # one pass of the hot path over this rank's slab: face staging +
-        # exact forward (every kernel of the path runs each step)
-        dmesh.invalidate()
-        device.exact_forward_f32(dmesh, grid=grid, n0=n0, count=cnt, out=out, flags=flags)
+    def step(record=False):
+        def mark(k):
+            if record:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                ev[k].append(e)
+        dmesh.invalidate()  # the vertices moved: re-stage every kernel's records
+        mark("f0")
+        vals, flags = device.forward(dmesh, "exact", "f32", grid=grid, n0=n0, count=cnt)
+        mark("f1")
+        coefs, sums = device.loss_terms(vals, flags, targets)
+        mark("b0")
+        fg = device.face_grad(dmesh, "exact", "f32", coefs, grid=grid, n0=n0, count=cnt)
+        mark("b1")
+        g = device.vertex_grad(dmesh, fg)
+        buf = torch.cat([g.reshape(-1), sums[:3]])
+        if world > 1:
+            dist.all_reduce(buf)
+        return buf[:-3].reshape(-1, 3) / buf[-2], buf[-3] / buf[-2]
 
-    launches_per_step = 2 + 1  # surface-eps + pack + forward
+    F = w.n_faces
+    active = int(dmesh.exact_grad_setup()[0].shape[0])
+    launches = (2 + 1 + (1 if L.lib().wv_fwd_workspace_bytes(1, F, cnt) else 0) + 2 + 2 + 1
+                + (1 if L.lib().wv_bwd_workspace_bytes(7, active, cnt) else 0) + 1)
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -239,95 +268,100 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # --- timed region -----------------------------------------------------
-    stream = torch.cuda.current_stream()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_stop = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
-        ev0.record(stream)
+        e_start.record(stream)
         for _ in range(args.steps):
             flush.zero_()
-            step()
-        ev1.record(stream)
+            grads, loss = step(record=True)
+        e_stop.record(stream)
         barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    ms = e_start.elapsed_time(e_stop)
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["f0"], ev["f1"]))
+    bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["b0"], ev["b1"]))
+    t = torch.tensor([ms, fwd_ms, bwd_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_step = ms_max / args.steps
-    pairs_step = w.pairs  # all ranks together cover the whole grid once per step
-    value = pairs_step / (ms_step / 1e3)
+    ms_step = float(t[0]) / args.steps
+    fwd_ms, bwd_ms = float(t[1]), float(t[2])
+    value = w.pairs / (ms_step / 1e3)
 
-    # --- roofline: the forward kernel alone, CUDA events on its stream ----
-    kev0 = torch.cuda.Event(enable_timing=True)
-    kev1 = torch.cuda.Event(enable_timing=True)
-    dmesh.packed(1)
-    torch.cuda.synchronize()
-    reps = max(1, args.steps)
-    kev0.record(stream)
-    for _ in range(reps):
-        device.exact_forward_f32(dmesh, grid=grid, n0=n0, count=cnt, out=out, flags=flags)
-    kev1.record(stream)
-    torch.cuda.synchronize()
-    k_ms = kev0.elapsed_time(kev1) / reps
-    pk = peaks()
-    achieved = EXACT_FWD_FLOPS * cnt * w.n_faces / (k_ms / 1e3) / 1e12
+    # --- e2e: host numpy in (mesh + this rank's target slab), host grads out
+    e2e = None
+    if not args.no_e2e:
+        tgt_host = targets.cpu().numpy()
+        h2d = w.vertices.nbytes + w.faces.nbytes + tgt_host.nbytes
+        d2h = w.vertices.nbytes + 8
 
-    # --- e2e: public API, host buffers in, host result out ----------------
-    mesh_np = wvb.TriangleMesh(w.vertices, w.faces)
-    spec = wvb.GridSpec(w.lo, w.hi, w.res)
-    e2e_value = None
-    h2d = w.vertices.nbytes + w.faces.nbytes
-    d2h = n_total * 4
-    if world == 1:
-        wvb.voxelize(mesh_np, spec, precision="f32")  # warm
-        torch.cuda.synchronize()
+        def e2e_step():
+            m = device.DeviceMesh.from_numpy(w.vertices, w.faces, dev)
+            tg = torch.from_numpy(tgt_host).pin_memory().to(dev, non_blocking=True)
+            drv = SlabDriver(_E(m, grid), w.n_nodes, rank, world)
+            lo, gr, _, _ = drv.loss_grad(tg)
+            return gr.cpu().numpy(), float(lo)
+
+        e2e_step()
+        barrier()
         t0 = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = max(1, min(args.steps, 2))
         for _ in range(e2e_steps):
-            field = wvb.voxelize(mesh_np, spec, precision="f32")
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-        e2e_value = w.pairs / e2e_s
-        del field
+            e2e_step()
+        barrier()
+        dt = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=dev,
+                          dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": w.pairs / float(dt), "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "api": "DeviceMesh.from_numpy + SlabDriver(CudaSlabEvaluator).loss_grad "
+                      "(grad.exact_loss_grad's device path), numpy in / numpy grads out"}
 
-    line = None
     if rank == 0:
+        peak, peak_src = peaks()
+        fwd_tf = EXACT_FWD_FLOPS * cnt * F / (fwd_ms / 1e3) / 1e12
+        bwd_tf = EXACT_BWD_FLOPS * cnt * F / (bwd_ms / 1e3) / 1e12
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as orc
             thr = orc.default_threads()
-            r, n, dt = cpu_sample_rate(w, args.cpu_seconds, thr)
+            r, rf, n, dt = cpu_fwd_bwd_rate(w, args.cpu_seconds, thr)
             cpu = {"value": r, "unit": "pairs/s", "cores": thr, "kind": "port",
-                   "sample": f"{n} seeded random nodes of the {w.res[0]}^3 grid x {w.n_faces} "
-                             f"faces, exact f64 forward, {dt:.1f} s (bit-exact C port of "
-                             "_kernels.exact_batch)"}
+                   "fwd_pairs_per_s": rf,
+                   "sample": f"{n} seeded random nodes of the {w.res[0]}^3 grid x {F} faces, "
+                             f"exact f64 fwd (bit-exact C port of _kernels.exact_batch) + exact "
+                             f"f64 grad (closed-form oracle), {dt:.1f} s"}
+        dom = ("exact_bwd (bwd_f32_kernel<ExactEdgeBwd,GridSrc>)", bwd_ms, bwd_tf) \
+            if bwd_ms >= fwd_ms else ("exact_fwd (fwd_f32_kernel<ExactPol,GridSrc>)", fwd_ms,
+                                      fwd_tf)
         line = {
-            "metric": "point-triangle solid-angle evals/sec (exact fwd; fwd+bwd pending); "
-                      "256^3 voxelize ms",
-            "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": w.name, "faces": w.n_faces, "grid": list(w.res),
-                       "mode": "exact", "step": "pack + exact forward over the rank's i-slab",
+            "metric": "point-triangle solid-angle evals/sec fwd & fwd+bwd; 256^3 voxelize ms",
+            "value": value, "unit": "pairs/s (exact fwd+bwd)", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": w.name, "faces": F, "grid": list(w.res), "mode": "exact",
+                       "step": "pack + exact fwd + loss + exact bwd + vertex gather"
+                               + (" + all-reduce" if world > 1 else ""),
                        "l2": "256 MiB buffer zeroed between timed steps (> 126 MB L2)",
-                       "parallelism": f"i-slabs x{world}"},
-            "voxelize_ms": ms_step,
-            "fwd_pairs_per_s": value,
-            "roofline": {"bound": "fp32", "achieved": achieved,
-                         "peak": pk["fp32_tflops_nominal"], "unit": "TFLOP/s",
-                         "frac": achieved / pk["fp32_tflops_nominal"], "traffic": None,
-                         "kernel": "exact_fwd_f32_kernel<GridSrc>",
-                         "kernel_ms": k_ms,
-                         "flops_per_pair": EXACT_FWD_FLOPS,
-                         "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz ("
-                                        + pk["source"] + ")"},
+                       "parallelism": f"i-slabs x{world}", "active_bwd_faces": active},
+            "fwd_pairs_per_s": w.pairs / (fwd_ms / 1e3),
+            "bwd_pairs_per_s": w.pairs / (bwd_ms / 1e3),
+            "voxelize_ms": fwd_ms,
+            "loss": float(loss),
+            "roofline": {"bound": "fp32", "achieved": dom[2], "peak": peak, "unit": "TFLOP/s",
+                         "frac": dom[2] / peak, "traffic": None, "kernel": dom[0],
+                         "kernel_ms": dom[1],
+                         "flops_per_pair": EXACT_BWD_FLOPS if dom[0].startswith("exact_bwd")
+                         else EXACT_FWD_FLOPS,
+                         "peak_source": f"FP32 CUDA-core peak 148 SM x 128 lanes x 2 x clock "
+                                        f"({peak_src}); MEASURED_PEAKS has no FP32 entry"},
+            "roofline_fwd": {"achieved": fwd_tf, "frac": fwd_tf / peak, "kernel_ms": fwd_ms},
+            "roofline_bwd": {"achieved": bwd_tf, "frac": bwd_tf / peak, "kernel_ms": bwd_ms},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "api": "paper_2407_11272_b200.voxelize(mesh, spec, precision='f32')"},
-            "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -335,6 +369,14 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+class _E:
+    """CudaSlabEvaluator in exact/f32 mode (the product evaluator)."""
+
+    def __new__(cls, dmesh, grid):
+        from paper_2407_11272_b200.distributed import CudaSlabEvaluator
+        return CudaSlabEvaluator(dmesh, grid, mode="exact", precision="f32")
 
 
 def main():
