@@ -147,6 +147,9 @@ def make(name: str) -> Workload:
     if name == "c3":
         v, f = soup(*torus(0.7, 0.3, 250, 200), seed=0)
         return Workload("c3_torus100k_soup_256", v, f, *g, (256,) * 3)
+    if name == "c3s":  # quarter-size C3 for profiling (25k-face soup, 128^3)
+        v, f = soup(*torus(0.7, 0.3, 125, 100), seed=0)
+        return Workload("c3s_torus25k_soup_128", v, f, *g, (128,) * 3)
     if name == "c5":
         v, f = torus(0.7, 0.3, 1000, 500)
         return Workload("c5_torus1M_512", v, f, *g, (512,) * 3)

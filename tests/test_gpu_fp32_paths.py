@@ -159,6 +159,7 @@ def test_autograd_matches_device_kernels(torch_):
     import paper_2407_11272_b200 as wv
     from paper_2407_11272_b200 import configs
     v, f = configs.icosphere(2, 0.6)
+    f = f[v[f].mean(axis=1)[:, 2] < 0.3]  # open cap: the exact gradient lives on the rim
     verts = torch.tensor(v, dtype=torch.float32, device="cuda", requires_grad=True)
     faces = torch.tensor(f, dtype=torch.int32, device="cuda")
     grid = ((-1.0,) * 3, (1.0,) * 3, (12, 12, 12))
