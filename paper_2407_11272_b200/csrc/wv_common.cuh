@@ -238,25 +238,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Producer-side wait: the slot frees only after every consumer warp has
-// finished a whole tile (tens of microseconds), so poll with a sleep instead
-// of spinning -- a spinning producer steals issue slots from the consumers.
-__device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (;;) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, P1;\n"
-        "}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(2000);
-  }
-}
 __device__ __forceinline__ void tma_bulk_g2s(void* smem_dst, const void* gmem_src,
                                              uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -267,44 +248,63 @@ __device__ __forceinline__ void tma_bulk_g2s(void* smem_dst, const void* gmem_sr
 }
 
 // ---------------------------------------------------------------------------
-// Face-tile ring: one producer warp streams TILE-record tiles of the packed
-// face array into STAGES shared-memory slots with TMA bulk copies; consumer
-// warps wait on full[s], read, and arrive on empty[s].
+// Face-tile ring without a producer warp.  TILE-record tiles of the packed
+// face array stream into STAGES shared-memory slots by TMA bulk copy
+// (cp.async.bulk, completion counted on the slot's mbarrier).  Every warp
+// waits on full[s], computes, then bumps a CTA-scope counter; the LAST warp to
+// finish a tile re-arms the slot and issues the copy of tile t+STAGES into it.
+// Nobody ever waits for a slot to drain, so no warp spins: a dedicated
+// producer warp polling an "empty" barrier measurably stole ~15% of the issue
+// slots (profiles/README.md, round 1).
 template <typename Rec, int TILE, int STAGES>
 struct FaceRing {
   Rec tiles[STAGES][TILE];
   uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+  int done[STAGES];
 };
 
 template <typename Rec, int TILE, int STAGES>
-__device__ __forceinline__ void ring_init(FaceRing<Rec, TILE, STAGES>& r,
-                                          int n_consumer_warps) {
+__device__ __forceinline__ void ring_issue(FaceRing<Rec, TILE, STAGES>& r, int s,
+                                           const Rec* __restrict__ recs, int64_t n_recs,
+                                           int64_t t) {
+  const int64_t first = t * TILE;
+  const int64_t cnt = (n_recs - first) < TILE ? (n_recs - first) : TILE;
+  const uint32_t bytes = (uint32_t)(cnt * (int64_t)sizeof(Rec));
+  mbar_arrive_expect_tx(&r.full[s], bytes);
+  tma_bulk_g2s(&r.tiles[s][0], recs + first, bytes, &r.full[s]);
+}
+
+// Initialise barriers and issue the first STAGES tiles of [t_begin, t_end).
+template <typename Rec, int TILE, int STAGES>
+__device__ __forceinline__ void ring_start(FaceRing<Rec, TILE, STAGES>& r,
+                                           const Rec* __restrict__ recs, int64_t n_recs,
+                                           int64_t t_begin, int64_t t_end) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&r.full[s], 1);
-      mbar_init(&r.empty[s], n_consumer_warps);
+      r.done[s] = 0;
     }
     fence_barrier_init();
+    for (int s = 0; s < STAGES && t_begin + s < t_end; ++s)
+      ring_issue(r, s, recs, n_recs, t_begin + s);
   }
   __syncthreads();
 }
 
-// Producer loop, executed by one thread.
+// Called by lane 0 of every warp after it finished tile t (slot s).
 template <typename Rec, int TILE, int STAGES>
-__device__ __forceinline__ void ring_produce(FaceRing<Rec, TILE, STAGES>& r,
-                                             const Rec* __restrict__ recs,
-                                             int64_t n_recs, int64_t t_begin,
-                                             int64_t t_end) {
-  for (int64_t t = t_begin; t < t_end; ++t) {
-    const int64_t it = t - t_begin;
-    const int s = (int)(it % STAGES);
-    if (it >= STAGES) mbar_wait_sleepy(&r.empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
-    const int64_t first = t * TILE;
-    const int64_t cnt = (n_recs - first) < TILE ? (n_recs - first) : TILE;
-    const uint32_t bytes = (uint32_t)(cnt * (int64_t)sizeof(Rec));
-    mbar_arrive_expect_tx(&r.full[s], bytes);
-    tma_bulk_g2s(&r.tiles[s][0], recs + first, bytes, &r.full[s]);
+__device__ __forceinline__ void ring_release(FaceRing<Rec, TILE, STAGES>& r, int s,
+                                             int n_warps, const Rec* __restrict__ recs,
+                                             int64_t n_recs, int64_t t, int64_t t_end) {
+  __threadfence_block();  // this warp's reads of slot s precede the counter bump
+  // monotonically increasing: round k of slot s takes the values
+  // [k*n_warps, (k+1)*n_warps); round k+1 cannot start before round k's
+  // last increment re-issued the slot, so rounds never interleave
+  const int old = atomicAdd(&r.done[s], 1);
+  if (old % n_warps == n_warps - 1) {  // last reader of this slot
+    __threadfence_block();
+    fence_proxy_async();  // generic-proxy reads before the async-proxy overwrite
+    if (t + STAGES < t_end) ring_issue(r, s, recs, n_recs, t + STAGES);
   }
 }
 

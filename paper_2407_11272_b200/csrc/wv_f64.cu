@@ -18,7 +18,7 @@ constexpr int kF64Tile = 64;
 constexpr int kF64Stages = 4;
 constexpr int kF64ConsumerWarps = 4;
 constexpr int kF64NC = kF64ConsumerWarps * 32;
-constexpr int kF64Threads = kF64NC + 32;
+constexpr int kF64Threads = kF64NC;
 constexpr int kF64P = 4;
 constexpr double kBaryTol = 1e-12;  // _kernels.py:31
 
@@ -97,12 +97,8 @@ fwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
                double* __restrict__ out, uint8_t* __restrict__ flags) {
   using Rec = typename Pol::Rec;
   __shared__ FaceRing<Rec, kF64Tile, kF64Stages> ring;
-  ring_init(ring, kF64ConsumerWarps);
   const int64_t n_tiles = (n_faces + kF64Tile - 1) / kF64Tile;
-  if ((threadIdx.x >> 5) == kF64ConsumerWarps) {
-    if ((threadIdx.x & 31) == 0 && n_tiles > 0) ring_produce(ring, recs, n_faces, 0, n_tiles);
-    return;
-  }
+  ring_start(ring, recs, n_faces, 0, n_tiles);
   const double eps = hdr->eps;
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * (kF64NC * kF64P);
@@ -129,7 +125,7 @@ fwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       for (int p = 0; p < kF64P; ++p) Pol::pair(R, qx[p], qy[p], qz[p], eps, use_atan2, acc[p], hit[p]);
     }
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&ring.empty[s]);
+    if ((tid & 31) == 0) ring_release(ring, s, kF64ConsumerWarps, recs, n_faces, t, n_tiles);
   }
 #pragma unroll
   for (int p = 0; p < kF64P; ++p) {

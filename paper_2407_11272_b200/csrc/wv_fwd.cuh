@@ -2,8 +2,9 @@
 // streamed through a TMA ring).  Instantiated by wv_fwd_f32.cu with the exact
 // (Van Oosterom-Strackee) and soft (dipole) pair policies.
 //
-//  * one producer warp streams TILE-record tiles of the packed face array into
-//    a STAGES-deep shared-memory ring with cp.async.bulk (TMA, SASS UBLKCP);
+//  * TILE-record tiles of the packed face array stream into a STAGES-deep
+//    shared-memory ring with cp.async.bulk (TMA, SASS UBLKCP); the last warp
+//    to finish a tile issues the refill of its slot (no producer warp);
 //  * each consumer thread holds P query points in registers and walks the
 //    tiles in face order; per face it evaluates the common path for all P
 //    points branch-free and defers the few "rare" pairs (near-plane /
@@ -26,18 +27,11 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   constexpr int NC = CW * 32;
   constexpr int P = Pol::kP;
   __shared__ FaceRing<Rec, TILE, STAGES> ring;
-  ring_init(ring, CW);
-
   const int64_t n_tiles = (n_faces + TILE - 1) / TILE;
   const int64_t t_begin = (int64_t)blockIdx.y * tiles_per_split;
   int64_t t_end = t_begin + tiles_per_split;
   if (t_end > n_tiles) t_end = n_tiles;
-
-  if ((threadIdx.x >> 5) == CW) {  // producer warp
-    if ((threadIdx.x & 31) == 0 && t_begin < t_end)
-      ring_produce(ring, recs, n_faces, t_begin, t_end);
-    return;
-  }
+  ring_start(ring, recs, n_faces, t_begin, t_end);
 
   const float eps = hdr->eps_f32;
   const int tid = threadIdx.x;
@@ -87,7 +81,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
     for (int p = 0; p < P; ++p) accd[p] += (double)tacc[p];
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&ring.empty[s]);
+    if ((tid & 31) == 0) ring_release(ring, s, CW, recs, n_faces, t, t_end);
   }
 
 #pragma unroll

@@ -60,8 +60,8 @@ struct ExactPol {
   static constexpr int kTile = 128;
   static constexpr int kStages = 4;
   static constexpr int kConsumerWarps = 4;
-  static constexpr int kThreads = kConsumerWarps * 32 + 32;
-  static constexpr int kMinBlocks = 3;
+  static constexpr int kThreads = kConsumerWarps * 32;
+  static constexpr int kMinBlocks = 4;
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (2.0 * kPi);
   struct Ctx {};
@@ -101,8 +101,8 @@ struct SoftPol {
   static constexpr int kTile = 256;
   static constexpr int kStages = 4;
   static constexpr int kConsumerWarps = 4;
-  static constexpr int kThreads = kConsumerWarps * 32 + 32;
-  static constexpr int kMinBlocks = 4;
+  static constexpr int kThreads = kConsumerWarps * 32;
+  static constexpr int kMinBlocks = 5;
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (8.0 * kPi);
   struct Ctx {
