@@ -6,8 +6,9 @@
 // exact_batch hot loop, :34-116, under the 1e-5 tolerance of north_star):
 //   theta = atan2(alpha, beta),  Omega = 2 theta,  W = sum(theta) / (2 pi)
 //   alpha = N.(v0-q) (= det(a,b,c)), beta grouped as _kernels.py:98-103.
-//   Common pairs (beta >= |alpha|, |alpha| >= eps|N|) need one MUFU.RCP and an
-//   8-term minimax polynomial; the rest go to exact_rare().
+//   Common pairs (|alpha| < beta/8: every far face) need one MUFU.RCP and a
+//   3-term polynomial; the rest (wide angles, on-surface candidates,
+//   degenerate faces) go to exact_rare().
 // Soft (replaces _kernels.soft_batch_f32, :312-349, and soft_batch, :119-158):
 //   term = N.(c-q) / |c-q|^3 with one MUFU.RSQ,  W = sum(term) / (8 pi);
 //   |c-q| < eps flags the point and skips the face.
@@ -84,11 +85,18 @@ struct ExactPol {
     const float g1 = fmaf(bc, la, la * (lb * lc));
     const float g2 = __fadd_rn(__fmul_rn(ab, lc), __fmul_rn(ca, lb));
     const float beta = g1 + g2;
-    const float aa = fabsf(alpha);
-    const bool r = (aa > beta) || (aa < R.v0e.w);
-    const float tt = r ? 0.0f : alpha * rcp_approx(beta);
-    tacc = fmaf(tt, atan_poly_coef(tt * tt), tacc);
-    return r;
+    // Common pairs: |theta| < atan(1/8) (|alpha| < beta/8, so beta > 0).  On
+    // a face's closed triangle beta <= 0 (on a vertex alpha = beta = 0), so
+    // every on-surface candidate fails this test and reaches exact_rare()
+    // (as do degenerate faces, N = 0); far faces -- nearly all pairs of a
+    // fine mesh -- stay here.  atan(t) = t (1 + s (c1 + c2 s)), s = t^2,
+    // |t| <= 1/8: relative error 1.2e-7 in fp32 (fit: DESIGN.md 3.5).
+    const bool common = fabsf(alpha) < 0.125f * beta;
+    const float tt = alpha * rcp_approx(beta);
+    const float s = tt * tt;
+    const float p = fmaf(fmaf(0.19669890403747559f, s, -0.33331409096717834f), s, 1.0f);
+    if (common) tacc = fmaf(tt, p, tacc);
+    return !common;
   }
   __device__ __forceinline__ static float rare(const Rec& R, float qx, float qy, float qz,
                                                float eps) {
