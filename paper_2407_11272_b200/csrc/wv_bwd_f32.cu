@@ -40,8 +40,16 @@ constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
 struct ExactEdgeBwd {
   using Rec = ExactGradRecF32;
   static constexpr int kMinBlocks = 4;
-  static constexpr double kCoefScale = -1.0 / (4.0 * kPi);
+  // -1/(4 pi) and the factor 2 of d = 2 (|a||b| + a.b) below
+  static constexpr double kCoefScale = -2.0 / (4.0 * kPi);
   static constexpr int kAcc = 9;
+  __device__ __forceinline__ static bool unit_weights(const Rec& R) {
+    return R.a.w == 1.0f && R.b.w == 1.0f && R.c.w == 1.0f;
+  }
+  // |a||b| + a.b = ((|a|+|b|)^2 - |P-Q|^2) / 2 (a.b = (|a|^2+|b|^2-|a-b|^2)/2,
+  // a-b = P-Q): no dot products, one FADD + one FFMA per edge, and the FFMA
+  // rounds (|a|+|b|)^2 - U once.
+  template <bool kUnit>
   __device__ __forceinline__ static void pair(const Rec& R, float qx, float qy, float qz,
                                               float coef, float, float, float* g) {
     const float ax = R.a.x - qx, ay = R.a.y - qy, az = R.a.z - qz;
@@ -51,13 +59,14 @@ struct ExactEdgeBwd {
     const float b2 = fmaf(bz, bz, fmaf(by, by, bx * bx));
     const float c2 = fmaf(cz, cz, fmaf(cy, cy, cx * cx));
     const float ia = rsqrt_approx(a2), ib = rsqrt_approx(b2), ic = rsqrt_approx(c2);
-    const float la = a2 * ia, lb = b2 * ib, lc = c2 * ic;
-    const float ab = fmaf(az, bz, fmaf(ay, by, ax * bx));
-    const float bc = fmaf(bz, cz, fmaf(by, cy, bx * cx));
-    const float ca = fmaf(az, cz, fmaf(ay, cy, ax * cx));
-    const float t01 = (coef * R.a.w) * rcp_approx(fmaf(la, lb, ab));
-    const float t12 = (coef * R.b.w) * rcp_approx(fmaf(lb, lc, bc));
-    const float t20 = (coef * R.c.w) * rcp_approx(fmaf(lc, la, ca));
+    const float lb = b2 * ib, lc = c2 * ic;
+    const float s01 = fmaf(a2, ia, lb), s12 = lb + lc, s20 = fmaf(a2, ia, lc);
+    const float r01 = rcp_approx(fmaf(s01, s01, -R.u.x));
+    const float r12 = rcp_approx(fmaf(s12, s12, -R.u.y));
+    const float r20 = rcp_approx(fmaf(s20, s20, -R.u.z));
+    const float t01 = (kUnit ? coef : coef * R.a.w) * r01;
+    const float t12 = (kUnit ? coef : coef * R.b.w) * r12;
+    const float t20 = (kUnit ? coef : coef * R.c.w) * r20;
     // m01 = a x b, m12 = b x c, m20 = c x a
     const float m01x = ay * bz - az * by, m01y = az * bx - ax * bz, m01z = ax * by - ay * bx;
     const float m12x = by * cz - bz * cy, m12y = bz * cx - bx * cz, m12z = bx * cy - by * cx;
@@ -79,11 +88,14 @@ struct ExactEdgeBwd {
     for (int j = 0; j < 9; ++j) out9[j] = acc[j];
   }
 };
+
 struct SoftBwd {
   using Rec = SoftGradRecF32;
   static constexpr int kMinBlocks = 4;
   static constexpr double kCoefScale = 1.0 / (8.0 * kPi);
   static constexpr int kAcc = 10;  // acc1(3) acc2(3) T(1) D(3)
+  __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
+  template <bool kUnit>
   __device__ __forceinline__ static void pair(const Rec& R, float qx, float qy, float qz,
                                               float coef, float, float eps2, float* g) {
     const float dx = R.c.x - qx, dy = R.c.y - qy, dz = R.c.z - qz;
@@ -124,6 +136,17 @@ struct SoftBwd {
   }
 };
 
+template <class Pol, bool kUnit>
+__device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const float4* chunk, int n,
+                                           float eps, float eps2, float* g) {
+#pragma unroll 2
+  for (int i = 0; i < n; ++i) {
+    const float4 q = chunk[i];
+    if (q.w == 0.0f) continue;  // warp-uniform: every lane reads the same point
+    Pol::template pair<kUnit>(R, q.x, q.y, q.z, q.w, eps, eps2, g);
+  }
+}
+
 template <class Pol, class Src>
 __global__ void __launch_bounds__(kBwdThreads, Pol::kMinBlocks)
 bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
@@ -139,6 +162,9 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   int64_t p_end = p_begin + pts_per_split;
   if (p_end > n_count) p_end = n_count;
 
+  // warp-uniform fast path when every face of the warp has unit edge
+  // weights (soups, boundary strips): saves the per-edge weight multiply
+  const bool unit = __all_sync(0xffffffffu, Pol::unit_weights(R));
   double acc[Pol::kAcc];
 #pragma unroll
   for (int j = 0; j < Pol::kAcc; ++j) acc[j] = 0.0;
@@ -155,11 +181,10 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     float g[Pol::kAcc];
 #pragma unroll
     for (int j = 0; j < Pol::kAcc; ++j) g[j] = 0.0f;
-#pragma unroll 2
-    for (int i = 0; i < n; ++i) {
-      const float4 q = chunk[i];
-      if (q.w == 0.0f) continue;  // warp-uniform: every lane reads the same point
-      Pol::pair(R, q.x, q.y, q.z, q.w, eps, eps2, g);
+    if (unit) {
+      chunk_loop<Pol, true>(R, chunk, n, eps, eps2, g);
+    } else {
+      chunk_loop<Pol, false>(R, chunk, n, eps, eps2, g);
     }
 #pragma unroll
     for (int j = 0; j < Pol::kAcc; ++j) acc[j] += (double)g[j];

@@ -58,8 +58,9 @@ struct __align__(16) ExactGradRecF32 {
   float4 a;  // v0.xyz, w01
   float4 b;  // v1.xyz, w12
   float4 c;  // v2.xyz, w20
+  float4 u;  // squared edge lengths |v1-v0|^2, |v2-v1|^2, |v0-v2|^2 (from f64), 0
 };
-static_assert(sizeof(ExactGradRecF32) == 48, "record size");
+static_assert(sizeof(ExactGradRecF32) == 64, "record size");
 
 struct __align__(16) ExactGradRecF64 {
   double v[9];

@@ -171,6 +171,13 @@ __global__ void pack_exact_grad_kernel(int kind, const V* __restrict__ verts,
       r->a = make_float4((float)v0[0], (float)v0[1], (float)v0[2], weights[3 * i + 0]);
       r->b = make_float4((float)v1[0], (float)v1[1], (float)v1[2], weights[3 * i + 1]);
       r->c = make_float4((float)v2[0], (float)v2[1], (float)v2[2], weights[3 * i + 2]);
+      double U[3] = {0.0, 0.0, 0.0};
+      for (int d = 0; d < 3; ++d) {
+        U[0] += (v1[d] - v0[d]) * (v1[d] - v0[d]);
+        U[1] += (v2[d] - v1[d]) * (v2[d] - v1[d]);
+        U[2] += (v0[d] - v2[d]) * (v0[d] - v2[d]);
+      }
+      r->u = make_float4((float)U[0], (float)U[1], (float)U[2], 0.0f);
     } else {
       ExactGradRecF64* r = static_cast<ExactGradRecF64*>(recs) + i;
       for (int d = 0; d < 3; ++d) {

@@ -94,6 +94,10 @@ def exact_edge_weights(faces: np.ndarray, dead: np.ndarray | None = None):
     w[first] = (net * sgn[first]).astype(np.float32)   # sgn[first] in {+1,-1,0}
     w = w.reshape(nf, 3)
     active = np.flatnonzero(np.any(w != 0, axis=1)).astype(np.int64)
+    # unit-weight faces first: the kernel takes a warp-uniform fast path when
+    # all 32 faces of a warp have unit weights
+    unit = np.all(w[active] == 1, axis=1)
+    active = np.concatenate([active[unit], active[~unit]])
     return active, np.ascontiguousarray(w[active])
 
 

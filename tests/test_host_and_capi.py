@@ -34,7 +34,7 @@ def test_packed_sizes():
     assert lib.wv_packed_bytes(1, 10) == 64 + 10 * 64
     assert lib.wv_packed_bytes(2, 10) == 64 + 10 * 32
     assert lib.wv_packed_bytes(3, 10) == 64 + 10 * 128
-    assert lib.wv_packed_bytes(7, 10) == 64 + 10 * 48
+    assert lib.wv_packed_bytes(7, 10) == 64 + 10 * 64
     assert lib.wv_packed_bytes(99, 10) == 0
 
 
