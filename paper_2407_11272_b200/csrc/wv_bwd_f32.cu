@@ -19,6 +19,7 @@
 //   G_2 = d x u, G_0 = -G_1 - G_2; the N/3 and d terms are shared by the three
 //   corners, so they are accumulated once per face.
 // Per-chunk fp32 partials are folded into fp64 accumulators.
+#include "wv_f32x2.cuh"
 #include "wv_kernels.h"
 
 namespace wv {
@@ -46,43 +47,47 @@ struct ExactEdgeBwd {
   __device__ __forceinline__ static bool unit_weights(const Rec& R) {
     return R.a.w == 1.0f && R.b.w == 1.0f && R.c.w == 1.0f;
   }
-  // |a||b| + a.b = ((|a|+|b|)^2 - |P-Q|^2) / 2 (a.b = (|a|^2+|b|^2-|a-b|^2)/2,
-  // a-b = P-Q): no dot products, one FADD + one FFMA per edge, and the FFMA
-  // rounds (|a|+|b|)^2 - U once.
+  // Two query points per instruction (packed f32x2).  |a||b| + a.b =
+  // ((|a|+|b|)^2 - |P-Q|^2) / 2  (a.b = (|a|^2+|b|^2-|a-b|^2)/2, a-b = P-Q):
+  // no dot products, one FADD + one FFMA per edge, and the FFMA rounds
+  // (|a|+|b|)^2 - U once.
   template <bool kUnit>
-  __device__ __forceinline__ static void pair(const Rec& R, float qx, float qy, float qz,
-                                              float coef, float, float, float* g) {
-    const float ax = R.a.x - qx, ay = R.a.y - qy, az = R.a.z - qz;
-    const float bx = R.b.x - qx, by = R.b.y - qy, bz = R.b.z - qz;
-    const float cx = R.c.x - qx, cy = R.c.y - qy, cz = R.c.z - qz;
-    const float a2 = fmaf(az, az, fmaf(ay, ay, ax * ax));
-    const float b2 = fmaf(bz, bz, fmaf(by, by, bx * bx));
-    const float c2 = fmaf(cz, cz, fmaf(cy, cy, cx * cx));
-    const float ia = rsqrt_approx(a2), ib = rsqrt_approx(b2), ic = rsqrt_approx(c2);
-    const float lb = b2 * ib, lc = c2 * ic;
-    const float s01 = fmaf(a2, ia, lb), s12 = lb + lc, s20 = fmaf(a2, ia, lc);
-    const float r01 = rcp_approx(fmaf(s01, s01, -R.u.x));
-    const float r12 = rcp_approx(fmaf(s12, s12, -R.u.y));
-    const float r20 = rcp_approx(fmaf(s20, s20, -R.u.z));
-    const float t01 = (kUnit ? coef : coef * R.a.w) * r01;
-    const float t12 = (kUnit ? coef : coef * R.b.w) * r12;
-    const float t20 = (kUnit ? coef : coef * R.c.w) * r20;
+  __device__ __forceinline__ static void pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                               float, F2* g) {
+    const F2 ax = sub2(f2s(R.a.x), qx), ay = sub2(f2s(R.a.y), qy), az = sub2(f2s(R.a.z), qz);
+    const F2 bx = sub2(f2s(R.b.x), qx), by = sub2(f2s(R.b.y), qy), bz = sub2(f2s(R.b.z), qz);
+    const F2 cx = sub2(f2s(R.c.x), qx), cy = sub2(f2s(R.c.y), qy), cz = sub2(f2s(R.c.z), qz);
+    const F2 a2 = dot2(ax, ay, az, ax, ay, az);
+    const F2 b2 = dot2(bx, by, bz, bx, by, bz);
+    const F2 c2 = dot2(cx, cy, cz, cx, cy, cz);
+    const F2 ia = rsqrt2(a2), ib = rsqrt2(b2), ic = rsqrt2(c2);
+    const F2 lb = mul2(b2, ib), lc = mul2(c2, ic);
+    const F2 s01 = fma2(a2, ia, lb), s12 = add2(lb, lc), s20 = fma2(a2, ia, lc);
+    const F2 r01 = rcp2(fma2(s01, s01, f2s(-R.u.x)));
+    const F2 r12 = rcp2(fma2(s12, s12, f2s(-R.u.y)));
+    const F2 r20 = rcp2(fma2(s20, s20, f2s(-R.u.z)));
+    const F2 t01 = mul2(kUnit ? coef : mul2(coef, f2s(R.a.w)), r01);
+    const F2 t12 = mul2(kUnit ? coef : mul2(coef, f2s(R.b.w)), r12);
+    const F2 t20 = mul2(kUnit ? coef : mul2(coef, f2s(R.c.w)), r20);
     // m01 = a x b, m12 = b x c, m20 = c x a
-    const float m01x = ay * bz - az * by, m01y = az * bx - ax * bz, m01z = ax * by - ay * bx;
-    const float m12x = by * cz - bz * cy, m12y = bz * cx - bx * cz, m12z = bx * cy - by * cx;
-    const float m20x = cy * az - cz * ay, m20y = cz * ax - cx * az, m20z = cx * ay - cy * ax;
-    const float s01a = t01 * ia, s20a = t20 * ia;  // v0 is P of 01, Q of 20
-    const float s01b = t01 * ib, s12b = t12 * ib;  // v1 is Q of 01, P of 12
-    const float s12c = t12 * ic, s20c = t20 * ic;  // v2 is Q of 12, P of 20
-    g[0] = fmaf(m20x, s20a, fmaf(m01x, s01a, g[0]));
-    g[1] = fmaf(m20y, s20a, fmaf(m01y, s01a, g[1]));
-    g[2] = fmaf(m20z, s20a, fmaf(m01z, s01a, g[2]));
-    g[3] = fmaf(m12x, s12b, fmaf(m01x, s01b, g[3]));
-    g[4] = fmaf(m12y, s12b, fmaf(m01y, s01b, g[4]));
-    g[5] = fmaf(m12z, s12b, fmaf(m01z, s01b, g[5]));
-    g[6] = fmaf(m20x, s20c, fmaf(m12x, s12c, g[6]));
-    g[7] = fmaf(m20y, s20c, fmaf(m12y, s12c, g[7]));
-    g[8] = fmaf(m20z, s20c, fmaf(m12z, s12c, g[8]));
+    const F2 m01x = sub2(mul2(ay, bz), mul2(az, by)), m01y = sub2(mul2(az, bx), mul2(ax, bz)),
+             m01z = sub2(mul2(ax, by), mul2(ay, bx));
+    const F2 m12x = sub2(mul2(by, cz), mul2(bz, cy)), m12y = sub2(mul2(bz, cx), mul2(bx, cz)),
+             m12z = sub2(mul2(bx, cy), mul2(by, cx));
+    const F2 m20x = sub2(mul2(cy, az), mul2(cz, ay)), m20y = sub2(mul2(cz, ax), mul2(cx, az)),
+             m20z = sub2(mul2(cx, ay), mul2(cy, ax));
+    const F2 s01a = mul2(t01, ia), s20a = mul2(t20, ia);  // v0 is P of 01, Q of 20
+    const F2 s01b = mul2(t01, ib), s12b = mul2(t12, ib);  // v1 is Q of 01, P of 12
+    const F2 s12c = mul2(t12, ic), s20c = mul2(t20, ic);  // v2 is Q of 12, P of 20
+    g[0] = fma2(m20x, s20a, fma2(m01x, s01a, g[0]));
+    g[1] = fma2(m20y, s20a, fma2(m01y, s01a, g[1]));
+    g[2] = fma2(m20z, s20a, fma2(m01z, s01a, g[2]));
+    g[3] = fma2(m12x, s12b, fma2(m01x, s01b, g[3]));
+    g[4] = fma2(m12y, s12b, fma2(m01y, s01b, g[4]));
+    g[5] = fma2(m12z, s12b, fma2(m01z, s01b, g[5]));
+    g[6] = fma2(m20x, s20c, fma2(m12x, s12c, g[6]));
+    g[7] = fma2(m20y, s20c, fma2(m12y, s12c, g[7]));
+    g[8] = fma2(m20z, s20c, fma2(m12z, s12c, g[8]));
   }
   __device__ __forceinline__ static void finish(const Rec&, const double* acc, double* out9) {
     for (int j = 0; j < 9; ++j) out9[j] = acc[j];
@@ -96,30 +101,36 @@ struct SoftBwd {
   static constexpr int kAcc = 10;  // acc1(3) acc2(3) T(1) D(3)
   __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
   template <bool kUnit>
-  __device__ __forceinline__ static void pair(const Rec& R, float qx, float qy, float qz,
-                                              float coef, float, float eps2, float* g) {
-    const float dx = R.c.x - qx, dy = R.c.y - qy, dz = R.c.z - qz;
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const float rs = rsqrt_approx(r2);
-    const float S = fmaf(R.n.z, dz, fmaf(R.n.y, dy, R.n.x * dx));
-    const float rs2 = rs * rs;
-    const float c3 = (r2 < eps2) ? 0.0f : coef * rs2 * rs;  // r < eps: skipped (:203-204)
-    const float c5 = c3 * S * rs2;
+  __device__ __forceinline__ static void pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                               float eps2, F2* g) {
+    const F2 dx = sub2(f2s(R.c.x), qx), dy = sub2(f2s(R.c.y), qy), dz = sub2(f2s(R.c.z), qz);
+    const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
+    const F2 rs = rsqrt2(r2);
+    const F2 S = fma2(f2s(R.n.z), dz, fma2(f2s(R.n.y), dy, mul2(f2s(R.n.x), dx)));
+    const F2 rs2 = mul2(rs, rs);
+    float r2l, r2h, cl, ch;
+    split(r2, r2l, r2h);
+    split(mul2(mul2(coef, rs2), rs), cl, ch);
+    // r < eps: that face is skipped for that point (_kernels.py:203-204)
+    const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
+    const F2 c5 = mul2(mul2(c3, S), rs2);
     // G1 = w x d, G2 = d x u
-    const float g1x = R.w.y * dz - R.w.z * dy, g1y = R.w.z * dx - R.w.x * dz,
-                g1z = R.w.x * dy - R.w.y * dx;
-    const float g2x = dy * R.u.z - dz * R.u.y, g2y = dz * R.u.x - dx * R.u.z,
-                g2z = dx * R.u.y - dy * R.u.x;
-    g[0] = fmaf(c3, g1x, g[0]);
-    g[1] = fmaf(c3, g1y, g[1]);
-    g[2] = fmaf(c3, g1z, g[2]);
-    g[3] = fmaf(c3, g2x, g[3]);
-    g[4] = fmaf(c3, g2y, g[4]);
-    g[5] = fmaf(c3, g2z, g[5]);
-    g[6] += c3;
-    g[7] = fmaf(c5, dx, g[7]);
-    g[8] = fmaf(c5, dy, g[8]);
-    g[9] = fmaf(c5, dz, g[9]);
+    const F2 g1x = sub2(mul2(f2s(R.w.y), dz), mul2(f2s(R.w.z), dy));
+    const F2 g1y = sub2(mul2(f2s(R.w.z), dx), mul2(f2s(R.w.x), dz));
+    const F2 g1z = sub2(mul2(f2s(R.w.x), dy), mul2(f2s(R.w.y), dx));
+    const F2 g2x = sub2(mul2(dy, f2s(R.u.z)), mul2(dz, f2s(R.u.y)));
+    const F2 g2y = sub2(mul2(dz, f2s(R.u.x)), mul2(dx, f2s(R.u.z)));
+    const F2 g2z = sub2(mul2(dx, f2s(R.u.y)), mul2(dy, f2s(R.u.x)));
+    g[0] = fma2(c3, g1x, g[0]);
+    g[1] = fma2(c3, g1y, g[1]);
+    g[2] = fma2(c3, g1z, g[2]);
+    g[3] = fma2(c3, g2x, g[3]);
+    g[4] = fma2(c3, g2y, g[4]);
+    g[5] = fma2(c3, g2z, g[5]);
+    g[6] = add2(g[6], c3);
+    g[7] = fma2(c5, dx, g[7]);
+    g[8] = fma2(c5, dy, g[8]);
+    g[9] = fma2(c5, dz, g[9]);
   }
   __device__ __forceinline__ static void finish(const Rec& R, const double* a, double* out9) {
     const double t = a[6] / 3.0;
@@ -136,14 +147,24 @@ struct SoftBwd {
   }
 };
 
+// Query points of a chunk, stored as packed PAIRS: xy[j] = {x_2j, x_2j+1,
+// y_2j, y_2j+1}, zc[j] = {z_2j, z_2j+1, coef_2j, coef_2j+1}; two LDS.128
+// deliver one point pair already in f32x2 register pairs.
+struct PointChunk {
+  float4 xy[kBwdChunk / 2];
+  float4 zc[kBwdChunk / 2];
+};
+
 template <class Pol, bool kUnit>
-__device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const float4* chunk, int n,
-                                           float eps, float eps2, float* g) {
+__device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const PointChunk& ch,
+                                           int n_pairs, float eps2, F2* g) {
 #pragma unroll 2
-  for (int i = 0; i < n; ++i) {
-    const float4 q = chunk[i];
-    if (q.w == 0.0f) continue;  // warp-uniform: every lane reads the same point
-    Pol::template pair<kUnit>(R, q.x, q.y, q.z, q.w, eps, eps2, g);
+  for (int j = 0; j < n_pairs; ++j) {
+    const float4 zc = ch.zc[j];
+    if (zc.z == 0.0f && zc.w == 0.0f) continue;  // warp-uniform (_kernels.py:182-184)
+    const float4 xy = ch.xy[j];
+    Pol::template pair2<kUnit>(R, f2(xy.x, xy.y), f2(xy.z, xy.w), f2(zc.x, zc.y),
+                               f2(zc.z, zc.w), eps2, g);
   }
 }
 
@@ -152,7 +173,7 @@ __global__ void __launch_bounds__(kBwdThreads, Pol::kMinBlocks)
 bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
                int64_t n_faces, Src src, const float* __restrict__ coefs, int64_t n_count,
                int64_t pts_per_split, float coef_scale, double* __restrict__ out) {
-  __shared__ float4 chunk[kBwdChunk];
+  __shared__ PointChunk chunk;
   const int64_t f = (int64_t)blockIdx.x * kBwdThreads + threadIdx.x;
   const bool live = f < n_faces;
   typename Pol::Rec R = recs[live ? f : 0];
@@ -171,23 +192,38 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 
   for (int64_t c0 = p_begin; c0 < p_end; c0 += kBwdChunk) {
     const int n = (int)((p_end - c0) < kBwdChunk ? (p_end - c0) : kBwdChunk);
+    const int n_pairs = (n + 1) / 2;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += kBwdThreads) {
-      float x, y, z;
-      src.point(c0 + i, x, y, z);
-      chunk[i] = make_float4(x, y, z, coefs[c0 + i] * coef_scale);
+    for (int i = threadIdx.x; i < 2 * n_pairs; i += kBwdThreads) {
+      float x = 1.0e6f, y = 1.0e6f, z = 1.0e6f, c = 0.0f;
+      if (i < n) {
+        c = coefs[c0 + i] * coef_scale;
+        // zero-coefficient points contribute nothing; park them far away so
+        // the other half of their pair never sees an on-segment 0 * inf
+        if (c != 0.0f) src.point(c0 + i, x, y, z);
+      }
+      float* xy = reinterpret_cast<float*>(&chunk.xy[i >> 1]);
+      float* zc = reinterpret_cast<float*>(&chunk.zc[i >> 1]);
+      xy[i & 1] = x;
+      xy[2 + (i & 1)] = y;
+      zc[i & 1] = z;
+      zc[2 + (i & 1)] = c;
     }
     __syncthreads();
-    float g[Pol::kAcc];
+    F2 g[Pol::kAcc];
 #pragma unroll
-    for (int j = 0; j < Pol::kAcc; ++j) g[j] = 0.0f;
+    for (int j = 0; j < Pol::kAcc; ++j) g[j] = f2(0.0f, 0.0f);
     if (unit) {
-      chunk_loop<Pol, true>(R, chunk, n, eps, eps2, g);
+      chunk_loop<Pol, true>(R, chunk, n_pairs, eps2, g);
     } else {
-      chunk_loop<Pol, false>(R, chunk, n, eps, eps2, g);
+      chunk_loop<Pol, false>(R, chunk, n_pairs, eps2, g);
     }
 #pragma unroll
-    for (int j = 0; j < Pol::kAcc; ++j) acc[j] += (double)g[j];
+    for (int j = 0; j < Pol::kAcc; ++j) {
+      float lo, hi;
+      split(g[j], lo, hi);
+      acc[j] += (double)lo + (double)hi;
+    }
   }
   if (live) {
     double o9[9];
@@ -197,7 +233,6 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     for (int j = 0; j < 9; ++j) dst[j] = o9[j];
   }
 }
-
 // out[f*9+j] = sum_s part[s][f*9+j], fixed split order
 __global__ void reduce_splits_kernel(const double* __restrict__ part, int splits, int64_t n,
                                      double* __restrict__ out) {

@@ -12,6 +12,7 @@
 //  * per tile the terms are summed in fp32, tile partials in fp64.
 #pragma once
 
+#include "wv_f32x2.cuh"
 #include "wv_kernels.h"
 
 namespace wv {
@@ -36,14 +37,22 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   const float eps = hdr->eps_f32;
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * (NC * P);
-  float qx[P], qy[P], qz[P];
+  constexpr int PP = P / 2;  // point pairs (packed f32x2)
+  F2 qx[PP], qy[PP], qz[PP];
   double accd[P];
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    int64_t l = base + p * NC + tid;
-    if (l >= n_count) l = n_count - 1;  // padded lanes recompute a valid node
-    src.point(l, qx[p], qy[p], qz[p]);
-    accd[p] = 0.0;
+  for (int pp = 0; pp < PP; ++pp) {
+    float x[2], y[2], z[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int64_t l = base + (2 * pp + h) * NC + tid;
+      if (l >= n_count) l = n_count - 1;  // padded lanes recompute a valid node
+      src.point(l, x[h], y[h], z[h]);
+      accd[2 * pp + h] = 0.0;
+    }
+    qx[pp] = f2(x[0], x[1]);
+    qy[pp] = f2(y[0], y[1]);
+    qz[pp] = f2(z[0], z[1]);
   }
   typename Pol::Ctx ctx = Pol::make_ctx(eps);
   uint32_t hits = 0;
@@ -55,31 +64,40 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     const int64_t first = t * TILE;
     const int cnt = (int)((n_faces - first) < TILE ? (n_faces - first) : TILE);
     const Rec* tile = ring.tiles[s];
-    float tacc[P];
+    F2 tacc[PP];
 #pragma unroll
-    for (int p = 0; p < P; ++p) tacc[p] = 0.0f;
+    for (int pp = 0; pp < PP; ++pp) tacc[pp] = f2(0.0f, 0.0f);
 
 #pragma unroll 1
     for (int f = 0; f < cnt; ++f) {
       const Rec R = tile[f];
       uint32_t rare = 0;
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        if (Pol::common(R, qx[p], qy[p], qz[p], ctx, tacc[p])) rare |= 1u << p;
-      }
+      for (int pp = 0; pp < PP; ++pp)
+        rare |= Pol::common2(R, qx[pp], qy[pp], qz[pp], ctx, tacc[pp]) << (2 * pp);
       if (rare != 0u) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           if (rare & (1u << p)) {
-            const float th = Pol::rare(R, qx[p], qy[p], qz[p], eps);
+            float xl, xh, yl, yh, zl, zh;
+            split(qx[p / 2], xl, xh);
+            split(qy[p / 2], yl, yh);
+            split(qz[p / 2], zl, zh);
+            const bool hi = p & 1;
+            const float th = Pol::rare(R, hi ? xh : xl, hi ? yh : yl, hi ? zh : zl, eps);
             if (th != th) hits |= 1u << p;  // NaN marks an on-surface pair
-            else tacc[p] += th;
+            else tacc[p / 2] = add2(tacc[p / 2], hi ? f2(0.0f, th) : f2(th, 0.0f));
           }
         }
       }
     }
 #pragma unroll
-    for (int p = 0; p < P; ++p) accd[p] += (double)tacc[p];
+    for (int pp = 0; pp < PP; ++pp) {
+      float lo, hi;
+      split(tacc[pp], lo, hi);
+      accd[2 * pp] += (double)lo;
+      accd[2 * pp + 1] += (double)hi;
+    }
     __syncwarp();
     if ((tid & 31) == 0) ring_release(ring, s, CW, recs, n_faces, t, t_end);
   }

@@ -56,6 +56,9 @@ __device__ __noinline__ float exact_rare(float4 A, float4 B, float4 C, float4 N,
   return atan2_full(alpha, beta);
 }
 
+// Both policies evaluate TWO query points per instruction (packed f32x2, see
+// wv_f32x2.cuh) against one face; common2 returns a 2-bit mask of the pairs
+// that must go to the rare path (they contribute nothing here).
 struct ExactPol {
   using Rec = ExactRecF32;
   static constexpr int kTile = 128;
@@ -67,36 +70,39 @@ struct ExactPol {
   static constexpr double kScale = 1.0 / (2.0 * kPi);
   struct Ctx {};
   __device__ static Ctx make_ctx(float) { return Ctx{}; }
-  // returns true when the pair must go to the rare path (contributes 0 here)
-  __device__ __forceinline__ static bool common(const Rec& R, float qx, float qy, float qz,
-                                                const Ctx&, float& tacc) {
-    const float ax = R.v0e.x - qx, ay = R.v0e.y - qy, az = R.v0e.z - qz;
-    const float bx = R.v1.x - qx, by = R.v1.y - qy, bz = R.v1.z - qz;
-    const float cx = R.v2.x - qx, cy = R.v2.y - qy, cz = R.v2.z - qz;
-    const float alpha = fmaf(R.n.z, az, fmaf(R.n.y, ay, R.n.x * ax));
-    const float la = sqrt_approx(fmaf(az, az, fmaf(ay, ay, ax * ax)));
-    const float lb = sqrt_approx(fmaf(bz, bz, fmaf(by, by, bx * bx)));
-    const float lc = sqrt_approx(fmaf(cz, cz, fmaf(cy, cy, cx * cx)));
-    const float ab = fmaf(az, bz, fmaf(ay, by, ax * bx));
-    const float bc = fmaf(bz, cz, fmaf(by, cy, bx * cx));
-    const float ca = fmaf(az, cz, fmaf(ay, cy, ax * cx));
-    // beta grouped as _kernels.py:98-103: swapping v1<->v2 leaves it
-    // bit-identical, so orientation flips negate W exactly.
-    const float g1 = fmaf(bc, la, la * (lb * lc));
-    const float g2 = __fadd_rn(__fmul_rn(ab, lc), __fmul_rn(ca, lb));
-    const float beta = g1 + g2;
+  __device__ __forceinline__ static uint32_t common2(const Rec& R, F2 qx, F2 qy, F2 qz,
+                                                     const Ctx&, F2& tacc) {
+    const F2 ax = sub2(f2s(R.v0e.x), qx), ay = sub2(f2s(R.v0e.y), qy), az = sub2(f2s(R.v0e.z), qz);
+    const F2 bx = sub2(f2s(R.v1.x), qx), by = sub2(f2s(R.v1.y), qy), bz = sub2(f2s(R.v1.z), qz);
+    const F2 cx = sub2(f2s(R.v2.x), qx), cy = sub2(f2s(R.v2.y), qy), cz = sub2(f2s(R.v2.z), qz);
+    // alpha = N.(v0-q) = det(a,b,c)
+    const F2 alpha = fma2(f2s(R.n.z), az, fma2(f2s(R.n.y), ay, mul2(f2s(R.n.x), ax)));
+    const F2 la = sqrt2(dot2(ax, ay, az, ax, ay, az));
+    const F2 lb = sqrt2(dot2(bx, by, bz, bx, by, bz));
+    const F2 lc = sqrt2(dot2(cx, cy, cz, cx, cy, cz));
+    const F2 ab = dot2(ax, ay, az, bx, by, bz);
+    const F2 bc = dot2(bx, by, bz, cx, cy, cz);
+    const F2 ca = dot2(ax, ay, az, cx, cy, cz);
+    // beta = |a||b||c| + (b.c)|a| + (a.b)|c| + (c.a)|b|  (_kernels.py:98-103)
+    const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, mul2(la, mul2(lb, lc)))));
     // Common pairs: |theta| < atan(1/8) (|alpha| < beta/8, so beta > 0).  On
     // a face's closed triangle beta <= 0 (on a vertex alpha = beta = 0), so
-    // every on-surface candidate fails this test and reaches exact_rare()
-    // (as do degenerate faces, N = 0); far faces -- nearly all pairs of a
-    // fine mesh -- stay here.  atan(t) = t (1 + s (c1 + c2 s)), s = t^2,
+    // every on-surface candidate fails this test and reaches exact_rare(), as
+    // do degenerate faces (N = 0); far faces -- nearly all pairs of a fine
+    // mesh -- stay here.  atan(t) = t (1 + s (c1 + c2 s)), s = t^2,
     // |t| <= 1/8: relative error 1.2e-7 in fp32 (fit: DESIGN.md 3.5).
-    const bool common = fabsf(alpha) < 0.125f * beta;
-    const float tt = alpha * rcp_approx(beta);
-    const float s = tt * tt;
-    const float p = fmaf(fmaf(0.19669890403747559f, s, -0.33331409096717834f), s, 1.0f);
-    if (common) tacc = fmaf(tt, p, tacc);
-    return !common;
+    float al, ah, bl, bh;
+    split(alpha, al, ah);
+    split(beta, bl, bh);
+    const bool cl = fabsf(al) < 0.125f * bl, ch = fabsf(ah) < 0.125f * bh;
+    const F2 tt = mul2(alpha, rcp2(beta));
+    const F2 s = mul2(tt, tt);
+    const F2 p = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
+                      f2s(1.0f));
+    float tl, th;
+    split(tt, tl, th);
+    tacc = fma2(f2(cl ? tl : 0.0f, ch ? th : 0.0f), p, tacc);
+    return (cl ? 0u : 1u) | (ch ? 0u : 2u);
   }
   __device__ __forceinline__ static float rare(const Rec& R, float qx, float qy, float qz,
                                                float eps) {
@@ -117,22 +123,26 @@ struct SoftPol {
     float eps2;
   };
   __device__ static Ctx make_ctx(float eps) { return Ctx{eps * eps}; }
-  __device__ __forceinline__ static bool common(const Rec& R, float qx, float qy, float qz,
-                                                const Ctx& ctx, float& tacc) {
-    const float dx = R.c.x - qx, dy = R.c.y - qy, dz = R.c.z - qz;
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const float rs = rsqrt_approx(r2);
-    const float s = fmaf(R.n.y, dz, fmaf(R.n.x, dy, R.c.w * dx));
-    const bool h = r2 < ctx.eps2;  // |c - q| < eps: on a centroid (_kernels.py:150)
-    const float rs3 = h ? 0.0f : rs * rs * rs;
-    tacc = fmaf(s, rs3, tacc);
-    return h;
+  __device__ __forceinline__ static uint32_t common2(const Rec& R, F2 qx, F2 qy, F2 qz,
+                                                     const Ctx& ctx, F2& tacc) {
+    const F2 dx = sub2(f2s(R.c.x), qx), dy = sub2(f2s(R.c.y), qy), dz = sub2(f2s(R.c.z), qz);
+    const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
+    const F2 s = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
+    float r2l, r2h;
+    split(r2, r2l, r2h);
+    // |c - q| < eps: on a centroid, the face is skipped and the point flagged
+    // (_kernels.py:150-152)
+    const bool hl = r2l < ctx.eps2, hh = r2h < ctx.eps2;
+    float rl, rh;
+    split(rsqrt2(r2), rl, rh);
+    const F2 rs = f2(hl ? 0.0f : rl, hh ? 0.0f : rh);
+    tacc = fma2(s, mul2(rs, mul2(rs, rs)), tacc);
+    return (hl ? 1u : 0u) | (hh ? 2u : 0u);
   }
   __device__ __forceinline__ static float rare(const Rec&, float, float, float, float) {
     return __int_as_float(0x7fc00000);  // always an on-surface (flagged) pair
   }
 };
-
 // Sum split partials in split order (deterministic), then W = sum * scale.
 __global__ void finalize_theta_kernel(const double* __restrict__ part,
                                       const uint8_t* __restrict__ pflags, int splits,
