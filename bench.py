@@ -72,6 +72,21 @@ def peaks():
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, src
 
 
+def measured_fp32_peak():
+    """FP32 FMA throughput measured on this GPU by tools/ffma2_probe (16
+    independent FMA chains per thread, FFMA and packed FFMA2), TFLOP/s."""
+    import subprocess
+    exe = ROOT / "tools" / "ffma2_probe"
+    if not exe.exists():
+        return None
+    try:
+        out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout
+        vals = [float(line.split()[-2]) for line in out.splitlines() if "TFLOP/s" in line]
+        return max(vals) if vals else None
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clock / throttle reasons sampled (NVML) DURING the timed region."""
 
@@ -259,6 +274,7 @@ def run_ours(args):
     launches = (2 + 1 + (1 if L.lib().wv_fwd_workspace_bytes(1, F, cnt) else 0) + 2 + 2 + 1
                 + (1 if L.lib().wv_bwd_workspace_bytes(7, active, cnt) else 0) + 1)
 
+    fp32_meas = measured_fp32_peak() if rank == 0 else None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -321,7 +337,9 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         fwd_tf = EXACT_FWD_FLOPS * cnt * F / (fwd_ms / 1e3) / 1e12
-        bwd_tf = EXACT_BWD_FLOPS * cnt * F / (bwd_ms / 1e3) / 1e12
+        # the exact backward launches only faces with a non-cancelling edge
+        # (all of them for a soup): count the pairs it actually evaluates
+        bwd_tf = EXACT_BWD_FLOPS * cnt * active / (bwd_ms / 1e3) / 1e12
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as orc
@@ -356,7 +374,12 @@ def run_ours(args):
                          "flops_per_pair": EXACT_BWD_FLOPS if dom[0].startswith("exact_bwd")
                          else EXACT_FWD_FLOPS,
                          "peak_source": f"FP32 CUDA-core peak 148 SM x 128 lanes x 2 x clock "
-                                        f"({peak_src}); MEASURED_PEAKS has no FP32 entry"},
+                                        f"({peak_src}); MEASURED_PEAKS has no FP32 entry",
+                         "peak_measured": fp32_meas,
+                         "peak_measured_source": "tools/ffma2_probe (FFMA/FFMA2 chains, this "
+                                                 "GPU, before the timed region)",
+                         "traffic_note": "dram bytes per launch from ncu --set full: "
+                                         "profiles/README.md (MB-scale, negligible)"},
             "roofline_fwd": {"achieved": fwd_tf, "frac": fwd_tf / peak, "kernel_ms": fwd_ms},
             "roofline_bwd": {"achieved": bwd_tf, "frac": bwd_tf / peak, "kernel_ms": bwd_ms},
             "cpu_baseline": cpu,

@@ -73,6 +73,16 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     return LIB
 
 
+def build_probe() -> Path:
+    """tools/ffma2_probe: the FP32 peak microbenchmark bench.py reports."""
+    src = PKG.parent / "tools" / "ffma2_probe.cu"
+    exe = src.with_suffix("")
+    if _stale(exe, [src]):
+        subprocess.run([_nvcc(), *ARCH, "-O3", "-o", str(exe), str(src)], check=True)
+    return exe
+
+
 if __name__ == "__main__":
     build(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
+    build_probe()
     print(LIB)
