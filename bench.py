@@ -40,6 +40,13 @@ sys.path.insert(0, str(ROOT))
 # algorithmic work per point-triangle pair
 EXACT_FWD_FLOPS = 63
 EXACT_BWD_FLOPS = 170
+# FP32 FLOPs the kernels actually EXECUTE per pair (FMA = 2), counted from the
+# SASS of the inner loops (profiles/README.md): the forward follows the
+# pinned VOS count; the backward's edge (Biot-Savart) form needs fewer
+# operations than the pinned face-wise closed form, which is why its
+# algorithmic-FLOP rate can reach the FP32 peak.
+EXACT_FWD_EXEC_FLOPS = 61
+EXACT_BWD_EXEC_FLOPS = 104
 
 
 def parse():
@@ -380,8 +387,19 @@ def run_ours(args):
                                                  "GPU, before the timed region)",
                          "traffic_note": "dram bytes per launch from ncu --set full: "
                                          "profiles/README.md (MB-scale, negligible)"},
-            "roofline_fwd": {"achieved": fwd_tf, "frac": fwd_tf / peak, "kernel_ms": fwd_ms},
-            "roofline_bwd": {"achieved": bwd_tf, "frac": bwd_tf / peak, "kernel_ms": bwd_ms},
+            "roofline_fwd": {"achieved": fwd_tf, "frac": fwd_tf / peak, "kernel_ms": fwd_ms,
+                             "executed_flops_per_pair": EXACT_FWD_EXEC_FLOPS,
+                             "frac_executed": fwd_tf * EXACT_FWD_EXEC_FLOPS / EXACT_FWD_FLOPS
+                             / peak},
+            "roofline_bwd": {"achieved": bwd_tf, "frac": bwd_tf / peak, "kernel_ms": bwd_ms,
+                             "executed_flops_per_pair": EXACT_BWD_EXEC_FLOPS,
+                             "frac_executed": bwd_tf * EXACT_BWD_EXEC_FLOPS / EXACT_BWD_FLOPS
+                             / peak},
+            "roofline_step": {"achieved": (EXACT_FWD_FLOPS + EXACT_BWD_FLOPS) * w.pairs
+                              / (ms_step / 1e3) / 1e12,
+                              "frac": (EXACT_FWD_FLOPS + EXACT_BWD_FLOPS) * w.pairs
+                              / (ms_step / 1e3) / 1e12 / peak,
+                              "note": "whole fwd+bwd step at the pinned 233 FLOP/pair"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,

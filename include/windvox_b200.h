@@ -86,6 +86,15 @@ int wv_pack_exact_grad(int kind, const void *vertices, int vert_f64, int64_t n_v
                        const void *faces, int faces_i64, const int64_t *active,
                        const float *weights, int64_t n_active, void *packed, void *stream);
 
+/* Area-weighted vertex normals (mesh_io.vertex_normals, mesh_io.py:176-195),
+ * the staging of flipped duplication for open meshes (openmesh.py:21-48).
+ * vertices (V,3) f64, faces (F,3) int64; the CSR lists, per vertex, the slots
+ * k*F + f of its face corners in ascending order (np.add.at's order, so the
+ * result is bit-identical).  normals (V,3) f64; zero (V,) u8 may be NULL. */
+int wv_vertex_normals(const double *vertices, int64_t n_verts, const int64_t *faces,
+                      int64_t n_faces, const int64_t *csr_offsets, const int64_t *csr_slots,
+                      double *normals, uint8_t *zero, void *stream);
+
 /* ---- forward: winding numbers at lattice nodes or explicit points -------
  * exact f32: replaces _kernels.exact_batch_f32 (_kernels.py:235-309); FP32
  *   compute with fp64 tile-partial accumulation, within 1e-5 of the f64

@@ -13,6 +13,9 @@ from .winding import (binarize, solid_angle_triangle, voxelize, winding_number_b
                       winding_number_exact, winding_number_soft)
 from .grad import exact_loss_grad, occupancy_loss_grad, soft_winding_vertex_jacobian
 from .autograd import WindingNumber, winding_number
+from .fieldio import load_field, save_field
+from .morph import MorphConfig, MorphReport, morph
+from .openmesh import flipped_duplication, vertex_normals
 
 __version__ = "0.1.0"
 
@@ -24,5 +27,7 @@ __all__ = [
     "winding_number_batch", "voxelize", "binarize",
     "soft_winding_vertex_jacobian", "occupancy_loss_grad", "exact_loss_grad",
     "WindingNumber", "winding_number",
+    "save_field", "load_field", "MorphConfig", "MorphReport", "morph",
+    "flipped_duplication", "vertex_normals",
     "__version__",
 ]

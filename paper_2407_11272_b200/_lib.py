@@ -29,7 +29,7 @@ POLICY_HALF = 1
 # every symbol the public header declares (checked by tests/test_capi_symbols.py)
 EXPORTED = (
     "wv_version", "wv_status_string", "wv_set_device", "wv_packed_bytes", "wv_pack_faces",
-    "wv_pack_exact_grad", "wv_fwd_workspace_bytes", "wv_exact_fwd_grid_f32", "wv_exact_fwd_points_f32",
+    "wv_pack_exact_grad", "wv_vertex_normals", "wv_fwd_workspace_bytes", "wv_exact_fwd_grid_f32", "wv_exact_fwd_points_f32",
     "wv_soft_fwd_grid_f32", "wv_soft_fwd_points_f32", "wv_exact_fwd_grid_f64",
     "wv_exact_fwd_points_f64", "wv_soft_fwd_grid_f64", "wv_soft_fwd_points_f64",
     "wv_bwd_workspace_bytes", "wv_exact_bwd_grid_f32", "wv_exact_bwd_points_f32",
@@ -70,6 +70,7 @@ def _declare(lib):
         "wv_packed_bytes": ([I, I64], SZ),
         "wv_pack_faces": ([I, P, I, I64, P, I, I64, P, P], I),
         "wv_pack_exact_grad": ([I, P, I, I64, P, I, P, P, I64, P, P], I),
+        "wv_vertex_normals": ([P, I64, P, I64, P, P, P, P, P], I),
         "wv_fwd_workspace_bytes": ([I, I64, I64], SZ),
         "wv_exact_fwd_grid_f32": (fwd32_grid, I),
         "wv_exact_fwd_points_f32": (fwd32_pts, I),

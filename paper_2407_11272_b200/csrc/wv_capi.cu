@@ -103,6 +103,17 @@ int wv_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t n_v
                                     weights, n_active, packed, as_stream(stream));
 }
 
+int wv_vertex_normals(const double* vertices, int64_t n_verts, const int64_t* faces,
+                      int64_t n_faces, const int64_t* csr_offsets, const int64_t* csr_slots,
+                      double* normals, uint8_t* zero, void* stream) {
+  if (n_verts < 0 || n_faces < 0) return WV_ERR_ARG;
+  if (n_verts > 0 && (vertices == nullptr || csr_offsets == nullptr || normals == nullptr))
+    return WV_ERR_ARG;
+  if (n_faces > 0 && (faces == nullptr || csr_slots == nullptr)) return WV_ERR_ARG;
+  return wv::launch_vertex_normals(vertices, faces, n_faces, csr_offsets, csr_slots, n_verts,
+                                   normals, zero, as_stream(stream));
+}
+
 // ---- forward ---------------------------------------------------------------
 size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {

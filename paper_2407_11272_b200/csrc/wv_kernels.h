@@ -106,6 +106,9 @@ int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
 int launch_surface_eps(const void* vertices, int vert_f64, int64_t n_verts, double* eps_dev,
                        cudaStream_t stream);
 size_t packed_bytes(int kind, int64_t n_faces);
+int launch_vertex_normals(const double* verts, const int64_t* faces, int64_t n_faces,
+                          const int64_t* off, const int64_t* slots, int64_t n_verts,
+                          double* normals, uint8_t* zero, cudaStream_t stream);
 int launch_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t n_verts,
                            const void* faces, int faces_i64, const int64_t* active,
                            const float* weights, int64_t n_active, void* packed,

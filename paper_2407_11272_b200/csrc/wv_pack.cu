@@ -218,6 +218,49 @@ int launch_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
+// Area-weighted vertex normals (mesh_io.py:176-195): every face adds its
+// unnormalised cross product to its three corners, then sums are normalised
+// (zero sums flagged).  The gather walks a CSR whose slots are ordered
+// corner-major (k*F + f), the exact order np.add.at(n, faces[:, k], fn),
+// k = 0,1,2, accumulates in -- so results are bit-identical (-fmad=false).
+__global__ void vertex_normals_kernel(const double* __restrict__ verts,
+                                      const int64_t* __restrict__ faces, int64_t n_faces,
+                                      const int64_t* __restrict__ off,
+                                      const int64_t* __restrict__ slots, int64_t n_verts,
+                                      double* __restrict__ normals, uint8_t* __restrict__ zero) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_verts;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+      const int64_t f = slots[e] % n_faces;
+      double p0[3], p1[3], p2[3];
+      load_vertex(verts, faces[3 * f + 0], p0);
+      load_vertex(verts, faces[3 * f + 1], p1);
+      load_vertex(verts, faces[3 * f + 2], p2);
+      const double ux = p1[0] - p0[0], uy = p1[1] - p0[1], uz = p1[2] - p0[2];
+      const double wx = p2[0] - p0[0], wy = p2[1] - p0[1], wz = p2[2] - p0[2];
+      s[0] += uy * wz - uz * wy;
+      s[1] += uz * wx - ux * wz;
+      s[2] += ux * wy - uy * wx;
+    }
+    const double nrm = sqrt(s[0] * s[0] + s[1] * s[1] + s[2] * s[2]);
+    const bool z = nrm == 0.0;
+    for (int d = 0; d < 3; ++d) normals[3 * v + d] = z ? s[d] : s[d] / nrm;
+    if (zero) zero[v] = z ? 1 : 0;
+  }
+}
+
+int launch_vertex_normals(const double* verts, const int64_t* faces, int64_t n_faces,
+                          const int64_t* off, const int64_t* slots, int64_t n_verts,
+                          double* normals, uint8_t* zero, cudaStream_t stream) {
+  if (n_verts <= 0) return kOk;
+  int64_t blocks = (n_verts + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  vertex_normals_kernel<<<(unsigned)blocks, 256, 0, stream>>>(verts, faces, n_faces > 0 ? n_faces : 1,
+                                                              off, slots, n_verts, normals, zero);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
 size_t packed_bytes(int kind, int64_t n_faces) {
   size_t rec = 0;
   switch (kind) {

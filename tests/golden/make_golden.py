@@ -221,6 +221,36 @@ def main():
          exact32=out32, exact32_flags=fl32, soft=sout, soft_flags=sfl, soft32=sout32,
          soft32_flags=sfl32, coefs=coefs, soft_grad=grad)
 
+    # 11. morph traces (test_acceptance.py:268-278 and test_morph.py setups)
+    from windvox.morph import MorphConfig, morph
+    tgt_spec = wv.GridSpec([-0.8] * 3, [0.8] * 3, 12)
+    target = wv.voxelize(shapes.cube(0.5), tgt_spec)
+    tmpl = shapes.icosphere(1, 0.4)
+    res_mesh, rep = morph(tmpl, target, MorphConfig(iterations=10))
+    res2, rep2 = morph(tmpl, target, MorphConfig(iterations=6, momentum=0.0, smooth_weight=0.0,
+                                                 step_size=0.2))
+    save("morph_traces", tmpl_vertices=tmpl.vertices, tmpl_faces=tmpl.faces,
+         target=target.values, **grid_dict("grid", tgt_spec),
+         final=res_mesh.vertices, losses=np.array([e["loss"] for e in rep.entries]),
+         gnorms=np.array([e["grad_inf_norm"] for e in rep.entries]),
+         final2=res2.vertices, losses2=np.array([e["loss"] for e in rep2.entries]))
+
+    # 12. flipped duplication and WVOX1 bytes (openmesh.py:21-48, winding.py:403-443)
+    import tempfile
+    hemi = shapes.hemisphere(2)
+    dup = wv.flipped_duplication(hemi, epsilon=0.02)
+    fld = wv.ScalarField(wv.GridSpec((-1.0, 0.0, 0.5), (1.0, 2.0, 0.75), (4, 3, 5)),
+                         np.random.default_rng(53).normal(size=60))
+    with tempfile.TemporaryDirectory() as d:
+        wv.save_field(fld, f"{d}/f.wvox")
+        raw64 = np.frombuffer(open(f"{d}/f.wvox", "rb").read(), dtype=np.uint8)
+        f32 = wv.ScalarField(fld.spec, fld.values.astype(np.float32))
+        wv.save_field(f32, f"{d}/g.wvox")
+        raw32 = np.frombuffer(open(f"{d}/g.wvox", "rb").read(), dtype=np.uint8)
+    save("openmesh_and_io", hemi_vertices=hemi.vertices, hemi_faces=hemi.faces,
+         dup_vertices=dup.vertices, dup_faces=dup.faces, field_values=fld.values,
+         wvox_f64=raw64, wvox_f32=raw32)
+
     # 10. solid-angle known answers (test_winding.py:45-83)
     save("solid_angle_known",
          octant=np.array(wv.solid_angle_triangle([1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, 0])),

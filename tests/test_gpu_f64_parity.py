@@ -132,3 +132,16 @@ def test_exact_grad_f64_vs_reference_fd(wv):
         fg = device.face_grad(dm, "exact", "f64", cf, points=pts)
         got = device.vertex_grad(dm, fg).cpu().numpy()
         assert np.abs(got - fd).max() / np.abs(fd).max() < 1e-6, i
+
+
+def test_flipped_duplication_bit_exact(wv):
+    g = golden("openmesh_and_io")
+    hemi = wv.TriangleMesh(g["hemi_vertices"], g["hemi_faces"])
+    dup = wv.flipped_duplication(hemi, epsilon=0.02)
+    assert dup.vertices.tobytes() == g["dup_vertices"].tobytes()
+    assert np.array_equal(dup.faces, g["dup_faces"])
+    with pytest.raises(ValueError):
+        wv.flipped_duplication(hemi, epsilon=0.0)
+    with pytest.raises(wv.DegenerateError):
+        wv.flipped_duplication(wv.TriangleMesh(np.array([[0.0, 0, 0], [1, 0, 0], [2, 0, 0]]),
+                                               [[0, 1, 2]]))

@@ -133,3 +133,38 @@ def test_exact_edge_weights_reproduce_face_closed_form(case):
     assert np.abs(got - ref).max() <= 1e-10 * max(np.abs(ref).max(), 1e-12)
     if case == "holes":
         assert len(active) < len(f) // 2
+
+
+def test_wvox1_bytes_match_reference(tmp_path):
+    """WVOX1 writer reproduces the reference's bytes (golden) and round-trips."""
+    import paper_2407_11272_b200 as wv
+    from conftest import golden
+    g = golden("openmesh_and_io")
+    spec = wv.GridSpec((-1.0, 0.0, 0.5), (1.0, 2.0, 0.75), (4, 3, 5))
+    f64 = wv.ScalarField(spec, g["field_values"])
+    wv.save_field(f64, tmp_path / "a.wvox")
+    assert (tmp_path / "a.wvox").read_bytes() == g["wvox_f64"].tobytes()
+    wv.save_field(wv.ScalarField(spec, g["field_values"].astype(np.float32)), tmp_path / "b.wvox")
+    assert (tmp_path / "b.wvox").read_bytes() == g["wvox_f32"].tobytes()
+    back = wv.load_field(tmp_path / "a.wvox")
+    assert back.spec == spec and back.values.tobytes() == f64.values.tobytes()
+    bad = tmp_path / "bad.wvox"
+    bad.write_bytes(g["wvox_f64"].tobytes().replace(b"WVOX1", b"WVOX9", 1))
+    with pytest.raises(wv.ParseError):
+        wv.load_field(bad)
+    short = tmp_path / "short.wvox"
+    short.write_bytes(g["wvox_f64"].tobytes()[:-8])
+    with pytest.raises(wv.ParseError):
+        wv.load_field(short)
+
+
+def test_uniform_laplacian_matches_definition():
+    from paper_2407_11272_b200 import configs
+    from paper_2407_11272_b200.morph import uniform_laplacian
+    v, f = configs.icosphere(1, 0.5)
+    ip, ix, d = uniform_laplacian(f, len(v))
+    dense = np.zeros((len(v), len(v)))
+    for r in range(len(v)):
+        dense[r, ix[ip[r]:ip[r + 1]]] += d[ip[r]:ip[r + 1]]
+    assert np.allclose(dense.sum(axis=1), 0.0)  # rows of I - D^-1 A sum to 0
+    assert np.allclose(np.diag(dense), 1.0)
