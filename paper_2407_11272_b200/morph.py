@@ -106,7 +106,8 @@ class _DeviceProblem:
         ip, ix, dv = uniform_laplacian(template.faces, template.num_vertices)
         V = template.num_vertices
         self.L = torch.sparse_csr_tensor(torch.from_numpy(ip), torch.from_numpy(ix),
-                                         torch.from_numpy(dv), size=(V, V)).to(dev, self.dt)
+                                         torch.from_numpy(dv), size=(V, V),
+                                         check_invariants=True).to(dev, self.dt)
         self.LT = self.L.to_sparse_coo().t().coalesce().to_sparse_csr()
 
     def _occupancy(self, verts: torch.Tensor):
