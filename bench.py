@@ -63,6 +63,24 @@ def parse():
     return ap.parse_args()
 
 
+def init_dist(local: int, world: int):
+    """One process per GPU; NCCL over NVLink.  WV_BENCH_BACKEND=gloo (with
+    ranks wrapped onto the visible GPUs) exercises the N>1 code path on a
+    single GPU -- a functional check only, never a reported number."""
+    import torch
+    import torch.distributed as dist
+    gpu = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    if world > 1:
+        backend = os.environ.get("WV_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -233,14 +251,12 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = init_dist(local, world)
+    local = dev.index
     from paper_2407_11272_b200 import configs, device
     from paper_2407_11272_b200 import _lib as L
     from paper_2407_11272_b200.distributed import SlabDriver, slab_range
 
-    dev = torch.device("cuda", local)
     w = configs.make(args.config)
     n0, cnt = slab_range(w.n_nodes, rank, world)
     grid = (w.lo, w.hi, w.res)
@@ -431,13 +447,11 @@ def run_c4(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = init_dist(local, world)
+    local = dev.index
     from paper_2407_11272_b200 import configs, device
     from paper_2407_11272_b200.batch import DeformationNet, batch_occupancy_loss
 
-    dev = torch.device("cuda", local)
     B, R = 64, 64
     grid = ((-1.0,) * 3, (1.0,) * 3, (R, R, R))
     per = B // world
