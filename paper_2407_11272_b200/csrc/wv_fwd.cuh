@@ -35,6 +35,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   ring_start(ring, recs, n_faces, t_begin, t_end);
 
   const float eps = hdr->eps_f32;
+  const double eps64 = hdr->eps;
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * (NC * P);
   constexpr int PP = P / 2;  // point pairs (packed f32x2)
@@ -84,9 +85,9 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
             split(qy[p / 2], yl, yh);
             split(qz[p / 2], zl, zh);
             const bool hi = p & 1;
-            const float th = Pol::rare(R, hi ? xh : xl, hi ? yh : yl, hi ? zh : zl, eps);
+            const double th = Pol::rare(R, hi ? xh : xl, hi ? yh : yl, hi ? zh : zl, eps64);
             if (th != th) hits |= 1u << p;  // NaN marks an on-surface pair
-            else tacc[p / 2] = add2(tacc[p / 2], hi ? f2(0.0f, th) : f2(th, 0.0f));
+            else accd[p] += th;             // rare terms go straight to fp64
           }
         }
       }

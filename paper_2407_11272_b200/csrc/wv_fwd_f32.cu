@@ -16,44 +16,51 @@
 
 namespace wv {
 
-// Rare exact pairs: on-surface candidates (plane distance < eps,
-// _kernels.py:65-88) and wide angles (|theta| > pi/4, incl. beta < 0).
-// Recomputes the pair; returns theta, or NaN for an on-surface pair.
-__device__ __noinline__ float exact_rare(float4 A, float4 B, float4 C, float4 N, float qx,
-                                         float qy, float qz, float eps) {
-  const float ax = A.x - qx, ay = A.y - qy, az = A.z - qz;
-  const float bx = B.x - qx, by = B.y - qy, bz = B.z - qz;
-  const float cx = C.x - qx, cy = C.y - qy, cz = C.z - qz;
-  const float alpha = fmaf(N.z, az, fmaf(N.y, ay, N.x * ax));
-  const float la = sqrt_approx(fmaf(az, az, fmaf(ay, ay, ax * ax)));
-  const float lb = sqrt_approx(fmaf(bz, bz, fmaf(by, by, bx * bx)));
-  const float lc = sqrt_approx(fmaf(cz, cz, fmaf(cy, cy, cx * cx)));
-  const float ab = fmaf(az, bz, fmaf(ay, by, ax * bx));
-  const float bc = fmaf(bz, cz, fmaf(by, cy, bx * cx));
-  const float ca = fmaf(az, cz, fmaf(ay, cy, ax * cx));
-  const float g1 = fmaf(bc, la, la * (lb * lc));
-  const float g2 = __fadd_rn(__fmul_rn(ab, lc), __fmul_rn(ca, lb));
-  const float beta = g1 + g2;
-  const float epsN = A.w;
-  if (fabsf(alpha) < epsN) {
-    if (epsN == __int_as_float(0x7f800000)) return 0.0f;  // degenerate face
-    // _kernels.py:65-67 vertex test, then :70-88 plane + barycentric test
-    if (la < eps || lb < eps || lc < eps) return __int_as_float(0x7fc00000);
-    const float ux = B.x - A.x, uy = B.y - A.y, uz = B.z - A.z;
-    const float wx = C.x - A.x, wy = C.y - A.y, wz = C.z - A.z;
-    const float d00 = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
-    const float d01 = fmaf(uz, wz, fmaf(uy, wy, ux * wx));
-    const float d11 = fmaf(wz, wz, fmaf(wy, wy, wx * wx));
-    const float denom = __fsub_rn(__fmul_rn(d00, d11), __fmul_rn(d01, d01));
-    const float ru = -fmaf(az, uz, fmaf(ay, uy, ax * ux));
-    const float rw = -fmaf(az, wz, fmaf(ay, wy, ax * wx));
-    const float b1 = __fdiv_rn(__fsub_rn(__fmul_rn(d11, ru), __fmul_rn(d01, rw)), denom);
-    const float b2 = __fdiv_rn(__fsub_rn(__fmul_rn(d00, rw), __fmul_rn(d01, ru)), denom);
-    const float btol = 1e-12f;
-    if (b1 >= -btol && b2 >= -btol && b1 + b2 <= 1.0f + btol)
-      return __int_as_float(0x7fc00000);
+// Rare exact pairs -- wide angles (|theta| >= atan(1/8), incl. beta <= 0),
+// on-surface candidates and degenerate faces.  They are few (only faces
+// within about a face size of the node), and they are where fp32 loses
+// digits to cancellation in beta, so they are evaluated in FP64 on the same
+// fp32-rounded inputs, in the reference kernel's operation order
+// (_kernels.py:52-105): vertex test, plane + barycentric test (eps of the
+// f64 header), triple product, beta grouping, atan2.  Returns theta =
+// Omega/2 in f64, 0 for a degenerate face, NaN for an on-surface pair.
+__device__ __noinline__ double exact_rare(float4 A, float4 B, float4 C, float qxf, float qyf,
+                                          float qzf, double eps) {
+  if (A.w == __int_as_float(0x7f800000)) return 0.0;  // degenerate (dropped) face
+  const double qx = qxf, qy = qyf, qz = qzf;
+  const double ax = (double)A.x - qx, ay = (double)A.y - qy, az = (double)A.z - qz;
+  const double bx = (double)B.x - qx, by = (double)B.y - qy, bz = (double)B.z - qz;
+  const double cx = (double)C.x - qx, cy = (double)C.y - qy, cz = (double)C.z - qz;
+  const double na = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
+  const double nb = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(bx, bx), __dmul_rn(by, by)), __dmul_rn(bz, bz)));
+  const double nc = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz)));
+  if (na < eps || nb < eps || nc < eps) return __longlong_as_double(0x7ff8000000000000ll);
+  const double ux = (double)B.x - A.x, uy = (double)B.y - A.y, uz = (double)B.z - A.z;
+  const double wx = (double)C.x - A.x, wy = (double)C.y - A.y, wz = (double)C.z - A.z;
+  const double nx = uy * wz - uz * wy, ny = uz * wx - ux * wz, nz = ux * wy - uy * wx;
+  const double nn = sqrt(nx * nx + ny * ny + nz * nz);
+  const double pd = -(nx * ax + ny * ay + nz * az) / nn;  // nhat.(q - v0)
+  if (-eps < pd && pd < eps) {
+    const double d00 = ux * ux + uy * uy + uz * uz;
+    const double d01 = ux * wx + uy * wy + uz * wz;
+    const double d11 = wx * wx + wy * wy + wz * wz;
+    const double denom = d00 * d11 - d01 * d01;
+    const double ru = -(ax * ux + ay * uy + az * uz);
+    const double rw = -(ax * wx + ay * wy + az * wz);
+    const double b1 = (d11 * ru - d01 * rw) / denom;
+    const double b2 = (d00 * rw - d01 * ru) / denom;
+    if (b1 >= -1e-12 && b2 >= -1e-12 && b1 + b2 <= 1.0 + 1e-12)
+      return __longlong_as_double(0x7ff8000000000000ll);
   }
-  return atan2_full(alpha, beta);
+  const double alpha = __dadd_rn(__dadd_rn(__dmul_rn(ax, __dsub_rn(__dmul_rn(by, cz), __dmul_rn(bz, cy))),
+                                           __dmul_rn(ay, __dsub_rn(__dmul_rn(bz, cx), __dmul_rn(bx, cz)))),
+                                 __dmul_rn(az, __dsub_rn(__dmul_rn(bx, cy), __dmul_rn(by, cx))));
+  const double bc = __dadd_rn(__dadd_rn(__dmul_rn(bx, cx), __dmul_rn(by, cy)), __dmul_rn(bz, cz));
+  const double ab = __dadd_rn(__dadd_rn(__dmul_rn(ax, bx), __dmul_rn(ay, by)), __dmul_rn(az, bz));
+  const double ca = __dadd_rn(__dadd_rn(__dmul_rn(cx, ax), __dmul_rn(cy, ay)), __dmul_rn(cz, az));
+  const double beta = __dadd_rn(__dadd_rn(__dmul_rn(na, __dmul_rn(nb, nc)), __dmul_rn(bc, na)),
+                                __dadd_rn(__dmul_rn(ab, nc), __dmul_rn(ca, nb)));
+  return atan2(alpha, beta);
 }
 
 // Both policies evaluate TWO query points per instruction (packed f32x2, see
@@ -104,9 +111,9 @@ struct ExactPol {
     tacc = fma2(f2(cl ? tl : 0.0f, ch ? th : 0.0f), p, tacc);
     return (cl ? 0u : 1u) | (ch ? 0u : 2u);
   }
-  __device__ __forceinline__ static float rare(const Rec& R, float qx, float qy, float qz,
-                                               float eps) {
-    return exact_rare(R.v0e, R.v1, R.v2, R.n, qx, qy, qz, eps);
+  __device__ __forceinline__ static double rare(const Rec& R, float qx, float qy, float qz,
+                                                double eps) {
+    return exact_rare(R.v0e, R.v1, R.v2, qx, qy, qz, eps);
   }
 };
 
@@ -139,8 +146,8 @@ struct SoftPol {
     tacc = fma2(s, mul2(rs, mul2(rs, rs)), tacc);
     return (hl ? 1u : 0u) | (hh ? 2u : 0u);
   }
-  __device__ __forceinline__ static float rare(const Rec&, float, float, float, float) {
-    return __int_as_float(0x7fc00000);  // always an on-surface (flagged) pair
+  __device__ __forceinline__ static double rare(const Rec&, float, float, float, double) {
+    return __longlong_as_double(0x7ff8000000000000ll);  // always an on-surface (flagged) pair
   }
 };
 // Sum split partials in split order (deterministic), then W = sum * scale.
