@@ -91,17 +91,26 @@ struct ExactPol {
     const F2 bc = dot2(bx, by, bz, cx, cy, cz);
     const F2 ca = dot2(ax, ay, az, cx, cy, cz);
     // beta = |a||b||c| + (b.c)|a| + (a.b)|c| + (c.a)|b|  (_kernels.py:98-103)
-    const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, mul2(la, mul2(lb, lc)))));
+    const F2 labc = mul2(la, mul2(lb, lc));
+    const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
     // Common pairs: |theta| < atan(1/8) (|alpha| < beta/8, so beta > 0).  On
     // a face's closed triangle beta <= 0 (on a vertex alpha = beta = 0), so
     // every on-surface candidate fails this test and reaches exact_rare(), as
     // do degenerate faces (N = 0); far faces -- nearly all pairs of a fine
     // mesh -- stay here.  atan(t) = t (1 + s (c1 + c2 s)), s = t^2,
     // |t| <= 1/8: relative error 1.2e-7 in fp32 (fit: DESIGN.md 3.5).
-    float al, ah, bl, bh;
+    // Well-conditioned pairs only: beta = |a||b||c| (1 + sum cos) must not
+    // have cancelled below |a||b||c|/2 (near-edge / grazing configurations,
+    // where fp32 loses digits); those go to the fp64 rare path too.  beta/8
+    // is an exponent subtract on the ALU pipe (exact for normal beta; any
+    // beta <= 0 or subnormal yields a negative bound, i.e. "rare").
+    float al, ah, bl, bh, pl, ph;
     split(alpha, al, ah);
     split(beta, bl, bh);
-    const bool cl = fabsf(al) < 0.125f * bl, ch = fabsf(ah) < 0.125f * bh;
+    split(sub2(add2(beta, beta), labc), pl, ph);  // 2 beta - |a||b||c|
+    const float b8l = __int_as_float(__float_as_int(bl) - (3 << 23));
+    const float b8h = __int_as_float(__float_as_int(bh) - (3 << 23));
+    const bool cl = fabsf(al) < b8l && pl > 0.0f, ch = fabsf(ah) < b8h && ph > 0.0f;
     const F2 tt = mul2(alpha, rcp2(beta));
     const F2 s = mul2(tt, tt);
     const F2 p = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
