@@ -25,9 +25,9 @@ constexpr double kPi = 3.14159265358979311599796346854;  // np.pi
 //   f64, dropped by the reference at winding.py:258-268) carry epsN = +inf.
 struct __align__(16) ExactRecF32 {
   float4 v0e;  // v0.xyz, epsN
-  float4 v1;   // v1.xyz, 0
-  float4 v2;   // v2.xyz, 0
-  float4 n;    // N.xyz, 0
+  float4 v1;   // v1.xyz, |v1-v0|^2/2
+  float4 v2;   // v2.xyz, |v2-v1|^2/2
+  float4 n;    // N.xyz,  |v0-v2|^2/2
 };
 static_assert(sizeof(ExactRecF32) == 64, "record size");
 

@@ -28,6 +28,10 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   constexpr int NC = CW * 32;
   constexpr int P = Pol::kP;
   __shared__ FaceRing<Rec, TILE, STAGES> ring;
+  // fp64 per-point accumulators live in shared memory ([p][thread]): they are
+  // touched once per tile (and by rare pairs), and keeping them out of the
+  // register file leaves the 128-register budget to the pair arithmetic
+  __shared__ double accs[P][NC];
   const int64_t n_tiles = (n_faces + TILE - 1) / TILE;
   const int64_t t_begin = (int64_t)blockIdx.y * tiles_per_split;
   int64_t t_end = t_begin + tiles_per_split;
@@ -40,7 +44,6 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   const int64_t base = (int64_t)blockIdx.x * (NC * P);
   constexpr int PP = P / 2;  // point pairs (packed f32x2)
   F2 qx[PP], qy[PP], qz[PP];
-  double accd[P];
 #pragma unroll
   for (int pp = 0; pp < PP; ++pp) {
     float x[2], y[2], z[2];
@@ -49,7 +52,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       int64_t l = base + (2 * pp + h) * NC + tid;
       if (l >= n_count) l = n_count - 1;  // padded lanes recompute a valid node
       src.point(l, x[h], y[h], z[h]);
-      accd[2 * pp + h] = 0.0;
+      accs[2 * pp + h][tid] = 0.0;
     }
     qx[pp] = f2(x[0], x[1]);
     qy[pp] = f2(y[0], y[1]);
@@ -87,7 +90,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
             const bool hi = p & 1;
             const double th = Pol::rare(R, hi ? xh : xl, hi ? yh : yl, hi ? zh : zl, eps64);
             if (th != th) hits |= 1u << p;  // NaN marks an on-surface pair
-            else accd[p] += th;             // rare terms go straight to fp64
+            else accs[p][tid] += th;        // rare terms go straight to fp64
           }
         }
       }
@@ -96,8 +99,8 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     for (int pp = 0; pp < PP; ++pp) {
       float lo, hi;
       split(tacc[pp], lo, hi);
-      accd[2 * pp] += (double)lo;
-      accd[2 * pp + 1] += (double)hi;
+      accs[2 * pp][tid] += (double)lo;
+      accs[2 * pp + 1][tid] += (double)hi;
     }
     __syncwarp();
     if ((tid & 31) == 0) ring_release(ring, s, CW, recs, n_faces, t, t_end);
@@ -106,7 +109,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const int64_t l = base + p * NC + tid;
-    if (l < n_count) o.store(blockIdx.y, l, accd[p], (hits >> p) & 1u);
+    if (l < n_count) o.store(blockIdx.y, l, accs[p][tid], (hits >> p) & 1u);
   }
 }
 

@@ -84,12 +84,17 @@ struct ExactPol {
     const F2 cx = sub2(f2s(R.v2.x), qx), cy = sub2(f2s(R.v2.y), qy), cz = sub2(f2s(R.v2.z), qz);
     // alpha = N.(v0-q) = det(a,b,c)
     const F2 alpha = fma2(f2s(R.n.z), az, fma2(f2s(R.n.y), ay, mul2(f2s(R.n.x), ax)));
-    const F2 la = sqrt2(dot2(ax, ay, az, ax, ay, az));
-    const F2 lb = sqrt2(dot2(bx, by, bz, bx, by, bz));
-    const F2 lc = sqrt2(dot2(cx, cy, cz, cx, cy, cz));
-    const F2 ab = dot2(ax, ay, az, bx, by, bz);
-    const F2 bc = dot2(bx, by, bz, cx, cy, cz);
-    const F2 ca = dot2(ax, ay, az, cx, cy, cz);
+    const F2 la2 = dot2(ax, ay, az, ax, ay, az);
+    const F2 lb2 = dot2(bx, by, bz, bx, by, bz);
+    const F2 lc2 = dot2(cx, cy, cz, cx, cy, cz);
+    const F2 la = sqrt2(la2), lb = sqrt2(lb2), lc = sqrt2(lc2);
+    // a.b = (|a|^2 + |b|^2 - |v0-v1|^2)/2 etc. (half squared edge lengths are
+    // packed): 2 ops instead of 3.  It can cancel only where beta itself is
+    // ill-conditioned, and those pairs leave for the fp64 path below.
+    const F2 half = f2s(0.5f);
+    const F2 ab = fma2(add2(la2, lb2), half, f2s(-R.v1.w));
+    const F2 bc = fma2(add2(lb2, lc2), half, f2s(-R.v2.w));
+    const F2 ca = fma2(add2(lc2, la2), half, f2s(-R.n.w));
     // beta = |a||b||c| + (b.c)|a| + (a.b)|c| + (c.a)|b|  (_kernels.py:98-103)
     const F2 labc = mul2(la, mul2(lb, lc));
     const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
@@ -107,10 +112,12 @@ struct ExactPol {
     float al, ah, bl, bh, pl, ph;
     split(alpha, al, ah);
     split(beta, bl, bh);
-    split(sub2(add2(beta, beta), labc), pl, ph);  // 2 beta - |a||b||c|
+    split(labc, pl, ph);
     const float b8l = __int_as_float(__float_as_int(bl) - (3 << 23));
     const float b8h = __int_as_float(__float_as_int(bh) - (3 << 23));
-    const bool cl = fabsf(al) < b8l && pl > 0.0f, ch = fabsf(ah) < b8h && ph > 0.0f;
+    const float p2l = __int_as_float(__float_as_int(pl) - (1 << 23));  // |a||b||c| / 2
+    const float p2h = __int_as_float(__float_as_int(ph) - (1 << 23));
+    const bool cl = fabsf(al) < b8l && bl > p2l, ch = fabsf(ah) < b8h && bh > p2h;
     const F2 tt = mul2(alpha, rcp2(beta));
     const F2 s = mul2(tt, tt);
     const F2 p = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,

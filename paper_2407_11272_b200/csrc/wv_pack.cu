@@ -85,9 +85,14 @@ __global__ void pack_kernel(int kind, const V* __restrict__ verts,
         ExactRecF32* r = static_cast<ExactRecF32*>(recs) + f;
         const float epsN = dead ? __int_as_float(0x7f800000) : (float)(eps * norm);
         r->v0e = make_float4((float)v0[0], (float)v0[1], (float)v0[2], epsN);
-        r->v1 = make_float4((float)v1[0], (float)v1[1], (float)v1[2], 0.0f);
-        r->v2 = make_float4((float)v2[0], (float)v2[1], (float)v2[2], 0.0f);
-        r->n = make_float4((float)nx, (float)ny, (float)nz, 0.0f);
+        // half squared edge lengths, for a.b = (|a|^2 + |b|^2 - |v0-v1|^2) / 2
+        const double h01 = 0.5 * (ux * ux + uy * uy + uz * uz);
+        const double h20 = 0.5 * (wx * wx + wy * wy + wz * wz);
+        const double ex = v2[0] - v1[0], ey = v2[1] - v1[1], ez = v2[2] - v1[2];
+        const double h12 = 0.5 * (ex * ex + ey * ey + ez * ez);
+        r->v1 = make_float4((float)v1[0], (float)v1[1], (float)v1[2], (float)h01);
+        r->v2 = make_float4((float)v2[0], (float)v2[1], (float)v2[2], (float)h12);
+        r->n = make_float4((float)nx, (float)ny, (float)nz, (float)h20);
       } else {
         ExactRecF64* r = static_cast<ExactRecF64*>(recs) + f;
         for (int d = 0; d < 3; ++d) {
