@@ -45,7 +45,7 @@ EXACT_BWD_FLOPS = 170
 # pinned VOS count; the backward's edge (Biot-Savart) form needs fewer
 # operations than the pinned face-wise closed form, which is why its
 # algorithmic-FLOP rate can reach the FP32 peak.
-EXACT_FWD_EXEC_FLOPS = 61
+EXACT_FWD_EXEC_FLOPS = 54
 EXACT_BWD_EXEC_FLOPS = 104
 
 
