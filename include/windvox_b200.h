@@ -188,6 +188,31 @@ int wv_face_to_vertex(const double *face_grad, const int64_t *csr_offsets,
                       const int64_t *csr_slots, int64_t n_verts, const double *scale,
                       int accumulate, double *out64, float *out32, void *stream);
 
+/* ---- marching cubes on the device-resident grid (recon.py:39-108) --------
+ * Four stream-ordered passes; the caller computes exclusive prefix sums
+ * between them (counts -> tri_offsets, flags -> vertex_index).
+ *   wv_mc_classify: per cell (Rx-1)(Ry-1)(Rz-1): case (bit c = corner c
+ *     outside, value <= iso; corner c at (c&1, c>>1&1, c>>2&1)) and its
+ *     triangle count tri_count[case];
+ *   wv_mc_edges: per lattice edge g = axis*N + node (N = Rx*Ry*Rz), 1 if it
+ *     crosses iso (the reference's global edge id, recon.py:90-93);
+ *   wv_mc_vertices: vertex vertex_index[g] = pa + t (pb - pa),
+ *     t = (iso - va)/(vb - va), f64 -- bit-identical to the reference;
+ *   wv_mc_emit: triangles of each cell at tri_offsets[cell] from the case
+ *     table (max_tris triples per case, -1 terminated) and the per-edge
+ *     axis / base-corner tables of the table's edge numbering.
+ * values: the field, f32 (values_f64=0) or f64. */
+int wv_mc_classify(const void *values, int values_f64, wv_grid_t grid, double iso,
+                   const int8_t *tri_count, uint8_t *cases, int32_t *counts, void *stream);
+int wv_mc_edges(const void *values, int values_f64, wv_grid_t grid, double iso, int32_t *flags,
+                void *stream);
+int wv_mc_vertices(const void *values, int values_f64, wv_grid_t grid, double iso,
+                   const int32_t *flags, const int64_t *vertex_index, double *vertices,
+                   void *stream);
+int wv_mc_emit(const uint8_t *cases, const int64_t *tri_offsets, const int8_t *tri_table,
+               int max_tris, const int8_t *edge_axis, const int8_t *edge_base,
+               const int64_t *vertex_index, wv_grid_t grid, int64_t *faces, void *stream);
+
 /* ---- occupancy loss terms (grad.py:101-110), fused on the device ---------
  * coefs[n] = 2 w r (0 on flagged nodes); sums (8 doubles, device) =
  * {sum w r^2, sum w, n_flagged, 1/sum w, loss, 0, 0, 0}.  weights may be NULL

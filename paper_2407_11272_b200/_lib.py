@@ -36,7 +36,7 @@ EXPORTED = (
     "wv_soft_bwd_grid_f32", "wv_soft_bwd_points_f32", "wv_exact_bwd_grid_f64",
     "wv_exact_bwd_points_f64", "wv_soft_bwd_grid_f64", "wv_soft_bwd_points_f64",
     "wv_face_to_vertex", "wv_loss_workspace_bytes", "wv_loss_terms_f32", "wv_loss_terms_f64",
-    "wv_loss_finalize",
+    "wv_loss_finalize", "wv_mc_classify", "wv_mc_edges", "wv_mc_vertices", "wv_mc_emit",
 )
 
 
@@ -94,6 +94,10 @@ def _declare(lib):
         "wv_loss_terms_f32": (loss, I),
         "wv_loss_terms_f64": (loss, I),
         "wv_loss_finalize": ([P, P], I),
+        "wv_mc_classify": ([P, I, Grid, D, P, P, P, P], I),
+        "wv_mc_edges": ([P, I, Grid, D, P, P], I),
+        "wv_mc_vertices": ([P, I, Grid, D, P, P, P, P], I),
+        "wv_mc_emit": ([P, P, P, I, P, P, P, Grid, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

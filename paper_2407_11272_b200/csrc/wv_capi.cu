@@ -301,6 +301,45 @@ int wv_face_to_vertex(const double* face_grad, const int64_t* csr_offsets,
                                    out64, out32, sm_count(), as_stream(stream));
 }
 
+// ---- marching cubes ------------------------------------------------------------
+int wv_mc_classify(const void* values, int values_f64, wv_grid_t grid, double iso,
+                   const int8_t* tri_count, uint8_t* cases, int32_t* counts, void* stream) {
+  if (values == nullptr || tri_count == nullptr || cases == nullptr || counts == nullptr)
+    return WV_ERR_ARG;
+  for (int i = 0; i < 3; ++i)
+    if (grid.res[i] < 2) return WV_ERR_ARG;
+  return wv::launch_mc_classify(values, values_f64, grid.res[0], grid.res[1], grid.res[2], iso,
+                                tri_count, cases, counts, sm_count(), as_stream(stream));
+}
+
+int wv_mc_edges(const void* values, int values_f64, wv_grid_t grid, double iso, int32_t* flags,
+                void* stream) {
+  if (values == nullptr || flags == nullptr) return WV_ERR_ARG;
+  for (int i = 0; i < 3; ++i)
+    if (grid.res[i] < 2) return WV_ERR_ARG;
+  return wv::launch_mc_edges(values, values_f64, grid.res[0], grid.res[1], grid.res[2], iso,
+                             flags, sm_count(), as_stream(stream));
+}
+
+int wv_mc_vertices(const void* values, int values_f64, wv_grid_t grid, double iso,
+                   const int32_t* flags, const int64_t* vertex_index, double* vertices,
+                   void* stream) {
+  if (values == nullptr || flags == nullptr || vertex_index == nullptr) return WV_ERR_ARG;
+  return wv::launch_mc_vertices(values, values_f64, grid_src(grid, 0).grid, iso, flags,
+                                vertex_index, vertices, sm_count(), as_stream(stream));
+}
+
+int wv_mc_emit(const uint8_t* cases, const int64_t* tri_offsets, const int8_t* tri_table,
+               int max_tris, const int8_t* edge_axis, const int8_t* edge_base,
+               const int64_t* vertex_index, wv_grid_t grid, int64_t* faces, void* stream) {
+  if (cases == nullptr || tri_offsets == nullptr || tri_table == nullptr || max_tris < 1 ||
+      edge_axis == nullptr || edge_base == nullptr || vertex_index == nullptr)
+    return WV_ERR_ARG;
+  return wv::launch_mc_emit(cases, tri_offsets, tri_table, max_tris, edge_axis, edge_base,
+                            vertex_index, grid.res[0], grid.res[1], grid.res[2], faces,
+                            sm_count(), as_stream(stream));
+}
+
 // ---- loss --------------------------------------------------------------------
 size_t wv_loss_workspace_bytes(int64_t count) { return wv::loss_workspace_bytes(count); }
 

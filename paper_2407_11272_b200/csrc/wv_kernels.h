@@ -153,6 +153,20 @@ int launch_face_to_vertex(const double* face_grad, const int64_t* off, const int
                           int64_t n_verts, const double* scale, int accumulate, double* out64,
                           float* out32, int num_sms, cudaStream_t stream);
 
+// marching cubes (wv_mc.cu)
+int launch_mc_classify(const void* vals, int f64, int64_t rx, int64_t ry, int64_t rz, double iso,
+                       const int8_t* count_tab, uint8_t* cases, int32_t* counts, int num_sms,
+                       cudaStream_t stream);
+int launch_mc_edges(const void* vals, int f64, int64_t rx, int64_t ry, int64_t rz, double iso,
+                    int32_t* flags, int num_sms, cudaStream_t stream);
+int launch_mc_vertices(const void* vals, int f64, const GridDesc& g, double iso,
+                       const int32_t* flags, const int64_t* vidx, double* verts, int num_sms,
+                       cudaStream_t stream);
+int launch_mc_emit(const uint8_t* cases, const int64_t* tri_off, const int8_t* tri_tab,
+                   int max_tris, const int8_t* edge_axis, const int8_t* edge_base,
+                   const int64_t* vidx, int64_t rx, int64_t ry, int64_t rz, int64_t* faces,
+                   int num_sms, cudaStream_t stream);
+
 // loss (wv_loss.cu)
 size_t loss_workspace_bytes(int64_t n);
 int launch_loss_f32(const float* values, const uint8_t* flags, const float* targets,

@@ -251,6 +251,24 @@ def main():
          dup_vertices=dup.vertices, dup_faces=dup.faces, field_values=fld.values,
          wvox_f64=raw64, wvox_f32=raw32)
 
+    # 13. marching cubes + smoothing (recon.py:39-140) on a voxelized mesh and
+    #     on a smooth random field
+    mc = {}
+    spec16 = wv.GridSpec((-1.0,) * 3, (1.0,) * 3, 16)
+    occ = wv.voxelize(shapes.icosphere(2, 0.7), spec16)
+    m1 = wv.marching_cubes(occ, iso=0.5)
+    s1 = wv.laplacian_smooth(m1, lam=0.15, iterations=10)
+    rng = np.random.default_rng(21)
+    spec14 = wv.GridSpec((-1.0, -0.5, 0.0), (1.0, 1.5, 2.0), (14, 12, 13))
+    nodes = spec14.node_coordinates()
+    cen = rng.uniform([-0.6, 0.0, 0.5], [0.6, 1.0, 1.5], size=(5, 3))
+    smooth = sum(np.exp(-np.sum((nodes - c) ** 2, axis=1) / 0.08) for c in cen)
+    m2 = wv.marching_cubes(wv.ScalarField(spec14, smooth), iso=0.3)
+    mc.update(occ=occ.values, m1_vertices=m1.vertices, m1_faces=m1.faces,
+              s1_vertices=s1.vertices, smooth=smooth, m2_vertices=m2.vertices,
+              m2_faces=m2.faces, **grid_dict("g16", spec16), **grid_dict("g14", spec14))
+    save("marching_cubes", **mc)
+
     # 10. solid-angle known answers (test_winding.py:45-83)
     save("solid_angle_known",
          octant=np.array(wv.solid_angle_triangle([1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, 0])),
