@@ -110,8 +110,8 @@ def test_device_mc_matches(cuda_device):
     assert np.abs(s.vertices - g["s1_vertices"]).max() < 1e-12
     assert np.array_equal(laplacian_smooth(m, lam=0.15, iterations=10).faces, m.faces)
     # voxelize -> marching cubes entirely on the device
-    occ = wv.voxelize(wv.TriangleMesh(*__import__("paper_2407_11272_b200").configs.icosphere(2, 0.7)),
-                      spec, precision="f32")
+    from paper_2407_11272_b200 import configs
+    occ = wv.voxelize(wv.TriangleMesh(*configs.icosphere(2, 0.7)), spec, precision="f32")
     m2 = marching_cubes(occ, iso=0.5)
     assert_closed_oriented(m2.faces)
     assert abs(signed_volume(m2.vertices, m2.faces) - signed_volume(m.vertices, m.faces)) < 1e-3
