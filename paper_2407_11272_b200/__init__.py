@@ -16,6 +16,7 @@ from .autograd import WindingNumber, winding_number
 from .fieldio import load_field, save_field
 from .morph import MorphConfig, MorphReport, morph
 from .openmesh import flipped_duplication, vertex_normals
+from .recon import laplacian_smooth, marching_cubes
 
 __version__ = "0.1.0"
 
@@ -28,6 +29,6 @@ __all__ = [
     "soft_winding_vertex_jacobian", "occupancy_loss_grad", "exact_loss_grad",
     "WindingNumber", "winding_number",
     "save_field", "load_field", "MorphConfig", "MorphReport", "morph",
-    "flipped_duplication", "vertex_normals",
+    "flipped_duplication", "vertex_normals", "marching_cubes", "laplacian_smooth",
     "__version__",
 ]
