@@ -40,7 +40,7 @@ constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
 // into coef_scale by the launcher.
 struct ExactEdgeBwd {
   using Rec = ExactGradRecF32;
-  static constexpr int kMinBlocks = 4;
+  static constexpr int kMinBlocks = 5;
   // -1/(4 pi) and the factor 2 of d = 2 (|a||b| + a.b) below
   static constexpr double kCoefScale = -2.0 / (4.0 * kPi);
   static constexpr int kAcc = 9;
@@ -96,7 +96,7 @@ struct ExactEdgeBwd {
 
 struct SoftBwd {
   using Rec = SoftGradRecF32;
-  static constexpr int kMinBlocks = 4;
+  static constexpr int kMinBlocks = 5;
   static constexpr double kCoefScale = 1.0 / (8.0 * kPi);
   static constexpr int kAcc = 10;  // acc1(3) acc2(3) T(1) D(3)
   __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
@@ -186,9 +186,12 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   // warp-uniform fast path when every face of the warp has unit edge
   // weights (soups, boundary strips): saves the per-edge weight multiply
   const bool unit = __all_sync(0xffffffffu, Pol::unit_weights(R));
-  double acc[Pol::kAcc];
+  // fp64 accumulators in shared memory ([j][thread]), touched once per
+  // 256-point chunk: keeps the pair arithmetic inside the register budget of
+  // 5 CTAs per SM
+  __shared__ double acc[Pol::kAcc][kBwdThreads];
 #pragma unroll
-  for (int j = 0; j < Pol::kAcc; ++j) acc[j] = 0.0;
+  for (int j = 0; j < Pol::kAcc; ++j) acc[j][threadIdx.x] = 0.0;
 
   for (int64_t c0 = p_begin; c0 < p_end; c0 += kBwdChunk) {
     const int n = (int)((p_end - c0) < kBwdChunk ? (p_end - c0) : kBwdChunk);
@@ -222,12 +225,15 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     for (int j = 0; j < Pol::kAcc; ++j) {
       float lo, hi;
       split(g[j], lo, hi);
-      acc[j] += (double)lo + (double)hi;
+      acc[j][threadIdx.x] += (double)lo + (double)hi;
     }
   }
   if (live) {
     double o9[9];
-    Pol::finish(R, acc, o9);
+    double a[Pol::kAcc];
+#pragma unroll
+    for (int j = 0; j < Pol::kAcc; ++j) a[j] = acc[j][threadIdx.x];
+    Pol::finish(R, a, o9);
     double* dst = out + ((int64_t)blockIdx.y * n_faces + f) * 9;
 #pragma unroll
     for (int j = 0; j < 9; ++j) dst[j] = o9[j];
