@@ -26,6 +26,7 @@ namespace wv {
 
 constexpr int kBwdThreads = 128;   // faces per CTA
 constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
+constexpr int kBwdMinBlocks = 5;  // CTAs per SM (launch bounds and split plan)
 
 // Exact backward, edge form.  For a triangle seen from q, the variation of
 // its solid angle is a boundary integral (the integrand (x-q)/|x-q|^3 is
@@ -40,7 +41,7 @@ constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
 // into coef_scale by the launcher.
 struct ExactEdgeBwd {
   using Rec = ExactGradRecF32;
-  static constexpr int kMinBlocks = 5;
+  static constexpr int kMinBlocks = kBwdMinBlocks;
   // -1/(4 pi) and the factor 2 of d = 2 (|a||b| + a.b) below
   static constexpr double kCoefScale = -2.0 / (4.0 * kPi);
   static constexpr int kAcc = 9;
@@ -96,7 +97,7 @@ struct ExactEdgeBwd {
 
 struct SoftBwd {
   using Rec = SoftGradRecF32;
-  static constexpr int kMinBlocks = 5;
+  static constexpr int kMinBlocks = kBwdMinBlocks;
   static constexpr double kCoefScale = 1.0 / (8.0 * kPi);
   static constexpr int kAcc = 10;  // acc1(3) acc2(3) T(1) D(3)
   __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
@@ -327,7 +328,7 @@ int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& 
                              ws_bytes, num_sms, stream);
 }
 size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
-  return BwdPlan::make(n_faces, n_count, num_sms, 4).workspace(n_faces);
+  return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks).workspace(n_faces);
 }
 
 // ---------------------------------------------------------------------------
