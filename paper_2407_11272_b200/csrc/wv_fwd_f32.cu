@@ -87,6 +87,36 @@ struct ExactPol {
     const F2 la2 = dot2(ax, ay, az, ax, ay, az);
     const F2 lb2 = dot2(bx, by, bz, bx, by, bz);
     const F2 lc2 = dot2(cx, cy, cz, cx, cy, cz);
+    return tail2(R, alpha, la2, lb2, lc2, tacc);
+  }
+  // Lattice-row form: the P points of a thread share x and y, so the x/y
+  // parts of alpha and of the squared corner distances are per-face scalars
+  // (same operation order as common2, hence bit-identical terms).
+  struct Row {
+    float a2, b2, c2, alpha;
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    const float ax = R.v0e.x - qx, ay = R.v0e.y - qy;
+    const float bx = R.v1.x - qx, by = R.v1.y - qy;
+    const float cx = R.v2.x - qx, cy = R.v2.y - qy;
+    Row w;
+    w.a2 = fmaf(ay, ay, ax * ax);
+    w.b2 = fmaf(by, by, bx * bx);
+    w.c2 = fmaf(cy, cy, cx * cx);
+    w.alpha = fmaf(R.n.y, ay, R.n.x * ax);
+    return w;
+  }
+  __device__ __forceinline__ static uint32_t common_row2(const Rec& R, const Row& w, F2 qz,
+                                                         const Ctx&, F2& tacc) {
+    const F2 az = sub2(f2s(R.v0e.z), qz), bz = sub2(f2s(R.v1.z), qz), cz = sub2(f2s(R.v2.z), qz);
+    const F2 alpha = fma2(f2s(R.n.z), az, f2s(w.alpha));
+    const F2 la2 = fma2(az, az, f2s(w.a2));
+    const F2 lb2 = fma2(bz, bz, f2s(w.b2));
+    const F2 lc2 = fma2(cz, cz, f2s(w.c2));
+    return tail2(R, alpha, la2, lb2, lc2, tacc);
+  }
+  __device__ __forceinline__ static uint32_t tail2(const Rec& R, F2 alpha, F2 la2, F2 lb2, F2 lc2,
+                                                   F2& tacc) {
     const F2 la = sqrt2(la2), lb = sqrt2(lb2), lc = sqrt2(lc2);
     // a.b = (|a|^2 + |b|^2 - |v0-v1|^2)/2 etc. (half squared edge lengths are
     // packed): 2 ops instead of 3.  It can cancel only where beta itself is
@@ -151,6 +181,24 @@ struct SoftPol {
     const F2 dx = sub2(f2s(R.c.x), qx), dy = sub2(f2s(R.c.y), qy), dz = sub2(f2s(R.c.z), qz);
     const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
     const F2 s = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
+    return tail2(r2, s, ctx, tacc);
+  }
+  struct Row {
+    float r2, s;
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    const float dx = R.c.x - qx, dy = R.c.y - qy;
+    Row w;
+    w.r2 = fmaf(dy, dy, dx * dx);
+    w.s = fmaf(R.n.x, dy, R.c.w * dx);
+    return w;
+  }
+  __device__ __forceinline__ static uint32_t common_row2(const Rec& R, const Row& w, F2 qz,
+                                                         const Ctx& ctx, F2& tacc) {
+    const F2 dz = sub2(f2s(R.c.z), qz);
+    return tail2(fma2(dz, dz, f2s(w.r2)), fma2(f2s(R.n.y), dz, f2s(w.s)), ctx, tacc);
+  }
+  __device__ __forceinline__ static uint32_t tail2(F2 r2, F2 s, const Ctx& ctx, F2& tacc) {
     float r2l, r2h;
     split(r2, r2l, r2h);
     // |c - q| < eps: on a centroid, the face is skipped and the point flagged

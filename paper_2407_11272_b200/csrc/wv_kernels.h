@@ -31,6 +31,7 @@ struct PointSource {
 };
 
 struct GridSrc {
+  static constexpr bool kRows = false;
   GridDesc g;
   int64_t n0;
   __device__ __forceinline__ void point(int64_t l, float& x, float& y, float& z) const {
@@ -45,7 +46,18 @@ struct GridSrc {
   }
 };
 
+// Lattice nodes taken in runs of consecutive k (the row-mode kernels):
+// identical coordinates to GridSrc, different thread -> node mapping.
+struct RowSrc : GridSrc {
+  static constexpr bool kRows = true;
+};
+// Row mode needs every run of `run` nodes to stay inside one k-row.
+inline bool row_aligned(const GridDesc& g, int64_t n0, int64_t count, int run) {
+  return g.res[2] % run == 0 && n0 % run == 0 && count % run == 0 && count > 0;
+}
+
 struct ListSrc {
+  static constexpr bool kRows = false;
   const float* pts;
   __device__ __forceinline__ void point(int64_t l, float& x, float& y, float& z) const {
     x = pts[3 * l + 0];
@@ -55,6 +67,7 @@ struct ListSrc {
 };
 
 struct ListSrc64 {
+  static constexpr bool kRows = false;
   const double* pts;
   __device__ __forceinline__ void point(int64_t l, double& x, double& y, double& z) const {
     x = pts[3 * l + 0];

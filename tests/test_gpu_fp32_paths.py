@@ -173,3 +173,23 @@ def test_autograd_matches_device_kernels(torch_):
         vv = v.astype(np.float32).astype(np.float64)
         ref = (orc.soft_grad if mode == "soft" else orc.exact_grad)(vv, f, pts, coefs)
         assert rel_err(g.double().cpu().numpy(), ref) <= G_TOL, mode
+
+
+@pytest.mark.parametrize("mode", ["exact", "soft"])
+def test_row_kernels_match_generic_bitwise(torch_, c2, mode):
+    """Row-aligned grid ranges run the lattice-row kernels (x/y parts hoisted
+    per face); they must reproduce the generic point kernels bit for bit on
+    the same f32 coordinates, flags included.  rz=40 (row mode), rz=36
+    (generic grid), and an unaligned slab start."""
+    from paper_2407_11272_b200 import device as D
+    dm = D.DeviceMesh.from_numpy(c2.vertices, c2.faces)
+    for res, n0, count in [((24, 20, 40), 0, None), ((24, 20, 40), 40 * 20 * 5, 40 * 20 * 7),
+                           ((22, 18, 36), 0, None), ((24, 20, 40), 12, 4000)]:
+        grid = ((-1.0, -1.0, -1.0), (1.0, 1.0, 1.0), res)
+        n = int(np.prod(res))
+        count = n - n0 if count is None else count
+        wg, fg = D.forward(dm, mode, "f32", grid=grid, n0=n0, count=count)
+        pts = orc.node_coordinates(*grid)[n0:n0 + count].astype(np.float32)
+        wp, fp = D.forward(dm, mode, "f32", points=torch_.from_numpy(pts).cuda())
+        assert np.array_equal(fg.cpu().numpy(), fp.cpu().numpy())
+        assert wg.cpu().numpy().tobytes() == wp.cpu().numpy().tobytes()
