@@ -90,6 +90,63 @@ struct ExactEdgeBwd {
     g[7] = fma2(m20y, s20c, fma2(m12y, s12c, g[7]));
     g[8] = fma2(m20z, s20c, fma2(m12z, s12c, g[8]));
   }
+  // Lattice-row form (points of one k-row share x and y): the x/y parts of
+  // the corner vectors, their squared lengths and the z components of the
+  // edge moments m = a x b are per-face, per-row scalars.
+  struct Row {
+    float ax, ay, bx, by, cx, cy;  // corner - q, x/y parts
+    float a2, b2, c2;              // x/y parts of |corner - q|^2
+    float m01z, m12z, m20z;        // z components of a x b, b x c, c x a
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    Row w;
+    w.ax = R.a.x - qx; w.ay = R.a.y - qy;
+    w.bx = R.b.x - qx; w.by = R.b.y - qy;
+    w.cx = R.c.x - qx; w.cy = R.c.y - qy;
+    w.a2 = fmaf(w.ay, w.ay, w.ax * w.ax);
+    w.b2 = fmaf(w.by, w.by, w.bx * w.bx);
+    w.c2 = fmaf(w.cy, w.cy, w.cx * w.cx);
+    w.m01z = fmaf(w.ax, w.by, -(w.ay * w.bx));
+    w.m12z = fmaf(w.bx, w.cy, -(w.by * w.cx));
+    w.m20z = fmaf(w.cx, w.ay, -(w.cy * w.ax));
+    return w;
+  }
+  template <bool kUnit>
+  __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
+                                                   float, F2* g) {
+    const F2 az = sub2(f2s(R.a.z), qz), bz = sub2(f2s(R.b.z), qz), cz = sub2(f2s(R.c.z), qz);
+    const F2 a2 = fma2(az, az, f2s(w.a2));
+    const F2 b2 = fma2(bz, bz, f2s(w.b2));
+    const F2 c2 = fma2(cz, cz, f2s(w.c2));
+    const F2 ia = rsqrt2(a2), ib = rsqrt2(b2), ic = rsqrt2(c2);
+    const F2 lb = mul2(b2, ib), lc = mul2(c2, ic);
+    const F2 s01 = fma2(a2, ia, lb), s12 = add2(lb, lc), s20 = fma2(a2, ia, lc);
+    const F2 r01 = rcp2(fma2(s01, s01, f2s(-R.u.x)));
+    const F2 r12 = rcp2(fma2(s12, s12, f2s(-R.u.y)));
+    const F2 r20 = rcp2(fma2(s20, s20, f2s(-R.u.z)));
+    const F2 t01 = mul2(kUnit ? coef : mul2(coef, f2s(R.a.w)), r01);
+    const F2 t12 = mul2(kUnit ? coef : mul2(coef, f2s(R.b.w)), r12);
+    const F2 t20 = mul2(kUnit ? coef : mul2(coef, f2s(R.c.w)), r20);
+    // x/y components of the edge moments (z components are in the row)
+    const F2 m01x = fma2(f2s(w.ay), bz, mul2(az, f2s(-w.by)));
+    const F2 m01y = fma2(az, f2s(w.bx), mul2(f2s(-w.ax), bz));
+    const F2 m12x = fma2(f2s(w.by), cz, mul2(bz, f2s(-w.cy)));
+    const F2 m12y = fma2(bz, f2s(w.cx), mul2(f2s(-w.bx), cz));
+    const F2 m20x = fma2(f2s(w.cy), az, mul2(cz, f2s(-w.ay)));
+    const F2 m20y = fma2(cz, f2s(w.ax), mul2(f2s(-w.cx), az));
+    const F2 s01a = mul2(t01, ia), s20a = mul2(t20, ia);
+    const F2 s01b = mul2(t01, ib), s12b = mul2(t12, ib);
+    const F2 s12c = mul2(t12, ic), s20c = mul2(t20, ic);
+    g[0] = fma2(m20x, s20a, fma2(m01x, s01a, g[0]));
+    g[1] = fma2(m20y, s20a, fma2(m01y, s01a, g[1]));
+    g[2] = fma2(f2s(w.m20z), s20a, fma2(f2s(w.m01z), s01a, g[2]));
+    g[3] = fma2(m12x, s12b, fma2(m01x, s01b, g[3]));
+    g[4] = fma2(m12y, s12b, fma2(m01y, s01b, g[4]));
+    g[5] = fma2(f2s(w.m12z), s12b, fma2(f2s(w.m01z), s01b, g[5]));
+    g[6] = fma2(m20x, s20c, fma2(m12x, s12c, g[6]));
+    g[7] = fma2(m20y, s20c, fma2(m12y, s12c, g[7]));
+    g[8] = fma2(f2s(w.m20z), s20c, fma2(f2s(w.m12z), s12c, g[8]));
+  }
   __device__ __forceinline__ static void finish(const Rec&, const double* acc, double* out9) {
     for (int j = 0; j < 9; ++j) out9[j] = acc[j];
   }
@@ -133,6 +190,51 @@ struct SoftBwd {
     g[8] = fma2(c5, dy, g[8]);
     g[9] = fma2(c5, dz, g[9]);
   }
+  // Lattice-row form: d = c - q has row-constant x/y parts, so r^2, S and
+  // the x/y components of G1 = w x d, G2 = d x u take one op each per pair
+  // and their z components are per-row constants.
+  struct Row {
+    float dx, dy, r2, s;
+    float g1x, g1y, g1z, g2x, g2y, g2z;  // row-constant parts
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    Row w;
+    w.dx = R.c.x - qx;
+    w.dy = R.c.y - qy;
+    w.r2 = fmaf(w.dy, w.dy, w.dx * w.dx);
+    w.s = fmaf(R.n.y, w.dy, R.n.x * w.dx);
+    w.g1x = -(R.w.z * w.dy);                    // + wy dz
+    w.g1y = R.w.z * w.dx;                       // - wx dz
+    w.g1z = fmaf(R.w.x, w.dy, -(R.w.y * w.dx));
+    w.g2x = w.dy * R.u.z;                       // - dz uy
+    w.g2y = -(w.dx * R.u.z);                    // + dz ux
+    w.g2z = fmaf(w.dx, R.u.y, -(w.dy * R.u.x));
+    return w;
+  }
+  template <bool kUnit>
+  __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
+                                                   float eps2, F2* g) {
+    const F2 dz = sub2(f2s(R.c.z), qz);
+    const F2 r2 = fma2(dz, dz, f2s(w.r2));
+    const F2 rs = rsqrt2(r2);
+    const F2 S = fma2(f2s(R.n.z), dz, f2s(w.s));
+    const F2 rs2 = mul2(rs, rs);
+    float r2l, r2h, cl, ch;
+    split(r2, r2l, r2h);
+    split(mul2(mul2(coef, rs2), rs), cl, ch);
+    const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
+    const F2 c5 = mul2(mul2(c3, S), rs2);
+    g[0] = fma2(c3, fma2(f2s(R.w.y), dz, f2s(w.g1x)), g[0]);
+    g[1] = fma2(c3, fma2(f2s(-R.w.x), dz, f2s(w.g1y)), g[1]);
+    g[2] = fma2(c3, f2s(w.g1z), g[2]);
+    g[3] = fma2(c3, fma2(f2s(-R.u.y), dz, f2s(w.g2x)), g[3]);
+    g[4] = fma2(c3, fma2(f2s(R.u.x), dz, f2s(w.g2y)), g[4]);
+    g[5] = fma2(c3, f2s(w.g2z), g[5]);
+    g[6] = add2(g[6], c3);
+    g[7] = fma2(c5, f2s(w.dx), g[7]);
+    g[8] = fma2(c5, f2s(w.dy), g[8]);
+    g[9] = fma2(c5, dz, g[9]);
+  }
   __device__ __forceinline__ static void finish(const Rec& R, const double* a, double* out9) {
     const double t = a[6] / 3.0;
     const double cx = t * R.n.x - a[7], cy = t * R.n.y - a[8], cz = t * R.n.z - a[9];
@@ -166,6 +268,30 @@ __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const Poi
     const float4 xy = ch.xy[j];
     Pol::template pair2<kUnit>(R, f2(xy.x, xy.y), f2(xy.z, xy.w), f2(zc.x, zc.y),
                                f2(zc.z, zc.w), eps2, g);
+  }
+}
+
+// Row mode: the chunk is cut at k-row boundaries (warp-uniform), each run of
+// pairs shares the row's x/y, and the per-face row constants are computed
+// once per run.  Needs rz and the range start even (pairs never straddle).
+template <class Pol, bool kUnit>
+__device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const PointChunk& ch,
+                                           int n_pairs, int64_t flat0, int64_t rz, float eps2,
+                                           F2* g) {
+  int j = 0;
+  int k = (int)(flat0 % rz);  // k of the chunk's first node
+  while (j < n_pairs) {
+    int run = (int)((rz - k) >> 1);
+    if (run > n_pairs - j) run = n_pairs - j;
+    const float4 xy0 = ch.xy[j];
+    const typename Pol::Row w = Pol::row(R, xy0.x, xy0.z);
+#pragma unroll 2
+    for (int e = j + run; j < e; ++j) {
+      const float4 zc = ch.zc[j];
+      if (zc.z == 0.0f && zc.w == 0.0f) continue;  // warp-uniform (_kernels.py:182-184)
+      Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, g);
+    }
+    k = 0;
   }
 }
 
@@ -204,7 +330,9 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         c = coefs[c0 + i] * coef_scale;
         // zero-coefficient points contribute nothing; park them far away so
         // the other half of their pair never sees an on-segment 0 * inf
-        if (c != 0.0f) src.point(c0 + i, x, y, z);
+        // (row mode keeps the row's x/y and parks z only)
+        if (c != 0.0f || Src::kRows) src.point(c0 + i, x, y, z);
+        if (c == 0.0f) z = 1.0e6f;
       }
       float* xy = reinterpret_cast<float*>(&chunk.xy[i >> 1]);
       float* zc = reinterpret_cast<float*>(&chunk.zc[i >> 1]);
@@ -217,7 +345,14 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     F2 g[Pol::kAcc];
 #pragma unroll
     for (int j = 0; j < Pol::kAcc; ++j) g[j] = f2(0.0f, 0.0f);
-    if (unit) {
+    if constexpr (Src::kRows) {
+      const int64_t flat0 = src.n0 + c0;
+      if (unit) {
+        chunk_rows<Pol, true>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, g);
+      } else {
+        chunk_rows<Pol, false>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, g);
+      }
+    } else if (unit) {
       chunk_loop<Pol, true>(R, chunk, n_pairs, eps2, g);
     } else {
       chunk_loop<Pol, false>(R, chunk, n_pairs, eps2, g);
@@ -295,7 +430,12 @@ static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps
   }
   const float cs = (float)(coef_scale * Pol::kCoefScale);
   dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits);
-  if (ps.kind == PointSource::kGrid) {
+  if (ps.kind == PointSource::kGrid && ps.grid.res[2] >= 16 &&
+      row_aligned(ps.grid, ps.n0, 2 * ((n_count + 1) / 2), 2)) {
+    RowSrc src{{ps.grid, ps.n0}};
+    bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
+        hdr, recs, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+  } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
     bwd_f32_kernel<Pol, GridSrc><<<grid, kBwdThreads, 0, stream>>>(
         hdr, recs, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);

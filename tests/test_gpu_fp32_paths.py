@@ -193,3 +193,31 @@ def test_row_kernels_match_generic_bitwise(torch_, c2, mode):
         wp, fp = D.forward(dm, mode, "f32", points=torch_.from_numpy(pts).cuda())
         assert np.array_equal(fg.cpu().numpy(), fp.cpu().numpy())
         assert wg.cpu().numpy().tobytes() == wp.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("mode", ["exact", "soft"])
+def test_row_backward_matches_generic_and_oracle(torch_, c2, mode):
+    """Grid backward in row mode (k-row runs, per-face row constants) vs the
+    generic point-list kernel on the same f32 nodes and coefficients, and vs
+    the f64 oracle.  Includes zero coefficients (skipped / parked pairs), an
+    odd count, a slab start inside a row, and rz=18 (short runs)."""
+    torch = torch_
+    from paper_2407_11272_b200 import device as D
+    dm = D.DeviceMesh.from_numpy(c2.vertices, c2.faces)
+    rng = np.random.default_rng(9)
+    for res, n0, count in [((12, 10, 40), 0, 4800), ((12, 10, 40), 402, 3001),
+                           ((14, 12, 18), 36, 2000)]:
+        grid = ((-1.0, -1.0, -1.0), (1.0, 1.0, 1.0), res)
+        coefs = rng.normal(size=count)
+        coefs[rng.random(count) < 0.3] = 0.0
+        ct = torch.as_tensor(coefs, dtype=torch.float32)
+        got = D.vertex_grad(dm, D.face_grad(dm, mode, "f32", ct, grid=grid, n0=n0,
+                                            count=count)).cpu().numpy()
+        pts32 = orc.node_coordinates(*grid)[n0:n0 + count].astype(np.float32)
+        gen = D.vertex_grad(dm, D.face_grad(dm, mode, "f32", ct,
+                                            points=torch.from_numpy(pts32).cuda())).cpu().numpy()
+        assert rel_err(got, gen) <= 2e-6
+        ofn = orc.soft_grad if mode == "soft" else orc.exact_grad
+        ref = ofn(c2.vertices, c2.faces, pts32.astype(np.float64),
+                  coefs.astype(np.float32).astype(np.float64), chunk=256)
+        assert rel_err(got, ref) <= G_TOL
