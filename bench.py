@@ -53,6 +53,17 @@ EXACT_FWD_MUFU = 4
 EXACT_BWD_MUFU = 6
 
 
+def traffic(workload: str, kernel: str):
+    """DRAM bytes per launch of ``kernel`` from a committed ncu capture."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(workload)
+    except (OSError, ValueError):
+        return None
+    if not t or t["kernel"].split("<")[0] not in kernel:
+        return None
+    return t["read"] + t["write"]
+
+
 def executed(alg_tf, alg_flops, exec_flops, mufu, ms, peak, clk_mhz):
     """Roofline of one kernel: pinned-algorithmic rate plus the utilisation of
     the two pipes it actually runs on (FP32 FMA pipe, XU/MUFU pipe at 16 ops
@@ -393,6 +404,8 @@ def run_ours(args):
             if bwd_ms >= fwd_ms else ("exact_fwd (fwd_f32_kernel<ExactPol,RowSrc>)", fwd_ms,
                                       fwd_tf)
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        step_tf = (EXACT_FWD_FLOPS * cnt * F + EXACT_BWD_FLOPS * cnt * active) \
+            / (ms_step / 1e3) / 1e12
         line = {
             "metric": "point-triangle solid-angle evals/sec fwd & fwd+bwd; 256^3 voxelize ms",
             "value": value, "unit": "pairs/s (exact fwd+bwd)", "n_gpus": world,
@@ -409,7 +422,8 @@ def run_ours(args):
             "voxelize_ms": fwd_ms,
             "loss": float(loss),
             "roofline": {"bound": "fp32", "achieved": dom[2], "peak": peak, "unit": "TFLOP/s",
-                         "frac": dom[2] / peak, "traffic": None, "kernel": dom[0],
+                         "frac": dom[2] / peak, "traffic": traffic(w.name, dom[0]),
+                         "traffic_unit": "bytes per launch", "kernel": dom[0],
                          "kernel_ms": dom[1],
                          "flops_per_pair": EXACT_BWD_FLOPS if dom[0].startswith("exact_bwd")
                          else EXACT_FWD_FLOPS,
@@ -418,8 +432,10 @@ def run_ours(args):
                          "peak_measured": fp32_meas,
                          "peak_measured_source": "tools/ffma2_probe (FFMA/FFMA2 chains, this "
                                                  "GPU, before the timed region)",
-                         "traffic_note": "dram bytes per launch from ncu --set full: "
-                                         "profiles/README.md (MB-scale, negligible)",
+                         "traffic_note": "dram read+write bytes per launch of this kernel "
+                                         "from one ncu --set full capture "
+                                         "(profiles/traffic.json); null if not captured for "
+                                         "this workload",
                          "frac_note": "achieved uses the pinned algorithmic FLOPs/pair (SURVEY "
                                       "8d); the kernels execute fewer (roofline_fwd/bwd "
                                       "executed_flops_per_pair), so frac may exceed 1 -- "
@@ -428,11 +444,9 @@ def run_ours(args):
                                      fwd_ms, peak, clk_mhz),
             "roofline_bwd": executed(bwd_tf, EXACT_BWD_FLOPS, EXACT_BWD_EXEC_FLOPS, EXACT_BWD_MUFU,
                                      bwd_ms, peak, clk_mhz),
-            "roofline_step": {"achieved": (EXACT_FWD_FLOPS + EXACT_BWD_FLOPS) * w.pairs
-                              / (ms_step / 1e3) / 1e12,
-                              "frac": (EXACT_FWD_FLOPS + EXACT_BWD_FLOPS) * w.pairs
-                              / (ms_step / 1e3) / 1e12 / peak,
-                              "note": "whole fwd+bwd step at the pinned 233 FLOP/pair"},
+            "roofline_step": {"achieved": step_tf, "frac": step_tf / peak,
+                              "note": "whole step: 63 FLOP per forward pair + 170 per "
+                                      "backward pair actually evaluated (active faces)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
