@@ -227,6 +227,31 @@ int wv_loss_terms_f64(const double *values, const uint8_t *flags, const double *
                       void *workspace, size_t workspace_bytes, void *stream);
 int wv_loss_finalize(double *sums, void *stream);
 
+/* ---- reconstruction metrics (metrics.py:43-150), bit-identical ------------
+ * wv_splitmix64_uniform: out[i] = (SplitMix64(seed + (i+1)*golden) >> 11)
+ *   * 2^-53, i < count (replaces splitmix64_uniform, metrics.py:43-51).
+ * wv_surface_cdf: per face area 0.5*|(v1-v0)x(v2-v0)| (numpy's expression
+ *   order), cdf = np.cumsum(areas), *total = np.sum(areas) (numpy pairwise
+ *   order); total stays on the device.  faces int64 (F,3), vertices f64.
+ * wv_sample_surface: n points by area (metrics.py:58-93): face =
+ *   searchsorted(cdf, r[3i]*total, 'right') clamped, folded barycentrics
+ *   r[3i+1], r[3i+2]; out (n,3) f64.
+ * wv_nearest_distances: out[i] = min_j |q_i - t_j| (brute force, equal bit
+ *   for bit to the reference's k-d tree, metrics.py:96-104).  nt >= 1.
+ * wv_pairwise_sum: *out = np.sum(x) (numpy pairwise summation order). */
+int wv_splitmix64_uniform(uint64_t seed, int64_t count, double *out, void *stream);
+size_t wv_pairwise_sum_workspace_bytes(int64_t n);
+int wv_pairwise_sum(const double *x, int64_t n, double *out, void *workspace,
+                    size_t workspace_bytes, void *stream);
+int wv_surface_cdf(const double *vertices, const int64_t *faces, int64_t n_faces, double *areas,
+                   double *cdf, double *total, void *workspace, size_t workspace_bytes,
+                   void *stream);
+int wv_sample_surface(const double *vertices, const int64_t *faces, int64_t n_faces,
+                      const double *cdf, const double *total, uint64_t seed, int64_t n,
+                      double *out, void *stream);
+int wv_nearest_distances(const double *queries, int64_t n_queries, const double *targets,
+                         int64_t n_targets, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

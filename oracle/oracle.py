@@ -18,6 +18,9 @@ numpy the reference host-side staging it needs:
 * ``occupancy_loss_grad`` <- grad.py:71-127
 * ``exact_loss_grad``     <- NEW (exact d(Omega)/dv), same
                              loss definition with the exact forward.
+* ``splitmix64_uniform``, ``sample_surface``, ``nearest_distances``,
+  ``chamfer_distance``, ``hausdorff_distance`` <- metrics.py:43-130
+                             (reconstruction metrics).
 
 Parity is pinned: ``tests/test_oracle_golden.py`` checks every function here
 bit-for-bit against fixtures produced by importing the reference itself
@@ -287,3 +290,58 @@ def solid_angle_fd_grad(vertices, faces, points, coefs, h=1e-6):
             wm, _ = winding_number_batch(vm, faces, points, threads=1)
             out[vi, c] = float(((wp - wm) * cf).sum()) / (2 * h)
     return out
+
+
+# ---------------------------------------------------------------------------
+# reconstruction metrics (metrics.py:43-130)
+
+_SM_GOLD = np.uint64(0x9E3779B97F4A7C15)
+_SM_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_SM_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64_uniform(seed: int, count: int) -> np.ndarray:
+    """metrics.py:43-51: counter-based SplitMix64, top 53 bits -> [0, 1)."""
+    i = np.arange(1, int(count) + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(int(seed) & ((1 << 64) - 1)) + i * _SM_GOLD
+        z = (z ^ (z >> np.uint64(30))) * _SM_M1
+        z = (z ^ (z >> np.uint64(27))) * _SM_M2
+    z ^= z >> np.uint64(31)
+    return (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def sample_surface(vertices, faces, n: int, seed: int) -> np.ndarray:
+    """metrics.py:58-93: faces by area (searchsorted on the cumulative
+    areas, side="right"), folded uniform barycentrics."""
+    tri = triangle_corners(vertices, faces)
+    e1, e2 = tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]
+    areas = 0.5 * np.sqrt((np.cross(e1, e2) ** 2).sum(axis=1))
+    total = float(areas.sum())
+    r = splitmix64_uniform(seed, 3 * int(n))
+    face = np.minimum(np.searchsorted(np.cumsum(areas), r[0::3] * total, side="right"),
+                      len(areas) - 1)
+    u, v = r[1::3].copy(), r[2::3].copy()
+    flip = u + v > 1.0
+    u[flip], v[flip] = 1.0 - u[flip], 1.0 - v[flip]
+    c = tri[face]
+    return (c[:, 0] + u[:, None] * (c[:, 1] - c[:, 0])) + v[:, None] * (c[:, 2] - c[:, 0])
+
+
+def nearest_distances(q, t, block: int = 512) -> np.ndarray:
+    """Brute-force nearest distances (the scan metrics.py:96-104 equals)."""
+    q = _c(q, np.float64).reshape(-1, 3)
+    t = _c(t, np.float64).reshape(-1, 3)
+    out = np.empty(len(q))
+    for s in range(0, len(q), block):
+        d = q[s:s + block, None, :] - t[None, :, :]
+        out[s:s + block] = np.sqrt((d * d).sum(axis=2).min(axis=1))
+    return out
+
+
+def chamfer_distance(a, b) -> float:
+    return 0.5 * (float(nearest_distances(a, b).mean()) + float(nearest_distances(b, a).mean()))
+
+
+def hausdorff_distance(a, b) -> float:
+    return max(float(nearest_distances(a, b).max()), float(nearest_distances(b, a).max()))

@@ -17,6 +17,8 @@ from .fieldio import load_field, save_field
 from .morph import MorphConfig, MorphReport, morph
 from .openmesh import flipped_duplication, vertex_normals
 from .recon import laplacian_smooth, marching_cubes
+from .metrics import (chamfer_distance, evaluate_reconstruction, hausdorff_distance,
+                      sample_surface, splitmix64_uniform)
 
 __version__ = "0.1.0"
 
@@ -30,5 +32,7 @@ __all__ = [
     "WindingNumber", "winding_number",
     "save_field", "load_field", "MorphConfig", "MorphReport", "morph",
     "flipped_duplication", "vertex_normals", "marching_cubes", "laplacian_smooth",
+    "splitmix64_uniform", "sample_surface", "chamfer_distance", "hausdorff_distance",
+    "evaluate_reconstruction",
     "__version__",
 ]

@@ -37,6 +37,8 @@ EXPORTED = (
     "wv_exact_bwd_points_f64", "wv_soft_bwd_grid_f64", "wv_soft_bwd_points_f64",
     "wv_face_to_vertex", "wv_loss_workspace_bytes", "wv_loss_terms_f32", "wv_loss_terms_f64",
     "wv_loss_finalize", "wv_mc_classify", "wv_mc_edges", "wv_mc_vertices", "wv_mc_emit",
+    "wv_splitmix64_uniform", "wv_pairwise_sum_workspace_bytes", "wv_pairwise_sum",
+    "wv_surface_cdf", "wv_sample_surface", "wv_nearest_distances",
 )
 
 
@@ -98,6 +100,12 @@ def _declare(lib):
         "wv_mc_edges": ([P, I, Grid, D, P, P], I),
         "wv_mc_vertices": ([P, I, Grid, D, P, P, P, P], I),
         "wv_mc_emit": ([P, P, P, I, P, P, P, Grid, P, P], I),
+        "wv_splitmix64_uniform": ([ctypes.c_uint64, I64, P, P], I),
+        "wv_pairwise_sum_workspace_bytes": ([I64], SZ),
+        "wv_pairwise_sum": ([P, I64, P, P, SZ, P], I),
+        "wv_surface_cdf": ([P, P, I64, P, P, P, P, SZ, P], I),
+        "wv_sample_surface": ([P, P, I64, P, P, ctypes.c_uint64, I64, P, P], I),
+        "wv_nearest_distances": ([P, I64, P, I64, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -368,4 +368,46 @@ int wv_loss_finalize(double* sums, void* stream) {
   return wv::launch_loss_finalize(sums, as_stream(stream));
 }
 
+// ---- reconstruction metrics ---------------------------------------------------
+int wv_splitmix64_uniform(uint64_t seed, int64_t count, double* out, void* stream) {
+  if (count < 0 || (count > 0 && out == nullptr)) return WV_ERR_ARG;
+  return wv::launch_splitmix(seed, count, out, sm_count(), as_stream(stream));
+}
+
+size_t wv_pairwise_sum_workspace_bytes(int64_t n) { return wv::pairwise_workspace_bytes(n); }
+
+int wv_pairwise_sum(const double* x, int64_t n, double* out, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (n < 0 || out == nullptr || (n > 0 && x == nullptr)) return WV_ERR_ARG;
+  return wv::launch_pairwise_sum(x, n, out, workspace, workspace_bytes, as_stream(stream));
+}
+
+int wv_surface_cdf(const double* vertices, const int64_t* faces, int64_t n_faces, double* areas,
+                   double* cdf, double* total, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  if (n_faces <= 0 || vertices == nullptr || faces == nullptr || areas == nullptr ||
+      cdf == nullptr || total == nullptr)
+    return WV_ERR_ARG;
+  return wv::launch_surface_cdf(vertices, faces, n_faces, areas, cdf, total, workspace,
+                                workspace_bytes, sm_count(), as_stream(stream));
+}
+
+int wv_sample_surface(const double* vertices, const int64_t* faces, int64_t n_faces,
+                      const double* cdf, const double* total, uint64_t seed, int64_t n,
+                      double* out, void* stream) {
+  if (n < 0 || n_faces <= 0) return WV_ERR_ARG;
+  if (n > 0 && (vertices == nullptr || faces == nullptr || cdf == nullptr || total == nullptr ||
+                out == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_sample_surface(vertices, faces, n_faces, cdf, total, seed, n, out, sm_count(),
+                                   as_stream(stream));
+}
+
+int wv_nearest_distances(const double* queries, int64_t n_queries, const double* targets,
+                         int64_t n_targets, double* out, void* stream) {
+  if (n_queries < 0 || n_targets < 1 || targets == nullptr) return WV_ERR_ARG;
+  if (n_queries > 0 && (queries == nullptr || out == nullptr)) return WV_ERR_ARG;
+  return wv::launch_nearest(queries, n_queries, targets, n_targets, out, as_stream(stream));
+}
+
 }  // extern "C"

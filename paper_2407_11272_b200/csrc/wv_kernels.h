@@ -190,4 +190,18 @@ int launch_loss_f64(const double* values, const uint8_t* flags, const double* ta
                     size_t ws_bytes, cudaStream_t stream);
 int launch_loss_finalize(double* sums, cudaStream_t stream);
 
+// reconstruction metrics (wv_metrics.cu)
+int launch_splitmix(uint64_t seed, int64_t count, double* out, int num_sms, cudaStream_t s);
+size_t pairwise_workspace_bytes(int64_t n);
+int launch_pairwise_sum(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes,
+                        cudaStream_t s);
+int launch_surface_cdf(const double* v, const int64_t* f, int64_t n_faces, double* areas,
+                       double* cdf, double* total, void* ws, size_t ws_bytes, int num_sms,
+                       cudaStream_t s);
+int launch_sample_surface(const double* v, const int64_t* f, int64_t n_faces, const double* cdf,
+                          const double* total, uint64_t seed, int64_t n, double* out, int num_sms,
+                          cudaStream_t s);
+int launch_nearest(const double* q, int64_t nq, const double* t, int64_t nt, double* out,
+                   cudaStream_t s);
+
 }  // namespace wv

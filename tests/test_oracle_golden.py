@@ -151,3 +151,36 @@ def test_solid_angle_known_answers():
     w, _ = orc.winding_number_batch(np.array([[0, 0, 0], [1.0, 0, 0], [0, 1.0, 0]]),
                                     [[0, 1, 2]], np.array([[0.2, 0.3, 0.7]]))
     assert abs(float(g["cube_face_center"]) - 0.5) < 1e-9
+
+
+def big_vector():
+    """Same seeds as tests/golden/make_golden.py:big_vector."""
+    return (np.random.default_rng(62).random(100003)
+            * 10.0 ** np.random.default_rng(63).integers(-3, 3, size=100003))
+
+
+def test_metrics_oracle_bit_exact():
+    """Reconstruction metrics (metrics.py:43-150) restated in numpy vs the
+    reference's own outputs: SplitMix64 streams, area-weighted samples (with
+    zero-area faces present), nearest distances, Chamfer / Hausdorff, and the
+    evaluate_reconstruction statistics."""
+    g = golden("metrics")
+    assert np.array_equal(orc.splitmix64_uniform(7, 10000), g["u_seed7"])
+    assert np.array_equal(orc.splitmix64_uniform((1 << 64) - 3, 999), g["u_seed_big"])
+    assert orc.sample_surface(g["ico_vertices"], g["ico_faces"], 4001, 3).tobytes() \
+        == g["s_ico"].tobytes()
+    assert orc.sample_surface(g["degen_vertices"], g["degen_faces"], 2000, 11).tobytes() \
+        == g["s_degen"].tobytes()
+    assert orc.nearest_distances(g["pa"], g["pb"]).tobytes() == g["nn_ab"].tobytes()
+    assert orc.chamfer_distance(g["pa"], g["pb"]) == float(g["chamfer_ab"])
+    assert orc.hausdorff_distance(g["pa"], g["pb"]) == float(g["hausdorff_ab"])
+    ch, hd = [], []
+    for r in range(3):
+        a = orc.sample_surface(g["ico_vertices"], g["ico_faces"], 3000, 5 + r)
+        b = orc.sample_surface(g["cube_vertices"], g["cube_faces"], 3000, 5 + r)
+        ch.append(orc.chamfer_distance(a, b))
+        hd.append(orc.hausdorff_distance(a, b))
+    got = np.array([np.mean(ch), np.std(ch), np.mean(hd), np.std(hd)])
+    assert got.tobytes() == g["recon"].tobytes()
+    big = big_vector()
+    assert float(np.sum(big)) == float(g["big_sum"]) and float(big.mean()) == float(g["big_mean"])
