@@ -22,7 +22,7 @@
 namespace wv {
 
 template <class Pol, class Src>
-__global__ void __launch_bounds__(Pol::kThreads, Pol::kMinBlocks)
+__global__ void __launch_bounds__(Pol::kThreads, Src::kRows ? Pol::kMinBlocksRow : Pol::kMinBlocks)
 fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
                int64_t n_faces, Src src, int64_t n_count, int64_t tiles_per_split, OutF32 o) {
   using Rec = typename Pol::Rec;

@@ -73,6 +73,7 @@ struct ExactPol {
   static constexpr int kConsumerWarps = 4;
   static constexpr int kThreads = kConsumerWarps * 32;
   static constexpr int kMinBlocks = 4;
+  static constexpr int kMinBlocksRow = 4;  // 5 (96 regs) spills and measured 2% slower
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (2.0 * kPi);
   struct Ctx {};
@@ -170,6 +171,7 @@ struct SoftPol {
   static constexpr int kConsumerWarps = 4;
   static constexpr int kThreads = kConsumerWarps * 32;
   static constexpr int kMinBlocks = 5;
+  static constexpr int kMinBlocksRow = 5;
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (8.0 * kPi);
   struct Ctx {
