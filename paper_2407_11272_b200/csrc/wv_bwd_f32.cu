@@ -394,12 +394,14 @@ struct BwdPlan {
     BwdPlan p;
     p.blocks_x = (n_faces + kBwdThreads - 1) / kBwdThreads;
     if (p.blocks_x < 1) p.blocks_x = 1;
-    const int64_t want = (int64_t)num_sms * min_blocks * 4;  // ~4 waves for balance
-    int64_t s = (want + p.blocks_x - 1) / p.blocks_x;
-    const int64_t max_s = (n_count + kBwdChunk - 1) / kBwdChunk;  // >= one chunk per split
-    if (s > max_s) s = max_s;
-    if (s > 4096) s = 4096;
-    if (s < 1) s = 1;
+    const int64_t slots = (int64_t)num_sms * min_blocks;
+    int64_t lo = (4 * slots + p.blocks_x - 1) / p.blocks_x;  // >= ~4 waves
+    int64_t hi = 4 * lo;  // then the split count with the fullest last wave
+    int64_t max_s = (n_count + kBwdChunk - 1) / kBwdChunk;  // >= one chunk per split
+    if (max_s > 4096) max_s = 4096;
+    if (lo > max_s) lo = max_s;
+    if (hi > max_s) hi = max_s;
+    int64_t s = best_splits(p.blocks_x, lo, hi, slots);
     p.pts_per_split = (n_count + s - 1) / s;
     p.pts_per_split = ((p.pts_per_split + kBwdChunk - 1) / kBwdChunk) * kBwdChunk;
     p.splits = (int)((n_count + p.pts_per_split - 1) / p.pts_per_split);

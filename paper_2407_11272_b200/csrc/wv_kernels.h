@@ -102,14 +102,39 @@ struct OutF32 {
 // face range so that >= ~2 waves of CTAs exist; partials are summed in fixed
 // split order by a finalize kernel (deterministic).  Depends only on the
 // problem shape, never on timing.
+// Work splits against wave quantization: every CTA of these kernels does the
+// same work, so a grid of W waves (W = CTAs / resident slots) costs ceil(W)
+// wave times.  Pick the split count in [s_lo, s_hi] whose last wave is
+// fullest (a larger count must win by > 0.5% to be preferred).
+inline int64_t best_splits(int64_t blocks, int64_t s_lo, int64_t s_hi, int64_t slots) {
+  if (s_lo < 1) s_lo = 1;
+  if (s_hi < s_lo) s_hi = s_lo;
+  int64_t best = s_lo;
+  double best_eff = -1.0;
+  for (int64_t s = s_lo; s <= s_hi; ++s) {
+    const int64_t ctas = blocks * s;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (eff > best_eff + 0.005) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+// Forward: split the face range over blockIdx.y when the node blocks alone
+// give few waves (small grids, or one slab of a multi-GPU run).
 inline int choose_splits(int64_t blocks_x, int64_t n_tiles, int num_sms, int ctas_per_sm) {
   if (n_tiles <= 1) return 1;
-  const int64_t want = (int64_t)num_sms * ctas_per_sm * 2;
-  if (blocks_x >= want) return 1;
-  int64_t s = (want + blocks_x - 1) / blocks_x;
-  if (s > n_tiles) s = n_tiles;
-  if (s > 64) s = 64;
-  return (int)(s < 1 ? 1 : s);
+  const int64_t slots = (int64_t)num_sms * ctas_per_sm;
+  if (blocks_x >= 16 * slots) return 1;  // >= 16 waves: the last one costs < 6%
+  int64_t lo = (2 * slots + blocks_x - 1) / blocks_x;  // at least 2 waves
+  int64_t hi = 4 * lo;
+  const int64_t cap = n_tiles < 64 ? n_tiles : 64;
+  if (lo > cap) lo = cap;
+  if (hi > cap) hi = cap;
+  return (int)best_splits(blocks_x, lo, hi, slots);
 }
 
 // packing (wv_pack.cu)
