@@ -22,6 +22,20 @@ from .grad import device_loss_grad
 __all__ = ["BatchOccupancyLoss", "batch_occupancy_loss", "DeformationNet"]
 
 
+# meshes are independent: round-robin them over a few streams so one mesh's
+# kernels fill the wave tails of another's (each mesh alone is ~1 ms of work)
+N_STREAMS = 4
+_STREAMS: dict = {}
+
+
+def _side_streams(dev):
+    st = _STREAMS.get(dev)
+    if st is None:
+        st = [torch.cuda.Stream(device=dev) for _ in range(N_STREAMS)]
+        _STREAMS[dev] = st
+    return st
+
+
 class BatchOccupancyLoss(torch.autograd.Function):
     @staticmethod
     def forward(ctx, verts, faces, grid, targets, mode, precision, csr):
@@ -29,11 +43,19 @@ class BatchOccupancyLoss(torch.autograd.Function):
         losses = torch.empty(B, dtype=torch.float64, device=verts.device)
         grads = torch.empty((B,) + tuple(verts.shape[1:]), dtype=verts.dtype,
                             device=verts.device)
+        main = torch.cuda.current_stream(verts.device)
+        side = _side_streams(verts.device)
+        for s in side:
+            s.wait_stream(main)
         for b in range(B):
-            m = DeviceMesh(verts[b].detach().contiguous(), faces, _csr=csr)
-            sums, g = device_loss_grad(m, grid, targets[b], None, mode=mode, precision=precision)
-            losses[b] = sums[4]
-            grads[b] = (g * sums[3]).to(verts.dtype)
+            with torch.cuda.stream(side[b % len(side)]):
+                m = DeviceMesh(verts[b].detach().contiguous(), faces, _csr=csr)
+                sums, g = device_loss_grad(m, grid, targets[b], None, mode=mode,
+                                           precision=precision)
+                losses[b] = sums[4]
+                grads[b] = (g * sums[3]).to(verts.dtype)
+        for s in side:
+            main.wait_stream(s)
         ctx.save_for_backward(grads)
         return losses
 
