@@ -90,30 +90,52 @@ struct ExactEdgeBwd {
     g[7] = fma2(m20y, s20c, fma2(m12y, s12c, g[7]));
     g[8] = fma2(m20z, s20c, fma2(m12z, s12c, g[8]));
   }
-  // Lattice-row form (points of one k-row share x and y): the x/y parts of
-  // the corner vectors, their squared lengths and the z components of the
-  // edge moments m = a x b are per-face, per-row scalars.
+  // Lattice-row form (points of one k-row share x and y).
+  //  * The edge moment is m = a x b = a x e with the edge vector e = Q - P
+  //    (a x a = 0): with a's x/y fixed along the row, m's x/y components are
+  //    affine in a_z and its z component is a row constant -- and a x e has
+  //    no |a|/|e|-fold cancellation (a x b has, for far points).
+  //  * So sum_q m(q) s(q) = K sum_q s(q) + E sum_q s(q) a_z(q) per (edge,
+  //    corner): a pair only adds to 12 running sums (6 sums of s, 6 of
+  //    s * corner z); the moments are formed once per row run (flush_row, in
+  //    fp64, into the face's accumulators).
+  //  * The three edge reciprocals share ONE MUFU.RCP: 1/d01 = R d12 d20 with
+  //    R = 1/(d01 d12 d20) (products of O(|x|^2) terms: safe for coordinates
+  //    within ~1e6 of the origin and points farther than ~1e-6 from an edge;
+  //    R is clamped so the rest stays finite).
+  // Per pair: 41 FP32 lane-ops + 4 MUFU (was 53 + 6).
+  static constexpr int kRowAcc = 12;
   struct Row {
-    float ax, ay, bx, by, cx, cy;  // corner - q, x/y parts
     float a2, b2, c2;              // x/y parts of |corner - q|^2
-    float m01z, m12z, m20z;        // z components of a x b, b x c, c x a
+    float k01x, k01y, m01z;        // m01 = a x e01: x = k01x - e01y a_z, y = k01y + e01x a_z
+    float k12x, k12y, m12z;        // m12 = b x e12 (b_z)
+    float k20x, k20y, m20z;        // m20 = c x e20 (c_z)
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    const float ax = R.a.x - qx, ay = R.a.y - qy;
+    const float bx = R.b.x - qx, by = R.b.y - qy;
+    const float cx = R.c.x - qx, cy = R.c.y - qy;
+    const float e01x = R.b.x - R.a.x, e01y = R.b.y - R.a.y, e01z = R.b.z - R.a.z;
+    const float e12x = R.c.x - R.b.x, e12y = R.c.y - R.b.y, e12z = R.c.z - R.b.z;
+    const float e20x = R.a.x - R.c.x, e20y = R.a.y - R.c.y, e20z = R.a.z - R.c.z;
     Row w;
-    w.ax = R.a.x - qx; w.ay = R.a.y - qy;
-    w.bx = R.b.x - qx; w.by = R.b.y - qy;
-    w.cx = R.c.x - qx; w.cy = R.c.y - qy;
-    w.a2 = fmaf(w.ay, w.ay, w.ax * w.ax);
-    w.b2 = fmaf(w.by, w.by, w.bx * w.bx);
-    w.c2 = fmaf(w.cy, w.cy, w.cx * w.cx);
-    w.m01z = fmaf(w.ax, w.by, -(w.ay * w.bx));
-    w.m12z = fmaf(w.bx, w.cy, -(w.by * w.cx));
-    w.m20z = fmaf(w.cx, w.ay, -(w.cy * w.ax));
+    w.a2 = fmaf(ay, ay, ax * ax);
+    w.b2 = fmaf(by, by, bx * bx);
+    w.c2 = fmaf(cy, cy, cx * cx);
+    w.k01x = ay * e01z;
+    w.k01y = -(ax * e01z);
+    w.m01z = fmaf(ax, e01y, -(ay * e01x));
+    w.k12x = by * e12z;
+    w.k12y = -(bx * e12z);
+    w.m12z = fmaf(bx, e12y, -(by * e12x));
+    w.k20x = cy * e20z;
+    w.k20y = -(cx * e20z);
+    w.m20z = fmaf(cx, e20y, -(cy * e20x));
     return w;
   }
   template <bool kUnit>
   __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
-                                                   float, F2* g) {
+                                                   float, F2* z) {
     const F2 az = sub2(f2s(R.a.z), qz), bz = sub2(f2s(R.b.z), qz), cz = sub2(f2s(R.c.z), qz);
     const F2 a2 = fma2(az, az, f2s(w.a2));
     const F2 b2 = fma2(bz, bz, f2s(w.b2));
@@ -121,31 +143,64 @@ struct ExactEdgeBwd {
     const F2 ia = rsqrt2(a2), ib = rsqrt2(b2), ic = rsqrt2(c2);
     const F2 lb = mul2(b2, ib), lc = mul2(c2, ic);
     const F2 s01 = fma2(a2, ia, lb), s12 = add2(lb, lc), s20 = fma2(a2, ia, lc);
-    const F2 r01 = rcp2(fma2(s01, s01, f2s(-R.u.x)));
-    const F2 r12 = rcp2(fma2(s12, s12, f2s(-R.u.y)));
-    const F2 r20 = rcp2(fma2(s20, s20, f2s(-R.u.z)));
-    const F2 t01 = mul2(kUnit ? coef : mul2(coef, f2s(R.a.w)), r01);
-    const F2 t12 = mul2(kUnit ? coef : mul2(coef, f2s(R.b.w)), r12);
-    const F2 t20 = mul2(kUnit ? coef : mul2(coef, f2s(R.c.w)), r20);
-    // x/y components of the edge moments (z components are in the row)
-    const F2 m01x = fma2(f2s(w.ay), bz, mul2(az, f2s(-w.by)));
-    const F2 m01y = fma2(az, f2s(w.bx), mul2(f2s(-w.ax), bz));
-    const F2 m12x = fma2(f2s(w.by), cz, mul2(bz, f2s(-w.cy)));
-    const F2 m12y = fma2(bz, f2s(w.cx), mul2(f2s(-w.bx), cz));
-    const F2 m20x = fma2(f2s(w.cy), az, mul2(cz, f2s(-w.ay)));
-    const F2 m20y = fma2(cz, f2s(w.ax), mul2(f2s(-w.cx), az));
+    const F2 d01 = fma2(s01, s01, f2s(-R.u.x));
+    const F2 d12 = fma2(s12, s12, f2s(-R.u.y));
+    const F2 d20 = fma2(s20, s20, f2s(-R.u.z));
+    const F2 p12 = mul2(d12, d20);
+    F2 rr = rcp2(mul2(d01, p12));
+    {
+      float lo, hi;
+      split(rr, lo, hi);
+      rr = f2(fminf(lo, 3.0e38f), fminf(hi, 3.0e38f));
+    }
+    const F2 cr = mul2(coef, rr);  // coef / (d01 d12 d20)
+    const F2 q0 = mul2(cr, d01);
+    const F2 t01 = mul2(kUnit ? cr : mul2(cr, f2s(R.a.w)), p12);
+    const F2 t12 = mul2(kUnit ? q0 : mul2(q0, f2s(R.b.w)), d20);
+    const F2 t20 = mul2(kUnit ? q0 : mul2(q0, f2s(R.c.w)), d12);
     const F2 s01a = mul2(t01, ia), s20a = mul2(t20, ia);
     const F2 s01b = mul2(t01, ib), s12b = mul2(t12, ib);
     const F2 s12c = mul2(t12, ic), s20c = mul2(t20, ic);
-    g[0] = fma2(m20x, s20a, fma2(m01x, s01a, g[0]));
-    g[1] = fma2(m20y, s20a, fma2(m01y, s01a, g[1]));
-    g[2] = fma2(f2s(w.m20z), s20a, fma2(f2s(w.m01z), s01a, g[2]));
-    g[3] = fma2(m12x, s12b, fma2(m01x, s01b, g[3]));
-    g[4] = fma2(m12y, s12b, fma2(m01y, s01b, g[4]));
-    g[5] = fma2(f2s(w.m12z), s12b, fma2(f2s(w.m01z), s01b, g[5]));
-    g[6] = fma2(m20x, s20c, fma2(m12x, s12c, g[6]));
-    g[7] = fma2(m20y, s20c, fma2(m12y, s12c, g[7]));
-    g[8] = fma2(f2s(w.m20z), s20c, fma2(f2s(w.m12z), s12c, g[8]));
+    z[0] = add2(z[0], s01a);
+    z[1] = fma2(s01a, az, z[1]);
+    z[2] = add2(z[2], s20a);
+    z[3] = fma2(s20a, cz, z[3]);
+    z[4] = add2(z[4], s01b);
+    z[5] = fma2(s01b, az, z[5]);
+    z[6] = add2(z[6], s12b);
+    z[7] = fma2(s12b, bz, z[7]);
+    z[8] = add2(z[8], s12c);
+    z[9] = fma2(s12c, bz, z[9]);
+    z[10] = add2(z[10], s20c);
+    z[11] = fma2(s20c, cz, z[11]);
+  }
+  // sum_q m s for every (edge, corner) from the run's sums, into the face's
+  // fp64 accumulators (acc[j][thread], j = corner * 3 + axis)
+  __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
+                                                   double (*acc)[kBwdThreads]) {
+    double S[kRowAcc];
+#pragma unroll
+    for (int j = 0; j < kRowAcc; ++j) {
+      float lo, hi;
+      split(z[j], lo, hi);
+      S[j] = (double)lo + (double)hi;
+    }
+    const double e01x = (double)(R.b.x - R.a.x), e01y = (double)(R.b.y - R.a.y);
+    const double e12x = (double)(R.c.x - R.b.x), e12y = (double)(R.c.y - R.b.y);
+    const double e20x = (double)(R.a.x - R.c.x), e20y = (double)(R.a.y - R.c.y);
+    const int t = threadIdx.x;
+    // corner a: edges 01 (a_z sums S0,S1) and 20 (c_z sums S2,S3)
+    acc[0][t] += w.k01x * S[0] - e01y * S[1] + w.k20x * S[2] - e20y * S[3];
+    acc[1][t] += w.k01y * S[0] + e01x * S[1] + w.k20y * S[2] + e20x * S[3];
+    acc[2][t] += w.m01z * S[0] + w.m20z * S[2];
+    // corner b: edges 01 (S4,S5) and 12 (b_z sums S6,S7)
+    acc[3][t] += w.k01x * S[4] - e01y * S[5] + w.k12x * S[6] - e12y * S[7];
+    acc[4][t] += w.k01y * S[4] + e01x * S[5] + w.k12y * S[6] + e12x * S[7];
+    acc[5][t] += w.m01z * S[4] + w.m12z * S[6];
+    // corner c: edges 12 (S8,S9) and 20 (S10,S11)
+    acc[6][t] += w.k12x * S[8] - e12y * S[9] + w.k20x * S[10] - e20y * S[11];
+    acc[7][t] += w.k12y * S[8] + e12x * S[9] + w.k20y * S[10] + e20x * S[11];
+    acc[8][t] += w.m12z * S[8] + w.m20z * S[10];
   }
   __device__ __forceinline__ static void finish(const Rec&, const double* acc, double* out9) {
     for (int j = 0; j < 9; ++j) out9[j] = acc[j];
@@ -190,12 +245,14 @@ struct SoftBwd {
     g[8] = fma2(c5, dy, g[8]);
     g[9] = fma2(c5, dz, g[9]);
   }
-  // Lattice-row form: d = c - q has row-constant x/y parts, so r^2, S and
-  // the x/y components of G1 = w x d, G2 = d x u take one op each per pair
-  // and their z components are per-row constants.
+  // Lattice-row form: d = c - q has row-constant x/y parts, so r^2 and S take
+  // one op each per pair, and since G1 = w x d and G2 = d x u are affine in
+  // d_z, sum_q c3 G = K sum c3 + E sum c3 d_z: a pair only adds to 4 running
+  // sums (c3, c3 d_z, c5, c5 d_z); flush_row forms the 10 face sums per run.
+  // Per pair: 12 FP32 lane-ops + 1 MUFU (was 22 + 1).
+  static constexpr int kRowAcc = 4;
   struct Row {
     float dx, dy, r2, s;
-    float g1x, g1y, g1z, g2x, g2y, g2z;  // row-constant parts
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
     Row w;
@@ -203,17 +260,11 @@ struct SoftBwd {
     w.dy = R.c.y - qy;
     w.r2 = fmaf(w.dy, w.dy, w.dx * w.dx);
     w.s = fmaf(R.n.y, w.dy, R.n.x * w.dx);
-    w.g1x = -(R.w.z * w.dy);                    // + wy dz
-    w.g1y = R.w.z * w.dx;                       // - wx dz
-    w.g1z = fmaf(R.w.x, w.dy, -(R.w.y * w.dx));
-    w.g2x = w.dy * R.u.z;                       // - dz uy
-    w.g2y = -(w.dx * R.u.z);                    // + dz ux
-    w.g2z = fmaf(w.dx, R.u.y, -(w.dy * R.u.x));
     return w;
   }
   template <bool kUnit>
   __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
-                                                   float eps2, F2* g) {
+                                                   float eps2, F2* z) {
     const F2 dz = sub2(f2s(R.c.z), qz);
     const F2 r2 = fma2(dz, dz, f2s(w.r2));
     const F2 rs = rsqrt2(r2);
@@ -222,18 +273,37 @@ struct SoftBwd {
     float r2l, r2h, cl, ch;
     split(r2, r2l, r2h);
     split(mul2(mul2(coef, rs2), rs), cl, ch);
+    // r < eps: that face is skipped for that point (_kernels.py:203-204)
     const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
     const F2 c5 = mul2(mul2(c3, S), rs2);
-    g[0] = fma2(c3, fma2(f2s(R.w.y), dz, f2s(w.g1x)), g[0]);
-    g[1] = fma2(c3, fma2(f2s(-R.w.x), dz, f2s(w.g1y)), g[1]);
-    g[2] = fma2(c3, f2s(w.g1z), g[2]);
-    g[3] = fma2(c3, fma2(f2s(-R.u.y), dz, f2s(w.g2x)), g[3]);
-    g[4] = fma2(c3, fma2(f2s(R.u.x), dz, f2s(w.g2y)), g[4]);
-    g[5] = fma2(c3, f2s(w.g2z), g[5]);
-    g[6] = add2(g[6], c3);
-    g[7] = fma2(c5, f2s(w.dx), g[7]);
-    g[8] = fma2(c5, f2s(w.dy), g[8]);
-    g[9] = fma2(c5, dz, g[9]);
+    z[0] = add2(z[0], c3);
+    z[1] = fma2(c3, dz, z[1]);
+    z[2] = add2(z[2], c5);
+    z[3] = fma2(c5, dz, z[3]);
+  }
+  __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
+                                                   double (*acc)[kBwdThreads]) {
+    double S[kRowAcc];
+#pragma unroll
+    for (int j = 0; j < kRowAcc; ++j) {
+      float lo, hi;
+      split(z[j], lo, hi);
+      S[j] = (double)lo + (double)hi;
+    }
+    const double C = S[0], A = S[1], D = S[2], E = S[3];
+    const double dx = w.dx, dy = w.dy;
+    const int t = threadIdx.x;
+    // G1 = w x d, G2 = d x u with d = (dx, dy, dz): sum c3 G = row part * C + dz part * A
+    acc[0][t] += (double)R.w.y * A - (double)R.w.z * dy * C;
+    acc[1][t] += (double)R.w.z * dx * C - (double)R.w.x * A;
+    acc[2][t] += ((double)R.w.x * dy - (double)R.w.y * dx) * C;
+    acc[3][t] += dy * (double)R.u.z * C - (double)R.u.y * A;
+    acc[4][t] += (double)R.u.x * A - dx * (double)R.u.z * C;
+    acc[5][t] += (dx * (double)R.u.y - dy * (double)R.u.x) * C;
+    acc[6][t] += C;
+    acc[7][t] += dx * D;
+    acc[8][t] += dy * D;
+    acc[9][t] += E;
   }
   __device__ __forceinline__ static void finish(const Rec& R, const double* a, double* out9) {
     const double t = a[6] / 3.0;
@@ -277,7 +347,7 @@ __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const Poi
 template <class Pol, bool kUnit>
 __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const PointChunk& ch,
                                            int n_pairs, int64_t flat0, int64_t rz, float eps2,
-                                           F2* g) {
+                                           double (*acc)[kBwdThreads]) {
   int j = 0;
   int k = (int)(flat0 % rz);  // k of the chunk's first node
   while (j < n_pairs) {
@@ -285,12 +355,16 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
     if (run > n_pairs - j) run = n_pairs - j;
     const float4 xy0 = ch.xy[j];
     const typename Pol::Row w = Pol::row(R, xy0.x, xy0.z);
+    F2 z[Pol::kRowAcc];
+#pragma unroll
+    for (int i = 0; i < Pol::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
 #pragma unroll 2
     for (int e = j + run; j < e; ++j) {
       const float4 zc = ch.zc[j];
       if (zc.z == 0.0f && zc.w == 0.0f) continue;  // warp-uniform (_kernels.py:182-184)
-      Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, g);
+      Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, z);
     }
+    Pol::flush_row(R, w, z, acc);
     k = 0;
   }
 }
@@ -342,26 +416,29 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       zc[2 + (i & 1)] = c;
     }
     __syncthreads();
-    F2 g[Pol::kAcc];
-#pragma unroll
-    for (int j = 0; j < Pol::kAcc; ++j) g[j] = f2(0.0f, 0.0f);
     if constexpr (Src::kRows) {
+      // row runs flush their sums straight into the fp64 accumulators
       const int64_t flat0 = src.n0 + c0;
       if (unit) {
-        chunk_rows<Pol, true>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, g);
+        chunk_rows<Pol, true>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, acc);
       } else {
-        chunk_rows<Pol, false>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, g);
+        chunk_rows<Pol, false>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, acc);
       }
-    } else if (unit) {
-      chunk_loop<Pol, true>(R, chunk, n_pairs, eps2, g);
     } else {
-      chunk_loop<Pol, false>(R, chunk, n_pairs, eps2, g);
-    }
+      F2 g[Pol::kAcc];
 #pragma unroll
-    for (int j = 0; j < Pol::kAcc; ++j) {
-      float lo, hi;
-      split(g[j], lo, hi);
-      acc[j][threadIdx.x] += (double)lo + (double)hi;
+      for (int j = 0; j < Pol::kAcc; ++j) g[j] = f2(0.0f, 0.0f);
+      if (unit) {
+        chunk_loop<Pol, true>(R, chunk, n_pairs, eps2, g);
+      } else {
+        chunk_loop<Pol, false>(R, chunk, n_pairs, eps2, g);
+      }
+#pragma unroll
+      for (int j = 0; j < Pol::kAcc; ++j) {
+        float lo, hi;
+        split(g[j], lo, hi);
+        acc[j][threadIdx.x] += (double)lo + (double)hi;
+      }
     }
   }
   if (live) {
