@@ -103,7 +103,7 @@ struct ExactEdgeBwd {
   //    R = 1/(d01 d12 d20) (products of O(|x|^2) terms: safe for coordinates
   //    within ~1e6 of the origin and points farther than ~1e-6 from an edge;
   //    R is clamped so the rest stays finite).
-  // Per pair: 41 FP32 lane-ops + 4 MUFU (was 53 + 6).
+  // Per pair: ~36 FP32 lane-ops + 4 MUFU (was 53 + 6).
   static constexpr int kRowAcc = 12;
   struct Row {
     float a2, b2, c2;              // x/y parts of |corner - q|^2
@@ -158,21 +158,21 @@ struct ExactEdgeBwd {
     const F2 t01 = mul2(kUnit ? cr : mul2(cr, f2s(R.a.w)), p12);
     const F2 t12 = mul2(kUnit ? q0 : mul2(q0, f2s(R.b.w)), d20);
     const F2 t20 = mul2(kUnit ? q0 : mul2(q0, f2s(R.c.w)), d12);
-    const F2 s01a = mul2(t01, ia), s20a = mul2(t20, ia);
-    const F2 s01b = mul2(t01, ib), s12b = mul2(t12, ib);
-    const F2 s12c = mul2(t12, ic), s20c = mul2(t20, ic);
-    z[0] = add2(z[0], s01a);
-    z[1] = fma2(s01a, az, z[1]);
-    z[2] = add2(z[2], s20a);
-    z[3] = fma2(s20a, cz, z[3]);
-    z[4] = add2(z[4], s01b);
-    z[5] = fma2(s01b, az, z[5]);
-    z[6] = add2(z[6], s12b);
-    z[7] = fma2(s12b, bz, z[7]);
-    z[8] = add2(z[8], s12c);
-    z[9] = fma2(s12c, bz, z[9]);
-    z[10] = add2(z[10], s20c);
-    z[11] = fma2(s20c, cz, z[11]);
+    // s_eP = t_e / |P - q|: each sum is one fma, t_e (or t_e * the edge's
+    // corner z) times 1/|P - q|
+    const F2 u01 = mul2(t01, az), u12 = mul2(t12, bz), u20 = mul2(t20, cz);
+    z[0] = fma2(t01, ia, z[0]);
+    z[1] = fma2(u01, ia, z[1]);
+    z[2] = fma2(t20, ia, z[2]);
+    z[3] = fma2(u20, ia, z[3]);
+    z[4] = fma2(t01, ib, z[4]);
+    z[5] = fma2(u01, ib, z[5]);
+    z[6] = fma2(t12, ib, z[6]);
+    z[7] = fma2(u12, ib, z[7]);
+    z[8] = fma2(t12, ic, z[8]);
+    z[9] = fma2(u12, ic, z[9]);
+    z[10] = fma2(t20, ic, z[10]);
+    z[11] = fma2(u20, ic, z[11]);
   }
   // sum_q m s for every (edge, corner) from the run's sums, into the face's
   // fp64 accumulators (acc[j][thread], j = corner * 3 + axis)
