@@ -146,6 +146,7 @@ class ClockSampler:
         self.index, self.period = index, period
         self.samples = []
         self._stop = threading.Event()
+        self._first = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
@@ -159,12 +160,17 @@ class ClockSampler:
                 r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
                 pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
                 self.samples.append((sm, mx, r, pw))
+                self._first.set()
                 self._stop.wait(self.period)
         except Exception as e:  # pragma: no cover - reported in the JSON line
             self.error = repr(e)
+        self._first.set()
 
     def __enter__(self):
+        # NVML is initialised and the first sample taken before the timed
+        # region opens, so even a millisecond-long region has a reading
         self._t.start()
+        self._first.wait(timeout=10)
         return self
 
     def __exit__(self, *a):

@@ -358,11 +358,23 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
     F2 z[Pol::kRowAcc];
 #pragma unroll
     for (int i = 0; i < Pol::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
-#pragma unroll 2
-    for (int e = j + run; j < e; ++j) {
+    const int e = j + run;
+    // two point pairs per step under one (warp-uniform) zero-coefficient
+    // test, so their dependency chains share a basic block and interleave
+    // (a zero-coefficient pair next to a live one adds 0 * finite: its point
+    // is parked far away)
+#pragma unroll 1
+    for (; j + 1 < e; j += 2) {
+      const float4 z0 = ch.zc[j], z1 = ch.zc[j + 1];
+      if (z0.z == 0.0f && z0.w == 0.0f && z1.z == 0.0f && z1.w == 0.0f) continue;
+      Pol::template pair_row2<kUnit>(R, w, f2(z0.x, z0.y), f2(z0.z, z0.w), eps2, z);
+      Pol::template pair_row2<kUnit>(R, w, f2(z1.x, z1.y), f2(z1.z, z1.w), eps2, z);
+    }
+    if (j < e) {
       const float4 zc = ch.zc[j];
-      if (zc.z == 0.0f && zc.w == 0.0f) continue;  // warp-uniform (_kernels.py:182-184)
-      Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, z);
+      if (!(zc.z == 0.0f && zc.w == 0.0f))  // warp-uniform (_kernels.py:182-184)
+        Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, z);
+      ++j;
     }
     Pol::flush_row(R, w, z, acc);
     k = 0;
