@@ -27,6 +27,7 @@ namespace wv {
 constexpr int kBwdThreads = 128;   // faces per CTA
 constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
 constexpr int kBwdMinBlocks = 5;  // CTAs per SM (launch bounds and split plan)
+constexpr int kRowStep = 4;       // point pairs per basic block in the row loop
 
 // Exact backward, edge form.  For a triangle seen from q, the variation of
 // its solid angle is a boundary integral (the integrand (x-q)/|x-q|^3 is
@@ -364,17 +365,24 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
     // (a zero-coefficient pair next to a live one adds 0 * finite: its point
     // is parked far away)
 #pragma unroll 1
-    for (; j + 1 < e; j += 2) {
-      const float4 z0 = ch.zc[j], z1 = ch.zc[j + 1];
-      if (z0.z == 0.0f && z0.w == 0.0f && z1.z == 0.0f && z1.w == 0.0f) continue;
-      Pol::template pair_row2<kUnit>(R, w, f2(z0.x, z0.y), f2(z0.z, z0.w), eps2, z);
-      Pol::template pair_row2<kUnit>(R, w, f2(z1.x, z1.y), f2(z1.z, z1.w), eps2, z);
+    for (; j + kRowStep <= e; j += kRowStep) {
+      float4 zc[kRowStep];
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < kRowStep; ++u) {
+        zc[u] = ch.zc[j + u];
+        any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
+      }
+      if (!any) continue;
+#pragma unroll
+      for (int u = 0; u < kRowStep; ++u)
+        Pol::template pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
     }
-    if (j < e) {
+#pragma unroll 1
+    for (; j < e; ++j) {
       const float4 zc = ch.zc[j];
       if (!(zc.z == 0.0f && zc.w == 0.0f))  // warp-uniform (_kernels.py:182-184)
         Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, z);
-      ++j;
     }
     Pol::flush_row(R, w, z, acc);
     k = 0;
