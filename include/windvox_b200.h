@@ -188,6 +188,26 @@ int wv_face_to_vertex(const double *face_grad, const int64_t *csr_offsets,
                       const int64_t *csr_slots, int64_t n_verts, const double *scale,
                       int accumulate, double *out64, float *out32, void *stream);
 
+/* ---- batched grid kernels (many meshes, one connectivity, one grid) ------
+ * The C4 training batch / batched morph trials: `batch` meshes sharing the
+ * face count and query range, evaluated by ONE launch per stage (blockIdx.z
+ * = mesh).  Mesh z's packed buffer (wv_pack_faces / wv_pack_exact_grad)
+ * starts at packed + z * pack_stride bytes (pack_stride a multiple of 16, at
+ * least the packed size); its values / flags / coefficients sit at
+ * z * count, its corner sums at z * n_faces * 9.  kind: WV_PACK_EXACT_F32 or
+ * WV_PACK_SOFT_F32 (forward), WV_PACK_EXACTGRAD_F32 or WV_PACK_SOFTGRAD_F32
+ * (backward).  Results equal `batch` single-mesh calls. */
+size_t wv_fwd_workspace_bytes_batch(int kind, int64_t n_faces, int64_t count, int64_t batch);
+int wv_fwd_grid_f32_batch(int kind, const void *packed, size_t pack_stride, int64_t n_faces,
+                          wv_grid_t grid, int64_t n0, int64_t count, int64_t batch, int policy,
+                          float *out, uint8_t *flags, void *workspace, size_t workspace_bytes,
+                          void *stream);
+size_t wv_bwd_workspace_bytes_batch(int kind, int64_t n_faces, int64_t count, int64_t batch);
+int wv_bwd_grid_f32_batch(int kind, const void *packed, size_t pack_stride, int64_t n_faces,
+                          wv_grid_t grid, int64_t n0, int64_t count, int64_t batch,
+                          const float *coefs, double coef_scale, double *face_grad,
+                          void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- marching cubes on the device-resident grid (recon.py:39-108) --------
  * Four stream-ordered passes; the caller computes exclusive prefix sums
  * between them (counts -> tri_offsets, flags -> vertex_index).

@@ -39,6 +39,8 @@ EXPORTED = (
     "wv_loss_finalize", "wv_mc_classify", "wv_mc_edges", "wv_mc_vertices", "wv_mc_emit",
     "wv_splitmix64_uniform", "wv_pairwise_sum_workspace_bytes", "wv_pairwise_sum",
     "wv_surface_cdf", "wv_sample_surface", "wv_nearest_distances",
+    "wv_fwd_workspace_bytes_batch", "wv_fwd_grid_f32_batch", "wv_bwd_workspace_bytes_batch",
+    "wv_bwd_grid_f32_batch",
 )
 
 
@@ -106,6 +108,10 @@ def _declare(lib):
         "wv_surface_cdf": ([P, P, I64, P, P, P, P, SZ, P], I),
         "wv_sample_surface": ([P, P, I64, P, P, ctypes.c_uint64, I64, P, P], I),
         "wv_nearest_distances": ([P, I64, P, I64, P, P], I),
+        "wv_fwd_workspace_bytes_batch": ([I, I64, I64, I64], SZ),
+        "wv_fwd_grid_f32_batch": ([I, P, SZ, I64, Grid, I64, I64, I64, I, P, P, P, SZ, P], I),
+        "wv_bwd_workspace_bytes_batch": ([I, I64, I64, I64], SZ),
+        "wv_bwd_grid_f32_batch": ([I, P, SZ, I64, Grid, I64, I64, I64, P, D, P, P, SZ, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

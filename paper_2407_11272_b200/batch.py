@@ -16,7 +16,8 @@ from __future__ import annotations
 
 import torch
 
-from .device import DeviceMesh
+from . import _lib as L
+from .device import DeviceMesh, _ptr, _stream
 from .grad import device_loss_grad
 
 __all__ = ["BatchOccupancyLoss", "batch_occupancy_loss", "DeformationNet"]
@@ -36,10 +37,79 @@ def _side_streams(dev):
     return st
 
 
+def _grid_count(grid) -> int:
+    r = grid[2]
+    return int(r[0]) * int(r[1]) * int(r[2])
+
+
+def batched_soft_loss_grad_f32(verts: torch.Tensor, faces: torch.Tensor, grid,
+                               targets: torch.Tensor, csr):
+    """Soft occupancy loss and its vertex gradients for a (B,V,3) batch with
+    one connectivity, by ONE forward and ONE backward launch for the whole
+    batch (include/windvox_b200.h "batched grid kernels"; blockIdx.z = mesh)
+    around per-mesh packing, loss terms and CSR gathers.  Returns
+    (losses (B,) f64, grads (B,V,3) f32, sums (B,8) f64); every mesh's
+    numbers equal the single-mesh path's (``device_loss_grad``)."""
+    lib = L.lib()
+    dev = verts.device
+    B, V, _ = verts.shape
+    F = int(faces.shape[0])
+    N = _grid_count(grid)
+    g = L.make_grid(*grid)
+    st = _stream()
+    v32 = verts.detach().to(torch.float32).contiguous()
+    f64i = faces.to(torch.int64).contiguous()
+
+    def pack(kind):
+        stride = (int(lib.wv_packed_bytes(kind, F)) + 15) // 16 * 16
+        buf = torch.empty(B * stride, dtype=torch.uint8, device=dev)
+        base = _ptr(buf)
+        for b in range(B):
+            L.check(lib.wv_pack_faces(kind, _ptr(v32[b]), 0, V, _ptr(f64i), 1, F,
+                                      base + b * stride, st), "wv_pack_faces")
+        return buf, stride
+
+    fbuf, fstride = pack(L.PACK_SOFT_F32)
+    gbuf, gstride = pack(L.PACK_SOFTGRAD_F32)
+    vals = torch.empty((B, N), dtype=torch.float32, device=dev)
+    flags = torch.empty((B, N), dtype=torch.uint8, device=dev)
+    wsb = max(int(lib.wv_fwd_workspace_bytes_batch(L.PACK_SOFT_F32, F, N, B)),
+              int(lib.wv_bwd_workspace_bytes_batch(L.PACK_SOFTGRAD_F32, F, N, B)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    L.check(lib.wv_fwd_grid_f32_batch(L.PACK_SOFT_F32, _ptr(fbuf), fstride, F, g, 0, N, B,
+                                      L.POLICY_RAW, _ptr(vals), _ptr(flags), _ptr(ws), wsb, st),
+            "wv_fwd_grid_f32_batch")
+    tg = targets.to(device=dev, dtype=torch.float32).reshape(B, N).contiguous()
+    coefs = torch.empty((B, N), dtype=torch.float32, device=dev)
+    sums = torch.zeros((B, 8), dtype=torch.float64, device=dev)
+    lwsb = int(lib.wv_loss_workspace_bytes(N))
+    lws = torch.empty(max(lwsb, 1), dtype=torch.uint8, device=dev)
+    for b in range(B):
+        L.check(lib.wv_loss_terms_f32(_ptr(vals[b]), _ptr(flags[b]), _ptr(tg[b]), None, N,
+                                      _ptr(coefs[b]), _ptr(sums[b]), _ptr(lws), lwsb, st),
+                "wv_loss_terms_f32")
+    fg = torch.empty((B, F, 3, 3), dtype=torch.float64, device=dev)
+    L.check(lib.wv_bwd_grid_f32_batch(L.PACK_SOFTGRAD_F32, _ptr(gbuf), gstride, F, g, 0, N, B,
+                                      _ptr(coefs), 1.0, _ptr(fg), _ptr(ws), wsb, st),
+            "wv_bwd_grid_f32_batch")
+    grads = torch.empty((B, V, 3), dtype=torch.float32, device=dev)
+    off, slots = csr
+    for b in range(B):
+        # 1/sum(w) (sums[b][3]) applied on the device by the gather
+        L.check(lib.wv_face_to_vertex(_ptr(fg[b]), _ptr(off), _ptr(slots), V,
+                                      _ptr(sums[b]) + 3 * 8, 0, None, _ptr(grads[b]), st),
+                "wv_face_to_vertex")
+    return sums[:, 4].clone(), grads, sums
+
+
 class BatchOccupancyLoss(torch.autograd.Function):
     @staticmethod
     def forward(ctx, verts, faces, grid, targets, mode, precision, csr):
         B = verts.shape[0]
+        if mode == "soft" and precision == "f32" and verts.dtype == torch.float32:
+            losses, grads, _ = batched_soft_loss_grad_f32(verts, faces, grid, targets, csr)
+            ctx.save_for_backward(grads)
+            return losses
         losses = torch.empty(B, dtype=torch.float64, device=verts.device)
         grads = torch.empty((B,) + tuple(verts.shape[1:]), dtype=verts.dtype,
                             device=verts.device)

@@ -392,9 +392,16 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
 template <class Pol, class Src>
 __global__ void __launch_bounds__(kBwdThreads, Pol::kMinBlocks)
 bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
-               int64_t n_faces, Src src, const float* __restrict__ coefs, int64_t n_count,
-               int64_t pts_per_split, float coef_scale, double* __restrict__ out) {
+               size_t pack_stride, int64_t n_faces, Src src, const float* __restrict__ coefs,
+               int64_t n_count, int64_t pts_per_split, float coef_scale,
+               double* __restrict__ out) {
   __shared__ PointChunk chunk;
+  // batched launches: blockIdx.z selects the mesh (records pack_stride bytes
+  // apart, coefficients n_count apart, partials (mesh, split)-major)
+  hdr = reinterpret_cast<const PackHeader*>(reinterpret_cast<const char*>(hdr) +
+                                            blockIdx.z * pack_stride);
+  recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
+  coefs += (int64_t)blockIdx.z * n_count;
   const int64_t f = (int64_t)blockIdx.x * kBwdThreads + threadIdx.x;
   const bool live = f < n_faces;
   typename Pol::Rec R = recs[live ? f : 0];
@@ -467,18 +474,20 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
     for (int j = 0; j < Pol::kAcc; ++j) a[j] = acc[j][threadIdx.x];
     Pol::finish(R, a, o9);
-    double* dst = out + ((int64_t)blockIdx.y * n_faces + f) * 9;
+    double* dst = out + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * n_faces + f) * 9;
 #pragma unroll
     for (int j = 0; j < 9; ++j) dst[j] = o9[j];
   }
 }
 // out[f*9+j] = sum_s part[s][f*9+j], fixed split order
 __global__ void reduce_splits_kernel(const double* __restrict__ part, int splits, int64_t n,
-                                     double* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+                                     int64_t batch, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * batch;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i / n, k = i - z * n;
+    const double* p = part + z * splits * n + k;
     double a = 0.0;
-    for (int s = 0; s < splits; ++s) a += part[(int64_t)s * n + i];
+    for (int s = 0; s < splits; ++s) a += p[(int64_t)s * n];
     out[i] = a;
   }
 }
@@ -487,67 +496,72 @@ struct BwdPlan {
   int64_t blocks_x = 0;
   int splits = 1;
   int64_t pts_per_split = 0;
-  static BwdPlan make(int64_t n_faces, int64_t n_count, int num_sms, int min_blocks) {
+  static BwdPlan make(int64_t n_faces, int64_t n_count, int num_sms, int min_blocks,
+                      int64_t batch = 1) {
     BwdPlan p;
     p.blocks_x = (n_faces + kBwdThreads - 1) / kBwdThreads;
     if (p.blocks_x < 1) p.blocks_x = 1;
     const int64_t slots = (int64_t)num_sms * min_blocks;
-    int64_t lo = (4 * slots + p.blocks_x - 1) / p.blocks_x;  // >= ~4 waves
+    const int64_t blocks = p.blocks_x * batch;
+    int64_t lo = (4 * slots + blocks - 1) / blocks;  // >= ~4 waves
     int64_t hi = 4 * lo;  // then the split count with the fullest last wave
     int64_t max_s = (n_count + kBwdChunk - 1) / kBwdChunk;  // >= one chunk per split
     if (max_s > 4096) max_s = 4096;
     if (lo > max_s) lo = max_s;
     if (hi > max_s) hi = max_s;
-    int64_t s = best_splits(p.blocks_x, lo, hi, slots);
+    int64_t s = best_splits(blocks, lo, hi, slots);
     p.pts_per_split = (n_count + s - 1) / s;
     p.pts_per_split = ((p.pts_per_split + kBwdChunk - 1) / kBwdChunk) * kBwdChunk;
     p.splits = (int)((n_count + p.pts_per_split - 1) / p.pts_per_split);
     if (p.splits < 1) p.splits = 1;
     return p;
   }
-  size_t workspace(int64_t n_faces) const {
-    return splits > 1 ? (size_t)splits * (size_t)n_faces * 9 * sizeof(double) : 0;
+  size_t workspace(int64_t n_faces, int64_t batch = 1) const {
+    return splits > 1 ? (size_t)splits * (size_t)batch * (size_t)n_faces * 9 * sizeof(double)
+                      : 0;
   }
 };
 
 template <class Pol>
 static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps,
                       int64_t n_count, const float* coefs, double coef_scale, double* face_grad,
-                      void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream) {
-  if (n_faces <= 0) return kOk;
+                      void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream,
+                      const Batch& bt) {
+  if (n_faces <= 0 || bt.n <= 0) return kOk;
+  if (bt.n > 65535 || (bt.n > 1 && ps.kind != PointSource::kGrid)) return kErrArg;
   if (n_count <= 0) {
-    return cudaMemsetAsync(face_grad, 0, (size_t)n_faces * 9 * sizeof(double), stream) ==
+    return cudaMemsetAsync(face_grad, 0, (size_t)bt.n * n_faces * 9 * sizeof(double), stream) ==
                    cudaSuccess ? kOk : kErrCuda;
   }
   const PackHeader* hdr = static_cast<const PackHeader*>(packed);
   const auto* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
-  const BwdPlan pl = BwdPlan::make(n_faces, n_count, num_sms, Pol::kMinBlocks);
+  const BwdPlan pl = BwdPlan::make(n_faces, n_count, num_sms, Pol::kMinBlocks, bt.n);
   double* dst = face_grad;
   if (pl.splits > 1) {
-    if (workspace == nullptr || ws_bytes < pl.workspace(n_faces)) return kErrWorkspace;
+    if (workspace == nullptr || ws_bytes < pl.workspace(n_faces, bt.n)) return kErrWorkspace;
     dst = static_cast<double*>(workspace);
   }
   const float cs = (float)(coef_scale * Pol::kCoefScale);
-  dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits);
+  dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits, (unsigned)bt.n);
   if (ps.kind == PointSource::kGrid && ps.grid.res[2] >= 16 &&
       row_aligned(ps.grid, ps.n0, 2 * ((n_count + 1) / 2), 2)) {
     RowSrc src{{ps.grid, ps.n0}};
     bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
   } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
     bwd_f32_kernel<Pol, GridSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
   } else {
     ListSrc src{ps.points};
     bwd_f32_kernel<Pol, ListSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
   }
   if (pl.splits > 1) {
     const int64_t n = n_faces * 9;
-    int blocks = (int)((n + 255) / 256);
+    int blocks = (int)((n * bt.n + 255) / 256);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
-    reduce_splits_kernel<<<blocks, 256, 0, stream>>>(dst, pl.splits, n, face_grad);
+    reduce_splits_kernel<<<blocks, 256, 0, stream>>>(dst, pl.splits, n, bt.n, face_grad);
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -555,19 +569,19 @@ static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps
 int launch_exact_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, const float* coefs, double coef_scale,
                          double* face_grad, void* ws, size_t ws_bytes, int num_sms,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, const Batch& bt) {
   return launch_bwd<ExactEdgeBwd>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad, ws,
-                              ws_bytes, num_sms, stream);
+                                  ws_bytes, num_sms, stream, bt);
 }
 int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, const float* coefs, double coef_scale,
                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const Batch& bt) {
   return launch_bwd<SoftBwd>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad, ws,
-                             ws_bytes, num_sms, stream);
+                             ws_bytes, num_sms, stream, bt);
 }
-size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
-  return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks).workspace(n_faces);
+size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
+  return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);
 }
 
 // ---------------------------------------------------------------------------

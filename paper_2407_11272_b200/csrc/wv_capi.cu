@@ -410,4 +410,69 @@ int wv_nearest_distances(const double* queries, int64_t n_queries, const double*
   return wv::launch_nearest(queries, n_queries, targets, n_targets, out, as_stream(stream));
 }
 
+// ---- batched grid kernels ------------------------------------------------------
+size_t wv_fwd_workspace_bytes_batch(int kind, int64_t n_faces, int64_t count, int64_t batch) {
+  if (batch < 1) return 0;
+  switch (kind) {
+    case WV_PACK_EXACT_F32: return wv::exact_fwd_workspace_bytes(n_faces, count, sm_count(), batch);
+    case WV_PACK_SOFT_F32: return wv::soft_fwd_workspace_bytes(n_faces, count, sm_count(), batch);
+    default: return 0;
+  }
+}
+
+static bool batch_ok(const void* packed, size_t stride, int64_t batch) {
+  return packed != nullptr && batch >= 1 && batch <= 65535 && stride % 16 == 0 &&
+         (batch == 1 || stride >= 64);
+}
+
+int wv_fwd_grid_f32_batch(int kind, const void* packed, size_t pack_stride, int64_t n_faces,
+                          wv_grid_t grid, int64_t n0, int64_t count, int64_t batch, int policy,
+                          float* out, uint8_t* flags, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count) ||
+      !batch_ok(packed, pack_stride, batch))
+    return WV_ERR_ARG;
+  wv::Batch bt;
+  bt.n = batch;
+  bt.pack_stride = pack_stride;
+  if (kind == WV_PACK_EXACT_F32)
+    return wv::launch_exact_fwd_f32(packed, n_faces, grid_src(grid, n0), count, policy, out,
+                                    flags, workspace, workspace_bytes, sm_count(),
+                                    as_stream(stream), bt);
+  if (kind == WV_PACK_SOFT_F32)
+    return wv::launch_soft_fwd_f32(packed, n_faces, grid_src(grid, n0), count, policy, out, flags,
+                                   workspace, workspace_bytes, sm_count(), as_stream(stream), bt);
+  return WV_ERR_ARG;
+}
+
+size_t wv_bwd_workspace_bytes_batch(int kind, int64_t n_faces, int64_t count, int64_t batch) {
+  if (batch < 1) return 0;
+  switch (kind) {
+    case WV_PACK_EXACTGRAD_F32:
+    case WV_PACK_SOFTGRAD_F32: return wv::bwd_workspace_bytes(n_faces, count, sm_count(), batch);
+    default: return 0;
+  }
+}
+
+int wv_bwd_grid_f32_batch(int kind, const void* packed, size_t pack_stride, int64_t n_faces,
+                          wv_grid_t grid, int64_t n0, int64_t count, int64_t batch,
+                          const float* coefs, double coef_scale, double* face_grad,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || !grid_ok(grid, n0, count) ||
+      !batch_ok(packed, pack_stride, batch))
+    return WV_ERR_ARG;
+  wv::Batch bt;
+  bt.n = batch;
+  bt.pack_stride = pack_stride;
+  if (kind == WV_PACK_EXACTGRAD_F32)
+    return wv::launch_exact_bwd_f32(packed, n_faces, grid_src(grid, n0), count, coefs, coef_scale,
+                                    face_grad, workspace, workspace_bytes, sm_count(),
+                                    as_stream(stream), bt);
+  if (kind == WV_PACK_SOFTGRAD_F32)
+    return wv::launch_soft_bwd_f32(packed, n_faces, grid_src(grid, n0), count, coefs, coef_scale,
+                                   face_grad, workspace, workspace_bytes, sm_count(),
+                                   as_stream(stream), bt);
+  return WV_ERR_ARG;
+}
+
 }  // extern "C"

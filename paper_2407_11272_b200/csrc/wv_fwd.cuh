@@ -24,7 +24,8 @@ namespace wv {
 template <class Pol, class Src>
 __global__ void __launch_bounds__(Pol::kThreads, Src::kRows ? Pol::kMinBlocksRow : Pol::kMinBlocks)
 fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
-               int64_t n_faces, Src src, int64_t n_count, int64_t tiles_per_split, OutF32 o) {
+               size_t pack_stride, int64_t n_faces, Src src, int64_t n_count,
+               int64_t tiles_per_split, OutF32 o) {
   using Rec = typename Pol::Rec;
   constexpr int TILE = Pol::kTile;
   constexpr int STAGES = Pol::kStages;
@@ -36,6 +37,12 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   // touched once per tile (and by rare pairs), and keeping them out of the
   // register file leaves the 128-register budget to the pair arithmetic
   __shared__ double accs[P][NC];
+  // batched launches: blockIdx.z selects the mesh (its packed records lie
+  // pack_stride bytes apart; its outputs n_count apart)
+  hdr = reinterpret_cast<const PackHeader*>(reinterpret_cast<const char*>(hdr) +
+                                            blockIdx.z * pack_stride);
+  recs = reinterpret_cast<const Rec*>(hdr + 1);
+  const int64_t zoff = (int64_t)blockIdx.z * n_count;
   const int64_t n_tiles = (n_faces + TILE - 1) / TILE;
   const int64_t t_begin = (int64_t)blockIdx.y * tiles_per_split;
   int64_t t_end = t_begin + tiles_per_split;
@@ -87,16 +94,12 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll 1
     for (int f = 0; f < cnt; ++f) {
       const Rec R = tile[f];
-      uint32_t rare = 0;
+      uint32_t rare;
       if constexpr (kRows) {
         const typename Pol::Row w = Pol::row(R, rx, ry);
-#pragma unroll
-        for (int pp = 0; pp < PP; ++pp)
-          rare |= Pol::common_row2(R, w, qz[pp], ctx, tacc[pp]) << (2 * pp);
+        rare = Pol::template face_row<PP>(R, w, qz, ctx, tacc);
       } else {
-#pragma unroll
-        for (int pp = 0; pp < PP; ++pp)
-          rare |= Pol::common2(R, qx[pp], qy[pp], qz[pp], ctx, tacc[pp]) << (2 * pp);
+        rare = Pol::template face<PP>(R, qx, qy, qz, ctx, tacc);
       }
       if (rare != 0u) {
 #pragma unroll
@@ -130,7 +133,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   for (int p = 0; p < P; ++p) {
     const int64_t l = kRows ? grp * P + p : base + p * NC + tid;
     if (kRows ? grp < n_groups : l < n_count)
-      o.store(blockIdx.y, l, accs[p][tid], (hits >> p) & 1u);
+      o.store(blockIdx.y, zoff + l, accs[p][tid], (hits >> p) & 1u);
   }
 }
 
@@ -139,12 +142,12 @@ struct FwdPlan {
   int64_t blocks_x = 0;
   int splits = 1;
   int64_t tiles_per_split = 0;
-  static FwdPlan make(int64_t n_faces, int64_t n_count, int num_sms) {
+  static FwdPlan make(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch = 1) {
     FwdPlan pl;
     const int64_t per_block = (int64_t)Pol::kConsumerWarps * 32 * Pol::kP;
     pl.blocks_x = (n_count + per_block - 1) / per_block;
     const int64_t n_tiles = (n_faces + Pol::kTile - 1) / Pol::kTile;
-    const int s = choose_splits(pl.blocks_x, n_tiles, num_sms, Pol::kMinBlocks);
+    const int s = choose_splits(pl.blocks_x * batch, n_tiles, num_sms, Pol::kMinBlocks);
     pl.tiles_per_split = n_tiles > 0 ? (n_tiles + s - 1) / s : 0;
     pl.splits = pl.tiles_per_split > 0 ? (int)((n_tiles + pl.tiles_per_split - 1) / pl.tiles_per_split) : 1;
     return pl;
@@ -162,42 +165,44 @@ __global__ void finalize_theta_kernel(const double* __restrict__ part,
 template <class Pol>
 int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, int64_t n_count,
                    int policy, float* out, uint8_t* flags, void* workspace, size_t ws_bytes,
-                   int num_sms, cudaStream_t stream) {
-  if (n_count <= 0) return kOk;
+                   int num_sms, cudaStream_t stream, const Batch& bt) {
+  if (n_count <= 0 || bt.n <= 0) return kOk;
+  if (bt.n > 65535 || (bt.n > 1 && ps.kind != PointSource::kGrid)) return kErrArg;
   const PackHeader* hdr = static_cast<const PackHeader*>(packed);
   const typename Pol::Rec* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
-  const FwdPlan<Pol> pl = FwdPlan<Pol>::make(n_faces, n_count, num_sms);
+  const FwdPlan<Pol> pl = FwdPlan<Pol>::make(n_faces, n_count, num_sms, bt.n);
   OutF32 o;
   o.out = out;
   o.flags = flags;
   o.policy = policy;
   o.scale = Pol::kScale;
+  const int64_t total = n_count * bt.n;  // outputs of all meshes, mesh-major
   if (pl.splits > 1) {
-    if (workspace == nullptr || ws_bytes < pl.workspace(n_count)) return kErrWorkspace;
+    if (workspace == nullptr || ws_bytes < pl.workspace(total)) return kErrWorkspace;
     o.part = static_cast<double*>(workspace);
-    o.part_flags = reinterpret_cast<uint8_t*>(o.part + (size_t)pl.splits * n_count);
-    o.n_count = n_count;
+    o.part_flags = reinterpret_cast<uint8_t*>(o.part + (size_t)pl.splits * total);
+    o.n_count = total;
   }
-  dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits);
+  dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits, (unsigned)bt.n);
   const unsigned threads = Pol::kThreads;
   if (ps.kind == PointSource::kGrid && row_aligned(ps.grid, ps.n0, n_count, Pol::kP)) {
     RowSrc src{{ps.grid, ps.n0}};
-    fwd_f32_kernel<Pol, RowSrc><<<grid, threads, 0, stream>>>(hdr, recs, n_faces, src, n_count,
-                                                                pl.tiles_per_split, o);
+    fwd_f32_kernel<Pol, RowSrc><<<grid, threads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
   } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
-    fwd_f32_kernel<Pol, GridSrc><<<grid, threads, 0, stream>>>(hdr, recs, n_faces, src, n_count,
-                                                                 pl.tiles_per_split, o);
+    fwd_f32_kernel<Pol, GridSrc><<<grid, threads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
   } else {
     ListSrc src{ps.points};
-    fwd_f32_kernel<Pol, ListSrc><<<grid, threads, 0, stream>>>(hdr, recs, n_faces, src, n_count,
-                                                                 pl.tiles_per_split, o);
+    fwd_f32_kernel<Pol, ListSrc><<<grid, threads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
   }
   if (pl.splits > 1) {
     const int t = 256;
-    int blocks = (int)((n_count + t - 1) / t);
+    int blocks = (int)((total + t - 1) / t);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
-    finalize_theta_kernel<<<blocks, t, 0, stream>>>(o.part, o.part_flags, pl.splits, n_count,
+    finalize_theta_kernel<<<blocks, t, 0, stream>>>(o.part, o.part_flags, pl.splits, total,
                                                     policy, out, flags, o.scale);
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;

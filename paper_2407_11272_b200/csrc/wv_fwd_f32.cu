@@ -158,6 +158,24 @@ struct ExactPol {
     tacc = fma2(f2(cl ? tl : 0.0f, ch ? th : 0.0f), p, tacc);
     return (cl ? 0u : 1u) | (ch ? 0u : 2u);
   }
+  // all PP point pairs of a thread against one face
+  template <int PP>
+  __device__ __forceinline__ static uint32_t face_row(const Rec& R, const Row& w, const F2* qz,
+                                                      const Ctx& ctx, F2* tacc) {
+    uint32_t rare = 0;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) rare |= common_row2(R, w, qz[pp], ctx, tacc[pp]) << (2 * pp);
+    return rare;
+  }
+  template <int PP>
+  __device__ __forceinline__ static uint32_t face(const Rec& R, const F2* qx, const F2* qy,
+                                                  const F2* qz, const Ctx& ctx, F2* tacc) {
+    uint32_t rare = 0;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp)
+      rare |= common2(R, qx[pp], qy[pp], qz[pp], ctx, tacc[pp]) << (2 * pp);
+    return rare;
+  }
   __device__ __forceinline__ static double rare(const Rec& R, float qx, float qy, float qz,
                                                 double eps) {
     return exact_rare(R.v0e, R.v1, R.v2, qx, qy, qz, eps);
@@ -212,6 +230,59 @@ struct SoftPol {
     tacc = fma2(s, mul2(rs, mul2(rs, rs)), tacc);
     return (hl ? 1u : 0u) | (hh ? 2u : 0u);
   }
+  // All PP point pairs against one face.  The on-centroid test is done once
+  // per face on the minimum r^2 of the thread's points (nearly every face is
+  // far from every point): the common path has no per-lane selects, which
+  // otherwise cost as many issue slots as the arithmetic (the soft term is
+  // only ~7 FP32 ops + 1 MUFU per pair).
+  template <int PP>
+  __device__ __forceinline__ static uint32_t finish(const F2* r2, const F2* s, const Ctx& ctx,
+                                                    F2* tacc) {
+    float m = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      float l, h;
+      split(r2[pp], l, h);
+      m = fminf(m, fminf(l, h));
+    }
+    if (m >= ctx.eps2) {
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) {
+        const F2 rs = rsqrt2(r2[pp]);
+        tacc[pp] = fma2(s[pp], mul2(rs, mul2(rs, rs)), tacc[pp]);
+      }
+      return 0u;
+    }
+    uint32_t rare = 0;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) rare |= tail2(r2[pp], s[pp], ctx, tacc[pp]) << (2 * pp);
+    return rare;
+  }
+  template <int PP>
+  __device__ __forceinline__ static uint32_t face_row(const Rec& R, const Row& w, const F2* qz,
+                                                      const Ctx& ctx, F2* tacc) {
+    F2 r2[PP], s[PP];
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 dz = sub2(f2s(R.c.z), qz[pp]);
+      r2[pp] = fma2(dz, dz, f2s(w.r2));
+      s[pp] = fma2(f2s(R.n.y), dz, f2s(w.s));
+    }
+    return finish<PP>(r2, s, ctx, tacc);
+  }
+  template <int PP>
+  __device__ __forceinline__ static uint32_t face(const Rec& R, const F2* qx, const F2* qy,
+                                                  const F2* qz, const Ctx& ctx, F2* tacc) {
+    F2 r2[PP], s[PP];
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 dx = sub2(f2s(R.c.x), qx[pp]), dy = sub2(f2s(R.c.y), qy[pp]);
+      const F2 dz = sub2(f2s(R.c.z), qz[pp]);
+      r2[pp] = dot2(dx, dy, dz, dx, dy, dz);
+      s[pp] = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
+    }
+    return finish<PP>(r2, s, ctx, tacc);
+  }
   __device__ __forceinline__ static double rare(const Rec&, float, float, float, double) {
     return __longlong_as_double(0x7ff8000000000000ll);  // always an on-surface (flagged) pair
   }
@@ -238,21 +309,23 @@ __global__ void finalize_theta_kernel(const double* __restrict__ part,
 
 int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, int policy, float* out, uint8_t* flags,
-                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream) {
+                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream,
+                         const Batch& bt) {
   return launch_fwd_f32<ExactPol>(packed, n_faces, ps, n_count, policy, out, flags, workspace,
-                                  ws_bytes, num_sms, stream);
+                                  ws_bytes, num_sms, stream, bt);
 }
-size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
-  return FwdPlan<ExactPol>::make(n_faces, n_count, num_sms).workspace(n_count);
+size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
+  return FwdPlan<ExactPol>::make(n_faces, n_count, num_sms, batch).workspace(n_count * batch);
 }
 int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, int policy, float* out, uint8_t* flags,
-                        void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream) {
+                        void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream,
+                        const Batch& bt) {
   return launch_fwd_f32<SoftPol>(packed, n_faces, ps, n_count, policy, out, flags, workspace,
-                                 ws_bytes, num_sms, stream);
+                                 ws_bytes, num_sms, stream, bt);
 }
-size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
-  return FwdPlan<SoftPol>::make(n_faces, n_count, num_sms).workspace(n_count);
+size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
+  return FwdPlan<SoftPol>::make(n_faces, n_count, num_sms, batch).workspace(n_count * batch);
 }
 
 }  // namespace wv

@@ -77,6 +77,15 @@ struct ListSrc64 {
 };
 
 // Forward output sink: final values (single split) or per-split partials.
+// Batched launches over meshes with one connectivity and one query range:
+// mesh z's packed records start z * pack_stride bytes after the first's
+// (a multiple of 16 for the TMA copies), its outputs / coefficients lie
+// z * count entries after the first's.
+struct Batch {
+  int64_t n = 1;
+  size_t pack_stride = 0;
+};
+
 struct OutF32 {
   float* out = nullptr;
   uint8_t* flags = nullptr;
@@ -155,12 +164,16 @@ int launch_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t
 // forward (wv_exact_fwd.cu, wv_soft_fwd.cu, wv_f64.cu)
 int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, int policy, float* out, uint8_t* flags,
-                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream);
-size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream,
+                         const Batch& bt = Batch());
+size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms,
+                                 int64_t batch = 1);
 int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, int policy, float* out, uint8_t* flags,
-                        void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream);
-size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+                        void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream,
+                         const Batch& bt = Batch());
+size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms,
+                                int64_t batch = 1);
 int launch_exact_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, int use_atan2, int policy, double* out, uint8_t* flags,
                          cudaStream_t stream);
@@ -172,12 +185,14 @@ int launch_soft_fwd_f64(const void* packed, int64_t n_faces, const PointSource& 
 int launch_exact_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, const float* coefs, double coef_scale,
                          double* face_grad, void* ws, size_t ws_bytes, int num_sms,
-                         cudaStream_t stream);
+                         cudaStream_t stream,
+                         const Batch& bt = Batch());
 int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, const float* coefs, double coef_scale,
                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
-                        cudaStream_t stream);
-size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+                        cudaStream_t stream,
+                         const Batch& bt = Batch());
+size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch = 1);
 int launch_exact_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, const double* coefs, double coef_scale,
                          double* face_grad, void* ws, size_t ws_bytes, int num_sms,
