@@ -175,6 +175,13 @@ struct ExactEdgeBwd {
     z[10] = fma2(t20, ic, z[10]);
     z[11] = fma2(u20, ic, z[11]);
   }
+  template <bool kUnit, int N>
+  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
+                                                  float eps2, F2* z) {
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+      pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
+  }
   // sum_q m s for every (edge, corner) from the run's sums, into the face's
   // fp64 accumulators (acc[j][thread], j = corner * 3 + axis)
   __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
@@ -282,6 +289,40 @@ struct SoftBwd {
     z[2] = add2(z[2], c5);
     z[3] = fma2(c5, dz, z[3]);
   }
+  // N point pairs; the r < eps test is done once on the minimum r^2 of the
+  // step (nearly always passes), so the common path has no per-lane selects
+  template <bool kUnit, int N>
+  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
+                                                  float eps2, F2* z) {
+    F2 dz[N], r2[N];
+    float m = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      dz[u] = sub2(f2s(R.c.z), f2(zc[u].x, zc[u].y));
+      r2[u] = fma2(dz[u], dz[u], f2s(w.r2));
+      float l, h;
+      split(r2[u], l, h);
+      m = fminf(m, fminf(l, h));
+    }
+    if (m < eps2) {  // some point of the step sits on this face's centroid
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+        pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      const F2 rs = rsqrt2(r2[u]);
+      const F2 S = fma2(f2s(R.n.z), dz[u], f2s(w.s));
+      const F2 rs2 = mul2(rs, rs);
+      const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), rs2), rs);
+      const F2 c5 = mul2(mul2(c3, S), rs2);
+      z[0] = add2(z[0], c3);
+      z[1] = fma2(c3, dz[u], z[1]);
+      z[2] = add2(z[2], c5);
+      z[3] = fma2(c5, dz[u], z[3]);
+    }
+  }
   __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
                                                    double (*acc)[kBwdThreads]) {
     double S[kRowAcc];
@@ -374,9 +415,7 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
         any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
       }
       if (!any) continue;
-#pragma unroll
-      for (int u = 0; u < kRowStep; ++u)
-        Pol::template pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
+      Pol::template step_row<kUnit, kRowStep>(R, w, zc, eps2, z);
     }
 #pragma unroll 1
     for (; j < e; ++j) {
