@@ -32,6 +32,7 @@ struct PointSource {
 
 struct GridSrc {
   static constexpr bool kRows = false;
+  static constexpr bool kGrid = true;
   GridDesc g;
   int64_t n0;
   __device__ __forceinline__ void point(int64_t l, float& x, float& y, float& z) const {
@@ -58,6 +59,7 @@ inline bool row_aligned(const GridDesc& g, int64_t n0, int64_t count, int run) {
 
 struct ListSrc {
   static constexpr bool kRows = false;
+  static constexpr bool kGrid = false;
   const float* pts;
   __device__ __forceinline__ void point(int64_t l, float& x, float& y, float& z) const {
     x = pts[3 * l + 0];
@@ -68,6 +70,7 @@ struct ListSrc {
 
 struct ListSrc64 {
   static constexpr bool kRows = false;
+  static constexpr bool kGrid = false;
   const double* pts;
   __device__ __forceinline__ void point(int64_t l, double& x, double& y, double& z) const {
     x = pts[3 * l + 0];
