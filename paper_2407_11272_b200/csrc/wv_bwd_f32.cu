@@ -19,6 +19,8 @@
 //   G_2 = d x u, G_0 = -G_1 - G_2; the N/3 and d terms are shared by the three
 //   corners, so they are accumulated once per face.
 // Per-chunk fp32 partials are folded into fp64 accumulators.
+#include <cmath>
+
 #include "wv_f32x2.cuh"
 #include "wv_kernels.h"
 
@@ -43,6 +45,13 @@ constexpr int kAxisMax = 1024;    // lattice axes up to this length use node tab
 // into coef_scale by the launcher.
 struct ExactEdgeBwd {
   using Rec = ExactGradRecF32;
+  static constexpr bool kScaled = true;
+  __device__ __forceinline__ static void scale(Rec& R, float s) {
+    R.a.x *= s; R.a.y *= s; R.a.z *= s;
+    R.b.x *= s; R.b.y *= s; R.b.z *= s;
+    R.c.x *= s; R.c.y *= s; R.c.z *= s;
+    R.u.x *= s * s; R.u.y *= s * s; R.u.z *= s * s;
+  }
   static constexpr int kMinBlocks = kBwdMinBlocks;
   // -1/(4 pi) and the factor 2 of d = 2 (|a||b| + a.b) below
   static constexpr double kCoefScale = -2.0 / (4.0 * kPi);
@@ -218,6 +227,8 @@ struct ExactEdgeBwd {
 
 struct SoftBwd {
   using Rec = SoftGradRecF32;
+  static constexpr bool kScaled = false;
+  __device__ __forceinline__ static void scale(Rec&, float) {}
   static constexpr int kMinBlocks = kBwdMinBlocks;
   static constexpr double kCoefScale = 1.0 / (8.0 * kPi);
   static constexpr int kAcc = 10;  // acc1(3) acc2(3) T(1) D(3)
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(kBwdThreads, Pol::kMinBlocks)
 bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
                size_t pack_stride, int64_t n_faces, Src src, const float* __restrict__ coefs,
                int64_t n_count, int64_t pts_per_split, float coef_scale,
-               double* __restrict__ out) {
+               double* __restrict__ out, float gscale) {
   __shared__ PointChunk chunk;
   // batched launches: blockIdx.z selects the mesh (records pack_stride bytes
   // apart, coefficients n_count apart, partials (mesh, split)-major)
@@ -445,6 +456,10 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   const int64_t f = (int64_t)blockIdx.x * kBwdThreads + threadIdx.x;
   const bool live = f < n_faces;
   typename Pol::Rec R = recs[live ? f : 0];
+  // power-of-two geometry scale (row mode of the exact backward, see
+  // launch_bwd): exact in floating point, so the arithmetic is the unscaled
+  // one; the corner sums are scaled back on the way out
+  if (gscale != 1.0f) Pol::scale(R, gscale);
   const float eps = hdr->eps_f32;
   const float eps2 = eps * eps;
   const int64_t p_begin = (int64_t)blockIdx.y * pts_per_split;
@@ -473,7 +488,7 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     if (tab) {
       for (int a = 0; a < 3; ++a)
         for (int t = threadIdx.x; t < src.g.res[a]; t += kBwdThreads)
-          axt[a][t] = (float)axis_node(src.g.lo[a], src.g.hi[a], src.g.res[a], t);
+          axt[a][t] = (float)axis_node(src.g.lo[a], src.g.hi[a], src.g.res[a], t) * gscale;
     }
   }
 
@@ -499,6 +514,9 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
               z = axt[2][gl - r * rz];
             } else {
               src.point(c0 + i, x, y, z);
+              x *= gscale;
+              y *= gscale;
+              z *= gscale;
             }
           } else {
             src.point(c0 + i, x, y, z);
@@ -547,7 +565,7 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     Pol::finish(R, a, o9);
     double* dst = out + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * n_faces + f) * 9;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) dst[j] = o9[j];
+    for (int j = 0; j < 9; ++j) dst[j] = o9[j] * (double)gscale;  // dW/dv = s dW/d(s v)
   }
 }
 // out[f*9+j] = sum_s part[s][f*9+j], fixed split order
@@ -593,6 +611,20 @@ struct BwdPlan {
   }
 };
 
+// Power of two bringing the lattice's largest |coordinate| into [1, 2): the
+// row backward's shared reciprocal forms d01 d12 d20 (~|x|^6), which must
+// stay inside the f32 range for any input scale.
+static float grid_scale(const GridDesc& g) {
+  double m = 0.0;
+  for (int a = 0; a < 3; ++a) m = fmax(m, fmax(fabs(g.lo[a]), fabs(g.hi[a])));
+  if (!(m > 0.0) || !std::isfinite(m)) return 1.0f;
+  int e;
+  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  if (e > 120) e = 120;
+  if (e < -120) e = -120;
+  return (float)ldexp(1.0, 1 - e);
+}
+
 template <class Pol>
 static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps,
                       int64_t n_count, const float* coefs, double coef_scale, double* face_grad,
@@ -618,15 +650,16 @@ static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps
       row_aligned(ps.grid, ps.n0, 2 * ((n_count + 1) / 2), 2)) {
     RowSrc src{{ps.grid, ps.n0}};
     bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst,
+        Pol::kScaled ? grid_scale(ps.grid) : 1.0f);
   } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
     bwd_f32_kernel<Pol, GridSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
   } else {
     ListSrc src{ps.points};
     bwd_f32_kernel<Pol, ListSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst);
+        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
   }
   if (pl.splits > 1) {
     const int64_t n = n_faces * 9;

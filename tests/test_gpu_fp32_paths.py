@@ -221,3 +221,23 @@ def test_row_backward_matches_generic_and_oracle(torch_, c2, mode):
         ref = ofn(c2.vertices, c2.faces, pts32.astype(np.float64),
                   coefs.astype(np.float32).astype(np.float64), chunk=256)
         assert rel_err(got, ref) <= G_TOL
+
+
+@pytest.mark.parametrize("scale", [1.0e6, 3.0e-4])
+def test_row_backward_scale_invariance(torch_, c2, scale):
+    """The row backward forms d01 d12 d20 (~|x|^6) for its shared reciprocal;
+    a power-of-two rescaling keeps that product in range at any input scale.
+    Scaling mesh and lattice by L scales dW/dv by 1/L (f32 tolerance)."""
+    torch = torch_
+    from paper_2407_11272_b200 import device as D
+    res = (12, 10, 40)
+    coefs = torch.from_numpy(np.random.default_rng(3).normal(size=int(np.prod(res)))).float()
+
+    def grads(L):
+        dm = D.DeviceMesh.from_numpy(c2.vertices * L, c2.faces)
+        grid = ((-L,) * 3, (L,) * 3, res)
+        return D.vertex_grad(dm, D.face_grad(dm, "exact", "f32", coefs, grid=grid)).cpu().numpy()
+
+    g1, gs = grads(1.0), grads(scale)
+    assert np.isfinite(gs).all()
+    assert rel_err(gs * scale, g1) <= G_TOL  # inputs re-rounded at the new scale
