@@ -158,23 +158,87 @@ struct ExactPol {
     tacc = fma2(f2(cl ? tl : 0.0f, ch ? th : 0.0f), p, tacc);
     return (cl ? 0u : 1u) | (ch ? 0u : 2u);
   }
-  // all PP point pairs of a thread against one face
+  // All PP point pairs of a thread against one face.  The common-pair test
+  // of tail2 (|alpha| < beta/8 and beta > |a||b||c|/2) is evaluated for the
+  // whole face as ONE predicate, max over lanes of (|alpha| - beta/8,
+  // |a||b||c| - 2 beta) < 0, from packed FFMAs and a 3-input max tree: when
+  // every point of the thread is a common pair (nearly always) the terms are
+  // added without per-lane selects or rare-mask building, which had cost
+  // ~1/3 of the issue slots.  Otherwise the per-lane path (tail2) runs.
+  template <int PP>
+  __device__ __forceinline__ static uint32_t finish(const Rec& R, const F2* alpha, const F2* la2,
+                                                    const F2* lb2, const F2* lc2, const Ctx& ctx,
+                                                    F2* tacc) {
+    F2 tq[PP], tp[PP];
+    float m = -1.0f;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 la = sqrt2(la2[pp]), lb = sqrt2(lb2[pp]), lc = sqrt2(lc2[pp]);
+      const F2 half = f2s(0.5f);
+      const F2 ab = fma2(add2(la2[pp], lb2[pp]), half, f2s(-R.v1.w));
+      const F2 bc = fma2(add2(lb2[pp], lc2[pp]), half, f2s(-R.v2.w));
+      const F2 ca = fma2(add2(lc2[pp], la2[pp]), half, f2s(-R.n.w));
+      const F2 labc = mul2(la, mul2(lb, lc));
+      const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
+      // |alpha| - beta/8 and |a||b||c| - 2 beta: the scalings are exact and
+      // an fma rounds once, so each sign is the exact comparison's (the same
+      // classification as tail2's exponent-subtract test)
+      const F2 dd = fma2(beta, f2s(-0.125f), abs2(alpha[pp]));
+      const F2 ee = fma2(beta, f2s(-2.0f), labc);
+      float d0, d1, e0, e1;
+      split(dd, d0, d1);
+      split(ee, e0, e1);
+      m = fmaxf(m, fmaxf(fmaxf(d0, d1), fmaxf(e0, e1)));
+      const F2 tt = mul2(alpha[pp], rcp2(beta));
+      const F2 s = mul2(tt, tt);
+      tq[pp] = tt;
+      tp[pp] = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
+                    f2s(1.0f));
+    }
+    if (m < 0.0f) {  // tail2's exact operation for a common pair: tacc + t p, one rounding
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
+      return 0u;
+    }
+    uint32_t rare = 0;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp)
+      rare |= tail2(R, alpha[pp], la2[pp], lb2[pp], lc2[pp], tacc[pp]) << (2 * pp);
+    return rare;
+  }
   template <int PP>
   __device__ __forceinline__ static uint32_t face_row(const Rec& R, const Row& w, const F2* qz,
                                                       const Ctx& ctx, F2* tacc) {
-    uint32_t rare = 0;
+    F2 alpha[PP], la2[PP], lb2[PP], lc2[PP];
 #pragma unroll
-    for (int pp = 0; pp < PP; ++pp) rare |= common_row2(R, w, qz[pp], ctx, tacc[pp]) << (2 * pp);
-    return rare;
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
+      const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
+      alpha[pp] = fma2(f2s(R.n.z), az, f2s(w.alpha));
+      la2[pp] = fma2(az, az, f2s(w.a2));
+      lb2[pp] = fma2(bz, bz, f2s(w.b2));
+      lc2[pp] = fma2(cz, cz, f2s(w.c2));
+    }
+    return finish<PP>(R, alpha, la2, lb2, lc2, ctx, tacc);
   }
   template <int PP>
   __device__ __forceinline__ static uint32_t face(const Rec& R, const F2* qx, const F2* qy,
                                                   const F2* qz, const Ctx& ctx, F2* tacc) {
-    uint32_t rare = 0;
+    F2 alpha[PP], la2[PP], lb2[PP], lc2[PP];
 #pragma unroll
-    for (int pp = 0; pp < PP; ++pp)
-      rare |= common2(R, qx[pp], qy[pp], qz[pp], ctx, tacc[pp]) << (2 * pp);
-    return rare;
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 ax = sub2(f2s(R.v0e.x), qx[pp]), ay = sub2(f2s(R.v0e.y), qy[pp]);
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]);
+      const F2 bx = sub2(f2s(R.v1.x), qx[pp]), by = sub2(f2s(R.v1.y), qy[pp]);
+      const F2 bz = sub2(f2s(R.v1.z), qz[pp]);
+      const F2 cx = sub2(f2s(R.v2.x), qx[pp]), cy = sub2(f2s(R.v2.y), qy[pp]);
+      const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
+      alpha[pp] = fma2(f2s(R.n.z), az, fma2(f2s(R.n.y), ay, mul2(f2s(R.n.x), ax)));
+      la2[pp] = dot2(ax, ay, az, ax, ay, az);
+      lb2[pp] = dot2(bx, by, bz, bx, by, bz);
+      lc2[pp] = dot2(cx, cy, cz, cx, cy, cz);
+    }
+    return finish<PP>(R, alpha, la2, lb2, lc2, ctx, tacc);
   }
   __device__ __forceinline__ static double rare(const Rec& R, float qx, float qy, float qz,
                                                 double eps) {
