@@ -47,7 +47,7 @@ EXACT_BWD_FLOPS = 170
 # face-wise closed form, so they execute FEWER FLOPs than the pinned
 # algorithmic counts above: the algorithmic-FLOP rate can exceed the FP32
 # peak, and the executed-work fractions below are the pipe utilisation.
-EXACT_FWD_EXEC_FLOPS = 38.25   # fwd_f32_kernel<ExactPol,RowSrc>, 4 MUFU
+EXACT_FWD_EXEC_FLOPS = 42.25   # fwd_f32_kernel<ExactPol,RowSrc> all-common fast path, 4 MUFU
 EXACT_BWD_EXEC_FLOPS = 60.5    # bwd_f32_kernel<ExactEdgeBwd,RowSrc> unit-weight loop, 4 MUFU
 EXACT_FWD_MUFU = 4
 EXACT_BWD_MUFU = 4
