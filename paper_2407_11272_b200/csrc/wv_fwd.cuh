@@ -97,9 +97,19 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       uint32_t rare;
       if constexpr (kRows) {
         const typename Pol::Row w = Pol::row(R, rx, ry);
-        rare = Pol::template face_row<PP>(R, w, qz, ctx, tacc);
+        // groups of (at most) 4 point pairs: the per-face row constants are
+        // shared by all of a thread's points, the temporaries by one group
+        rare = 0;
+#pragma unroll
+        for (int g0 = 0; g0 < PP; g0 += 4)
+          rare |= Pol::template face_row<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, tacc + g0)
+                  << (2 * g0);
       } else {
-        rare = Pol::template face<PP>(R, qx, qy, qz, ctx, tacc);
+        rare = 0;
+#pragma unroll
+        for (int g0 = 0; g0 < PP; g0 += 4)
+          rare |= Pol::template face<(PP < 4 ? PP : 4)>(R, qx + g0, qy + g0, qz + g0, ctx,
+                                                          tacc + g0) << (2 * g0);
       }
       if (rare != 0u) {
 #pragma unroll
