@@ -1,4 +1,4 @@
-"""Multi-process (gloo, world_size 2, CPU) test of the slab-sharded driver.
+"""Multi-process (gloo, world sizes 2 and 3, CPU) test of the slab-sharded driver.
 
 The driver's sharding, all-gather and single packed all-reduce are the
 product code; the per-slab compute is injected as an oracle evaluator
@@ -88,9 +88,12 @@ def test_slab_ranges_cover_grid():
             assert (covered == 1).all()
 
 
-def test_two_rank_loss_grad_matches_single_process(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_loss_grad_matches_single_process(tmp_path, world):
+    """world 2: equal slabs; world 3: uneven slabs (the node count is not a
+    multiple of 3)."""
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
     out = np.load(tmp_path / "out.npz")
     from oracle import oracle as orc
     g = golden("loss_grad")
