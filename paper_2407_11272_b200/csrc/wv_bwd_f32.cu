@@ -1,11 +1,15 @@
 // wv_bwd_f32.cu -- FP32 backward kernels: per-face vertex gradients of the
 // exact and soft winding numbers, reduced over query points.
 //
-// Mapping (the transpose of the forward): every thread OWNS one face and keeps
-// its 9 gradient partials in registers; the CTA streams chunks of query
-// points (coordinates + coefficient) through shared memory, so every warp
-// reads the same point at the same time (broadcast LDS) and the per-point
-// "coef == 0" skip of the reference (_kernels.py:182-184) is warp-uniform.
+// Mapping (the transpose of the forward): every thread OWNS one face; the CTA
+// streams chunks of query points (coordinates + coefficient) through shared
+// memory, so every warp reads the same point at the same time (broadcast
+// LDS) and the per-point "coef == 0" skip of the reference
+// (_kernels.py:182-184) is warp-uniform.  Generic sources keep fp32 partials
+// per chunk; lattice sources (RowSrc) cut each chunk into k-row runs and keep
+// a few running sums per run that are expanded into the face's corner sums
+// once per run (flush_row) -- see ExactEdgeBwd / SoftBwd "Lattice-row form".
+// The face's fp64 accumulators live in shared memory (5 CTAs per SM).
 // No shuffles and no atomics: each (face block, point split) CTA writes its
 // partials once, a fixed-order reduction sums the splits, and a CSR gather
 // (wv_face_to_vertex) sums face corners into vertices -- bit-reproducible
@@ -18,7 +22,7 @@
 //   dW/dv_k = [(G_k + N/3) / r^3 - S d / r^5] / (8 pi),  G_1 = w x d,
 //   G_2 = d x u, G_0 = -G_1 - G_2; the N/3 and d terms are shared by the three
 //   corners, so they are accumulated once per face.
-// Per-chunk fp32 partials are folded into fp64 accumulators.
+// fp32 partials (per chunk or per run) are folded into fp64 accumulators.
 #include <cmath>
 
 #include "wv_f32x2.cuh"
