@@ -57,3 +57,65 @@ def test_batch_loss_matches_oracle_per_mesh(cuda_device):
         opt.step()
         first = float(l) if first is None else first
     assert float(l) < first
+
+
+@pytest.mark.parametrize("mode", ["exact", "soft"])
+def test_batched_grid_kernels_match_per_mesh_calls(cuda_device, mode):
+    """wv_fwd_grid_f32_batch / wv_bwd_grid_f32_batch (blockIdx.z = mesh, packs
+    pack_stride bytes apart) against one single-mesh launch per mesh.  The
+    split plan can differ between the two (it sees the whole batch), which
+    only reorders fp64 partial sums: values agree to f32 rounding, flags
+    exactly, corner sums to 1e-6 relative.  Also a node range that starts
+    inside the grid (n0 > 0); open meshes (the exact backward's active
+    faces are the boundary strip)."""
+    import torch
+    from paper_2407_11272_b200 import _lib as L, configs, device
+    from paper_2407_11272_b200.device import _ptr, _stream
+    lib = L.lib()
+    meshes = configs.c4_batch(5)
+    # open the icospheres (a closed mesh has no active exact-gradient faces)
+    faces = torch.from_numpy(np.ascontiguousarray(meshes[0][1][40:])).cuda()
+    B, R = len(meshes), 24
+    grid = ((-1.0,) * 3, (1.0,) * 3, (R, R, R))
+    n0, N = 3 * R * R, 17 * R * R
+    g = L.make_grid(*grid)
+    dms = [device.DeviceMesh(torch.from_numpy(m[0]).float().cuda(), faces) for m in meshes]
+    fkind = L.PACK_EXACT_F32 if mode == "exact" else L.PACK_SOFT_F32
+    packs = [dm.packed(fkind) for dm in dms]
+    stride = (packs[0].numel() + 15) // 16 * 16
+    buf = torch.zeros(B * stride, dtype=torch.uint8, device="cuda")
+    for b, p in enumerate(packs):
+        buf[b * stride:b * stride + p.numel()] = p
+    F = int(faces.shape[0])
+    vals = torch.empty((B, N), dtype=torch.float32, device="cuda")
+    flags = torch.empty((B, N), dtype=torch.uint8, device="cuda")
+    wsb = int(lib.wv_fwd_workspace_bytes_batch(fkind, F, N, B))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    L.check(lib.wv_fwd_grid_f32_batch(fkind, _ptr(buf), stride, F, g, n0, N, B, L.POLICY_RAW,
+                                      _ptr(vals), _ptr(flags), _ptr(ws), wsb, _stream()), "fwd")
+    coefs = torch.from_numpy(np.random.default_rng(1).normal(size=(B, N))).float().cuda()
+    for b, dm in enumerate(dms):
+        v1, f1 = device.forward(dm, mode, "f32", grid=grid, n0=n0, count=N)
+        assert torch.equal(f1, flags[b])
+        assert (v1 - vals[b]).abs().max().item() <= 1e-6
+        coefs[b][f1.bool()] = 0.0
+    # backward
+    if mode == "exact":
+        gpacks = [dm.packed_exact_grad("f32") for dm in dms]
+        gkind, A = L.PACK_EXACTGRAD_F32, int(dms[0].exact_grad_setup()[0].shape[0])
+    else:
+        gpacks = [dm.packed(L.PACK_SOFTGRAD_F32) for dm in dms]
+        gkind, A = L.PACK_SOFTGRAD_F32, F
+    gstride = (gpacks[0].numel() + 15) // 16 * 16
+    gbuf = torch.zeros(B * gstride, dtype=torch.uint8, device="cuda")
+    for b, p in enumerate(gpacks):
+        gbuf[b * gstride:b * gstride + p.numel()] = p
+    fg = torch.empty((B, A, 3, 3), dtype=torch.float64, device="cuda")
+    wsb = int(lib.wv_bwd_workspace_bytes_batch(gkind, A, N, B))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    L.check(lib.wv_bwd_grid_f32_batch(gkind, _ptr(gbuf), gstride, A, g, n0, N, B, _ptr(coefs),
+                                      1.0, _ptr(fg), _ptr(ws), wsb, _stream()), "bwd")
+    for b, dm in enumerate(dms):
+        one, _ = device.face_grad(dm, mode, "f32", coefs[b], grid=grid, n0=n0, count=N)
+        ref = one.reshape(A, 3, 3)
+        assert (fg[b] - ref).abs().max().item() <= 1e-6 * ref.abs().max().item()
