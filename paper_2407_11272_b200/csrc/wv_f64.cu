@@ -19,7 +19,7 @@ constexpr int kF64Stages = 4;
 constexpr int kF64ConsumerWarps = 4;
 constexpr int kF64NC = kF64ConsumerWarps * 32;
 constexpr int kF64Threads = kF64NC;
-constexpr int kF64P = 4;
+constexpr int kF64P = 1;
 constexpr double kBaryTol = 1e-12;  // _kernels.py:31
 
 struct ExactF64Pol {
@@ -91,7 +91,7 @@ struct SoftF64Pol {
 };
 
 template <class Pol, class Src>
-__global__ void __launch_bounds__(kF64Threads, 2)
+__global__ void __launch_bounds__(kF64Threads, 6)
 fwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
                int64_t n_faces, Src src, int64_t n_count, int use_atan2, int policy,
                double* __restrict__ out, uint8_t* __restrict__ flags) {
