@@ -49,6 +49,8 @@ constexpr int kAxisMax = 1024;    // lattice axes up to this length use node tab
 // into coef_scale by the launcher.
 struct ExactEdgeBwd {
   using Rec = ExactGradRecF32;
+  static constexpr int kFaces = 1;  // faces per thread (per record)
+  static constexpr int kOut = 9;
   static constexpr bool kScaled = true;
   __device__ __forceinline__ static void scale(Rec& R, float s) {
     R.a.x *= s; R.a.y *= s; R.a.z *= s;
@@ -231,6 +233,8 @@ struct ExactEdgeBwd {
 
 struct SoftBwd {
   using Rec = SoftGradRecF32;
+  static constexpr int kFaces = 1;
+  static constexpr int kOut = 9;
   static constexpr bool kScaled = false;
   __device__ __forceinline__ static void scale(Rec&, float) {}
   static constexpr int kMinBlocks = kBwdMinBlocks;
@@ -375,6 +379,99 @@ struct SoftBwd {
     out9[6] = a[3] + cx;
     out9[7] = a[4] + cy;
     out9[8] = a[5] + cz;
+  }
+};
+
+// Soft backward with TWO faces per thread (the C4 meshes): the point loads,
+// loop control and on-centroid test of a step are shared by both faces, and
+// their two independent dependency chains interleave.  Faces 2r and 2r+1 form
+// record r (so the face count must be even); their corner sums are the 18
+// consecutive doubles of faces 2r, 2r+1 in the output.
+struct SoftPairRec {
+  SoftGradRecF32 f[2];
+};
+struct SoftBwdPair {
+  using One = SoftBwd;
+  using Rec = SoftPairRec;
+  static constexpr int kFaces = 2;
+  static constexpr int kOut = 18;
+  static constexpr int kRowStep = 4;
+  static constexpr bool kScaled = false;
+  __device__ __forceinline__ static void scale(Rec&, float) {}
+  static constexpr int kMinBlocks = 4;  // two faces' state: up to 128 registers
+  static constexpr double kCoefScale = One::kCoefScale;
+  static constexpr int kAcc = 2 * One::kAcc;
+  static constexpr int kRowAcc = 2 * One::kRowAcc;
+  __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
+  template <bool kUnit>
+  __device__ __forceinline__ static void pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                               float eps2, F2* g) {
+    One::pair2<kUnit>(R.f[0], qx, qy, qz, coef, eps2, g);
+    One::pair2<kUnit>(R.f[1], qx, qy, qz, coef, eps2, g + One::kAcc);
+  }
+  struct Row {
+    One::Row r[2];
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    Row w;
+    w.r[0] = One::row(R.f[0], qx, qy);
+    w.r[1] = One::row(R.f[1], qx, qy);
+    return w;
+  }
+  template <bool kUnit>
+  __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
+                                                   float eps2, F2* z) {
+    One::pair_row2<kUnit>(R.f[0], w.r[0], qz, coef, eps2, z);
+    One::pair_row2<kUnit>(R.f[1], w.r[1], qz, coef, eps2, z + One::kRowAcc);
+  }
+  // both faces' r^2 first, one on-centroid test for the whole step
+  template <bool kUnit, int N>
+  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
+                                                  float eps2, F2* z) {
+    F2 dz[2][N], r2[2][N];
+    float m = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        dz[k][u] = sub2(f2s(R.f[k].c.z), f2(zc[u].x, zc[u].y));
+        r2[k][u] = fma2(dz[k][u], dz[k][u], f2s(w.r[k].r2));
+        float l, h;
+        split(r2[k][u], l, h);
+        m = fminf(m, fminf(l, h));
+      }
+    }
+    if (m < eps2) {
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+        pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        F2* zk = z + k * One::kRowAcc;
+        const F2 rs = rsqrt2(r2[k][u]);
+        const F2 S = fma2(f2s(R.f[k].n.z), dz[k][u], f2s(w.r[k].s));
+        const F2 rs2 = mul2(rs, rs);
+        const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), rs2), rs);
+        const F2 c5 = mul2(mul2(c3, S), rs2);
+        zk[0] = add2(zk[0], c3);
+        zk[1] = fma2(c3, dz[k][u], zk[1]);
+        zk[2] = add2(zk[2], c5);
+        zk[3] = fma2(c5, dz[k][u], zk[3]);
+      }
+    }
+  }
+  __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
+                                                   double (*acc)[kBwdThreads]) {
+    One::flush_row(R.f[0], w.r[0], z, acc);
+    One::flush_row(R.f[1], w.r[1], z + One::kRowAcc, acc + One::kAcc);
+  }
+  __device__ __forceinline__ static void finish(const Rec& R, const double* a, double* out) {
+    One::finish(R.f[0], a, out);
+    One::finish(R.f[1], a + One::kAcc, out + 9);
   }
 };
 
@@ -562,14 +659,14 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     }
   }
   if (live) {
-    double o9[9];
+    double o9[Pol::kOut];
     double a[Pol::kAcc];
 #pragma unroll
     for (int j = 0; j < Pol::kAcc; ++j) a[j] = acc[j][threadIdx.x];
     Pol::finish(R, a, o9);
-    double* dst = out + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * n_faces + f) * 9;
+    double* dst = out + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * n_faces + f) * Pol::kOut;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) dst[j] = o9[j] * (double)gscale;  // dW/dv = s dW/d(s v)
+    for (int j = 0; j < Pol::kOut; ++j) dst[j] = o9[j] * (double)gscale;  // dW/dv = s dW/d(s v)
   }
 }
 // out[f*9+j] = sum_s part[s][f*9+j], fixed split order
@@ -609,8 +706,9 @@ struct BwdPlan {
     if (p.splits < 1) p.splits = 1;
     return p;
   }
-  size_t workspace(int64_t n_faces, int64_t batch = 1) const {
-    return splits > 1 ? (size_t)splits * (size_t)batch * (size_t)n_faces * 9 * sizeof(double)
+  // n_rec records of k_out doubles each (9 per face)
+  size_t workspace(int64_t n_rec, int64_t batch = 1, int k_out = 9) const {
+    return splits > 1 ? (size_t)splits * (size_t)batch * (size_t)n_rec * k_out * sizeof(double)
                       : 0;
   }
 };
@@ -629,6 +727,9 @@ static float grid_scale(const GridDesc& g) {
   return (float)ldexp(1.0, 1 - e);
 }
 
+// two faces per thread for the soft backward whenever the face count is even
+static bool soft_pairs(int64_t n_faces) { return n_faces >= 2 && n_faces % 2 == 0; }
+
 template <class Pol>
 static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps,
                       int64_t n_count, const float* coefs, double coef_scale, double* face_grad,
@@ -642,10 +743,12 @@ static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps
   }
   const PackHeader* hdr = static_cast<const PackHeader*>(packed);
   const auto* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
-  const BwdPlan pl = BwdPlan::make(n_faces, n_count, num_sms, Pol::kMinBlocks, bt.n);
+  const int64_t n_rec = n_faces / Pol::kFaces;  // callers pass a multiple of kFaces
+  const BwdPlan pl = BwdPlan::make(n_rec, n_count, num_sms, Pol::kMinBlocks, bt.n);
   double* dst = face_grad;
   if (pl.splits > 1) {
-    if (workspace == nullptr || ws_bytes < pl.workspace(n_faces, bt.n)) return kErrWorkspace;
+    if (workspace == nullptr || ws_bytes < pl.workspace(n_rec, bt.n, Pol::kOut))
+      return kErrWorkspace;
     dst = static_cast<double*>(workspace);
   }
   const float cs = (float)(coef_scale * Pol::kCoefScale);
@@ -654,19 +757,19 @@ static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps
       row_aligned(ps.grid, ps.n0, 2 * ((n_count + 1) / 2), 2)) {
     RowSrc src{{ps.grid, ps.n0}};
     bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst,
+        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst,
         Pol::kScaled ? grid_scale(ps.grid) : 1.0f);
   } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
     bwd_f32_kernel<Pol, GridSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
+        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
   } else {
     ListSrc src{ps.points};
     bwd_f32_kernel<Pol, ListSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
+        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
   }
   if (pl.splits > 1) {
-    const int64_t n = n_faces * 9;
+    const int64_t n = n_rec * Pol::kOut;
     int blocks = (int)((n * bt.n + 255) / 256);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
     reduce_splits_kernel<<<blocks, 256, 0, stream>>>(dst, pl.splits, n, bt.n, face_grad);
@@ -685,8 +788,17 @@ int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& 
                         int64_t n_count, const float* coefs, double coef_scale,
                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                         cudaStream_t stream, const Batch& bt) {
+  if (soft_pairs(n_faces))
+    return launch_bwd<SoftBwdPair>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad,
+                                   ws, ws_bytes, num_sms, stream, bt);
   return launch_bwd<SoftBwd>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad, ws,
                              ws_bytes, num_sms, stream, bt);
+}
+size_t soft_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
+  if (soft_pairs(n_faces))
+    return BwdPlan::make(n_faces / 2, n_count, num_sms, SoftBwdPair::kMinBlocks, batch)
+        .workspace(n_faces / 2, batch, SoftBwdPair::kOut);
+  return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);
 }
 size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
   return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);

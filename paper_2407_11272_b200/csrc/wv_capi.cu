@@ -195,8 +195,8 @@ int wv_soft_fwd_points_f64(const void* packed, int64_t n_faces, const double* po
 // ---- backward --------------------------------------------------------------
 size_t wv_bwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {
-    case WV_PACK_EXACTGRAD_F32:
-    case WV_PACK_SOFTGRAD_F32: return wv::bwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_EXACTGRAD_F32: return wv::bwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_SOFTGRAD_F32: return wv::soft_bwd_workspace_bytes(n_faces, count, sm_count());
     case WV_PACK_EXACTGRAD_F64:
     case WV_PACK_SOFTGRAD_F64: return wv::bwd64_workspace_bytes(n_faces, count, sm_count());
     default: return 0;
@@ -449,7 +449,9 @@ size_t wv_bwd_workspace_bytes_batch(int kind, int64_t n_faces, int64_t count, in
   if (batch < 1) return 0;
   switch (kind) {
     case WV_PACK_EXACTGRAD_F32:
-    case WV_PACK_SOFTGRAD_F32: return wv::bwd_workspace_bytes(n_faces, count, sm_count(), batch);
+      return wv::bwd_workspace_bytes(n_faces, count, sm_count(), batch);
+    case WV_PACK_SOFTGRAD_F32:
+      return wv::soft_bwd_workspace_bytes(n_faces, count, sm_count(), batch);
     default: return 0;
   }
 }

@@ -196,6 +196,8 @@ int launch_soft_bwd_f32(const void* packed, int64_t n_faces, const PointSource& 
                         cudaStream_t stream,
                          const Batch& bt = Batch());
 size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch = 1);
+size_t soft_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms,
+                                int64_t batch = 1);
 int launch_exact_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, const double* coefs, double coef_scale,
                          double* face_grad, void* ws, size_t ws_bytes, int num_sms,
