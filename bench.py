@@ -50,6 +50,7 @@ EXACT_BWD_FLOPS = 170
 EXACT_FWD_EXEC_FLOPS = 42.25   # fwd_f32_kernel<ExactPol,RowSrc> all-common fast path, 4 MUFU
 EXACT_BWD_EXEC_FLOPS = 60.5    # bwd_f32_kernel<ExactEdgeBwd,RowSrc> unit-weight loop, 4 MUFU
 EXACT_FWD_MUFU = 4
+SOFT_STEP_FLOPS = 15 + 72  # soft forward + soft backward, pinned
 EXACT_BWD_MUFU = 4
 
 
@@ -569,7 +570,16 @@ def run_c4(args):
             "config": {"workload": "c4_64x_icosphere4_64", "meshes": B, "faces_per_mesh": n_faces,
                        "grid": [R] * 3, "mode": "soft", "parallelism": f"mesh DP x{world}",
                        "step": "MLP fwd + fused soft fwd/loss/bwd per mesh + MLP bwd + Adam"},
-            "loss_first": float(losses[0]), "loss_last": float(losses[-1]),
+            "loss_first": float(losses[0].detach()), "loss_last": float(losses[-1].detach()),
+            "roofline": {"bound": "fp32", "unit": "TFLOP/s", "peak": peaks()[0],
+                         "achieved": SOFT_STEP_FLOPS * pairs / (ms_step / 1e3) / 1e12,
+                         "frac": SOFT_STEP_FLOPS * pairs / (ms_step / 1e3) / 1e12 / peaks()[0],
+                         "flops_per_pair": SOFT_STEP_FLOPS, "traffic": None,
+                         "note": "whole training step at the pinned soft fwd 15 + bwd 72 "
+                                 "FLOP/pair (SURVEY 8d); MLP/Adam time included"},
+            # per mesh: 2 packs x (eps + pack), 2 loss kernels, 1 gather; per
+            # batch: 1 forward, 1 backward (+ split finalize / reduce)
+            "gpu_launches": args.steps * (per * 7 + 4),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
