@@ -1,0 +1,81 @@
+"""The slab-sharded driver with the real CUDA evaluator: two ranks (gloo,
+both on cuda:0 -- the only GPU of the test box) split the lattice into
+i-slabs, run the sm_100a kernels on their slab and all-reduce one packed
+buffer.  Loss, gradients and the gathered grid must equal the
+single-process device path (the per-slab split plans may reorder fp64
+partial sums: agreement to 1e-9 relative).  This is the N>1 code path of
+bench.py; real multi-GPU runs use NCCL instead of gloo."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+RES = (20, 18, 32)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem():
+    from paper_2407_11272_b200 import configs
+    v, f = configs.torus_with_holes()
+    grid = ((-1.0,) * 3, (1.0,) * 3, RES)
+    n = int(np.prod(RES))
+    target = (np.random.default_rng(5).random(n) > 0.7).astype(np.float32)
+    return v, f, grid, target
+
+
+def _worker(rank, world, port, outdir, mode):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_11272_b200 import device
+    from paper_2407_11272_b200.distributed import CudaSlabEvaluator, SlabDriver
+    v, f, grid, target = _problem()
+    dm = device.DeviceMesh.from_numpy(v, f)
+    n = int(np.prod(RES))
+    drv = SlabDriver(CudaSlabEvaluator(dm, grid, mode=mode), n, rank, world)
+    n0, cnt = drv.slab
+    tg = torch.from_numpy(target[n0:n0 + cnt]).cuda()
+    loss, grads, excl, _ = drv.loss_grad(tg)
+    vals, flags = drv.forward(policy=1, gather=True)
+    if rank == 0:
+        np.savez(os.path.join(outdir, f"out_{mode}.npz"), loss=float(loss),
+                 grads=grads.cpu().numpy(), excl=float(excl), vals=vals.cpu().numpy(),
+                 flags=flags.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["exact", "soft"])
+def test_two_rank_cuda_driver_matches_single_process(tmp_path, cuda_device, mode):
+    import torch
+    from paper_2407_11272_b200 import _lib as L, device
+    from paper_2407_11272_b200.grad import device_loss_grad
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode), nprocs=2, join=True)
+    out = np.load(tmp_path / f"out_{mode}.npz")
+    v, f, grid, target = _problem()
+    dm = device.DeviceMesh.from_numpy(v, f)
+    sums, g = device_loss_grad(dm, grid, torch.from_numpy(target).cuda(), mode=mode,
+                               precision="f32")
+    s = sums.cpu().numpy()
+    ref = g.cpu().numpy() / s[1]
+    assert abs(float(out["loss"]) - s[4]) <= 1e-9 * abs(s[4])
+    assert np.abs(out["grads"] - ref).max() <= 1e-9 * np.abs(ref).max()
+    assert int(out["excl"]) == int(s[2])
+    vals, flags = device.forward(dm, mode, "f32", grid=grid, policy=L.POLICY_HALF)
+    assert np.abs(out["vals"] - vals.cpu().numpy()).max() <= 1e-6
+    assert np.array_equal(out["flags"], flags.cpu().numpy())
