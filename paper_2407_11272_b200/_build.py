@@ -11,7 +11,6 @@ expressions are the same IEEE sequence as the numpy/numba reference.
 
 from __future__ import annotations
 
-import os
 import shutil
 import subprocess
 import sys
