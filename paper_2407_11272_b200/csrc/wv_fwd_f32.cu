@@ -76,10 +76,18 @@ struct ExactPol {
   static constexpr int kMinBlocksRow = 4;  // 5 (96 regs) spills and measured 2% slower
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (2.0 * kPi);
-  struct Ctx {};
-  __device__ static Ctx make_ctx(float) { return Ctx{}; }
+  // eps2: squared vertex-hit radius, eps (f32) inflated by 1% so that every
+  // pair within the reference's f64 eps of a vertex (winding.py:65-67) leaves
+  // the common path and is decided exactly by exact_rare
+  struct Ctx {
+    float eps2;
+  };
+  __device__ static Ctx make_ctx(float eps) {
+    const float e = eps * 1.01f;
+    return Ctx{e * e};
+  }
   __device__ __forceinline__ static uint32_t common2(const Rec& R, F2 qx, F2 qy, F2 qz,
-                                                     const Ctx&, F2& tacc) {
+                                                     const Ctx& ctx, F2& tacc) {
     const F2 ax = sub2(f2s(R.v0e.x), qx), ay = sub2(f2s(R.v0e.y), qy), az = sub2(f2s(R.v0e.z), qz);
     const F2 bx = sub2(f2s(R.v1.x), qx), by = sub2(f2s(R.v1.y), qy), bz = sub2(f2s(R.v1.z), qz);
     const F2 cx = sub2(f2s(R.v2.x), qx), cy = sub2(f2s(R.v2.y), qy), cz = sub2(f2s(R.v2.z), qz);
@@ -88,7 +96,7 @@ struct ExactPol {
     const F2 la2 = dot2(ax, ay, az, ax, ay, az);
     const F2 lb2 = dot2(bx, by, bz, bx, by, bz);
     const F2 lc2 = dot2(cx, cy, cz, cx, cy, cz);
-    return tail2(R, alpha, la2, lb2, lc2, tacc);
+    return tail2(R, alpha, la2, lb2, lc2, ctx, tacc);
   }
   // Lattice-row form: the P points of a thread share x and y, so the x/y
   // parts of alpha and of the squared corner distances are per-face scalars
@@ -108,16 +116,16 @@ struct ExactPol {
     return w;
   }
   __device__ __forceinline__ static uint32_t common_row2(const Rec& R, const Row& w, F2 qz,
-                                                         const Ctx&, F2& tacc) {
+                                                         const Ctx& ctx, F2& tacc) {
     const F2 az = sub2(f2s(R.v0e.z), qz), bz = sub2(f2s(R.v1.z), qz), cz = sub2(f2s(R.v2.z), qz);
     const F2 alpha = fma2(f2s(R.n.z), az, f2s(w.alpha));
     const F2 la2 = fma2(az, az, f2s(w.a2));
     const F2 lb2 = fma2(bz, bz, f2s(w.b2));
     const F2 lc2 = fma2(cz, cz, f2s(w.c2));
-    return tail2(R, alpha, la2, lb2, lc2, tacc);
+    return tail2(R, alpha, la2, lb2, lc2, ctx, tacc);
   }
   __device__ __forceinline__ static uint32_t tail2(const Rec& R, F2 alpha, F2 la2, F2 lb2, F2 lc2,
-                                                   F2& tacc) {
+                                                   const Ctx& ctx, F2& tacc) {
     const F2 la = sqrt2(la2), lb = sqrt2(lb2), lc = sqrt2(lc2);
     // a.b = (|a|^2 + |b|^2 - |v0-v1|^2)/2 etc. (half squared edge lengths are
     // packed): 2 ops instead of 3.  It can cancel only where beta itself is
@@ -148,7 +156,15 @@ struct ExactPol {
     const float b8h = __int_as_float(__float_as_int(bh) - (3 << 23));
     const float p2l = __int_as_float(__float_as_int(pl) - (1 << 23));  // |a||b||c| / 2
     const float p2h = __int_as_float(__float_as_int(ph) - (1 << 23));
-    const bool cl = fabsf(al) < b8l && bl > p2l, ch = fabsf(ah) < b8h && bh > p2h;
+    // vertex-hit candidates (some corner within eps: |a||b||c| can be 0 and
+    // beta a rounding residue of either sign) are never common
+    float a2l, a2h, b2l, b2h, c2l, c2h;
+    split(la2, a2l, a2h);
+    split(lb2, b2l, b2h);
+    split(lc2, c2l, c2h);
+    const bool vl = fminf(a2l, fminf(b2l, c2l)) >= ctx.eps2;
+    const bool vh = fminf(a2h, fminf(b2h, c2h)) >= ctx.eps2;
+    const bool cl = fabsf(al) < b8l && bl > p2l && vl, ch = fabsf(ah) < b8h && bh > p2h && vh;
     const F2 tt = mul2(alpha, rcp2(beta));
     const F2 s = mul2(tt, tt);
     const F2 p = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
@@ -165,10 +181,12 @@ struct ExactPol {
   // every point of the thread is a common pair (nearly always) the terms are
   // added without per-lane selects or rare-mask building, which had cost
   // ~1/3 of the issue slots.  Otherwise the per-lane path (tail2) runs.
+  // near: some point of the group may be within eps of a vertex (then every
+  // lane takes tail2, which routes the candidates to exact_rare)
   template <int PP>
   __device__ __forceinline__ static uint32_t finish(const Rec& R, const F2* alpha, const F2* la2,
                                                     const F2* lb2, const F2* lc2, const Ctx& ctx,
-                                                    F2* tacc) {
+                                                    bool near, F2* tacc) {
     F2 tq[PP], tp[PP];
     float m = -1.0f;
 #pragma unroll
@@ -195,7 +213,7 @@ struct ExactPol {
       tp[pp] = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
                     f2s(1.0f));
     }
-    if (m < 0.0f) {  // tail2's exact operation for a common pair: tacc + t p, one rounding
+    if (m < 0.0f && !near) {  // tail2's operation for a common pair: tacc + t p, one rounding
 #pragma unroll
       for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
       return 0u;
@@ -203,7 +221,7 @@ struct ExactPol {
     uint32_t rare = 0;
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp)
-      rare |= tail2(R, alpha[pp], la2[pp], lb2[pp], lc2[pp], tacc[pp]) << (2 * pp);
+      rare |= tail2(R, alpha[pp], la2[pp], lb2[pp], lc2[pp], ctx, tacc[pp]) << (2 * pp);
     return rare;
   }
   template <int PP>
@@ -219,7 +237,9 @@ struct ExactPol {
       lb2[pp] = fma2(bz, bz, f2s(w.b2));
       lc2[pp] = fma2(cz, cz, f2s(w.c2));
     }
-    return finish<PP>(R, alpha, la2, lb2, lc2, ctx, tacc);
+    // the row's x/y part bounds every |corner - q|^2 of the row from below
+    const bool near = fminf(w.a2, fminf(w.b2, w.c2)) < ctx.eps2;
+    return finish<PP>(R, alpha, la2, lb2, lc2, ctx, near, tacc);
   }
   template <int PP>
   __device__ __forceinline__ static uint32_t face(const Rec& R, const F2* qx, const F2* qy,
@@ -238,7 +258,16 @@ struct ExactPol {
       lb2[pp] = dot2(bx, by, bz, bx, by, bz);
       lc2[pp] = dot2(cx, cy, cz, cx, cy, cz);
     }
-    return finish<PP>(R, alpha, la2, lb2, lc2, ctx, tacc);
+    float mn = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      float a0, a1, b0, b1, c0, c1;
+      split(la2[pp], a0, a1);
+      split(lb2[pp], b0, b1);
+      split(lc2[pp], c0, c1);
+      mn = fminf(mn, fminf(fminf(a0, a1), fminf(fminf(b0, b1), fminf(c0, c1))));
+    }
+    return finish<PP>(R, alpha, la2, lb2, lc2, ctx, mn < ctx.eps2, tacc);
   }
   __device__ __forceinline__ static double rare(const Rec& R, float qx, float qy, float qz,
                                                 double eps) {

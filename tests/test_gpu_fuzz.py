@@ -1,0 +1,102 @@
+"""Seeded random parity sweep: random meshes (generic, with degenerate and
+duplicated faces, at several coordinate scales) against query points that
+include random points, mesh vertices, edge points and face centroids -- the
+on-surface cases of _kernels.py:65-88.
+
+* f64 exact / soft vs the oracle (the reference's own arithmetic): values to
+  1e-12 (exact) / bitwise (soft), flags identical;
+* f32 exact: within 1e-5 of the f64 oracle (on the f32-rounded points,
+  winding.py:363) at every point farther than 1e-4 x scale from the surface
+  -- closer than that, f32 vertex rounding moves the surface across the
+  point and W is legitimately discontinuous -- and every mesh vertex used as
+  a query point is flagged (an exact hit in f32 coordinates).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def surface_distance(pts, tri):
+    """Unsigned distance from each point to the union of triangles (numpy,
+    closest point by region tests)."""
+    d = np.full(len(pts), np.inf)
+    for a, b, c in tri:
+        ab, ac = b - a, c - a
+        n = np.cross(ab, ac)
+        nn = float(n @ n)
+        for q0 in range(0, len(pts), 256):
+            q = pts[q0:q0 + 256]
+            best = np.minimum(np.minimum(np.linalg.norm(q - a, axis=1),
+                                         np.linalg.norm(q - b, axis=1)),
+                              np.linalg.norm(q - c, axis=1))
+            for p0, p1 in ((a, b), (b, c), (c, a)):
+                e = p1 - p0
+                ee = float(e @ e)
+                if ee > 0:
+                    t = np.clip(((q - p0) @ e) / ee, 0.0, 1.0)
+                    best = np.minimum(best, np.linalg.norm(q - (p0 + t[:, None] * e), axis=1))
+            if nn > 0:
+                w = q - a
+                dist = (w @ n) / np.sqrt(nn)
+                proj = q - dist[:, None] * n / np.sqrt(nn)
+                # barycentric inside test of the projection
+                v2 = proj - a
+                d00, d01, d11 = ab @ ab, ab @ ac, ac @ ac
+                d20, d21 = v2 @ ab, v2 @ ac
+                den = d00 * d11 - d01 * d01
+                bv = (d11 * d20 - d01 * d21) / den
+                bw = (d00 * d21 - d01 * d20) / den
+                inside = (bv >= 0) & (bw >= 0) & (bv + bw <= 1)
+                best = np.where(inside, np.minimum(best, np.abs(dist)), best)
+            d[q0:q0 + 256] = np.minimum(d[q0:q0 + 256], best)
+    return d
+
+
+def random_case(seed):
+    rng = np.random.default_rng(seed)
+    scale = 10.0 ** rng.integers(-2, 3)
+    nv = int(rng.integers(4, 40))
+    v = rng.uniform(-1, 1, size=(nv, 3)) * scale
+    nf = int(rng.integers(1, 60))
+    f = rng.integers(0, nv, size=(nf, 3))
+    f[0] = [0, 1, 1] if nf > 2 else f[0]          # a degenerate face
+    if nf > 3:
+        f[1] = f[2]                                # a duplicated face
+    pts = [rng.uniform(-1.2, 1.2, size=(60, 3)) * scale, v[:5]]
+    t = v[f]
+    pts.append(t.mean(axis=1)[:10])                # centroids (soft on-centroid, exact on-face)
+    pts.append((0.3 * t[:, 0] + 0.7 * t[:, 1])[:10])  # edge points
+    return v, f, np.concatenate(pts)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_meshes_parity(cuda_device, seed):
+    import paper_2407_11272_b200 as wv
+    v, f, pts = random_case(seed)
+    mesh = wv.TriangleMesh(v, f)
+    for mode in ("exact", "soft"):
+        got, gf = wv.winding_number_batch(mesh, pts, mode=mode, precision="f64")
+        ref, rf = orc.winding_number_batch(v, f, pts, mode=mode, threads=1)
+        assert np.array_equal(gf, rf), (mode, seed)
+        if mode == "soft":
+            assert got.tobytes() == ref.tobytes(), seed
+        else:
+            assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), seed
+    p32 = pts.astype(np.float32).astype(np.float64)
+    got, gf = wv.winding_number_batch(mesh, pts, mode="exact", precision="f32")
+    ref, rf = orc.winding_number_batch(v, f, p32, mode="exact", threads=1)
+    scale = np.abs(v).max()
+    far = surface_distance(p32, v[f]) > 1e-4 * scale
+    assert far.sum() >= 40
+    assert not gf[far].any() and not rf[far].any()
+    assert np.abs(got[far] - ref[far]).max() <= 1e-5, seed
+    # query points 60..64 are vertices 0..4: flagged when on a live face
+    # (degenerate faces are dropped, winding.py:262-264)
+    t = v[f]
+    live = np.linalg.norm(np.cross(t[:, 1] - t[:, 0], t[:, 2] - t[:, 0]), axis=1) > 0
+    used = np.isin(np.arange(5), f[live])
+    assert gf[60:60 + int(min(5, len(v)))][used[:min(5, len(v))]].all(), seed
