@@ -47,6 +47,42 @@ constexpr int kAxisMax = 1024;    // lattice axes up to this length use node tab
 // the NET weight of its edges (0 for cancelled ones) and faces whose three
 // weights vanish are not packed at all.  The sign and 1/(4 pi) are folded
 // into coef_scale by the launcher.
+// One ill-conditioned (face, point) pair of the exact backward in FP64,
+// straight into the face's fp64 accumulators.  Used where the point lies
+// close to an edge's segment ((|a|+|b|)^2 - |e|^2 < |e|^2 / 10): there the
+// fp32 denominator cancels (relative error ~1e-7 |e|^2 / d).  Here
+// |a||b| + a.b = |a x b|^2 / (|a||b| - a.b) has no cancellation, and the
+// contributions bypass the fp32 run sums.  c already carries coef_scale and
+// kCoefScale; corner k's three components are acc[3k .. 3k+2].
+__device__ __noinline__ void exact_pair_f64(const ExactGradRecF32& R, double qx, double qy,
+                                            double qz, double c, double (*acc)[kBwdThreads]) {
+  if (c == 0.0) return;
+  const double P[3][3] = {{(double)R.a.x - qx, (double)R.a.y - qy, (double)R.a.z - qz},
+                          {(double)R.b.x - qx, (double)R.b.y - qy, (double)R.b.z - qz},
+                          {(double)R.c.x - qx, (double)R.c.y - qy, (double)R.c.z - qz}};
+  const double w[3] = {R.a.w, R.b.w, R.c.w};
+  double len[3];
+  for (int k = 0; k < 3; ++k) len[k] = sqrt(P[k][0] * P[k][0] + P[k][1] * P[k][1] + P[k][2] * P[k][2]);
+  const int t = threadIdx.x;
+  for (int e = 0; e < 3; ++e) {
+    if (w[e] == 0.0) continue;
+    const int i = e, j = (e + 1) % 3;
+    const double* A = P[i];
+    const double* B = P[j];
+    const double m[3] = {A[1] * B[2] - A[2] * B[1], A[2] * B[0] - A[0] * B[2],
+                         A[0] * B[1] - A[1] * B[0]};
+    const double L = len[i] * len[j], ab = A[0] * B[0] + A[1] * B[1] + A[2] * B[2];
+    const double mm = m[0] * m[0] + m[1] * m[1] + m[2] * m[2];
+    const double den = (L - ab) > 0.0 ? mm / (L - ab) : L + ab;  // |a||b| + a.b
+    if (!(den > 0.0) || !(len[i] > 0.0) || !(len[j] > 0.0)) continue;  // on the edge: flagged
+    const double f = c * w[e] / (2.0 * den);  // c / d with d = 2 (|a||b| + a.b)
+    for (int x = 0; x < 3; ++x) {
+      acc[3 * i + x][t] += m[x] * (f / len[i]);
+      acc[3 * j + x][t] += m[x] * (f / len[j]);
+    }
+  }
+}
+
 struct ExactEdgeBwd {
   using Rec = ExactGradRecF32;
   static constexpr int kFaces = 1;  // faces per thread (per record)
@@ -69,9 +105,13 @@ struct ExactEdgeBwd {
   // ((|a|+|b|)^2 - |P-Q|^2) / 2  (a.b = (|a|^2+|b|^2-|a-b|^2)/2, a-b = P-Q):
   // no dot products, one FADD + one FFMA per edge, and the FFMA rounds
   // (|a|+|b|)^2 - U once.
+  // a pair is ill-conditioned when some edge has d_e < |e|^2 / kIllRatio
+  // (tested on the product of the three ratios |e|^2 / d_e; non-finite
+  // counts as ill): its lanes take exact_pair_f64 instead
+  static constexpr float kIllRatio = 10.0f;
   template <bool kUnit>
-  __device__ __forceinline__ static void pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
-                                               float, F2* g) {
+  __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                                   float, F2* g) {
     const F2 ax = sub2(f2s(R.a.x), qx), ay = sub2(f2s(R.a.y), qy), az = sub2(f2s(R.a.z), qz);
     const F2 bx = sub2(f2s(R.b.x), qx), by = sub2(f2s(R.b.y), qy), bz = sub2(f2s(R.b.z), qz);
     const F2 cx = sub2(f2s(R.c.x), qx), cy = sub2(f2s(R.c.y), qy), cz = sub2(f2s(R.c.z), qz);
@@ -84,9 +124,15 @@ struct ExactEdgeBwd {
     const F2 r01 = rcp2(fma2(s01, s01, f2s(-R.u.x)));
     const F2 r12 = rcp2(fma2(s12, s12, f2s(-R.u.y)));
     const F2 r20 = rcp2(fma2(s20, s20, f2s(-R.u.z)));
-    const F2 t01 = mul2(kUnit ? coef : mul2(coef, f2s(R.a.w)), r01);
-    const F2 t12 = mul2(kUnit ? coef : mul2(coef, f2s(R.b.w)), r12);
-    const F2 t20 = mul2(kUnit ? coef : mul2(coef, f2s(R.c.w)), r20);
+    float q0, q1;
+    split(mul2(mul2(r01, r12), mul2(r20, f2s(R.u.x * R.u.y * R.u.z))), q0, q1);
+    const bool ill0 = !(q0 < kIllRatio), ill1 = !(q1 < kIllRatio);
+    const F2 z2 = f2s(0.0f);
+    const F2 t01 = (ill0 || ill1) ? z2 : mul2(kUnit ? coef : mul2(coef, f2s(R.a.w)), r01);
+    const F2 t12 = (ill0 || ill1) ? z2 : mul2(kUnit ? coef : mul2(coef, f2s(R.b.w)), r12);
+    const F2 t20 = (ill0 || ill1) ? z2 : mul2(kUnit ? coef : mul2(coef, f2s(R.c.w)), r20);
+    // (a rare ill lane zeroes both lanes' fp32 terms; the caller redoes the
+    // other lane in fp64 too, so no inf * 0 can reach the sums)
     // m01 = a x b, m12 = b x c, m20 = c x a
     const F2 m01x = sub2(mul2(ay, bz), mul2(az, by)), m01y = sub2(mul2(az, bx), mul2(ax, bz)),
              m01z = sub2(mul2(ax, by), mul2(ay, bx));
@@ -106,6 +152,7 @@ struct ExactEdgeBwd {
     g[6] = fma2(m20x, s20c, fma2(m12x, s12c, g[6]));
     g[7] = fma2(m20y, s20c, fma2(m12y, s12c, g[7]));
     g[8] = fma2(m20z, s20c, fma2(m12z, s12c, g[8]));
+    return (ill0 || ill1) ? 3u : 0u;
   }
   // Lattice-row form (points of one k-row share x and y).
   //  * The edge moment is m = a x b = a x e with the edge vector e = Q - P
@@ -127,6 +174,7 @@ struct ExactEdgeBwd {
     float k01x, k01y, m01z;        // m01 = a x e01: x = k01x - e01y a_z, y = k01y + e01x a_z
     float k12x, k12y, m12z;        // m12 = b x e12 (b_z)
     float k20x, k20y, m20z;        // m20 = c x e20 (c_z)
+    float qx, qy;                  // the row (for exact_pair_f64)
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
     const float ax = R.a.x - qx, ay = R.a.y - qy;
@@ -148,11 +196,18 @@ struct ExactEdgeBwd {
     w.k20x = cy * e20z;
     w.k20y = -(cx * e20z);
     w.m20z = fmaf(cx, e20y, -(cy * e20x));
+    w.qx = qx;
+    w.qy = qy;
     return w;
   }
-  template <bool kUnit>
-  __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
-                                                   float, F2* z) {
+  // kMask = false (hot path): no masking; the |e|^2/d-products are summed
+  //   into *mr; a run whose sum reaches kIllRatio (an ill pair, or several
+  //   moderately close ones) is discarded and redone with kMask = true.
+  // kMask = true: ill lanes contribute nothing here (bits returned; the
+  //   caller adds them with exact_pair_f64).
+  template <bool kUnit, bool kMask = true>
+  __device__ __forceinline__ static uint32_t pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
+                                                       float, F2* z, F2* mr = nullptr) {
     const F2 az = sub2(f2s(R.a.z), qz), bz = sub2(f2s(R.b.z), qz), cz = sub2(f2s(R.c.z), qz);
     const F2 a2 = fma2(az, az, f2s(w.a2));
     const F2 b2 = fma2(bz, bz, f2s(w.b2));
@@ -164,13 +219,27 @@ struct ExactEdgeBwd {
     const F2 d12 = fma2(s12, s12, f2s(-R.u.y));
     const F2 d20 = fma2(s20, s20, f2s(-R.u.z));
     const F2 p12 = mul2(d12, d20);
-    F2 rr = rcp2(mul2(d01, p12));
-    {
-      float lo, hi;
-      split(rr, lo, hi);
-      rr = f2(fminf(lo, 3.0e38f), fminf(hi, 3.0e38f));
+    const F2 rr = rcp2(mul2(d01, p12));
+    // ill-conditioned lanes (some d_e < |e|^2 / kIllRatio, or a non-finite
+    // reciprocal) leave the fp32 sums: cr = 0 here, exact_pair_f64 later
+    const F2 ru = mul2(rr, f2s(R.u.x * R.u.y * R.u.z));
+    bool ill0 = false, ill1 = false;
+    F2 cr;  // coef / (d01 d12 d20)
+    if constexpr (kMask) {
+      float ru0, ru1;
+      split(ru, ru0, ru1);
+      ill0 = !(ru0 < kIllRatio);
+      ill1 = !(ru1 < kIllRatio);
+      float r0, r1;
+      split(mul2(coef, rr), r0, r1);
+      cr = f2(ill0 ? 0.0f : r0, ill1 ? 0.0f : r1);
+    } else {
+      // the pair's ratios go out; step_row sums them (>= 0; inf / NaN
+      // propagate), so any single ill pair pushes the run's sum past
+      // kIllRatio
+      *mr = ru;
+      cr = mul2(coef, rr);
     }
-    const F2 cr = mul2(coef, rr);  // coef / (d01 d12 d20)
     const F2 q0 = mul2(cr, d01);
     const F2 t01 = mul2(kUnit ? cr : mul2(cr, f2s(R.a.w)), p12);
     const F2 t12 = mul2(kUnit ? q0 : mul2(q0, f2s(R.b.w)), d20);
@@ -190,13 +259,40 @@ struct ExactEdgeBwd {
     z[9] = fma2(u12, ic, z[9]);
     z[10] = fma2(t20, ic, z[10]);
     z[11] = fma2(u20, ic, z[11]);
+    return (ill0 ? 1u : 0u) | (ill1 ? 2u : 0u);
   }
   template <bool kUnit, int N>
   __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
-                                                  float eps2, F2* z) {
+                                                  float eps2, F2* z, F2* mr) {
+    F2 ru[N];
 #pragma unroll
     for (int u = 0; u < N; ++u)
-      pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
+      pair_row2<kUnit, false>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z, &ru[u]);
+    // pairwise sum (short dependency chain), then one add into the run's sum
+#pragma unroll
+    for (int h = 1; h < N; h *= 2)
+#pragma unroll
+      for (int u = 0; u + h < N; u += 2 * h) ru[u] = add2(ru[u], ru[u + h]);
+    *mr = add2(*mr, ru[0]);
+  }
+  __device__ __forceinline__ static void rare_pair(const Rec& R, float qx, float qy, float qz,
+                                                   float c, double (*acc)[kBwdThreads]) {
+    exact_pair_f64(R, qx, qy, qz, c, acc);
+  }
+  // a run [j, e) holding an ill-conditioned pair, redone: fp32 sums without
+  // the ill lanes, the ill lanes in fp64 (out of line: rare)
+  template <bool kUnit>
+  __device__ __noinline__ static void redo_run(const Rec& R, const Row& w, const float4* zcs,
+                                               int j, int e, float eps2, F2* z,
+                                               double (*acc)[kBwdThreads]) {
+    for (int i = 0; i < kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
+    for (; j < e; ++j) {
+      const float4 zc = zcs[j];
+      if (zc.z == 0.0f && zc.w == 0.0f) continue;
+      const uint32_t ill = pair_row2<kUnit, true>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, z);
+      if (ill & 1u) exact_pair_f64(R, w.qx, w.qy, zc.x, zc.z, acc);
+      if (ill & 2u) exact_pair_f64(R, w.qx, w.qy, zc.y, zc.w, acc);
+    }
   }
   // sum_q m s for every (edge, corner) from the run's sums, into the face's
   // fp64 accumulators (acc[j][thread], j = corner * 3 + axis)
@@ -242,8 +338,8 @@ struct SoftBwd {
   static constexpr int kAcc = 10;  // acc1(3) acc2(3) T(1) D(3)
   __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
   template <bool kUnit>
-  __device__ __forceinline__ static void pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
-                                               float eps2, F2* g) {
+  __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                                   float eps2, F2* g) {
     const F2 dx = sub2(f2s(R.c.x), qx), dy = sub2(f2s(R.c.y), qy), dz = sub2(f2s(R.c.z), qz);
     const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
     const F2 rs = rsqrt2(r2);
@@ -272,6 +368,7 @@ struct SoftBwd {
     g[7] = fma2(c5, dx, g[7]);
     g[8] = fma2(c5, dy, g[8]);
     g[9] = fma2(c5, dz, g[9]);
+    return 0u;
   }
   // Lattice-row form: d = c - q has row-constant x/y parts, so r^2 and S take
   // one op each per pair, and since G1 = w x d and G2 = d x u are affine in
@@ -311,9 +408,14 @@ struct SoftBwd {
   }
   // N point pairs; the r < eps test is done once on the minimum r^2 of the
   // step (nearly always passes), so the common path has no per-lane selects
+  __device__ __forceinline__ static void rare_pair(const Rec&, float, float, float, float,
+                                                   double (*)[kBwdThreads]) {}
+  template <bool kUnit, class W>
+  __device__ __forceinline__ static void redo_run(const Rec&, const W&, const float4*, int, int,
+                                                  float, F2*, double (*)[kBwdThreads]) {}
   template <bool kUnit, int N>
   __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
-                                                  float eps2, F2* z) {
+                                                  float eps2, F2* z, F2*) {
     F2 dz[N], r2[N];
     float m = __int_as_float(0x7f800000);
 #pragma unroll
@@ -404,11 +506,17 @@ struct SoftBwdPair {
   static constexpr int kRowAcc = 2 * One::kRowAcc;
   __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
   template <bool kUnit>
-  __device__ __forceinline__ static void pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
-                                               float eps2, F2* g) {
+  __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                                   float eps2, F2* g) {
     One::pair2<kUnit>(R.f[0], qx, qy, qz, coef, eps2, g);
     One::pair2<kUnit>(R.f[1], qx, qy, qz, coef, eps2, g + One::kAcc);
+    return 0u;
   }
+  __device__ __forceinline__ static void rare_pair(const Rec&, float, float, float, float,
+                                                   double (*)[kBwdThreads]) {}
+  template <bool kUnit, class W>
+  __device__ __forceinline__ static void redo_run(const Rec&, const W&, const float4*, int, int,
+                                                  float, F2*, double (*)[kBwdThreads]) {}
   struct Row {
     One::Row r[2];
   };
@@ -427,7 +535,7 @@ struct SoftBwdPair {
   // both faces' r^2 first, one on-centroid test for the whole step
   template <bool kUnit, int N>
   __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
-                                                  float eps2, F2* z) {
+                                                  float eps2, F2* z, F2*) {
     F2 dz[2][N], r2[2][N];
     float m = __int_as_float(0x7f800000);
 #pragma unroll
@@ -485,17 +593,25 @@ struct PointChunk {
 
 template <class Pol, bool kUnit>
 __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const PointChunk& ch,
-                                           int n_pairs, float eps2, F2* g) {
+                                           int n_pairs, float eps2, F2* g,
+                                           double (*acc)[kBwdThreads]) {
 #pragma unroll 2
   for (int j = 0; j < n_pairs; ++j) {
     const float4 zc = ch.zc[j];
     if (zc.z == 0.0f && zc.w == 0.0f) continue;  // warp-uniform (_kernels.py:182-184)
     const float4 xy = ch.xy[j];
-    Pol::template pair2<kUnit>(R, f2(xy.x, xy.y), f2(xy.z, xy.w), f2(zc.x, zc.y),
-                               f2(zc.z, zc.w), eps2, g);
+    const uint32_t ill = Pol::template pair2<kUnit>(R, f2(xy.x, xy.y), f2(xy.z, xy.w),
+                                                    f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, g);
+    if (ill != 0u) {  // both lanes redone in fp64 (see ExactEdgeBwd::pair2)
+      Pol::rare_pair(R, xy.x, xy.z, zc.x, zc.z, acc);
+      Pol::rare_pair(R, xy.y, xy.w, zc.y, zc.w, acc);
+    }
   }
 }
 
+// Row mode: the chunk is cut at k-row boundaries (warp-uniform), each run of
+// pairs shares the row's x/y, and the per-face row constants are computed
+// once per run.  Needs rz and the range start even (pairs never straddle).
 // Row mode: the chunk is cut at k-row boundaries (warp-uniform), each run of
 // pairs shares the row's x/y, and the per-face row constants are computed
 // once per run.  Needs rz and the range start even (pairs never straddle).
@@ -513,11 +629,12 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
     F2 z[Pol::kRowAcc];
 #pragma unroll
     for (int i = 0; i < Pol::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
-    const int e = j + run;
-    // two point pairs per step under one (warp-uniform) zero-coefficient
-    // test, so their dependency chains share a basic block and interleave
-    // (a zero-coefficient pair next to a live one adds 0 * finite: its point
-    // is parked far away)
+    const int e = j + run, j0 = j;
+    F2 mr = f2(0.0f, 0.0f);  // summed ill-conditioning ratios of the run (exact only)
+    // kRowStep point pairs per step under one (warp-uniform)
+    // zero-coefficient test, so their dependency chains share a basic block
+    // and interleave (a zero-coefficient pair next to a live one adds
+    // 0 * finite: its point is parked far away)
 #pragma unroll 1
     for (; j + kRowStep <= e; j += kRowStep) {
       float4 zc[kRowStep];
@@ -528,14 +645,18 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
         any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
       }
       if (!any) continue;
-      Pol::template step_row<kUnit, kRowStep>(R, w, zc, eps2, z);
+      Pol::template step_row<kUnit, kRowStep>(R, w, zc, eps2, z, &mr);
     }
 #pragma unroll 1
     for (; j < e; ++j) {
       const float4 zc = ch.zc[j];
       if (!(zc.z == 0.0f && zc.w == 0.0f))  // warp-uniform (_kernels.py:182-184)
-        Pol::template pair_row2<kUnit>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, z);
+        Pol::template step_row<kUnit, 1>(R, w, &zc, eps2, z, &mr);
     }
+    float m0, m1;
+    split(mr, m0, m1);
+    if (!(m0 + m1 < ExactEdgeBwd::kIllRatio))  // rare: an ill-conditioned pair in the run
+      Pol::template redo_run<kUnit>(R, w, ch.zc, j0, e, eps2, z, acc);
     Pol::flush_row(R, w, z, acc);
     k = 0;
   }
@@ -646,9 +767,9 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
       for (int j = 0; j < Pol::kAcc; ++j) g[j] = f2(0.0f, 0.0f);
       if (unit) {
-        chunk_loop<Pol, true>(R, chunk, n_pairs, eps2, g);
+        chunk_loop<Pol, true>(R, chunk, n_pairs, eps2, g, acc);
       } else {
-        chunk_loop<Pol, false>(R, chunk, n_pairs, eps2, g);
+        chunk_loop<Pol, false>(R, chunk, n_pairs, eps2, g, acc);
       }
 #pragma unroll
       for (int j = 0; j < Pol::kAcc; ++j) {

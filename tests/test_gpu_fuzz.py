@@ -100,3 +100,31 @@ def test_random_meshes_parity(cuda_device, seed):
     live = np.linalg.norm(np.cross(t[:, 1] - t[:, 0], t[:, 2] - t[:, 0]), axis=1) > 0
     used = np.isin(np.arange(5), f[live])
     assert gf[60:60 + int(min(5, len(v)))][used[:min(5, len(v))]].all(), seed
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_meshes_gradient_parity(cuda_device, seed):
+    """Exact and soft f32 backward (generic point path) on the random cases
+    vs the f64 oracle, coefficients zeroed at points closer than 1e-4 x scale
+    to the surface (flagged or ill-conditioned), 1e-4 relative to the largest
+    component (the reference's gradient convention)."""
+    import torch
+    from paper_2407_11272_b200 import device
+    v, f, pts = random_case(seed)
+    p32 = pts.astype(np.float32).astype(np.float64)
+    scale = np.abs(v).max()
+    c = np.random.default_rng(100 + seed).normal(size=len(pts))
+    c[surface_distance(p32, v[f]) <= 1e-4 * scale] = 0.0
+    c32 = c.astype(np.float32).astype(np.float64)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    for mode, ofn in (("exact", orc.exact_grad), ("soft", orc.soft_grad)):
+        if mode == "soft":
+            cen = v[f].mean(axis=1)
+            d = np.linalg.norm(p32[:, None, :] - cen[None], axis=2).min(axis=1)
+            c32 = np.where(d <= 1e-4 * scale, 0.0, c32)
+        fg = device.face_grad(dm, mode, "f32", torch.from_numpy(c32).float().cuda(),
+                              points=torch.from_numpy(p32).float().cuda())
+        got = device.vertex_grad(dm, fg).cpu().numpy()
+        ref = ofn(v, f, p32, c32, threads=1)
+        assert np.isfinite(got).all(), (mode, seed)
+        assert np.abs(got - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-300), (mode, seed)
