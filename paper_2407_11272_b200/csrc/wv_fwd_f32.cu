@@ -6,9 +6,10 @@
 // exact_batch hot loop, :34-116, under the 1e-5 tolerance of north_star):
 //   theta = atan2(alpha, beta),  Omega = 2 theta,  W = sum(theta) / (2 pi)
 //   alpha = N.(v0-q) (= det(a,b,c)), beta grouped as _kernels.py:98-103.
-//   Common pairs (|alpha| < beta/8: every far face) need one MUFU.RCP and a
-//   3-term polynomial; the rest (wide angles, on-surface candidates,
-//   degenerate faces) go to exact_rare().
+//   Common pairs (|alpha| < beta/8, beta > |a||b||c|/2 and every corner
+//   farther than eps: every far face) need one MUFU.RCP and a 3-term
+//   polynomial; the rest (wide angles, ill-conditioned beta, vertex-hit and
+//   other on-surface candidates, degenerate faces) go to exact_rare().
 // Soft (replaces _kernels.soft_batch_f32, :312-349, and soft_batch, :119-158):
 //   term = N.(c-q) / |c-q|^3 with one MUFU.RSQ,  W = sum(term) / (8 pi);
 //   |c-q| < eps flags the point and skips the face.
