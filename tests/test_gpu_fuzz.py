@@ -128,3 +128,48 @@ def test_random_meshes_gradient_parity(cuda_device, seed):
         ref = ofn(v, f, p32, c32, threads=1)
         assert np.isfinite(got).all(), (mode, seed)
         assert np.abs(got - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-300), (mode, seed)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_meshes_lattice_parity(cuda_device, seed):
+    """The same random meshes on a lattice (rz = 32: the row kernels, both
+    directions) whose nodes include the mesh's own vertices for some seeds
+    (a lattice-aligned mesh): forward values at nodes farther than 1e-4 x
+    scale from the surface within 1e-5 of the f64 oracle, flags on vertex
+    nodes, exact and soft gradients within 1e-4 of the oracle."""
+    import torch
+    from paper_2407_11272_b200 import _lib as L, device
+    v, f, _ = random_case(seed)
+    scale = float(np.abs(v).max())
+    res = (10, 12, 32)
+    lo, hi = (-1.1 * scale,) * 3, (1.1 * scale,) * 3
+    if seed % 3 == 0:  # snap the vertices onto lattice nodes
+        ax = [orc.axis_nodes(lo[a], hi[a], res[a]) for a in range(3)]
+        v = np.stack([ax[a][np.abs(ax[a][None, :] - v[:, a:a + 1]).argmin(axis=1)]
+                      for a in range(3)], axis=1)
+    grid = (lo, hi, res)
+    nodes = orc.node_coordinates(*grid)
+    p32 = nodes.astype(np.float32).astype(np.float64)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    got, gf = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW)
+    got, gf = got.cpu().numpy(), gf.cpu().numpy().astype(bool)
+    ref, rf = orc.winding_number_batch(v, f, p32, mode="exact", threads=1)
+    far = surface_distance(p32, v[f]) > 1e-4 * scale
+    assert not gf[far].any() and np.abs(got[far] - ref[far]).max() <= 1e-5, seed
+    t = v[f]
+    live = np.linalg.norm(np.cross(t[:, 1] - t[:, 0], t[:, 2] - t[:, 0]), axis=1) > 0
+    on_vertex = np.isin(np.arange(len(v)), f[live])
+    idx = {tuple(p): i for i, p in enumerate(p32)}
+    for k in np.flatnonzero(on_vertex):
+        i = idx.get(tuple(v[k].astype(np.float32).astype(np.float64)))
+        if i is not None:
+            assert gf[i], (seed, k)
+    c = np.random.default_rng(200 + seed).normal(size=len(nodes))
+    c[~far] = 0.0
+    c32 = c.astype(np.float32).astype(np.float64)
+    for mode, ofn in (("exact", orc.exact_grad), ("soft", orc.soft_grad)):
+        fg = device.face_grad(dm, mode, "f32", torch.from_numpy(c32).float().cuda(), grid=grid)
+        g = device.vertex_grad(dm, fg).cpu().numpy()
+        r = ofn(v, f, p32, c32, threads=1)
+        assert np.isfinite(g).all(), (mode, seed)
+        assert np.abs(g - r).max() <= 1e-4 * max(np.abs(r).max(), 1e-300), (mode, seed)
