@@ -6,7 +6,7 @@
 // exact_batch hot loop, :34-116, under the 1e-5 tolerance of north_star):
 //   theta = atan2(alpha, beta),  Omega = 2 theta,  W = sum(theta) / (2 pi)
 //   alpha = N.(v0-q) (= det(a,b,c)), beta grouped as _kernels.py:98-103.
-//   Common pairs (|alpha| < beta/8, beta > |a||b||c|/2 and every corner
+//   Common pairs (|alpha/beta| < 1/8, beta > |a||b||c|/2 and every corner
 //   farther than eps: every far face) need one MUFU.RCP and a 3-term
 //   polynomial; the rest (wide angles, ill-conditioned beta, vertex-hit and
 //   other on-surface candidates, degenerate faces) go to exact_rare().
@@ -138,7 +138,7 @@ struct ExactPol {
     // beta = |a||b||c| + (b.c)|a| + (a.b)|c| + (c.a)|b|  (_kernels.py:98-103)
     const F2 labc = mul2(la, mul2(lb, lc));
     const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
-    // Common pairs: |theta| < atan(1/8) (|alpha| < beta/8, so beta > 0).  On
+    // Common pairs: |theta| < atan(1/8) (|alpha/beta| < 1/8, beta > 0).  On
     // a face's closed triangle beta <= 0 (on a vertex alpha = beta = 0), so
     // every on-surface candidate fails this test and reaches exact_rare(), as
     // do degenerate faces (N = 0); far faces -- nearly all pairs of a fine
@@ -146,15 +146,13 @@ struct ExactPol {
     // |t| <= 1/8: relative error 1.2e-7 in fp32 (fit: DESIGN.md 3.5).
     // Well-conditioned pairs only: beta = |a||b||c| (1 + sum cos) must not
     // have cancelled below |a||b||c|/2 (near-edge / grazing configurations,
-    // where fp32 loses digits); those go to the fp64 rare path too.  beta/8
-    // is an exponent subtract on the ALU pipe (exact for normal beta; any
-    // beta <= 0 or subnormal yields a negative bound, i.e. "rare").
-    float al, ah, bl, bh, pl, ph;
-    split(alpha, al, ah);
+    // where fp32 loses digits); those go to the fp64 rare path too.  The
+    // angle test is |t| < 1/8 on the computed t = alpha / beta (t^2 < 1/64;
+    // beta <= 0 already fails the conditioning test), the same operations
+    // as the face-wide fast path of finish(), so both classify alike.
+    float bl, bh, pl, ph;
     split(beta, bl, bh);
     split(labc, pl, ph);
-    const float b8l = __int_as_float(__float_as_int(bl) - (3 << 23));
-    const float b8h = __int_as_float(__float_as_int(bh) - (3 << 23));
     const float p2l = __int_as_float(__float_as_int(pl) - (1 << 23));  // |a||b||c| / 2
     const float p2h = __int_as_float(__float_as_int(ph) - (1 << 23));
     // vertex-hit candidates (some corner within eps: |a||b||c| can be 0 and
@@ -165,9 +163,12 @@ struct ExactPol {
     split(lc2, c2l, c2h);
     const bool vl = fminf(a2l, fminf(b2l, c2l)) >= ctx.eps2;
     const bool vh = fminf(a2h, fminf(b2h, c2h)) >= ctx.eps2;
-    const bool cl = fabsf(al) < b8l && bl > p2l && vl, ch = fabsf(ah) < b8h && bh > p2h && vh;
     const F2 tt = mul2(alpha, rcp2(beta));
     const F2 s = mul2(tt, tt);
+    // |t| < 1/8 on the computed t (the fast path's test, same operations)
+    float sl, sh;
+    split(add2(s, f2s(-1.0f / 64.0f)), sl, sh);
+    const bool cl = sl < 0.0f && bl > p2l && vl, ch = sh < 0.0f && bh > p2h && vh;
     const F2 p = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
                       f2s(1.0f));
     float tl, th;
@@ -176,9 +177,9 @@ struct ExactPol {
     return (cl ? 0u : 1u) | (ch ? 0u : 2u);
   }
   // All PP point pairs of a thread against one face.  The common-pair test
-  // of tail2 (|alpha| < beta/8 and beta > |a||b||c|/2) is evaluated for the
-  // whole face as ONE predicate, max over lanes of (|alpha| - beta/8,
-  // |a||b||c| - 2 beta) < 0, from packed FFMAs and a 3-input max tree: when
+  // of tail2 (t^2 < 1/64 and beta > |a||b||c|/2) is evaluated for the whole
+  // face as ONE predicate, max over lanes of (t^2 - 1/64, |a||b||c| - 2 beta)
+  // < 0, from packed ops and a 3-input max tree: when
   // every point of the thread is a common pair (nearly always) the terms are
   // added without per-lane selects or rare-mask building, which had cost
   // ~1/3 of the issue slots.  Otherwise the per-lane path (tail2) runs.
@@ -199,17 +200,18 @@ struct ExactPol {
       const F2 ca = fma2(add2(lc2[pp], la2[pp]), half, f2s(-R.n.w));
       const F2 labc = mul2(la, mul2(lb, lc));
       const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
-      // |alpha| - beta/8 and |a||b||c| - 2 beta: the scalings are exact and
-      // an fma rounds once, so each sign is the exact comparison's (the same
-      // classification as tail2's exponent-subtract test)
-      const F2 dd = fma2(beta, f2s(-0.125f), abs2(alpha[pp]));
+      // |a||b||c| - 2 beta (exact scaling, one rounding: the sign is the
+      // exact comparison's, as tail2's exponent-subtract test) and t^2 - 1/64
+      // (tail2's operations); beta <= 0 makes ee >= 0, so a non-finite t
+      // never passes
       const F2 ee = fma2(beta, f2s(-2.0f), labc);
+      const F2 tt = mul2(alpha[pp], rcp2(beta));
+      const F2 s = mul2(tt, tt);
+      const F2 dd = add2(s, f2s(-1.0f / 64.0f));  // t^2 - 1/64
       float d0, d1, e0, e1;
       split(dd, d0, d1);
       split(ee, e0, e1);
       m = fmaxf(m, fmaxf(fmaxf(d0, d1), fmaxf(e0, e1)));
-      const F2 tt = mul2(alpha[pp], rcp2(beta));
-      const F2 s = mul2(tt, tt);
       tq[pp] = tt;
       tp[pp] = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
                     f2s(1.0f));
