@@ -1,8 +1,14 @@
-"""Accuracy report of the FP32 exact forward against the f64 oracle on the
-BASELINE configs (seeded node subsets): max / p99.99 |dW| on unflagged nodes,
-flag and binarized-occupancy mismatches.  Run on a GPU box:
+"""Accuracy report of the FP32 hot path against the f64 oracle on the
+BASELINE configs, through the lattice (row) kernels the bench runs: a seeded
+set of whole k-rows of each grid is evaluated with grid launches (node range
+= one row), and compared with the oracle on the same f32-rounded nodes.
 
-    python tools/error_report.py [--nodes N]
+Forward: max / p99.99 |dW| on unflagged nodes, flag and binarized-occupancy
+mismatches (|w - 0.5| < 1e-3 excluded, north_star).  Backward (exact, and
+soft for C4's mode): vertex gradients of sum_p c_p W_p for seeded
+coefficients (0 on flagged nodes), max |dg| / max |g|.  Run on a GPU box:
+
+    python tools/error_report.py [--rows N]
 """
 
 import argparse
@@ -18,38 +24,58 @@ sys.path.insert(0, str(ROOT))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--nodes", type=int, default=4096)
+    ap.add_argument("--rows", type=int, default=16)
     args = ap.parse_args()
     import torch
     from oracle import oracle as orc
     from paper_2407_11272_b200 import configs, device
 
     out = {}
-    for name, n in (("c1", None), ("c2", args.nodes), ("c3", args.nodes // 2),
-                    ("c5", args.nodes // 16)):
+    for name in ("c1", "c2", "c3", "c5"):
         w = configs.make(name)
-        if n is None or n >= w.n_nodes:
-            idx = np.arange(w.n_nodes)
-        else:
-            idx = np.sort(np.random.default_rng(7).choice(w.n_nodes, size=n, replace=False))
-        i, rem = np.divmod(idx, w.res[1] * w.res[2])
-        j, k = np.divmod(rem, w.res[2])
+        rx, ry, rz = w.res
+        n_rows = rx * ry
+        rows = np.sort(np.random.default_rng(7).choice(n_rows, size=min(args.rows, n_rows),
+                                                       replace=False))
+        grid = (w.lo, w.hi, w.res)
         ax = [orc.axis_nodes(w.lo[a], w.hi[a], w.res[a]) for a in range(3)]
-        pts = np.stack([ax[0][i], ax[1][j], ax[2][k]], axis=1)
+        pts = np.concatenate([np.stack([np.full(rz, ax[0][r // ry]), np.full(rz, ax[1][r % ry]),
+                                        ax[2]], axis=1) for r in rows])
+        p32 = pts.astype(np.float32).astype(np.float64)
         dm = device.DeviceMesh.from_numpy(w.vertices, w.faces)
-        got, gf = device.forward(dm, "exact", "f32",
-                                 points=torch.as_tensor(pts, dtype=torch.float32))
-        got = got.double().cpu().numpy()
-        gf = gf.cpu().numpy().astype(bool)
-        ref, rf = orc.winding_number_batch(w.vertices, w.faces,
-                                           pts.astype(np.float32).astype(np.float64))
+        vals, flags = [], []
+        for r in rows:
+            v, f = device.forward(dm, "exact", "f32", grid=grid, n0=int(r) * rz, count=rz)
+            vals.append(v.double().cpu().numpy())
+            flags.append(f.cpu().numpy().astype(bool))
+        got, gf = np.concatenate(vals), np.concatenate(flags)
+        ref, rf = orc.winding_number_batch(w.vertices, w.faces, p32)
         err = np.abs(got - ref)[~rf]
         amb = (np.abs(ref - 0.5) < 1e-3) | (np.abs(got - 0.5) < 1e-3)
-        out[name] = {"nodes": int(len(idx)), "max_abs_err": float(err.max()),
-                     "p9999_abs_err": float(np.quantile(err, 0.9999)),
-                     "flag_mismatch": int((gf != rf).sum()),
-                     "binarize_mismatch": int(((got > 0.5) != (ref > 0.5))[~amb].sum())}
-        print(name, out[name], flush=True)
+        rep = {"nodes": int(len(pts)), "max_abs_err": float(err.max()),
+               "p9999_abs_err": float(np.quantile(err, 0.9999)),
+               "flag_mismatch": int((gf != rf).sum()),
+               "binarize_mismatch": int(((got > 0.5) != (ref > 0.5))[~amb].sum())}
+        if name != "c5":  # the 1M-face oracle gradient is too slow for a report
+            c = np.random.default_rng(11).normal(size=len(pts))
+            c[rf | gf] = 0.0
+            c32 = c.astype(np.float32).astype(np.float64)
+            g = torch.zeros((dm.num_vertices, 3), dtype=torch.float64, device="cuda")
+            for i, r in enumerate(rows):
+                cr = torch.from_numpy(c32[i * rz:(i + 1) * rz]).float().cuda()
+                fg = device.face_grad(dm, "exact", "f32", cr, grid=grid, n0=int(r) * rz, count=rz)
+                device.vertex_grad(dm, fg, out=g, accumulate=True)
+            gr = orc.exact_grad(w.vertices, w.faces, p32, c32)
+            if int(dm.exact_grad_setup()[0].shape[0]) == 0:
+                # closed mesh: the exact gradient is identically zero (every edge
+                # cancels); the oracle's face-wise sum shows its rounding noise
+                rep["exact_grad_abs"] = float(np.abs(g.cpu().numpy()).max())
+                rep["oracle_grad_noise"] = float(np.abs(gr).max())
+            else:
+                scale = max(np.abs(gr).max(), 1e-300)
+                rep["exact_grad_rel_err"] = float(np.abs(g.cpu().numpy() - gr).max() / scale)
+        out[name] = rep
+        print(name, rep, flush=True)
     print(json.dumps(out))
 
 
