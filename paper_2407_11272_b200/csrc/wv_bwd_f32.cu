@@ -49,7 +49,7 @@ constexpr int kAxisMax = 1024;    // lattice axes up to this length use node tab
 // into coef_scale by the launcher.
 // One ill-conditioned (face, point) pair of the exact backward in FP64,
 // straight into the face's fp64 accumulators.  Used where the point lies
-// close to an edge's segment ((|a|+|b|)^2 - |e|^2 < |e|^2 / 10): there the
+// close to an edge's segment ((|a|+|b|)^2 - |e|^2 < |e|^2 / 100): there the
 // fp32 denominator cancels (relative error ~1e-7 |e|^2 / d).  Here
 // |a||b| + a.b = |a x b|^2 / (|a||b| - a.b) has no cancellation, and the
 // contributions bypass the fp32 run sums.  c already carries coef_scale and
@@ -106,9 +106,10 @@ struct ExactEdgeBwd {
   // no dot products, one FADD + one FFMA per edge, and the FFMA rounds
   // (|a|+|b|)^2 - U once.
   // a pair is ill-conditioned when some edge has d_e < |e|^2 / kIllRatio
+  // (fp32 keeps ~1e-7 kIllRatio relative accuracy up to there: 1e-5)
   // (tested on the product of the three ratios |e|^2 / d_e; non-finite
   // counts as ill): its lanes take exact_pair_f64 instead
-  static constexpr float kIllRatio = 10.0f;
+  static constexpr float kIllRatio = 100.0f;
   template <bool kUnit>
   __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
                                                    float, F2* g) {
