@@ -619,7 +619,7 @@ __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const Poi
 template <class Pol, bool kUnit>
 __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const PointChunk& ch,
                                            int n_pairs, int64_t flat0, int64_t rz, float eps2,
-                                           double (*acc)[kBwdThreads]) {
+                                           bool dense, double (*acc)[kBwdThreads]) {
   int j = 0;
   int k = (int)(flat0 % rz);  // k of the chunk's first node
   while (j < n_pairs) {
@@ -639,13 +639,14 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
 #pragma unroll 1
     for (; j + kRowStep <= e; j += kRowStep) {
       float4 zc[kRowStep];
-      bool any = false;
 #pragma unroll
-      for (int u = 0; u < kRowStep; ++u) {
-        zc[u] = ch.zc[j + u];
-        any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
+      for (int u = 0; u < kRowStep; ++u) zc[u] = ch.zc[j + u];
+      if (!dense) {
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < kRowStep; ++u) any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
+        if (!any) continue;
       }
-      if (!any) continue;
       Pol::template step_row<kUnit, kRowStep>(R, w, zc, eps2, z, &mr);
     }
 #pragma unroll 1
@@ -719,6 +720,7 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     const int n = (int)((p_end - c0) < kBwdChunk ? (p_end - c0) : kBwdChunk);
     const int n_pairs = (n + 1) / 2;
     __syncthreads();
+    int zero = 0;  // some coefficient of this chunk is zero (or padding)
     for (int i = threadIdx.x; i < 2 * n_pairs; i += kBwdThreads) {
       float x = 1.0e6f, y = 1.0e6f, z = 1.0e6f, c = 0.0f;
       if (i < n) {
@@ -753,15 +755,18 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       xy[2 + (i & 1)] = y;
       zc[i & 1] = z;
       zc[2 + (i & 1)] = c;
+      zero |= c == 0.0f;
     }
-    __syncthreads();
+    // a chunk without zero coefficients (the common case of a loss over a
+    // grid) skips the per-step zero tests
+    const bool dense = __syncthreads_or(zero) == 0;
     if constexpr (Src::kRows) {
       // row runs flush their sums straight into the fp64 accumulators
       const int64_t flat0 = src.n0 + c0;
       if (unit) {
-        chunk_rows<Pol, true>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, acc);
+        chunk_rows<Pol, true>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, dense, acc);
       } else {
-        chunk_rows<Pol, false>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, acc);
+        chunk_rows<Pol, false>(R, chunk, n_pairs, flat0, src.g.res[2], eps2, dense, acc);
       }
     } else {
       F2 g[Pol::kAcc];
