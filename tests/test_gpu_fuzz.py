@@ -173,3 +173,28 @@ def test_random_meshes_lattice_parity(cuda_device, seed):
         r = ofn(v, f, p32, c32, threads=1)
         assert np.isfinite(g).all(), (mode, seed)
         assert np.abs(g - r).max() <= 1e-4 * max(np.abs(r).max(), 1e-300), (mode, seed)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_meshes_f64_gradient_parity(cuda_device, seed):
+    """The f64 parity backward (exact edge form and soft, the reference's
+    formula) on the random cases: 1e-9 of the largest component (fp64
+    rounding and a different summation order than the oracle)."""
+    import torch
+    from paper_2407_11272_b200 import device
+    v, f, pts = random_case(seed)
+    scale = np.abs(v).max()
+    c = np.random.default_rng(300 + seed).normal(size=len(pts))
+    c[surface_distance(pts, v[f]) <= 1e-6 * scale] = 0.0
+    cen = v[f].mean(axis=1)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    for mode, ofn in (("exact", orc.exact_grad), ("soft", orc.soft_grad)):
+        cc = c.copy()
+        if mode == "soft":
+            d = np.linalg.norm(pts[:, None, :] - cen[None], axis=2).min(axis=1)
+            cc[d <= 1e-6 * scale] = 0.0
+        fg = device.face_grad(dm, mode, "f64", torch.from_numpy(cc).cuda(),
+                              points=torch.from_numpy(pts).cuda())
+        g = device.vertex_grad(dm, fg).cpu().numpy()
+        r = ofn(v, f, pts, cc, threads=1)
+        assert np.abs(g - r).max() <= 1e-9 * max(np.abs(r).max(), 1e-300), (mode, seed)
