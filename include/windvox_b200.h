@@ -46,6 +46,7 @@ extern "C" {
 #define WV_PACK_SOFTGRAD_F64 6
 #define WV_PACK_EXACTGRAD_F32 7 /* wv_pack_exact_grad: active faces of the exact backward */
 #define WV_PACK_EXACTGRAD_F64 8
+#define WV_PACK_EXACTSTRIP_F32 9 /* wv_pack_exact_strip: exact f32 records in strip order */
 
 /* stored value for on-surface (flagged) nodes */
 #define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
@@ -131,6 +132,28 @@ int wv_soft_fwd_grid_f64(const void *packed, int64_t n_faces, wv_grid_t grid, in
 int wv_soft_fwd_points_f64(const void *packed, int64_t n_faces, const double *points,
                            int64_t count, int policy, double *out, uint8_t *flags,
                            void *stream);
+
+/* ---- strip-ordered exact f32 forward (same values as wv_exact_fwd_*_f32
+ * up to fp32 summation order; fewer square roots on lattice rows) --------
+ * wv_strip_order (HOST memory, CPU): welds vertices by bitwise-equal
+ *   position and walks the faces as strips: perm[k] = face at strip position
+ *   k, window[3k..3k+2] = its vertex indices in window order, flags[k] bit0
+ *   = strip start, bit1 = window reflects the face's orientation.
+ * wv_pack_exact_strip (device arrays): packs those records (kind
+ *   WV_PACK_EXACTSTRIP_F32, wv_packed_bytes sizes it); n_faces < 2^31.
+ * Outputs are per query point (face order does not matter to W). */
+int wv_strip_order(const double *vertices, int64_t n_verts, const int64_t *faces,
+                   int64_t n_faces, int64_t *perm, int64_t *window, uint8_t *flags);
+int wv_pack_exact_strip(const void *vertices, int vert_f64, int64_t n_verts, const void *faces,
+                        int faces_i64, int64_t n_faces, const int64_t *perm,
+                        const int64_t *window, const uint8_t *flags, void *packed,
+                        void *stream);
+int wv_exact_strip_fwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                                int64_t count, int policy, float *out, uint8_t *flags,
+                                void *workspace, size_t workspace_bytes, void *stream);
+int wv_exact_strip_fwd_points_f32(const void *packed, int64_t n_faces, const float *points,
+                                  int64_t count, int policy, float *out, uint8_t *flags,
+                                  void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---- backward: per-face corner gradients reduced over query points ------
  * face_grad (F,3,3) f64 is OVERWRITTEN with

@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", str(CSRC), "-I", str(INCLUDE)]
 # files whose f64 arithmetic must not be FMA-contracted
-NO_FMAD = {"wv_pack.cu", "wv_f64.cu", "wv_mc.cu", "wv_metrics.cu"}
+NO_FMAD = {"wv_pack.cu", "wv_f64.cu", "wv_mc.cu", "wv_metrics.cu", "wv_strip.cu"}
 
 
 def _nvcc() -> str:

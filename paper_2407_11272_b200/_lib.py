@@ -23,6 +23,7 @@ PACK_SOFTGRAD_F32 = 5
 PACK_SOFTGRAD_F64 = 6
 PACK_EXACTGRAD_F32 = 7
 PACK_EXACTGRAD_F64 = 8
+PACK_EXACTSTRIP_F32 = 9
 POLICY_RAW = 0
 POLICY_HALF = 1
 
@@ -40,7 +41,8 @@ EXPORTED = (
     "wv_splitmix64_uniform", "wv_pairwise_sum_workspace_bytes", "wv_pairwise_sum",
     "wv_surface_cdf", "wv_sample_surface", "wv_nearest_distances",
     "wv_fwd_workspace_bytes_batch", "wv_fwd_grid_f32_batch", "wv_bwd_workspace_bytes_batch",
-    "wv_bwd_grid_f32_batch",
+    "wv_bwd_grid_f32_batch", "wv_strip_order", "wv_pack_exact_strip",
+    "wv_exact_strip_fwd_grid_f32", "wv_exact_strip_fwd_points_f32",
 )
 
 
@@ -112,6 +114,10 @@ def _declare(lib):
         "wv_fwd_grid_f32_batch": ([I, P, SZ, I64, Grid, I64, I64, I64, I, P, P, P, SZ, P], I),
         "wv_bwd_workspace_bytes_batch": ([I, I64, I64, I64], SZ),
         "wv_bwd_grid_f32_batch": ([I, P, SZ, I64, Grid, I64, I64, I64, P, D, P, P, SZ, P], I),
+        "wv_strip_order": ([P, I64, P, I64, P, P, P], I),
+        "wv_pack_exact_strip": ([P, I, I64, P, I, I64, P, P, P, P, P], I),
+        "wv_exact_strip_fwd_grid_f32": (fwd32_grid, I),
+        "wv_exact_strip_fwd_points_f32": (fwd32_pts, I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -117,10 +117,54 @@ int wv_vertex_normals(const double* vertices, int64_t n_verts, const int64_t* fa
 // ---- forward ---------------------------------------------------------------
 size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {
-    case WV_PACK_EXACT_F32: return wv::exact_fwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_EXACT_F32:
+    case WV_PACK_EXACTSTRIP_F32: return wv::exact_fwd_workspace_bytes(n_faces, count, sm_count());
     case WV_PACK_SOFT_F32: return wv::soft_fwd_workspace_bytes(n_faces, count, sm_count());
     default: return 0;
   }
+}
+
+int wv_strip_order(const double* vertices, int64_t n_verts, const int64_t* faces,
+                   int64_t n_faces, int64_t* perm, int64_t* window, uint8_t* flags) {
+  if (n_verts < 0 || n_faces < 0 || n_faces >= ((int64_t)1 << 31)) return WV_ERR_ARG;
+  if (n_faces == 0) return WV_OK;
+  if (vertices == nullptr || faces == nullptr || perm == nullptr || window == nullptr ||
+      flags == nullptr)
+    return WV_ERR_ARG;
+  for (int64_t i = 0; i < 3 * n_faces; ++i)
+    if (faces[i] < 0 || faces[i] >= n_verts) return WV_ERR_ARG;
+  return wv::strip_order(vertices, n_verts, faces, n_faces, perm, window, flags);
+}
+
+int wv_pack_exact_strip(const void* vertices, int vert_f64, int64_t n_verts, const void* faces,
+                        int faces_i64, int64_t n_faces, const int64_t* perm,
+                        const int64_t* window, const uint8_t* flags, void* packed,
+                        void* stream) {
+  if (packed == nullptr || n_verts < 0 || n_faces < 0) return WV_ERR_ARG;
+  if (n_faces > 0 && (vertices == nullptr || faces == nullptr || perm == nullptr ||
+                      window == nullptr || flags == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_pack_strip(vertices, vert_f64, n_verts, faces, faces_i64, n_faces, perm,
+                               window, flags, packed, as_stream(stream));
+}
+
+int wv_exact_strip_fwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                                int64_t count, int policy, float* out, uint8_t* flags,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count)) return WV_ERR_ARG;
+  return wv::launch_exact_strip_fwd_f32(packed, n_faces, grid_src(grid, n0), count, policy, out,
+                                        flags, workspace, workspace_bytes, sm_count(),
+                                        as_stream(stream));
+}
+
+int wv_exact_strip_fwd_points_f32(const void* packed, int64_t n_faces, const float* points,
+                                  int64_t count, int policy, float* out, uint8_t* flags,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_strip_fwd_f32(packed, n_faces, list_src(points, nullptr), count, policy,
+                                        out, flags, workspace, workspace_bytes, sm_count(),
+                                        as_stream(stream));
 }
 
 int wv_exact_fwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,

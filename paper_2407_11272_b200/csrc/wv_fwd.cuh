@@ -79,6 +79,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   }
   typename Pol::Ctx ctx = Pol::make_ctx(eps);
   uint32_t hits = 0;
+  typename Pol::Carry carry[PP];  // strip policies: corner distances of the previous face
 
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int64_t it = t - t_begin;
@@ -100,10 +101,19 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         // groups of (at most) 4 point pairs: the per-face row constants are
         // shared by all of a thread's points, the temporaries by one group
         rare = 0;
+        if constexpr (Pol::kStrip) {
+          const bool restart = __float_as_int(R.v1.w) < 0;  // uniform per face
 #pragma unroll
-        for (int g0 = 0; g0 < PP; g0 += 4)
-          rare |= Pol::template face_row<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, tacc + g0)
-                  << (2 * g0);
+          for (int g0 = 0; g0 < PP; g0 += 4)
+            rare |= Pol::template face_strip<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, restart,
+                                                                 carry + g0, tacc + g0)
+                    << (2 * g0);
+        } else {
+#pragma unroll
+          for (int g0 = 0; g0 < PP; g0 += 4)
+            rare |= Pol::template face_row<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, tacc + g0)
+                    << (2 * g0);
+        }
       } else {
         rare = 0;
 #pragma unroll

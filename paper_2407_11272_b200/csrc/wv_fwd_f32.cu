@@ -77,6 +77,8 @@ struct ExactPol {
   static constexpr int kMinBlocksRow = 4;  // 5 (96 regs) spills and measured 2% slower
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (2.0 * kPi);
+  static constexpr bool kStrip = false;
+  struct Carry {};
   // eps2: squared vertex-hit radius, eps (f32) inflated by 1% so that every
   // pair within the reference's f64 eps of a vertex (winding.py:65-67) leaves
   // the common path and is decided exactly by exact_rare
@@ -132,8 +134,8 @@ struct ExactPol {
     // packed): 2 ops instead of 3.  It can cancel only where beta itself is
     // ill-conditioned, and those pairs leave for the fp64 path below.
     const F2 half = f2s(0.5f);
-    const F2 ab = fma2(add2(la2, lb2), half, f2s(-R.v1.w));
-    const F2 bc = fma2(add2(lb2, lc2), half, f2s(-R.v2.w));
+    const F2 ab = fma2(add2(la2, lb2), half, f2s(-fabsf(R.v1.w)));
+    const F2 bc = fma2(add2(lb2, lc2), half, f2s(-fabsf(R.v2.w)));
     const F2 ca = fma2(add2(lc2, la2), half, f2s(-R.n.w));
     // beta = |a||b||c| + (b.c)|a| + (a.b)|c| + (c.a)|b|  (_kernels.py:98-103)
     const F2 labc = mul2(la, mul2(lb, lc));
@@ -189,14 +191,30 @@ struct ExactPol {
   __device__ __forceinline__ static uint32_t finish(const Rec& R, const F2* alpha, const F2* la2,
                                                     const F2* lb2, const F2* lc2, const Ctx& ctx,
                                                     bool near, F2* tacc) {
+    F2 la[PP], lb[PP], lc[PP];
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      la[pp] = sqrt2(la2[pp]);
+      lb[pp] = sqrt2(lb2[pp]);
+      lc[pp] = sqrt2(lc2[pp]);
+    }
+    return finish_len<PP>(R, alpha, la2, lb2, lc2, la, lb, lc, ctx, near, tacc);
+  }
+  // finish() with the corner distances given (the strip form carries them)
+  template <int PP>
+  __device__ __forceinline__ static uint32_t finish_len(const Rec& R, const F2* alpha,
+                                                        const F2* la2, const F2* lb2,
+                                                        const F2* lc2, const F2* la_,
+                                                        const F2* lb_, const F2* lc_,
+                                                        const Ctx& ctx, bool near, F2* tacc) {
     F2 tq[PP], tp[PP];
     float m = -1.0f;
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
-      const F2 la = sqrt2(la2[pp]), lb = sqrt2(lb2[pp]), lc = sqrt2(lc2[pp]);
+      const F2 la = la_[pp], lb = lb_[pp], lc = lc_[pp];
       const F2 half = f2s(0.5f);
-      const F2 ab = fma2(add2(la2[pp], lb2[pp]), half, f2s(-R.v1.w));
-      const F2 bc = fma2(add2(lb2[pp], lc2[pp]), half, f2s(-R.v2.w));
+      const F2 ab = fma2(add2(la2[pp], lb2[pp]), half, f2s(-fabsf(R.v1.w)));
+      const F2 bc = fma2(add2(lb2[pp], lc2[pp]), half, f2s(-fabsf(R.v2.w)));
       const F2 ca = fma2(add2(lc2[pp], la2[pp]), half, f2s(-R.n.w));
       const F2 labc = mul2(la, mul2(lb, lc));
       const F2 beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
@@ -278,6 +296,66 @@ struct ExactPol {
   }
 };
 
+// Exact forward over STRIP-ordered records (wv_strip.cu): on lattice rows a
+// thread carries |A - q|^2, |A - q| of the next face from the current
+// face's B and C (bitwise the values a recomputation gives: the same
+// operations on the same coordinates), so a face costs 1 square root + 1
+// reciprocal per pair instead of 3 + 1 -- the MUFU pipe bounds this kernel.
+// Records restart (recompute A and B) at strip starts and at every tile.
+struct ExactStripPol : ExactPol {
+  static constexpr bool kStrip = true;
+  struct Carry {
+    F2 b2, b, c2, c;
+  };
+  template <int PP>
+  __device__ __forceinline__ static uint32_t face_strip(const Rec& R, const Row& w, const F2* qz,
+                                                        const Ctx& ctx, bool restart, Carry* cr,
+                                                        F2* tacc) {
+    F2 alpha[PP], la2[PP], lb2[PP], lc2[PP], la[PP], lb[PP], lc[PP];
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), cz = sub2(f2s(R.v2.z), qz[pp]);
+      alpha[pp] = fma2(f2s(R.n.z), az, f2s(w.alpha));
+      lc2[pp] = fma2(cz, cz, f2s(w.c2));
+      lc[pp] = sqrt2(lc2[pp]);
+    }
+    if (restart) {
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) {
+        const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
+        la2[pp] = fma2(az, az, f2s(w.a2));
+        lb2[pp] = fma2(bz, bz, f2s(w.b2));
+        la[pp] = sqrt2(la2[pp]);
+        lb[pp] = sqrt2(lb2[pp]);
+      }
+    } else {
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) {
+        la2[pp] = cr[pp].b2;
+        la[pp] = cr[pp].b;
+        lb2[pp] = cr[pp].c2;
+        lb[pp] = cr[pp].c;
+      }
+    }
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      cr[pp].b2 = lb2[pp];
+      cr[pp].b = lb[pp];
+      cr[pp].c2 = lc2[pp];
+      cr[pp].c = lc[pp];
+    }
+    const bool near = fminf(w.a2, fminf(w.b2, w.c2)) < ctx.eps2;
+    return finish_len<PP>(R, alpha, la2, lb2, lc2, la, lb, lc, ctx, near, tacc);
+  }
+  // the fp64 path needs the face's own orientation (triple product): a
+  // reflected window (v2.w < 0) swaps B and C back
+  __device__ __forceinline__ static double rare(const Rec& R, float qx, float qy, float qz,
+                                                double eps) {
+    const bool refl = __float_as_int(R.v2.w) < 0;
+    return exact_rare(R.v0e, refl ? R.v2 : R.v1, refl ? R.v1 : R.v2, qx, qy, qz, eps);
+  }
+};
+
 struct SoftPol {
   using Rec = SoftRecF32;
   static constexpr int kTile = 256;
@@ -288,6 +366,8 @@ struct SoftPol {
   static constexpr int kMinBlocksRow = 5;
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (8.0 * kPi);
+  static constexpr bool kStrip = false;
+  struct Carry {};
   struct Ctx {
     float eps2;
   };
@@ -409,6 +489,13 @@ int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource&
                          const Batch& bt) {
   return launch_fwd_f32<ExactPol>(packed, n_faces, ps, n_count, policy, out, flags, workspace,
                                   ws_bytes, num_sms, stream, bt);
+}
+int launch_exact_strip_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                               int64_t n_count, int policy, float* out, uint8_t* flags,
+                               void* workspace, size_t ws_bytes, int num_sms,
+                               cudaStream_t stream) {
+  return launch_fwd_f32<ExactStripPol>(packed, n_faces, ps, n_count, policy, out, flags,
+                                       workspace, ws_bytes, num_sms, stream, Batch{});
 }
 size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
   return FwdPlan<ExactPol>::make(n_faces, n_count, num_sms, batch).workspace(n_count * batch);

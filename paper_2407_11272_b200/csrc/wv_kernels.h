@@ -171,6 +171,16 @@ int launch_exact_fwd_f32(const void* packed, int64_t n_faces, const PointSource&
                          const Batch& bt = Batch());
 size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms,
                                  int64_t batch = 1);
+// strip-ordered exact forward (wv_strip.cu builds and packs, wv_fwd_f32.cu runs)
+int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int64_t n_faces,
+                int64_t* perm, int64_t* win, uint8_t* flags);
+int launch_pack_strip(const void* verts, int vert_f64, int64_t n_verts, const void* faces,
+                      int faces_i64, int64_t n_faces, const int64_t* perm, const int64_t* win,
+                      const uint8_t* flags, void* packed, cudaStream_t stream);
+int launch_exact_strip_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                               int64_t n_count, int policy, float* out, uint8_t* flags,
+                               void* workspace, size_t ws_bytes, int num_sms,
+                               cudaStream_t stream);
 int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, int policy, float* out, uint8_t* flags,
                         void* workspace, size_t ws_bytes, int num_sms, cudaStream_t stream,

@@ -25,6 +25,25 @@ _SOFT = {"f32": L.PACK_SOFT_F32, "f64": L.PACK_SOFT_F64}
 _SOFTGRAD = {"f32": L.PACK_SOFTGRAD_F32, "f64": L.PACK_SOFTGRAD_F64}
 _EXACTGRAD = {"f32": L.PACK_EXACTGRAD_F32, "f64": L.PACK_EXACTGRAD_F64}
 _DT = {"f32": torch.float32, "f64": torch.float64}
+# exact f32 forwards with at least this many row-aligned lattice nodes use
+# the strip-ordered records (wv_strip.cu): its host-side strip builder
+# (~0.5 us per face, once per DeviceMesh) pays off from ~2M nodes
+STRIP_MIN_NODES = 1 << 21
+
+
+def strip_order(vertices: np.ndarray, faces: np.ndarray):
+    """Face strips of a mesh (wv_strip_order, host code: no GPU needed):
+    (perm (F,), window (F,3), flags (F,) u8) -- see include/windvox_b200.h."""
+    v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+    f = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
+    F = len(f)
+    perm = np.empty(F, dtype=np.int64)
+    win = np.empty((F, 3), dtype=np.int64)
+    fl = np.empty(F, dtype=np.uint8)
+    L.check(L.load_library().wv_strip_order(v.ctypes.data, len(v), f.ctypes.data, F,
+                                            perm.ctypes.data, win.ctypes.data, fl.ctypes.data),
+            "wv_strip_order")
+    return perm, win, fl
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -172,11 +191,34 @@ class DeviceMesh:
         f = f.contiguous()
         nbytes = int(lib.wv_packed_bytes(kind, self.num_faces))
         buf = torch.empty(nbytes, dtype=torch.uint8, device=v.device)
-        L.check(lib.wv_pack_faces(kind, _ptr(v), int(v.dtype == torch.float64),
-                                  self.num_vertices, _ptr(f), int(f.dtype == torch.int64),
-                                  self.num_faces, _ptr(buf), _stream()), "wv_pack_faces")
+        if kind == L.PACK_EXACTSTRIP_F32:
+            perm, win, fl = self.strip_setup()
+            L.check(lib.wv_pack_exact_strip(_ptr(v), int(v.dtype == torch.float64),
+                                            self.num_vertices, _ptr(f),
+                                            int(f.dtype == torch.int64), self.num_faces,
+                                            _ptr(perm), _ptr(win), _ptr(fl), _ptr(buf),
+                                            _stream()), "wv_pack_exact_strip")
+        else:
+            L.check(lib.wv_pack_faces(kind, _ptr(v), int(v.dtype == torch.float64),
+                                      self.num_vertices, _ptr(f), int(f.dtype == torch.int64),
+                                      self.num_faces, _ptr(buf), _stream()), "wv_pack_faces")
         self._packs[kind] = buf
         return buf
+
+    def strip_setup(self):
+        """Device copies of the face strips (strip_order), built once from the
+        positions at setup time.  Later vertex moves may break the welds;
+        the packer then restarts the strip there (always correct)."""
+        st = getattr(self, "_strip", None)
+        if st is None:
+            vnp = getattr(self, "_verts_np", None)
+            if vnp is None:
+                vnp = self.vertices.detach().double().cpu().numpy()
+            perm, win, fl = strip_order(vnp, self.faces_np())
+            dev = self.vertices.device
+            st = tuple(torch.from_numpy(a).to(dev) for a in (perm, win, fl))
+            self._strip = st
+        return st
 
     def faces_np(self) -> np.ndarray:
         fn = getattr(self, "_faces_np", None)
@@ -247,9 +289,11 @@ def _grid_count(grid, n0, count):
 def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int = 0,
             count: int | None = None, points=None, policy: int = L.POLICY_RAW,
             use_atan2: bool = True, out: torch.Tensor | None = None,
-            flags: torch.Tensor | None = None):
+            flags: torch.Tensor | None = None, strip: bool | None = None):
     """Winding numbers on the device.  ``grid=(lo, hi, res)`` with the node
-    range [n0, n0+count), or ``points`` (n,3).  Returns (values, flags u8)."""
+    range [n0, n0+count), or ``points`` (n,3).  Returns (values, flags u8).
+    ``strip`` (exact f32 only): strip-ordered records; None = automatic
+    (lattice ranges of >= STRIP_MIN_NODES row-aligned nodes)."""
     _check_precision(precision)
     if mode not in ("exact", "soft"):
         raise ValueError(f"mode must be 'exact' or 'soft', got {mode!r}")
@@ -257,7 +301,6 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
     dev = mesh.vertices.device
     dt = _DT[precision]
     kind = (_EXACT if mode == "exact" else _SOFT)[precision]
-    packed = mesh.packed(kind)
     if points is not None:
         pts, count = _points_arg(points, dev, dt)
     else:
@@ -271,9 +314,25 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
     if precision == "f32":
         if not use_atan2:
             raise ValueError("the single-argument arctan branch exists only at precision='f64'")
+        if strip is None:
+            strip = (mode == "exact" and points is None and count >= STRIP_MIN_NODES
+                     and int(grid[2][2]) % 8 == 0 and int(n0) % 8 == 0 and count % 8 == 0)
+        if strip and mode != "exact":
+            raise ValueError("strip records exist for the exact forward only")
+        if strip:
+            kind = L.PACK_EXACTSTRIP_F32
+        packed = mesh.packed(kind)
         wsb = int(lib.wv_fwd_workspace_bytes(kind, F, count))
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
-        if points is not None:
+        if strip:
+            if points is not None:
+                rc = lib.wv_exact_strip_fwd_points_f32(_ptr(packed), F, _ptr(pts), count, policy,
+                                                       _ptr(out), _ptr(flags), _ptr(ws), wsb, st)
+            else:
+                rc = lib.wv_exact_strip_fwd_grid_f32(_ptr(packed), F, L.make_grid(*grid),
+                                                     int(n0), count, policy, _ptr(out),
+                                                     _ptr(flags), _ptr(ws), wsb, st)
+        elif points is not None:
             fn = lib.wv_exact_fwd_points_f32 if mode == "exact" else lib.wv_soft_fwd_points_f32
             rc = fn(_ptr(packed), F, _ptr(pts), count, policy, _ptr(out), _ptr(flags), _ptr(ws),
                     wsb, st)
@@ -282,6 +341,7 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
             rc = fn(_ptr(packed), F, L.make_grid(*grid), int(n0), count, policy, _ptr(out),
                     _ptr(flags), _ptr(ws), wsb, st)
     else:
+        packed = mesh.packed(kind)
         if mode == "exact":
             if points is not None:
                 rc = lib.wv_exact_fwd_points_f64(_ptr(packed), F, _ptr(pts), count,

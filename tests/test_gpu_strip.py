@@ -1,0 +1,91 @@
+"""Strip-ordered exact forward (wv_strip.cu + ExactStripPol): the same
+winding numbers as the face-ordered kernel up to fp32 summation order, and
+within the north_star 1e-5 of the f64 oracle, on welded meshes, shuffled
+soups (welded by position), random meshes with degenerate / duplicated faces
+(lattice-aligned vertices for the on-vertex flags) and soups whose welds were
+broken after the strip order was built (the packer restarts the strip)."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from test_gpu_fuzz import random_case, surface_distance
+
+pytestmark = pytest.mark.gpu
+
+
+def _both(dm, grid, **kw):
+    from paper_2407_11272_b200 import _lib as L, device
+    a, fa = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW, strip=False, **kw)
+    b, fb = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW, strip=True, **kw)
+    return (a.double().cpu().numpy(), fa.cpu().numpy().astype(bool),
+            b.double().cpu().numpy(), fb.cpu().numpy().astype(bool))
+
+
+@pytest.mark.parametrize("kind", ["welded", "soup"])
+def test_strip_matches_face_order(cuda_device, kind):
+    from paper_2407_11272_b200 import configs, device
+    v, f = configs.torus(0.7, 0.3, 60, 40)
+    if kind == "soup":
+        v, f = configs.soup(v, f, seed=1)
+    grid = ((-1.0,) * 3, (1.0,) * 3, (24, 20, 64))
+    dm = device.DeviceMesh.from_numpy(v, f)
+    a, fa, b, fb = _both(dm, grid)
+    assert np.array_equal(fa, fb)
+    assert np.abs(a - b)[~fa].max() <= 2e-6
+    # sub-ranges (splits start at tile boundaries, strips restart there)
+    a2, _, b2, _ = _both(dm, grid, n0=64 * 40, count=64 * 24)
+    assert np.abs(a2 - b2).max() <= 2e-6 and np.abs(b2 - b[64 * 40:64 * 64]).max() <= 2e-6
+    nodes = orc.node_coordinates(*grid)
+    p32 = nodes.astype(np.float32).astype(np.float64)
+    sel = np.random.default_rng(0).choice(len(nodes), 3000, replace=False)
+    ref, rf = orc.winding_number_batch(v, f, p32[sel], mode="exact")
+    assert np.array_equal(rf, fb[sel])
+    assert np.abs(ref - b[sel])[~rf].max() <= 1e-5
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_strip_random_meshes_lattice(cuda_device, seed):
+    from paper_2407_11272_b200 import device
+    v, f, pts = random_case(seed)
+    scale = float(np.abs(v).max())
+    res = (10, 12, 32)
+    lo, hi = (-1.1 * scale,) * 3, (1.1 * scale,) * 3
+    if seed % 3 == 0:  # lattice-aligned vertices: on-vertex nodes
+        ax = [orc.axis_nodes(lo[a], hi[a], res[a]) for a in range(3)]
+        v = np.stack([ax[a][np.abs(ax[a][None, :] - v[:, a:a + 1]).argmin(axis=1)]
+                      for a in range(3)], axis=1)
+    grid = (lo, hi, res)
+    p32 = orc.node_coordinates(*grid).astype(np.float32).astype(np.float64)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    a, fa, b, fb = _both(dm, grid)
+    assert np.array_equal(fa, fb), seed
+    ref, rf = orc.winding_number_batch(v, f, p32, mode="exact", threads=1)
+    far = surface_distance(p32, v[f]) > 1e-4 * scale
+    assert not fb[far].any() and np.abs(b[far] - ref[far]).max() <= 1e-5, seed
+    # the point-list launch of the strip records (generic face path)
+    got, gf = device.forward(dm, "exact", "f32", points=pts, strip=True)
+    ref, rf = orc.winding_number_batch(v, f, pts.astype(np.float32).astype(np.float64),
+                                       mode="exact", threads=1)
+    far = surface_distance(pts.astype(np.float32).astype(np.float64), v[f]) > 1e-4 * scale
+    assert np.abs(got.double().cpu().numpy()[far] - ref[far]).max() <= 1e-5, seed
+
+
+def test_strip_broken_welds(cuda_device):
+    """Strips built on the welded soup, then half of the vertex copies moved
+    (as after a morph step of a soup): the packer must restart wherever the
+    carried positions differ, and the values must still match."""
+    import torch
+    from paper_2407_11272_b200 import configs, device
+    v, f = configs.soup(*configs.torus(0.7, 0.3, 40, 30), seed=2)
+    grid = ((-1.0,) * 3, (1.0,) * 3, (16, 16, 32))
+    dm = device.DeviceMesh.from_numpy(v, f)
+    dm.strip_setup()
+    v2 = v.copy()
+    rng = np.random.default_rng(1)
+    moved = rng.random(len(v)) < 0.5
+    v2[moved] += rng.normal(scale=1e-3, size=(int(moved.sum()), 3))
+    dm.set_vertices(torch.from_numpy(v2).to(dm.vertices.device))
+    a, fa, b, fb = _both(dm, grid)
+    assert np.array_equal(fa, fb)
+    assert np.abs(a - b)[~fa].max() <= 2e-6

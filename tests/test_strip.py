@@ -1,0 +1,74 @@
+"""Face strips (wv_strip_order, host code in the C-ABI library, no GPU): the
+order is a permutation of the faces, every window is its face's vertex set,
+consecutive windows of a strip share two corner POSITIONS (the forward
+carries their distances), and the reflection flag is the parity of the
+window against the face's own vertex order (the fp64 rare path restores the
+orientation from it)."""
+
+import numpy as np
+import pytest
+
+from paper_2407_11272_b200 import configs
+
+
+def _strips(v, f):
+    from paper_2407_11272_b200 import _lib as L
+    try:
+        L.load_library()
+    except L.WindvoxCudaUnavailable:
+        pytest.skip("library not built")
+    from paper_2407_11272_b200.device import strip_order
+    return strip_order(v, f)
+
+
+def _check(v, f, max_restart_frac):
+    perm, win, fl = _strips(v, f)
+    F = len(f)
+    assert np.array_equal(np.sort(perm), np.arange(F))
+    assert np.array_equal(np.sort(win, axis=1), np.sort(f[perm], axis=1))
+    restart = (fl & 1).astype(bool)
+    assert restart[0]
+    k = np.flatnonzero(~restart)
+    assert np.array_equal(v[win[k, 0]], v[win[k - 1, 1]])
+    assert np.array_equal(v[win[k, 1]], v[win[k - 1, 2]])
+    # parity: window (A,B,C) is a rotation of the face's order iff bit1 clear
+    fo = f[perm]
+    pos = np.stack([np.argmax(fo == win[:, c:c + 1], axis=1) for c in range(3)], axis=1)
+    even = ((pos[:, 1] - pos[:, 0]) % 3 == 1) & ((pos[:, 2] - pos[:, 1]) % 3 == 1)
+    assert np.array_equal(even, (fl & 2) == 0)
+    assert restart.mean() <= max_restart_frac, restart.mean()
+    return restart.mean()
+
+
+def test_strips_welded_torus():
+    v, f = configs.torus(0.7, 0.3, 48, 24)
+    _check(v, f, 0.05)
+
+
+def test_strips_shuffled_soup_welds_by_position():
+    v, f = configs.soup(*configs.torus(0.7, 0.3, 40, 30), seed=3)
+    assert len(v) == 3 * len(f)  # private vertices: only positions are shared
+    _check(v, f, 0.08)
+
+
+def test_strips_degenerate_and_open_meshes():
+    v, f = configs.icosphere(2)
+    f = np.concatenate([f[:50], [[0, 0, 1], [2, 3, 3]], f[60:]])  # open + degenerate faces
+    _check(v, f, 0.5)
+    rng = np.random.default_rng(0)
+    v = rng.normal(size=(30, 3))
+    f = rng.integers(0, 30, size=(80, 3))
+    _check(v, f, 1.0)
+
+
+def test_strip_order_rejects_bad_indices():
+    from paper_2407_11272_b200 import _lib as L
+    try:
+        lib = L.load_library()
+    except L.WindvoxCudaUnavailable:
+        pytest.skip("library not built")
+    v = np.zeros((3, 3))
+    f = np.array([[0, 1, 3]], dtype=np.int64)
+    out = [np.empty(1, np.int64), np.empty(3, np.int64), np.empty(1, np.uint8)]
+    rc = lib.wv_strip_order(v.ctypes.data, 3, f.ctypes.data, 1, *(a.ctypes.data for a in out))
+    assert rc == L.WV_ERR_ARG if hasattr(L, "WV_ERR_ARG") else rc == 1

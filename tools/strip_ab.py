@@ -1,0 +1,55 @@
+"""A/B of the exact f32 forward: face-ordered vs strip-ordered records on a
+BASELINE configuration's full lattice (CUDA-event timing, after warm-up).
+
+    python tools/strip_ab.py [--config c3] [--reps 3]
+"""
+
+import argparse
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    import time
+    import torch
+    from paper_2407_11272_b200 import configs, device, _lib as L
+    w = configs.make(args.config)
+    grid = (w.lo, w.hi, w.res)
+    dm = device.DeviceMesh.from_numpy(w.vertices, w.faces)
+    t0 = time.perf_counter()
+    dm.strip_setup()
+    host = time.perf_counter() - t0
+    res = {}
+    outs = {}
+    for strip in (False, True, False, True):
+        v, f = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW, strip=strip)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.reps):
+            dm.invalidate()  # include the re-pack, as a step does
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            v, f = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW,
+                                  strip=strip)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        res.setdefault(strip, []).append(min(ts))
+        outs[strip] = (v.double(), f)
+    d = (outs[True][0] - outs[False][0]).abs()
+    ok = outs[True][1] == 0
+    print({"config": args.config, "face_order_ms": res[False], "strip_ms": res[True],
+           "speedup": min(res[False]) / min(res[True]), "strip_host_s": host,
+           "max_abs_diff": float(d[ok].max()),
+           "flag_mismatch": int((outs[True][1] != outs[False][1]).sum())})
+
+
+if __name__ == "__main__":
+    main()
