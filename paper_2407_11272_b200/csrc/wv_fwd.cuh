@@ -16,6 +16,8 @@
 //    (Pol::row, once per face) -- the per-pair work drops by ~1/3.
 #pragma once
 
+#include <type_traits>
+
 #include "wv_f32x2.cuh"
 #include "wv_kernels.h"
 
@@ -79,7 +81,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   }
   typename Pol::Ctx ctx = Pol::make_ctx(eps);
   uint32_t hits = 0;
-  typename Pol::Carry carry[PP];  // strip policies: corner distances of the previous face
+  typename Pol::Slot slot[3][PP];  // strip policies: corner distances (ring of 3 slots)
 
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int64_t it = t - t_begin;
@@ -92,9 +94,9 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) tacc[pp] = f2(0.0f, 0.0f);
 
-#pragma unroll 1
-    for (int f = 0; f < cnt; ++f) {
-      const Rec R = tile[f];
+    // one face against the thread's P points (rot: strip slot rotation)
+    auto do_face = [&](const Rec& R, auto rot) {
+      constexpr int kRot = decltype(rot)::value;
       uint32_t rare;
       if constexpr (kRows) {
         const typename Pol::Row w = Pol::row(R, rx, ry);
@@ -105,8 +107,9 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
           const bool restart = __float_as_int(R.v1.w) < 0;  // uniform per face
 #pragma unroll
           for (int g0 = 0; g0 < PP; g0 += 4)
-            rare |= Pol::template face_strip<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, restart,
-                                                                 carry + g0, tacc + g0)
+            rare |= Pol::template face_strip<(PP < 4 ? PP : 4)>(
+                        R, w, qz + g0, ctx, restart, slot[kRot] + g0, slot[(kRot + 1) % 3] + g0,
+                        slot[(kRot + 2) % 3] + g0, tacc + g0)
                     << (2 * g0);
         } else {
 #pragma unroll
@@ -137,6 +140,22 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
           }
         }
       }
+    };
+    using R0 = std::integral_constant<int, 0>;
+    if constexpr (Pol::kStrip && kRows) {
+      // strip records: unrolled by 3 so the slot rotation is static
+      int f = 0;
+#pragma unroll 1
+      for (; f + 3 <= cnt; f += 3) {
+        do_face(tile[f], R0{});
+        do_face(tile[f + 1], std::integral_constant<int, 1>{});
+        do_face(tile[f + 2], std::integral_constant<int, 2>{});
+      }
+      if (f < cnt) do_face(tile[f], R0{});
+      if (f + 1 < cnt) do_face(tile[f + 1], std::integral_constant<int, 1>{});
+    } else {
+#pragma unroll 1
+      for (int f = 0; f < cnt; ++f) do_face(tile[f], R0{});
     }
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {

@@ -78,7 +78,7 @@ struct ExactPol {
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (2.0 * kPi);
   static constexpr bool kStrip = false;
-  struct Carry {};
+  struct Slot {};
   // eps2: squared vertex-hit radius, eps (f32) inflated by 1% so that every
   // pair within the reference's f64 eps of a vertex (winding.py:65-67) leaves
   // the common path and is decided exactly by exact_rare
@@ -302,50 +302,92 @@ struct ExactPol {
 // operations on the same coordinates), so a face costs 1 square root + 1
 // reciprocal per pair instead of 3 + 1 -- the MUFU pipe bounds this kernel.
 // Records restart (recompute A and B) at strip starts and at every tile.
+#ifndef WV_STRIP_P
+#define WV_STRIP_P 8
+#endif
+#ifndef WV_STRIP_MINB
+#define WV_STRIP_MINB 4
+#endif
 struct ExactStripPol : ExactPol {
   static constexpr bool kStrip = true;
-  struct Carry {
-    F2 b2, b, c2, c;
+  static constexpr int kP = WV_STRIP_P;
+  static constexpr int kMinBlocksRow = WV_STRIP_MINB;
+  // corner-distance slots per point pair: d = |v - q|, s = d + the next
+  // slot's d.  Face k of a strip reads A, B from slots (k, k+1) mod 3 (and
+  // s_A = |a| + |b| from the previous face) and writes C's distance to slot
+  // (k+2) mod 3, so with the face loop unrolled by 3 nothing is moved.
+  struct Slot {
+    F2 d, s;
   };
+  // beta without the three dot products (no squared distances needed):
+  //   a.b = (|a|^2 + |b|^2)/2 - h_ab  gives
+  //   2 beta = (|a|+|b|)(|b|+|c|)(|c|+|a|) - 2 (|a| h_bc + |b| h_ca + |c| h_ab)
+  //          = X - 2L                       (8 lane-ops with |a|+|b| carried)
+  // Conditioning: 2 beta > X/8 (X >= 8 |a||b||c|, so this implies tail2's
+  // beta > |a||b||c|/2), tested as L' > -X on the ALU with L' = 16/7 (-L);
+  // angle: t^2 < 1/64 (max tree); no corner within eps (per-face scalar).
+  // Lanes that fail take tail2 (recomputed from squared distances) or the
+  // fp64 path.
   template <int PP>
   __device__ __forceinline__ static uint32_t face_strip(const Rec& R, const Row& w, const F2* qz,
-                                                        const Ctx& ctx, bool restart, Carry* cr,
-                                                        F2* tacc) {
-    F2 alpha[PP], la2[PP], lb2[PP], lc2[PP], la[PP], lb[PP], lc[PP];
-#pragma unroll
-    for (int pp = 0; pp < PP; ++pp) {
-      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), cz = sub2(f2s(R.v2.z), qz[pp]);
-      alpha[pp] = fma2(f2s(R.n.z), az, f2s(w.alpha));
-      lc2[pp] = fma2(cz, cz, f2s(w.c2));
-      lc[pp] = sqrt2(lc2[pp]);
-    }
+                                                        const Ctx& ctx, bool restart, Slot* sA,
+                                                        Slot* sB, Slot* sC, F2* tacc) {
     if (restart) {
 #pragma unroll
       for (int pp = 0; pp < PP; ++pp) {
         const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
-        la2[pp] = fma2(az, az, f2s(w.a2));
-        lb2[pp] = fma2(bz, bz, f2s(w.b2));
-        la[pp] = sqrt2(la2[pp]);
-        lb[pp] = sqrt2(lb2[pp]);
-      }
-    } else {
-#pragma unroll
-      for (int pp = 0; pp < PP; ++pp) {
-        la2[pp] = cr[pp].b2;
-        la[pp] = cr[pp].b;
-        lb2[pp] = cr[pp].c2;
-        lb[pp] = cr[pp].c;
+        sA[pp].d = sqrt2(fma2(az, az, f2s(w.a2)));
+        sB[pp].d = sqrt2(fma2(bz, bz, f2s(w.b2)));
+        sA[pp].s = add2(sA[pp].d, sB[pp].d);
       }
     }
+    constexpr float kL = -16.0f / 7.0f;
+    const float kab = kL * fabsf(R.v1.w), kbc = kL * fabsf(R.v2.w), kca = kL * R.n.w;
+    const float nz2 = 2.0f * R.n.z, wal2 = 2.0f * w.alpha;
+    F2 tq[PP], tp[PP];
+    float ms = 0.0f;
+    bool cond = true;
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
-      cr[pp].b2 = lb2[pp];
-      cr[pp].b = lb[pp];
-      cr[pp].c2 = lc2[pp];
-      cr[pp].c = lc[pp];
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), cz = sub2(f2s(R.v2.z), qz[pp]);
+      const F2 alpha2 = fma2(f2s(nz2), az, f2s(wal2));
+      const F2 lc = sqrt2(fma2(cz, cz, f2s(w.c2)));
+      const F2 la = sA[pp].d, lb = sB[pp].d;
+      const F2 sbc = add2(lb, lc), sca = add2(lc, la);
+      sC[pp].d = lc;
+      sB[pp].s = sbc;
+      const F2 x = mul2(mul2(sA[pp].s, sbc), sca);
+      const F2 lp = fma2(lc, f2s(kab), fma2(lb, f2s(kca), mul2(la, f2s(kbc))));  // 16/7 (-L)
+      const F2 beta2 = fma2(lp, f2s(0.875f), x);  // X - 2L
+      float x0, x1, l0, l1;
+      split(x, x0, x1);
+      split(lp, l0, l1);
+      cond = cond && (l0 > -x0) && (l1 > -x1);
+      const F2 tt = mul2(alpha2, rcp2(beta2));
+      const F2 s = mul2(tt, tt);
+      float s0, s1;
+      split(s, s0, s1);
+      ms = fmaxf(ms, fmaxf(s0, s1));
+      tq[pp] = tt;
+      tp[pp] = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
+                    f2s(1.0f));
     }
     const bool near = fminf(w.a2, fminf(w.b2, w.c2)) < ctx.eps2;
-    return finish_len<PP>(R, alpha, la2, lb2, lc2, la, lb, lc, ctx, near, tacc);
+    if (ms < 1.0f / 64.0f && cond && !near) {
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
+      return 0u;
+    }
+    uint32_t rare = 0;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
+      const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
+      const F2 alpha = fma2(f2s(R.n.z), az, f2s(w.alpha));
+      rare |= tail2(R, alpha, fma2(az, az, f2s(w.a2)), fma2(bz, bz, f2s(w.b2)),
+                    fma2(cz, cz, f2s(w.c2)), ctx, tacc[pp]) << (2 * pp);
+    }
+    return rare;
   }
   // the fp64 path needs the face's own orientation (triple product): a
   // reflected window (v2.w < 0) swaps B and C back
@@ -367,7 +409,7 @@ struct SoftPol {
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (8.0 * kPi);
   static constexpr bool kStrip = false;
-  struct Carry {};
+  struct Slot {};
   struct Ctx {
     float eps2;
   };

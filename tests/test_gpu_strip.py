@@ -14,6 +14,34 @@ from test_gpu_fuzz import random_case, surface_distance
 pytestmark = pytest.mark.gpu
 
 
+def _dist_to_faces(p, tri):
+    """Distance from one point to a set of triangles (vectorised over faces)."""
+    a, b, c = tri[:, 0], tri[:, 1], tri[:, 2]
+    best = np.minimum(np.minimum(np.linalg.norm(p - a, axis=1), np.linalg.norm(p - b, axis=1)),
+                      np.linalg.norm(p - c, axis=1))
+    for p0, p1 in ((a, b), (b, c), (c, a)):
+        e = p1 - p0
+        ee = np.maximum((e * e).sum(1), 1e-300)
+        t = np.clip(((p - p0) * e).sum(1) / ee, 0.0, 1.0)
+        best = np.minimum(best, np.linalg.norm(p - (p0 + t[:, None] * e), axis=1))
+    n = np.cross(b - a, c - a)
+    nn = np.sqrt((n * n).sum(1))
+    ok = nn > 0
+    nh = n[ok] / nn[ok, None]
+    dist = ((p - a[ok]) * nh).sum(1)
+    proj = p - dist[:, None] * nh
+    ab, ac, v2 = b[ok] - a[ok], c[ok] - a[ok], proj - a[ok]
+    d00, d01, d11 = (ab * ab).sum(1), (ab * ac).sum(1), (ac * ac).sum(1)
+    d20, d21 = (v2 * ab).sum(1), (v2 * ac).sum(1)
+    den = d00 * d11 - d01 * d01
+    bv = (d11 * d20 - d01 * d21) / den
+    bw = (d00 * d21 - d01 * d20) / den
+    inside = (bv >= 0) & (bw >= 0) & (bv + bw <= 1)
+    if inside.any():
+        best = min(best.min(), np.abs(dist[inside]).min())
+    return float(np.min(best))
+
+
 def _both(dm, grid, **kw):
     from paper_2407_11272_b200 import _lib as L, device
     a, fa = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW, strip=False, **kw)
@@ -89,3 +117,32 @@ def test_strip_broken_welds(cuda_device):
     a, fa, b, fb = _both(dm, grid)
     assert np.array_equal(fa, fb)
     assert np.abs(a - b)[~fa].max() <= 2e-6
+
+
+def test_strip_c3_disagreements_are_within_tolerance(cuda_device):
+    """C3 (the headline soup, full 256^3 lattice): wherever the strip and
+    face-ordered kernels differ by more than 1e-6, both must be within the
+    north_star 1e-5 of the f64 oracle at that node (differences come from
+    fp32 rounding near the surface: the two orders evaluate alpha from
+    different corners)."""
+    from paper_2407_11272_b200 import _lib as L, configs, device
+    w = configs.make("c3")
+    grid = (w.lo, w.hi, w.res)
+    dm = device.DeviceMesh.from_numpy(w.vertices, w.faces)
+    a, fa, b, fb = _both(dm, grid)
+    assert np.array_equal(fa, fb)
+    d = np.abs(a - b)
+    d[fa] = 0.0
+    idx = np.argsort(d)[::-1][:64]
+    idx = idx[d[idx] > 1e-6]
+    print("strip vs face order: max", d.max(), "nodes > 1e-6:", int((d > 1e-6).sum()))
+    if len(idx) == 0:
+        return
+    p32 = orc.node_coordinates(*grid)[idx].astype(np.float32).astype(np.float64)
+    ref, rf = orc.winding_number_batch(w.vertices, w.faces, p32, mode="exact")
+    ea, eb = np.abs(a[idx] - ref)[~rf], np.abs(b[idx] - ref)[~rf]
+    print("vs oracle: face order", ea.max(), "strip", eb.max())
+    dist = np.array([_dist_to_faces(p, w.vertices[w.faces]) for p in p32])
+    print(np.stack([d[idx], a[idx] - ref, b[idx] - ref, ref, dist], axis=1)[:16])
+    far = dist[~rf] > 1e-4  # as the fuzz sweep: closer, f32 input rounding dominates
+    assert eb[far].max(initial=0) <= 1e-5 and ea[far].max(initial=0) <= 1e-5
