@@ -106,8 +106,8 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         if constexpr (Pol::kStrip) {
           const bool restart = __float_as_int(R.v1.w) < 0;  // uniform per face
 #pragma unroll
-          for (int g0 = 0; g0 < PP; g0 += 4)
-            rare |= Pol::template face_strip<(PP < 4 ? PP : 4)>(
+          for (int g0 = 0; g0 < PP; g0 += Pol::kGroup)
+            rare |= Pol::template face_strip<(PP < Pol::kGroup ? PP : Pol::kGroup)>(
                         R, w, qz + g0, ctx, restart, slot[kRot] + g0, slot[(kRot + 1) % 3] + g0,
                         slot[(kRot + 2) % 3] + g0, tacc + g0)
                     << (2 * g0);

@@ -306,12 +306,16 @@ struct ExactPol {
 #define WV_STRIP_P 8
 #endif
 #ifndef WV_STRIP_MINB
-#define WV_STRIP_MINB 4
+#define WV_STRIP_MINB 3  // 160 registers, no spills: 1% faster than 4 blocks with spills
 #endif
 struct ExactStripPol : ExactPol {
   static constexpr bool kStrip = true;
   static constexpr int kP = WV_STRIP_P;
   static constexpr int kMinBlocksRow = WV_STRIP_MINB;
+#ifndef WV_STRIP_GROUP
+#define WV_STRIP_GROUP 4
+#endif
+  static constexpr int kGroup = WV_STRIP_GROUP;  // point pairs per common-path decision
   // corner-distance slots per point pair: d = |v - q|, s = d + the next
   // slot's d.  Face k of a strip reads A, B from slots (k, k+1) mod 3 (and
   // s_A = |a| + |b| from the previous face) and writes C's distance to slot
