@@ -47,9 +47,13 @@ EXACT_BWD_FLOPS = 170
 # face-wise closed form, so they execute FEWER FLOPs than the pinned
 # algorithmic counts above: the algorithmic-FLOP rate can exceed the FP32
 # peak, and the executed-work fractions below are the pipe utilisation.
-EXACT_FWD_EXEC_FLOPS = 42.25   # fwd_f32_kernel<ExactPol,RowSrc> all-common fast path, 4 MUFU
+# strip-ordered forward (the lattice default from 2M nodes): measured from the
+# ncu executed-instruction mix on c3s (tools/sass_exec_mix.py; 9.6% strip
+# restarts there, 4.3% on C3); the face-ordered kernel executed 42.25 / 4 MUFU
+EXACT_FWD_EXEC_FLOPS = 29.25   # fwd_f32_kernel<ExactStripPol,RowSrc>
+EXACT_FWD_FACE_ORDER_EXEC_FLOPS = 42.25  # fwd_f32_kernel<ExactPol,RowSrc>, all-common fast path
 EXACT_BWD_EXEC_FLOPS = 60.5    # bwd_f32_kernel<ExactEdgeBwd,RowSrc> unit-weight loop, 4 MUFU
-EXACT_FWD_MUFU = 4
+EXACT_FWD_MUFU = 2.2  # 1 sqrt (+2 per strip restart) + 1 rcp; face-ordered: 4
 SOFT_STEP_FLOPS = 15 + 72  # soft forward + soft backward, pinned
 EXACT_BWD_MUFU = 4
 
@@ -408,7 +412,7 @@ def run_ours(args):
                              f"exact f64 fwd (bit-exact C port of _kernels.exact_batch) + exact "
                              f"f64 grad (closed-form oracle), {dt:.1f} s"}
         dom = ("exact_bwd (bwd_f32_kernel<ExactEdgeBwd,RowSrc>)", bwd_ms, bwd_tf) \
-            if bwd_ms >= fwd_ms else ("exact_fwd (fwd_f32_kernel<ExactPol,RowSrc>)", fwd_ms,
+            if bwd_ms >= fwd_ms else ("exact_fwd (fwd_f32_kernel<ExactStripPol,RowSrc>)", fwd_ms,
                                       fwd_tf)
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
         step_tf = (EXACT_FWD_FLOPS * cnt * F + EXACT_BWD_FLOPS * cnt * active) \
@@ -658,7 +662,7 @@ def run_c5(args):
                        "parallelism": f"i-slabs x{world}"},
             "voxelize_ms": ms_step,
             "roofline": dict(rf, bound="xu+fp32", peak=peak, unit="TFLOP/s",
-                             kernel="exact_fwd (fwd_f32_kernel<ExactPol,RowSrc>)",
+                             kernel="exact_fwd (fwd_f32_kernel<ExactStripPol,RowSrc>)",
                              peak_source=peak_src, traffic=None),
             "clocks": clocks,
         }
