@@ -177,6 +177,22 @@ int wv_exact_bwd_points_f32(const void *packed, int64_t n_faces, const float *po
                             int64_t count, const float *coefs, double coef_scale,
                             double *face_grad, void *workspace, size_t workspace_bytes,
                             void *stream);
+/* exact f32 over STRIP PAIRS (same gradients, fewer operations on lattice
+ * rows): the packed array is wv_pack_exact_grad's (kind
+ * WV_PACK_EXACTGRAD_F32) over 2P faces given in pair order -- faces 2i and
+ * 2i+1 with corners in strip-window order (A, B, C), (B', C', D), B' and C'
+ * at B's and C's positions (a pair whose positions differ is evaluated as two
+ * separate faces), edge weights in window order (negated for a window that
+ * reflects the face).  face_grad rows follow that order.  n_faces even. */
+size_t wv_exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t count);
+int wv_exact_pair_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                               int64_t count, const float *coefs, double coef_scale,
+                               double *face_grad, void *workspace, size_t workspace_bytes,
+                               void *stream);
+int wv_exact_pair_bwd_points_f32(const void *packed, int64_t n_faces, const float *points,
+                                 int64_t count, const float *coefs, double coef_scale,
+                                 double *face_grad, void *workspace, size_t workspace_bytes,
+                                 void *stream);
 int wv_soft_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float *coefs, double coef_scale,
                          double *face_grad, void *workspace, size_t workspace_bytes,

@@ -43,6 +43,8 @@ EXPORTED = (
     "wv_fwd_workspace_bytes_batch", "wv_fwd_grid_f32_batch", "wv_bwd_workspace_bytes_batch",
     "wv_bwd_grid_f32_batch", "wv_strip_order", "wv_pack_exact_strip",
     "wv_exact_strip_fwd_grid_f32", "wv_exact_strip_fwd_points_f32",
+    "wv_exact_pair_bwd_workspace_bytes", "wv_exact_pair_bwd_grid_f32",
+    "wv_exact_pair_bwd_points_f32",
 )
 
 
@@ -118,6 +120,9 @@ def _declare(lib):
         "wv_pack_exact_strip": ([P, I, I64, P, I, I64, P, P, P, P, P], I),
         "wv_exact_strip_fwd_grid_f32": (fwd32_grid, I),
         "wv_exact_strip_fwd_points_f32": (fwd32_pts, I),
+        "wv_exact_pair_bwd_workspace_bytes": ([I64, I64], SZ),
+        "wv_exact_pair_bwd_grid_f32": (bwd_grid, I),
+        "wv_exact_pair_bwd_points_f32": (bwd_pts, I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -88,6 +88,8 @@ struct ExactEdgeBwd {
   static constexpr int kFaces = 1;  // faces per thread (per record)
   static constexpr int kOut = 9;
   static constexpr bool kScaled = true;
+  static constexpr bool kPairRuns = false;
+  static constexpr int kRowStep = wv::kRowStep;
   __device__ __forceinline__ static void scale(Rec& R, float s) {
     R.a.x *= s; R.a.y *= s; R.a.z *= s;
     R.b.x *= s; R.b.y *= s; R.b.z *= s;
@@ -277,7 +279,8 @@ struct ExactEdgeBwd {
     *mr = add2(*mr, ru[0]);
   }
   __device__ __forceinline__ static void rare_pair(const Rec& R, float qx, float qy, float qz,
-                                                   float c, double (*acc)[kBwdThreads]) {
+                                                   float c, double (*acc)[kBwdThreads],
+                                                   uint32_t = 3u) {
     exact_pair_f64(R, qx, qy, qz, c, acc);
   }
   // a run [j, e) holding an ill-conditioned pair, redone: fp32 sums without
@@ -297,6 +300,9 @@ struct ExactEdgeBwd {
   }
   // sum_q m s for every (edge, corner) from the run's sums, into the face's
   // fp64 accumulators (acc[j][thread], j = corner * 3 + axis)
+  // kW: the sums were taken without edge weights (strip pairs); weight them
+  // here (sums 0,1,4,5: edge 01; 6-9: edge 12; 2,3,10,11: edge 20)
+  template <bool kW = false>
   __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
                                                    double (*acc)[kBwdThreads]) {
     double S[kRowAcc];
@@ -305,6 +311,10 @@ struct ExactEdgeBwd {
       float lo, hi;
       split(z[j], lo, hi);
       S[j] = (double)lo + (double)hi;
+      if constexpr (kW) {
+        const int e = (j == 0 || j == 1 || j == 4 || j == 5) ? 0 : (j >= 6 && j <= 9) ? 1 : 2;
+        S[j] *= (double)(e == 0 ? R.a.w : e == 1 ? R.b.w : R.c.w);
+      }
     }
     const double e01x = (double)(R.b.x - R.a.x), e01y = (double)(R.b.y - R.a.y);
     const double e12x = (double)(R.c.x - R.b.x), e12y = (double)(R.c.y - R.b.y);
@@ -333,6 +343,8 @@ struct SoftBwd {
   static constexpr int kFaces = 1;
   static constexpr int kOut = 9;
   static constexpr bool kScaled = false;
+  static constexpr bool kPairRuns = false;
+  static constexpr int kRowStep = wv::kRowStep;
   __device__ __forceinline__ static void scale(Rec&, float) {}
   static constexpr int kMinBlocks = kBwdMinBlocks;
   static constexpr double kCoefScale = 1.0 / (8.0 * kPi);
@@ -410,7 +422,7 @@ struct SoftBwd {
   // N point pairs; the r < eps test is done once on the minimum r^2 of the
   // step (nearly always passes), so the common path has no per-lane selects
   __device__ __forceinline__ static void rare_pair(const Rec&, float, float, float, float,
-                                                   double (*)[kBwdThreads]) {}
+                                                   double (*)[kBwdThreads], uint32_t = 0u) {}
   template <bool kUnit, class W>
   __device__ __forceinline__ static void redo_run(const Rec&, const W&, const float4*, int, int,
                                                   float, F2*, double (*)[kBwdThreads]) {}
@@ -500,6 +512,7 @@ struct SoftBwdPair {
   static constexpr int kOut = 18;
   static constexpr int kRowStep = 4;
   static constexpr bool kScaled = false;
+  static constexpr bool kPairRuns = false;
   __device__ __forceinline__ static void scale(Rec&, float) {}
   static constexpr int kMinBlocks = 4;  // two faces' state: up to 128 registers
   static constexpr double kCoefScale = One::kCoefScale;
@@ -514,7 +527,7 @@ struct SoftBwdPair {
     return 0u;
   }
   __device__ __forceinline__ static void rare_pair(const Rec&, float, float, float, float,
-                                                   double (*)[kBwdThreads]) {}
+                                                   double (*)[kBwdThreads], uint32_t = 0u) {}
   template <bool kUnit, class W>
   __device__ __forceinline__ static void redo_run(const Rec&, const W&, const float4*, int, int,
                                                   float, F2*, double (*)[kBwdThreads]) {}
@@ -584,6 +597,191 @@ struct SoftBwdPair {
   }
 };
 
+// Exact backward over STRIP PAIRS: a record holds two faces F1 = (A, B, C)
+// and F2 = (B', C', D) whose corners are in strip-window order (see
+// wv_strip.cu), with B', C' at the positions of B, C (welded by position).
+// Per point the pair needs 4 corner distances instead of 6, 5 edge
+// denominators instead of 6, and the shared edge BC's four run sums serve
+// both faces (the Biot-Savart term of an edge depends only on its end
+// points): ~32 lane-ops and 3 MUFU per face and pair instead of ~38 and 4.
+// The run sums are taken WITHOUT edge weights, which are applied once per run
+// in the fp64 flush (F1's BC weight and F2's may differ).  A record whose
+// positions do not match bitwise (welds broken by a morph step) evaluates
+// its two faces one after the other with the single-face row code.
+struct ExactPairRec {
+  ExactGradRecF32 f[2];
+};
+struct ExactEdgeBwdPair {
+  using One = ExactEdgeBwd;
+  using Rec = ExactPairRec;
+  static constexpr int kFaces = 2;
+  static constexpr int kOut = 18;
+  static constexpr bool kScaled = true;
+  static constexpr bool kPairRuns = true;
+#ifndef WV_PAIR_STEP
+#define WV_PAIR_STEP 2
+#endif
+  static constexpr int kRowStep = WV_PAIR_STEP;
+  __device__ __forceinline__ static void scale(Rec& R, float s) {
+    One::scale(R.f[0], s);
+    One::scale(R.f[1], s);
+  }
+  static constexpr int kMinBlocks = 4;
+  static constexpr double kCoefScale = One::kCoefScale;
+  static constexpr int kAcc = 18;
+  static constexpr int kRowAcc = 20;
+  __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
+  // generic point sources: the two faces independently (weighted)
+  template <bool kUnit>
+  __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
+                                                   float eps2, F2* g) {
+    const uint32_t i0 = One::pair2<false>(R.f[0], qx, qy, qz, coef, eps2, g);
+    const uint32_t i1 = One::pair2<false>(R.f[1], qx, qy, qz, coef, eps2, g + One::kAcc);
+    return (i0 ? 1u : 0u) | (i1 ? 2u : 0u);
+  }
+  __device__ __forceinline__ static void rare_pair(const Rec& R, float qx, float qy, float qz,
+                                                   float c, double (*acc)[kBwdThreads],
+                                                   uint32_t ill) {
+    if (ill & 1u) exact_pair_f64(R.f[0], qx, qy, qz, c, acc);
+    if (ill & 2u) exact_pair_f64(R.f[1], qx, qy, qz, c, acc + One::kAcc);
+  }
+  struct Row {
+    float a2, b2, c2, d2;  // x/y parts of |corner - q|^2 (A, B, C, D)
+    float qx, qy;
+    bool paired;
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    const ExactGradRecF32& F = R.f[0];
+    const ExactGradRecF32& G = R.f[1];
+    Row w;
+    const float ax = F.a.x - qx, ay = F.a.y - qy, bx = F.b.x - qx, by = F.b.y - qy;
+    const float cx = F.c.x - qx, cy = F.c.y - qy, dx = G.c.x - qx, dy = G.c.y - qy;
+    w.a2 = fmaf(ay, ay, ax * ax);
+    w.b2 = fmaf(by, by, bx * bx);
+    w.c2 = fmaf(cy, cy, cx * cx);
+    w.d2 = fmaf(dy, dy, dx * dx);
+    w.qx = qx;
+    w.qy = qy;
+    w.paired = G.a.x == F.b.x && G.a.y == F.b.y && G.a.z == F.b.z && G.b.x == F.c.x &&
+               G.b.y == F.c.y && G.b.z == F.c.z;
+    return w;
+  }
+  // sums 0-11: F1 in ExactEdgeBwd's layout; 12-19: F2's own sums 2,3,6-11
+  // (its sums 0,1,4,5 are F1's 6,7,8,9: the shared edge)
+  template <bool kUnit, int N>
+  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
+                                                  float, F2* z, F2* mr) {
+    if (!w.paired) return;  // run_end evaluates the faces one by one
+    const ExactGradRecF32& F = R.f[0];
+    const ExactGradRecF32& G = R.f[1];
+    const float u1p = F.u.x * F.u.y * F.u.z, u2p = G.u.y * G.u.z;
+    F2 ru[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      const F2 qz = f2(zc[u].x, zc[u].y), coef = f2(zc[u].z, zc[u].w);
+      const F2 az = sub2(f2s(F.a.z), qz), bz = sub2(f2s(F.b.z), qz);
+      const F2 cz = sub2(f2s(F.c.z), qz), dz = sub2(f2s(G.c.z), qz);
+      const F2 a2 = fma2(az, az, f2s(w.a2)), b2 = fma2(bz, bz, f2s(w.b2));
+      const F2 c2 = fma2(cz, cz, f2s(w.c2)), d2 = fma2(dz, dz, f2s(w.d2));
+      const F2 ia = rsqrt2(a2), ib = rsqrt2(b2), ic = rsqrt2(c2), id = rsqrt2(d2);
+      const F2 lb = mul2(b2, ib), lc = mul2(c2, ic);
+      const F2 sab = fma2(a2, ia, lb), sbc = add2(lb, lc), sca = fma2(a2, ia, lc);
+      const F2 scd = fma2(d2, id, lc), sdb = fma2(d2, id, lb);
+      const F2 dab = fma2(sab, sab, f2s(-F.u.x)), dbc = fma2(sbc, sbc, f2s(-F.u.y));
+      const F2 dca = fma2(sca, sca, f2s(-F.u.z));
+      const F2 dcd = fma2(scd, scd, f2s(-G.u.y)), ddb = fma2(sdb, sdb, f2s(-G.u.z));
+      const F2 p1 = mul2(dbc, dca), rr1 = rcp2(mul2(dab, p1));
+      const F2 rr2 = rcp2(mul2(dcd, ddb));
+      ru[u] = fma2(rr2, f2s(u2p), mul2(rr1, f2s(u1p)));  // both faces' ratio products
+      const F2 cr1 = mul2(coef, rr1), q0 = mul2(cr1, dab);
+      const F2 tab = mul2(cr1, p1), tbc = mul2(q0, dca), tca = mul2(q0, dbc);
+      const F2 cr2 = mul2(coef, rr2);
+      const F2 tcd = mul2(cr2, ddb), tdb = mul2(cr2, dcd);
+      const F2 uab = mul2(tab, az), ubc = mul2(tbc, bz), uca = mul2(tca, cz);
+      const F2 ucd = mul2(tcd, cz), udb = mul2(tdb, dz);
+      z[0] = fma2(tab, ia, z[0]);
+      z[1] = fma2(uab, ia, z[1]);
+      z[2] = fma2(tca, ia, z[2]);
+      z[3] = fma2(uca, ia, z[3]);
+      z[4] = fma2(tab, ib, z[4]);
+      z[5] = fma2(uab, ib, z[5]);
+      z[6] = fma2(tbc, ib, z[6]);
+      z[7] = fma2(ubc, ib, z[7]);
+      z[8] = fma2(tbc, ic, z[8]);
+      z[9] = fma2(ubc, ic, z[9]);
+      z[10] = fma2(tca, ic, z[10]);
+      z[11] = fma2(uca, ic, z[11]);
+      z[12] = fma2(tdb, ib, z[12]);  // F2 edge D->B at its corner B'
+      z[13] = fma2(udb, ib, z[13]);
+      z[14] = fma2(tcd, ic, z[14]);  // F2 edge C->D at its corner C'
+      z[15] = fma2(ucd, ic, z[15]);
+      z[16] = fma2(tcd, id, z[16]);  // edge C->D at D
+      z[17] = fma2(ucd, id, z[17]);
+      z[18] = fma2(tdb, id, z[18]);  // edge D->B at D
+      z[19] = fma2(udb, id, z[19]);
+    }
+#pragma unroll
+    for (int h = 1; h < N; h *= 2)
+#pragma unroll
+      for (int u = 0; u + h < N; u += 2 * h) ru[u] = add2(ru[u], ru[u + h]);
+    *mr = add2(*mr, ru[0]);
+  }
+  // one face over a run with the single-face row code (broken welds), flushed
+  __device__ __noinline__ static void single_run(const ExactGradRecF32& Rk, float qx, float qy,
+                                                 const float4* zcs, int j, int e, float eps2,
+                                                 double (*acc)[kBwdThreads]) {
+    const One::Row rk = One::row(Rk, qx, qy);
+    F2 z[One::kRowAcc];
+    for (int i = 0; i < One::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
+    F2 mr = f2(0.0f, 0.0f);
+    const int j0 = j;
+    for (; j < e; ++j) {
+      const float4 zc = zcs[j];
+      if (!(zc.z == 0.0f && zc.w == 0.0f)) One::step_row<true, 1>(Rk, rk, &zc, eps2, z, &mr);
+    }
+    float m0, m1;
+    split(mr, m0, m1);
+    if (!(m0 + m1 < One::kIllRatio)) One::redo_run<true>(Rk, rk, zcs, j0, e, eps2, z, acc);
+    One::flush_row<true>(Rk, rk, z, acc);
+  }
+  __device__ __noinline__ static void redo_pair(const Rec& R, float qx, float qy,
+                                                const float4* zcs, int j0, int e, float eps2,
+                                                double (*acc)[kBwdThreads]) {
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      const One::Row rk = One::row(R.f[k], qx, qy);
+      F2 z[One::kRowAcc];
+      One::redo_run<true>(R.f[k], rk, zcs, j0, e, eps2, z, acc + k * One::kAcc);
+      One::flush_row<true>(R.f[k], rk, z, acc + k * One::kAcc);
+    }
+  }
+  // end of a row run [j0, e): flush the sums (or redo / evaluate per face)
+  template <bool kUnit>
+  __device__ __forceinline__ static void run_end(const Rec& R, const Row& w, const float4* zcs,
+                                                 int j0, int e, float eps2, const F2* z, F2 mr,
+                                                 double (*acc)[kBwdThreads]) {
+    if (!w.paired) {
+      single_run(R.f[0], w.qx, w.qy, zcs, j0, e, eps2, acc);
+      single_run(R.f[1], w.qx, w.qy, zcs, j0, e, eps2, acc + One::kAcc);
+      return;
+    }
+    float m0, m1;
+    split(mr, m0, m1);
+    if (!(m0 + m1 < One::kIllRatio)) {  // rare: an ill-conditioned pair in the run
+      redo_pair(R, w.qx, w.qy, zcs, j0, e, eps2, acc);
+      return;
+    }
+    One::flush_row<true>(R.f[0], One::row(R.f[0], w.qx, w.qy), z, acc);
+    const F2 z2[One::kRowAcc] = {z[6], z[7], z[12], z[13], z[8], z[9],
+                                 z[14], z[15], z[16], z[17], z[18], z[19]};
+    One::flush_row<true>(R.f[1], One::row(R.f[1], w.qx, w.qy), z2, acc + One::kAcc);
+  }
+  __device__ __forceinline__ static void finish(const Rec& R, const double* a, double* out) {
+    One::finish(R.f[0], a, out);
+    One::finish(R.f[1], a + One::kAcc, out + 9);
+  }
+};
+
 // Query points of a chunk, stored as packed PAIRS: xy[j] = {x_2j, x_2j+1,
 // y_2j, y_2j+1}, zc[j] = {z_2j, z_2j+1, coef_2j, coef_2j+1}; two LDS.128
 // deliver one point pair already in f32x2 register pairs.
@@ -604,8 +802,8 @@ __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const Poi
     const uint32_t ill = Pol::template pair2<kUnit>(R, f2(xy.x, xy.y), f2(xy.z, xy.w),
                                                     f2(zc.x, zc.y), f2(zc.z, zc.w), eps2, g);
     if (ill != 0u) {  // both lanes redone in fp64 (see ExactEdgeBwd::pair2)
-      Pol::rare_pair(R, xy.x, xy.z, zc.x, zc.z, acc);
-      Pol::rare_pair(R, xy.y, xy.w, zc.y, zc.w, acc);
+      Pol::rare_pair(R, xy.x, xy.z, zc.x, zc.z, acc, ill);
+      Pol::rare_pair(R, xy.y, xy.w, zc.y, zc.w, acc, ill);
     }
   }
 }
@@ -632,22 +830,22 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
     for (int i = 0; i < Pol::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
     const int e = j + run, j0 = j;
     F2 mr = f2(0.0f, 0.0f);  // summed ill-conditioning ratios of the run (exact only)
-    // kRowStep point pairs per step under one (warp-uniform)
+    // Pol::kRowStep point pairs per step under one (warp-uniform)
     // zero-coefficient test, so their dependency chains share a basic block
     // and interleave (a zero-coefficient pair next to a live one adds
     // 0 * finite: its point is parked far away)
 #pragma unroll 1
-    for (; j + kRowStep <= e; j += kRowStep) {
-      float4 zc[kRowStep];
+    for (; j + Pol::kRowStep <= e; j += Pol::kRowStep) {
+      float4 zc[Pol::kRowStep];
 #pragma unroll
-      for (int u = 0; u < kRowStep; ++u) zc[u] = ch.zc[j + u];
+      for (int u = 0; u < Pol::kRowStep; ++u) zc[u] = ch.zc[j + u];
       if (!dense) {
         bool any = false;
 #pragma unroll
-        for (int u = 0; u < kRowStep; ++u) any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
+        for (int u = 0; u < Pol::kRowStep; ++u) any |= zc[u].z != 0.0f || zc[u].w != 0.0f;
         if (!any) continue;
       }
-      Pol::template step_row<kUnit, kRowStep>(R, w, zc, eps2, z, &mr);
+      Pol::template step_row<kUnit, Pol::kRowStep>(R, w, zc, eps2, z, &mr);
     }
 #pragma unroll 1
     for (; j < e; ++j) {
@@ -655,11 +853,15 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
       if (!(zc.z == 0.0f && zc.w == 0.0f))  // warp-uniform (_kernels.py:182-184)
         Pol::template step_row<kUnit, 1>(R, w, &zc, eps2, z, &mr);
     }
-    float m0, m1;
-    split(mr, m0, m1);
-    if (!(m0 + m1 < ExactEdgeBwd::kIllRatio))  // rare: an ill-conditioned pair in the run
-      Pol::template redo_run<kUnit>(R, w, ch.zc, j0, e, eps2, z, acc);
-    Pol::flush_row(R, w, z, acc);
+    if constexpr (Pol::kPairRuns) {
+      Pol::template run_end<kUnit>(R, w, ch.zc, j0, e, eps2, z, mr, acc);
+    } else {
+      float m0, m1;
+      split(mr, m0, m1);
+      if (!(m0 + m1 < ExactEdgeBwd::kIllRatio))  // rare: an ill-conditioned pair in the run
+        Pol::template redo_run<kUnit>(R, w, ch.zc, j0, e, eps2, z, acc);
+      Pol::flush_row(R, w, z, acc);
+    }
     k = 0;
   }
 }
@@ -926,6 +1128,19 @@ size_t soft_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, i
     return BwdPlan::make(n_faces / 2, n_count, num_sms, SoftBwdPair::kMinBlocks, batch)
         .workspace(n_faces / 2, batch, SoftBwdPair::kOut);
   return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);
+}
+// strip pairs (ExactEdgeBwdPair): n_faces = 2 x records, faces in pair order
+int launch_exact_pair_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
+                              int64_t n_count, const float* coefs, double coef_scale,
+                              double* face_grad, void* ws, size_t ws_bytes, int num_sms,
+                              cudaStream_t stream) {
+  if (n_faces % 2 != 0) return kErrArg;
+  return launch_bwd<ExactEdgeBwdPair>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad,
+                                      ws, ws_bytes, num_sms, stream, Batch{});
+}
+size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+  return BwdPlan::make(n_faces / 2, n_count, num_sms, ExactEdgeBwdPair::kMinBlocks)
+      .workspace(n_faces / 2, 1, ExactEdgeBwdPair::kOut);
 }
 size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
   return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);

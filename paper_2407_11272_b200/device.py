@@ -120,6 +120,64 @@ def exact_edge_weights(faces: np.ndarray, dead: np.ndarray | None = None):
     return active, np.ascontiguousarray(w[active])
 
 
+def strip_pairs(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray):
+    """Pair consecutive faces of each strip (strip_order) for the exact
+    backward's pair kernel: returns (rows (2P,3) int64 vertex ids with
+    corners in window order, row weights (2P,3) f32, valid (2P,) bool).
+    Rows 2i, 2i+1 are a pair F1 = (A,B,C), F2 = (B',C',D); an unpaired face
+    gets a zero-weight partner (B,C,A) (valid False).  Window edge weights:
+    edge AB of a window is the face's directed edge between those corners,
+    negated when the window reflects the face's orientation."""
+    f = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
+    w = np.asarray(weights, dtype=np.float32).reshape(-1, 3)
+    A = len(f)
+    if A == 0:
+        return np.zeros((0, 3), np.int64), np.zeros((0, 3), np.float32), np.zeros(0, bool)
+    perm, win, fl = strip_order(vertices, f)
+    fo, wo = f[perm], w[perm]
+    pos = np.stack([np.argmax(fo == win[:, c:c + 1], axis=1) for c in range(3)], axis=1)
+    refl = (fl & 2) != 0
+    ar = np.arange(A)
+    ww = np.empty((A, 3), np.float32)
+    for e in range(3):  # window edge (e, e+1)
+        p0, p1 = pos[:, e], pos[:, (e + 1) % 3]
+        ww[:, e] = np.where(refl, -wo[ar, p1], wo[ar, p0])
+    restart = (fl & 1) != 0
+    start = np.maximum.accumulate(np.where(restart, ar, 0))
+    idx = ar - start                               # position within the strip
+    first = np.flatnonzero(idx % 2 == 0)           # pair heads
+    has2 = np.zeros(len(first), bool)
+    nxt = first + 1
+    ok = nxt < A
+    has2[ok] = ~restart[nxt[ok]]
+    P = len(first)
+    rows = np.empty((2 * P, 3), np.int64)
+    rw = np.zeros((2 * P, 3), np.float32)
+    valid = np.zeros(2 * P, bool)
+    rows[0::2] = win[first]
+    rw[0::2] = ww[first]
+    valid[0::2] = True
+    h = first[has2]
+    rows[1::2][has2] = win[h + 1]
+    rw[1::2][has2] = ww[h + 1]
+    valid[1::2][has2] = True
+    s = first[~has2]
+    rows[1::2][~has2] = win[s][:, [1, 2, 0]]       # zero-weight partner (B, C, A)
+    return rows, rw, valid
+
+
+def vertex_csr_rows(rows: np.ndarray, valid: np.ndarray, n_verts: int):
+    """vertex_csr over the valid rows only (slots keep their row indices)."""
+    flat = np.ascontiguousarray(rows, dtype=np.int64).reshape(-1)
+    ids = np.flatnonzero(np.repeat(np.asarray(valid, bool), 3))
+    vals = flat[ids]
+    slots = ids[np.argsort(vals, kind="stable")].astype(np.int64)
+    counts = np.bincount(vals, minlength=n_verts) if vals.size else np.zeros(n_verts, np.int64)
+    off = np.zeros(n_verts + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    return off, slots
+
+
 def dead_faces(vertices: np.ndarray, faces: np.ndarray) -> np.ndarray:
     """|N| == 0 in f64, the reference's degenerate-face test (winding.py:262-264)."""
     v = np.asarray(vertices, dtype=np.float64).reshape(-1, 3)
@@ -252,6 +310,50 @@ class DeviceMesh:
             self._exact_grad = eg
         return eg
 
+    def exact_pair_setup(self):
+        """Strip pairs of the active faces for the exact f32 backward
+        (wv_exact_pair_bwd_*): (faces (2P,3) int64 dev in pair order with
+        window-ordered corners, weights (2P,3) f32 dev, CSR over the real
+        rows).  Connectivity-only, built once from the setup-time positions
+        (a pair whose welds later break is evaluated face by face)."""
+        ps = getattr(self, "_exact_pair", None)
+        if ps is None:
+            vnp = getattr(self, "_verts_np", None)
+            if vnp is None:
+                vnp = self.vertices.detach().double().cpu().numpy()
+            fnp = self.faces_np()
+            active, w = exact_edge_weights(fnp, dead_faces(vnp, fnp))
+            rows_f, rows_w, valid = strip_pairs(vnp, fnp[active], w)
+            off, slots = vertex_csr_rows(rows_f, valid, self.num_vertices)
+            dev = self.vertices.device
+            ps = (torch.from_numpy(rows_f).to(dev), torch.from_numpy(rows_w).to(dev),
+                  (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev)))
+            self._exact_pair = ps
+        return ps
+
+    def packed_exact_pair(self) -> torch.Tensor:
+        key = "exact_pair_f32"
+        ver = (id(self.vertices), self.vertices._version)
+        if ver != self._version:
+            self._packs.clear()
+            self._version = ver
+        buf = self._packs.get(key)
+        if buf is not None:
+            return buf
+        rows_f, rows_w, _ = self.exact_pair_setup()
+        lib = L.lib()
+        v = self.vertices.contiguous()
+        n = int(rows_f.shape[0])
+        idx = torch.arange(n, dtype=torch.int64, device=v.device)
+        kind = L.PACK_EXACTGRAD_F32
+        buf = torch.empty(int(lib.wv_packed_bytes(kind, n)), dtype=torch.uint8, device=v.device)
+        L.check(lib.wv_pack_exact_grad(kind, _ptr(v), int(v.dtype == torch.float64),
+                                       self.num_vertices, _ptr(rows_f), 1, _ptr(idx),
+                                       _ptr(rows_w), n, _ptr(buf), _stream()),
+                "wv_pack_exact_grad (strip pairs)")
+        self._packs[key] = buf
+        return buf
+
     def packed_exact_grad(self, precision: str) -> torch.Tensor:
         kind = _EXACTGRAD[precision]
         ver = (id(self.vertices), self.vertices._version)
@@ -367,7 +469,8 @@ def exact_forward_f32(mesh: DeviceMesh, **kw):
 
 
 def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, *, grid=None,
-              n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0):
+              n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0,
+              pairs: bool | None = None):
     """Per-face corner gradients sum_p coef_scale*coefs[p]*dW_p/dv, f64.
     Returns (corner_grad (A,3,3), csr) where the rows are all faces (soft) or
     the active faces of the exact edge form (exact); feed both to
@@ -376,7 +479,20 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     lib = L.lib()
     dev = mesh.vertices.device
     dt = _DT[precision]
-    if mode == "exact":
+    if points is not None:
+        n_pts = int(torch.as_tensor(points).reshape(-1, 3).shape[0])
+    else:
+        n_pts = _grid_count(grid, n0, count)
+    if pairs is None:
+        pairs = mode == "exact" and precision == "f32" and n_pts >= STRIP_MIN_NODES
+    if pairs and not (mode == "exact" and precision == "f32"):
+        raise ValueError("strip pairs exist for the exact f32 backward only")
+    if pairs:
+        kind = None
+        packed = mesh.packed_exact_pair()
+        rows_f, _, csr = mesh.exact_pair_setup()
+        F = int(rows_f.shape[0])
+    elif mode == "exact":
         kind = _EXACTGRAD[precision]
         packed = mesh.packed_exact_grad(precision)
         active, _, csr = mesh.exact_grad_setup()
@@ -398,10 +514,15 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     out = torch.empty((F, 3, 3), dtype=torch.float64, device=dev)
     if F == 0:
         return out, csr
-    wsb = int(lib.wv_bwd_workspace_bytes(kind, F, count))
+    if pairs:
+        wsb = int(lib.wv_exact_pair_bwd_workspace_bytes(F, count))
+    else:
+        wsb = int(lib.wv_bwd_workspace_bytes(kind, F, count))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     st = _stream()
     name = f"wv_{mode}_bwd_{'points' if points is not None else 'grid'}_{precision}"
+    if pairs:
+        name = f"wv_exact_pair_bwd_{'points' if points is not None else 'grid'}_f32"
     fn = getattr(lib, name)
     if points is not None:
         rc = fn(_ptr(packed), F, _ptr(pts), count, _ptr(cf), float(coef_scale), _ptr(out),

@@ -146,3 +146,73 @@ def test_strip_c3_disagreements_are_within_tolerance(cuda_device):
     print(np.stack([d[idx], a[idx] - ref, b[idx] - ref, ref, dist], axis=1)[:16])
     far = dist[~rf] > 1e-4  # as the fuzz sweep: closer, f32 input rounding dominates
     assert eb[far].max(initial=0) <= 1e-5 and ea[far].max(initial=0) <= 1e-5
+
+
+def _grads(dm, coefs, **kw):
+    import torch
+    from paper_2407_11272_b200 import device
+    c = torch.from_numpy(coefs).float().cuda()
+    out = []
+    for pairs in (False, True):
+        fg = device.face_grad(dm, "exact", "f32", c, pairs=pairs, **kw)
+        out.append(device.vertex_grad(dm, fg).cpu().numpy())
+    return out
+
+
+@pytest.mark.parametrize("kind", ["soup", "holes", "broken"])
+def test_pair_backward_matches_single(cuda_device, kind):
+    """The strip-pair exact backward (ExactEdgeBwdPair) against the
+    single-face kernel: same vertex gradients up to fp32 summation order."""
+    import torch
+    from paper_2407_11272_b200 import configs, device
+    if kind == "holes":
+        v, f = configs.torus_with_holes(40, 30, holes=3, patch=4, seed=1)
+    else:
+        v, f = configs.soup(*configs.torus(0.7, 0.3, 60, 40), seed=1)
+    grid = ((-1.0,) * 3, (1.0,) * 3, (24, 20, 64))
+    dm = device.DeviceMesh.from_numpy(v, f)
+    if kind == "broken":
+        dm.exact_pair_setup()
+        v2 = v.copy()
+        rng = np.random.default_rng(2)
+        moved = rng.random(len(v)) < 0.3
+        v2[moved] += rng.normal(scale=1e-3, size=(int(moved.sum()), 3))
+        dm.set_vertices(torch.from_numpy(v2).to(dm.vertices.device))
+        v = v2
+    vals, flags = device.forward(dm, "exact", "f32", grid=grid)
+    p32 = orc.node_coordinates(*grid).astype(np.float32).astype(np.float64)
+    c = np.random.default_rng(3).normal(size=len(p32))
+    near = np.array([False] * len(p32))
+    c[flags.cpu().numpy().astype(bool)] = 0.0
+    a, b = _grads(dm, c, grid=grid)
+    scale = np.abs(a).max()
+    assert scale > 0 and np.isfinite(b).all()
+    assert np.abs(a - b).max() <= 2e-5 * scale, (kind, np.abs(a - b).max() / scale)
+    # generic (point-list) launch of the pair records
+    sel = np.random.default_rng(4).choice(len(p32), 2000, replace=False)
+    a2, b2 = _grads(dm, c[sel], points=torch.from_numpy(p32[sel]).float().cuda())
+    assert np.abs(a2 - b2).max() <= 2e-5 * np.abs(a2).max()
+    del near
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_pair_backward_random_meshes(cuda_device, seed):
+    """Random meshes (degenerate / duplicated faces, several scales) on a
+    lattice: pair backward within 1e-4 of the f64 oracle, coefficients zeroed
+    near the surface (as the fuzz sweep)."""
+    import torch
+    from paper_2407_11272_b200 import device
+    v, f, _ = random_case(seed)
+    scale = float(np.abs(v).max())
+    grid = ((-1.1 * scale,) * 3, (1.1 * scale,) * 3, (10, 12, 32))
+    p32 = orc.node_coordinates(*grid).astype(np.float32).astype(np.float64)
+    c = np.random.default_rng(200 + seed).normal(size=len(p32))
+    c[surface_distance(p32, v[f]) <= 1e-4 * scale] = 0.0
+    c32 = c.astype(np.float32).astype(np.float64)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    fg = device.face_grad(dm, "exact", "f32", torch.from_numpy(c32).float().cuda(), grid=grid,
+                          pairs=True)
+    g = device.vertex_grad(dm, fg).cpu().numpy()
+    r = orc.exact_grad(v, f, p32, c32, threads=1)
+    assert np.isfinite(g).all()
+    assert np.abs(g - r).max() <= 1e-4 * max(np.abs(r).max(), 1e-300), seed

@@ -72,3 +72,47 @@ def test_strip_order_rejects_bad_indices():
     out = [np.empty(1, np.int64), np.empty(3, np.int64), np.empty(1, np.uint8)]
     rc = lib.wv_strip_order(v.ctypes.data, 3, f.ctypes.data, 1, *(a.ctypes.data for a in out))
     assert rc == L.WV_ERR_ARG if hasattr(L, "WV_ERR_ARG") else rc == 1
+
+
+def _edge_weight_sums(rows, weights):
+    acc = {}
+    for (a, b, c), w in zip(rows, weights):
+        for (p, q), x in zip(((a, b), (b, c), (c, a)), w):
+            if x == 0:
+                continue
+            k = (min(p, q), max(p, q))
+            acc[k] = acc.get(k, 0.0) + (x if p < q else -x)
+    return {k: v for k, v in acc.items() if v != 0}
+
+
+@pytest.mark.parametrize("case", ["soup", "open_welded", "random"])
+def test_strip_pairs_preserve_edge_weights(case):
+    """strip_pairs (the exact backward's pair rows): every active face
+    appears once among the valid rows, pairs share two corner positions, and
+    the directed-edge weights (window order, negated for reflected windows)
+    sum to the same net per-edge weights as the original faces."""
+    from paper_2407_11272_b200 import device
+    _strips(np.zeros((3, 3)), np.zeros((0, 3), np.int64))  # skips if the library is absent
+    if case == "soup":
+        v, f = configs.soup(*configs.torus(0.7, 0.3, 24, 16), seed=4)
+    elif case == "open_welded":
+        v, f = configs.torus(0.7, 0.3, 30, 20)
+        f = f[: len(f) - 37]
+    else:
+        rng = np.random.default_rng(3)
+        v = rng.normal(size=(25, 3))
+        f = rng.integers(0, 25, size=(70, 3))
+    active, w = device.exact_edge_weights(f, device.dead_faces(v, f))
+    rows, rw, valid = device.strip_pairs(v, f[active], w)
+    assert len(rows) % 2 == 0 and valid[0::2].all()
+    assert np.array_equal(v[rows[1::2, 0]], v[rows[0::2, 1]])
+    assert np.array_equal(v[rows[1::2, 1]], v[rows[0::2, 2]])
+    got = np.sort(np.sort(rows[valid], axis=1), axis=0)
+    ref = np.sort(np.sort(f[active], axis=1), axis=0)
+    assert np.array_equal(got, ref)
+    assert not rw[~valid].any()
+    assert _edge_weight_sums(rows[valid], rw[valid]) == _edge_weight_sums(f[active], w)
+    if case == "soup":
+        assert valid.mean() > 0.9  # nearly every row is a real pair member
+    off, slots = device.vertex_csr_rows(rows, valid, len(v))
+    assert off[-1] == 3 * valid.sum() and np.all(valid[slots // 3])
