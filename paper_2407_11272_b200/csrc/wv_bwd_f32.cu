@@ -619,14 +619,17 @@ struct ExactEdgeBwdPair {
   static constexpr bool kScaled = true;
   static constexpr bool kPairRuns = true;
 #ifndef WV_PAIR_STEP
-#define WV_PAIR_STEP 2
+#define WV_PAIR_STEP 8  // c3s: 62.0 ms (8) vs 63.9 (6), 64.6 (4), 65.5 (16)
 #endif
   static constexpr int kRowStep = WV_PAIR_STEP;
   __device__ __forceinline__ static void scale(Rec& R, float s) {
     One::scale(R.f[0], s);
     One::scale(R.f[1], s);
   }
-  static constexpr int kMinBlocks = 4;
+#ifndef WV_PAIR_MINB
+#define WV_PAIR_MINB 3  // 168 registers; 4 blocks spill
+#endif
+  static constexpr int kMinBlocks = WV_PAIR_MINB;
   static constexpr double kCoefScale = One::kCoefScale;
   static constexpr int kAcc = 18;
   static constexpr int kRowAcc = 20;

@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--bwd", action="store_true", help="A/B the exact backward (pairs)")
     args = ap.parse_args()
     import time
     import torch
@@ -26,6 +27,8 @@ def main():
     t0 = time.perf_counter()
     dm.strip_setup()
     host = time.perf_counter() - t0
+    if args.bwd:
+        return bwd_ab(args, w, grid, dm)
     res = {}
     outs = {}
     for strip in (False, True, False, True):
@@ -49,6 +52,39 @@ def main():
            "speedup": min(res[False]) / min(res[True]), "strip_host_s": host,
            "max_abs_diff": float(d[ok].max()),
            "flag_mismatch": int((outs[True][1] != outs[False][1]).sum())})
+
+
+def bwd_ab(args, w, grid, dm):
+    import time
+    import torch
+    from paper_2407_11272_b200 import device
+    t0 = time.perf_counter()
+    dm.exact_pair_setup()
+    host = time.perf_counter() - t0
+    n = w.n_nodes
+    g = torch.Generator(device="cuda").manual_seed(0)
+    coefs = torch.randn(n, device="cuda", generator=g)
+    _, flags = device.forward(dm, "exact", "f32", grid=grid)
+    coefs[flags.bool()] = 0.0
+    res, outs = {}, {}
+    for pairs in (False, True, False, True):
+        fg = device.face_grad(dm, "exact", "f32", coefs, grid=grid, pairs=pairs)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.reps):
+            dm.invalidate()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fg = device.face_grad(dm, "exact", "f32", coefs, grid=grid, pairs=pairs)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        res.setdefault(pairs, []).append(min(ts))
+        outs[pairs] = device.vertex_grad(dm, fg)
+    d = (outs[True] - outs[False]).abs().max().item()
+    print({"config": args.config, "single_ms": res[False], "pairs_ms": res[True],
+           "speedup": min(res[False]) / min(res[True]), "pair_host_s": host,
+           "max_rel_diff": d / outs[False].abs().max().item()})
 
 
 if __name__ == "__main__":
