@@ -52,10 +52,12 @@ EXACT_BWD_FLOPS = 170
 # restarts there, 4.3% on C3); the face-ordered kernel executed 42.25 / 4 MUFU
 EXACT_FWD_EXEC_FLOPS = 29.25   # fwd_f32_kernel<ExactStripPol,RowSrc>
 EXACT_FWD_FACE_ORDER_EXEC_FLOPS = 42.25  # fwd_f32_kernel<ExactPol,RowSrc>, all-common fast path
-EXACT_BWD_EXEC_FLOPS = 60.5    # bwd_f32_kernel<ExactEdgeBwd,RowSrc> unit-weight loop, 4 MUFU
+# strip-pair backward (the lattice default from 2M nodes), ncu executed mix on
+# c3s; the single-face kernel executed 60.5 / 4 MUFU (static SASS count)
+EXACT_BWD_EXEC_FLOPS = 49.0    # bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>
 EXACT_FWD_MUFU = 2.2  # 1 sqrt (+2 per strip restart) + 1 rcp; face-ordered: 4
 SOFT_STEP_FLOPS = 15 + 72  # soft forward + soft backward, pinned
-EXACT_BWD_MUFU = 4
+EXACT_BWD_MUFU = 3.1  # 2 rsqrt + 1 rcp per face and pair (+ rare paths)
 
 
 def traffic(workload: str, kernel: str):
@@ -411,7 +413,7 @@ def run_ours(args):
                    "sample": f"{n} seeded random nodes of the {w.res[0]}^3 grid x {F} faces, "
                              f"exact f64 fwd (bit-exact C port of _kernels.exact_batch) + exact "
                              f"f64 grad (closed-form oracle), {dt:.1f} s"}
-        dom = ("exact_bwd (bwd_f32_kernel<ExactEdgeBwd,RowSrc>)", bwd_ms, bwd_tf) \
+        dom = ("exact_bwd (bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>)", bwd_ms, bwd_tf) \
             if bwd_ms >= fwd_ms else ("exact_fwd (fwd_f32_kernel<ExactStripPol,RowSrc>)", fwd_ms,
                                       fwd_tf)
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
