@@ -334,8 +334,18 @@ def run_ours(args):
 
     F = w.n_faces
     active = int(dmesh.exact_grad_setup()[0].shape[0])
-    launches = (2 + 1 + (1 if L.lib().wv_fwd_workspace_bytes(1, F, cnt) else 0) + 2 + 2 + 1
-                + (1 if L.lib().wv_bwd_workspace_bytes(7, active, cnt) else 0) + 1)
+    # per step: [surface eps + pack + forward (+ split finalize)] + [loss terms +
+    # loss final] + [surface eps + pack + backward (+ split reduce)] + gather.
+    # Large lattices take the strip forward and the strip-pair backward
+    # (device.STRIP_MIN_NODES), whose split plans decide the optional launches.
+    if cnt >= device.STRIP_MIN_NODES:
+        n_rows = int(dmesh.exact_pair_setup()[0].shape[0])
+        fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACTSTRIP_F32, F, cnt)
+        bws = L.lib().wv_exact_pair_bwd_workspace_bytes(n_rows, cnt)
+    else:
+        fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACT_F32, F, cnt)
+        bws = L.lib().wv_bwd_workspace_bytes(L.PACK_EXACTGRAD_F32, active, cnt)
+    launches = 3 + (1 if fws else 0) + 2 + 3 + (1 if bws else 0) + 1
 
     fp32_meas = measured_fp32_peak() if rank == 0 else None
     for _ in range(args.warmup):

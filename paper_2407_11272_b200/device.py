@@ -314,7 +314,7 @@ class DeviceMesh:
         """Strip pairs of the active faces for the exact f32 backward
         (wv_exact_pair_bwd_*): (faces (2P,3) int64 dev in pair order with
         window-ordered corners, weights (2P,3) f32 dev, CSR over the real
-        rows).  Connectivity-only, built once from the setup-time positions
+        rows, row ids 0..2P-1 for the packer).  Connectivity-only, built once from the setup-time positions
         (a pair whose welds later break is evaluated face by face)."""
         ps = getattr(self, "_exact_pair", None)
         if ps is None:
@@ -327,7 +327,8 @@ class DeviceMesh:
             off, slots = vertex_csr_rows(rows_f, valid, self.num_vertices)
             dev = self.vertices.device
             ps = (torch.from_numpy(rows_f).to(dev), torch.from_numpy(rows_w).to(dev),
-                  (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev)))
+                  (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev)),
+                  torch.arange(len(rows_f), dtype=torch.int64, device=dev))
             self._exact_pair = ps
         return ps
 
@@ -340,11 +341,10 @@ class DeviceMesh:
         buf = self._packs.get(key)
         if buf is not None:
             return buf
-        rows_f, rows_w, _ = self.exact_pair_setup()
+        rows_f, rows_w, _, idx = self.exact_pair_setup()
         lib = L.lib()
         v = self.vertices.contiguous()
         n = int(rows_f.shape[0])
-        idx = torch.arange(n, dtype=torch.int64, device=v.device)
         kind = L.PACK_EXACTGRAD_F32
         buf = torch.empty(int(lib.wv_packed_bytes(kind, n)), dtype=torch.uint8, device=v.device)
         L.check(lib.wv_pack_exact_grad(kind, _ptr(v), int(v.dtype == torch.float64),
@@ -490,7 +490,7 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     if pairs:
         kind = None
         packed = mesh.packed_exact_pair()
-        rows_f, _, csr = mesh.exact_pair_setup()
+        rows_f, _, csr, _ = mesh.exact_pair_setup()
         F = int(rows_f.shape[0])
     elif mode == "exact":
         kind = _EXACTGRAD[precision]
