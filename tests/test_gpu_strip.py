@@ -221,3 +221,35 @@ def test_pair_backward_random_meshes(cuda_device, seed):
     r = orc.exact_grad(v, f, p32, c32, threads=1)
     assert np.isfinite(g).all()
     assert np.abs(g - r).max() <= 1e-4 * max(np.abs(r).max(), 1e-300), seed
+
+
+def test_pair_backward_closed_mesh_and_tiny_meshes(cuda_device):
+    """Edge cases of the strip paths: a closed mesh (no active face: every
+    edge cancels), a single triangle (one pair with a zero-weight partner),
+    and a strip forward of a one-face mesh."""
+    import torch
+    from paper_2407_11272_b200 import configs, device
+    grid = ((-1.0,) * 3, (1.0,) * 3, (6, 6, 16))
+    n = 6 * 6 * 16
+    c = torch.ones(n, device="cuda")
+    v, f = configs.icosphere(2)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    fg = device.face_grad(dm, "exact", "f32", c, grid=grid, pairs=True)
+    assert fg[0].shape == (0, 3, 3)
+    assert float(device.vertex_grad(dm, fg).abs().max()) == 0.0
+    v1 = np.array([[0.1, 0.2, 0.05], [0.8, -0.1, 0.1], [0.2, 0.7, -0.2]])
+    f1 = np.array([[0, 1, 2]])
+    dm = device.DeviceMesh.from_numpy(v1, f1)
+    vals, flags = device.forward(dm, "exact", "f32", grid=grid, strip=True)
+    p32 = orc.node_coordinates(*grid).astype(np.float32).astype(np.float64)
+    ref, rf = orc.winding_number_batch(v1, f1, p32, mode="exact", threads=1)
+    assert np.array_equal(flags.cpu().numpy().astype(bool), rf)
+    assert np.abs(vals.double().cpu().numpy() - ref)[~rf].max() <= 1e-6
+    cc = np.random.default_rng(0).normal(size=n)
+    cc[rf] = 0.0
+    c32 = cc.astype(np.float32).astype(np.float64)
+    g = device.vertex_grad(dm, device.face_grad(dm, "exact", "f32",
+                                                torch.from_numpy(c32).float().cuda(),
+                                                grid=grid, pairs=True)).cpu().numpy()
+    r = orc.exact_grad(v1, f1, p32, c32, threads=1)
+    assert np.abs(g - r).max() <= 1e-4 * np.abs(r).max()
