@@ -302,6 +302,9 @@ struct ExactPol {
 // operations on the same coordinates), so a face costs 1 square root + 1
 // reciprocal per pair instead of 3 + 1 -- the MUFU pipe bounds this kernel.
 // Records restart (recompute A and B) at strip starts and at every tile.
+#ifndef WV_STRIP_CARRY_S
+#define WV_STRIP_CARRY_S 1
+#endif
 #ifndef WV_STRIP_P
 #define WV_STRIP_P 8
 #endif
@@ -321,7 +324,10 @@ struct ExactStripPol : ExactPol {
   // s_A = |a| + |b| from the previous face) and writes C's distance to slot
   // (k+2) mod 3, so with the face loop unrolled by 3 nothing is moved.
   struct Slot {
-    F2 d, s;
+    F2 d;
+#if WV_STRIP_CARRY_S
+    F2 s;
+#endif
   };
   // beta without the three dot products (no squared distances needed):
   //   a.b = (|a|^2 + |b|^2)/2 - h_ab  gives
@@ -342,7 +348,9 @@ struct ExactStripPol : ExactPol {
         const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
         sA[pp].d = sqrt2(fma2(az, az, f2s(w.a2)));
         sB[pp].d = sqrt2(fma2(bz, bz, f2s(w.b2)));
+#if WV_STRIP_CARRY_S
         sA[pp].s = add2(sA[pp].d, sB[pp].d);
+#endif
       }
     }
     constexpr float kL = -16.0f / 7.0f;
@@ -359,8 +367,13 @@ struct ExactStripPol : ExactPol {
       const F2 la = sA[pp].d, lb = sB[pp].d;
       const F2 sbc = add2(lb, lc), sca = add2(lc, la);
       sC[pp].d = lc;
+#if WV_STRIP_CARRY_S
       sB[pp].s = sbc;
-      const F2 x = mul2(mul2(sA[pp].s, sbc), sca);
+      const F2 sab = sA[pp].s;
+#else
+      const F2 sab = add2(la, lb);
+#endif
+      const F2 x = mul2(mul2(sab, sbc), sca);
       const F2 lp = fma2(lc, f2s(kab), fma2(lb, f2s(kca), mul2(la, f2s(kbc))));  // 16/7 (-L)
       const F2 beta2 = fma2(lp, f2s(0.875f), x);  // X - 2L
       float x0, x1, l0, l1;
