@@ -35,7 +35,30 @@ def test_packed_sizes():
     assert lib.wv_packed_bytes(2, 10) == 64 + 10 * 32
     assert lib.wv_packed_bytes(3, 10) == 64 + 10 * 128
     assert lib.wv_packed_bytes(7, 10) == 64 + 10 * 64
+    assert lib.wv_packed_bytes(9, 10) == 64 + 10 * 64  # strip-ordered exact records
     assert lib.wv_packed_bytes(99, 10) == 0
+
+
+def test_strip_and_pair_entry_points_validate_before_touching_the_gpu():
+    """Argument checks of the strip / pair entry points return WV_ERR_ARG
+    (1) without any CUDA call: odd face counts for pairs, bad ranges, null
+    buffers."""
+    import ctypes
+    from paper_2407_11272_b200 import _lib
+    lib = _lib.load_library()
+    g = _lib.make_grid((-1.0,) * 3, (1.0,) * 3, (4, 4, 4))
+    dummy = ctypes.c_void_p(16)
+    assert lib.wv_exact_pair_bwd_grid_f32(dummy, 3, g, 0, 8, dummy, 1.0, dummy, None, 0,
+                                          None) == 1
+    assert lib.wv_exact_pair_bwd_points_f32(dummy, 5, dummy, 8, dummy, 1.0, dummy, None, 0,
+                                            None) == 1
+    assert lib.wv_exact_pair_bwd_grid_f32(dummy, 2, g, 60, 8, dummy, 1.0, dummy, None, 0,
+                                          None) == 1  # range past the 64 nodes
+    assert lib.wv_exact_strip_fwd_grid_f32(None, 2, g, 0, 8, 0, dummy, None, None, 0,
+                                           None) == 1
+    assert lib.wv_pack_exact_strip(dummy, 1, 3, dummy, 1, 1, None, None, None, dummy,
+                                   None) == 1
+    assert lib.wv_exact_pair_bwd_workspace_bytes(0, 10) == 0
 
 
 def test_no_cpu_fallback():
