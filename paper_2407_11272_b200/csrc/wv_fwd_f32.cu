@@ -329,6 +329,13 @@ struct ExactStripPol : ExactPol {
     F2 s;
 #endif
   };
+  // alpha = N.(C - q) (any corner of the face gives alpha; C's z part is
+  // needed for |c - q| anyway, so alpha costs one FFMA2 per point pair)
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    Row w = ExactPol::row(R, qx, qy);
+    w.alpha = fmaf(R.n.y, R.v2.y - qy, R.n.x * (R.v2.x - qx));
+    return w;
+  }
   // beta without the three dot products (no squared distances needed):
   //   a.b = (|a|^2 + |b|^2)/2 - h_ab  gives
   //   2 beta = (|a|+|b|)(|b|+|c|)(|c|+|a|) - 2 (|a| h_bc + |b| h_ca + |c| h_ab)
@@ -355,14 +362,14 @@ struct ExactStripPol : ExactPol {
     }
     constexpr float kL = -16.0f / 7.0f;
     const float kab = kL * fabsf(R.v1.w), kbc = kL * fabsf(R.v2.w), kca = kL * R.n.w;
-    const float nz2 = 2.0f * R.n.z, wal2 = 2.0f * w.alpha;
+    const float nz2 = 2.0f * R.n.z, wal2 = 2.0f * w.alpha;  // alpha from corner C (row())
     F2 tq[PP], tp[PP];
     float ms = 0.0f;
     bool cond = true;
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
-      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), cz = sub2(f2s(R.v2.z), qz[pp]);
-      const F2 alpha2 = fma2(f2s(nz2), az, f2s(wal2));
+      const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
+      const F2 alpha2 = fma2(f2s(nz2), cz, f2s(wal2));
       const F2 lc = sqrt2(fma2(cz, cz, f2s(w.c2)));
       const F2 la = sA[pp].d, lb = sB[pp].d;
       const F2 sbc = add2(lb, lc), sca = add2(lc, la);
@@ -400,7 +407,7 @@ struct ExactStripPol : ExactPol {
     for (int pp = 0; pp < PP; ++pp) {
       const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
       const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
-      const F2 alpha = fma2(f2s(R.n.z), az, f2s(w.alpha));
+      const F2 alpha = fma2(f2s(R.n.z), cz, f2s(w.alpha));
       rare |= tail2(R, alpha, fma2(az, az, f2s(w.a2)), fma2(bz, bz, f2s(w.b2)),
                     fma2(cz, cz, f2s(w.c2)), ctx, tacc[pp]) << (2 * pp);
     }
