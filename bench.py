@@ -71,16 +71,28 @@ def traffic(workload: str, kernel: str):
     return t["read"] + t["write"]
 
 
-def executed(alg_tf, alg_flops, exec_flops, mufu, ms, peak, clk_mhz):
+# FMA-pipe lane-ops per pair (one per lane of every FFMA/FADD/FMUL, two per
+# packed f32x2 op), from the same ncu executed-instruction mixes: the FMA
+# pipe issues 128 lane-ops per clock per SM whatever the op, so this (not the
+# FLOP count, where an add is half an FMA) is what bounds the kernels.
+EXACT_FWD_LANE_OPS = 19.4   # strip forward (c3s mix, alpha from corner C)
+EXACT_BWD_LANE_OPS = 31.7   # strip-pair backward (c3s mix)
+
+
+def executed(alg_tf, alg_flops, exec_flops, mufu, ms, peak, clk_mhz, lane_ops=None):
     """Roofline of one kernel: pinned-algorithmic rate plus the utilisation of
     the two pipes it actually runs on (FP32 FMA pipe, XU/MUFU pipe at 16 ops
     per clock per SM)."""
     pairs_s = alg_tf * 1e12 / alg_flops
     xu_peak = 148 * 16 * clk_mhz * 1e6
-    return {"achieved": alg_tf, "frac": alg_tf / peak, "kernel_ms": ms,
-            "executed_flops_per_pair": exec_flops, "mufu_per_pair": mufu,
-            "fma_frac": pairs_s * exec_flops / 1e12 / peak,
-            "xu_frac": pairs_s * mufu / xu_peak}
+    r = {"achieved": alg_tf, "frac": alg_tf / peak, "kernel_ms": ms,
+         "executed_flops_per_pair": exec_flops, "mufu_per_pair": mufu,
+         "fma_frac": pairs_s * exec_flops / 1e12 / peak,
+         "xu_frac": pairs_s * mufu / xu_peak}
+    if lane_ops:
+        r["fma_lane_ops_per_pair"] = lane_ops
+        r["fma_pipe_frac"] = pairs_s * lane_ops / (148 * 128 * clk_mhz * 1e6)
+    return r
 
 
 def parse():
@@ -338,14 +350,16 @@ def run_ours(args):
     # loss final] + [surface eps + pack + backward (+ split reduce)] + gather.
     # Large lattices take the strip forward and the strip-pair backward
     # (device.STRIP_MIN_NODES), whose split plans decide the optional launches.
-    if cnt >= device.STRIP_MIN_NODES:
+    strip_path = cnt >= device.STRIP_MIN_NODES
+    if strip_path:
         n_rows = int(dmesh.exact_pair_setup()[0].shape[0])
         fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACTSTRIP_F32, F, cnt)
         bws = L.lib().wv_exact_pair_bwd_workspace_bytes(n_rows, cnt)
     else:
         fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACT_F32, F, cnt)
         bws = L.lib().wv_bwd_workspace_bytes(L.PACK_EXACTGRAD_F32, active, cnt)
-    launches = 3 + (1 if fws else 0) + 2 + 3 + (1 if bws else 0) + 1
+    bwd_launches = (3 + (1 if bws else 0)) if active > 0 else 1  # no active face: eps only
+    launches = 3 + (1 if fws else 0) + 2 + bwd_launches + 1
 
     fp32_meas = measured_fp32_peak() if rank == 0 else None
     for _ in range(args.warmup):
@@ -423,10 +437,19 @@ def run_ours(args):
                    "sample": f"{n} seeded random nodes of the {w.res[0]}^3 grid x {F} faces, "
                              f"exact f64 fwd (bit-exact C port of _kernels.exact_batch) + exact "
                              f"f64 grad (closed-form oracle), {dt:.1f} s"}
-        dom = ("exact_bwd (bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>)", bwd_ms, bwd_tf) \
-            if bwd_ms >= fwd_ms else ("exact_fwd (fwd_f32_kernel<ExactStripPol,RowSrc>)", fwd_ms,
-                                      fwd_tf)
+        if strip_path:  # strip forward + strip-pair backward (device.STRIP_MIN_NODES)
+            kf, kb = "fwd_f32_kernel<ExactStripPol,RowSrc>", "bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>"
+            xf = (EXACT_FWD_EXEC_FLOPS, EXACT_FWD_MUFU, EXACT_FWD_LANE_OPS)
+            xb = (EXACT_BWD_EXEC_FLOPS, EXACT_BWD_MUFU, EXACT_BWD_LANE_OPS)
+        else:
+            kf, kb = "fwd_f32_kernel<ExactPol,RowSrc>", "bwd_f32_kernel<ExactEdgeBwd,RowSrc>"
+            xf = (EXACT_FWD_FACE_ORDER_EXEC_FLOPS, 4, 26.75)
+            xb = (60.5, 4, 34.7)
+        dom = (f"exact_bwd ({kb})", bwd_ms, bwd_tf) if bwd_ms >= fwd_ms \
+            else (f"exact_fwd ({kf})", fwd_ms, fwd_tf)
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        rfwd = executed(fwd_tf, EXACT_FWD_FLOPS, xf[0], xf[1], fwd_ms, peak, clk_mhz, xf[2])
+        rbwd = executed(bwd_tf, EXACT_BWD_FLOPS, xb[0], xb[1], bwd_ms, peak, clk_mhz, xb[2])
         step_tf = (EXACT_FWD_FLOPS * cnt * F + EXACT_BWD_FLOPS * cnt * active) \
             / (ms_step / 1e3) / 1e12
         line = {
@@ -450,6 +473,10 @@ def run_ours(args):
                          "kernel_ms": dom[1],
                          "flops_per_pair": EXACT_BWD_FLOPS if dom[0].startswith("exact_bwd")
                          else EXACT_FWD_FLOPS,
+                         # the pipe that bounds the kernel: FMA-pipe lane-ops actually
+                         # issued per pair (ncu mix) against 128 per clock per SM
+                         "fma_pipe_frac": (rbwd if dom[0].startswith("exact_bwd")
+                                           else rfwd)["fma_pipe_frac"],
                          "peak_source": f"FP32 CUDA-core peak 148 SM x 128 lanes x 2 x clock "
                                         f"({peak_src}); MEASURED_PEAKS has no FP32 entry",
                          "peak_measured": fp32_meas,
@@ -463,10 +490,8 @@ def run_ours(args):
                                       "8d); the kernels execute fewer (roofline_fwd/bwd "
                                       "executed_flops_per_pair), so frac may exceed 1 -- "
                                       "fma_frac / xu_frac there are the pipe utilisation"},
-            "roofline_fwd": executed(fwd_tf, EXACT_FWD_FLOPS, EXACT_FWD_EXEC_FLOPS, EXACT_FWD_MUFU,
-                                     fwd_ms, peak, clk_mhz),
-            "roofline_bwd": executed(bwd_tf, EXACT_BWD_FLOPS, EXACT_BWD_EXEC_FLOPS, EXACT_BWD_MUFU,
-                                     bwd_ms, peak, clk_mhz),
+            "roofline_fwd": rfwd,
+            "roofline_bwd": rbwd,
             "roofline_step": {"achieved": step_tf, "frac": step_tf / peak,
                               "note": "whole step: 63 FLOP per forward pair + 170 per "
                                       "backward pair actually evaluated (active faces)"},
@@ -661,7 +686,7 @@ def run_c5(args):
         F = w.n_faces
         fwd_tf = EXACT_FWD_FLOPS * cnt * F / (ms_step / 1e3) / 1e12
         rf = executed(fwd_tf, EXACT_FWD_FLOPS, EXACT_FWD_EXEC_FLOPS, EXACT_FWD_MUFU, ms_step,
-                      peak, clk_mhz)
+                      peak, clk_mhz, EXACT_FWD_LANE_OPS)
         line = {
             "metric": "point-triangle solid-angle evals/sec (C5: exact forward / voxelize)",
             "value": w.pairs / (ms_step / 1e3), "unit": "pairs/s (exact fwd)", "n_gpus": world,
