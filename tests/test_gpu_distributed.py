@@ -35,7 +35,7 @@ def _problem():
     return v, f, grid, target
 
 
-def _worker(rank, world, port, outdir, mode):
+def _worker(rank, world, port, outdir, mode, strip):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -43,6 +43,8 @@ def _worker(rank, world, port, outdir, mode):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2407_11272_b200 import device
+    if strip:  # strip forward / strip-pair backward on every slab
+        device.STRIP_MIN_NODES = 0
     from paper_2407_11272_b200.distributed import CudaSlabEvaluator, SlabDriver
     v, f, grid, target = _problem()
     dm = device.DeviceMesh.from_numpy(v, f)
@@ -53,20 +55,23 @@ def _worker(rank, world, port, outdir, mode):
     loss, grads, excl, _ = drv.loss_grad(tg)
     vals, flags = drv.forward(policy=1, gather=True)
     if rank == 0:
-        np.savez(os.path.join(outdir, f"out_{mode}.npz"), loss=float(loss),
+        np.savez(os.path.join(outdir, f"out_{mode}_{int(strip)}.npz"), loss=float(loss),
                  grads=grads.cpu().numpy(), excl=float(excl), vals=vals.cpu().numpy(),
                  flags=flags.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["exact", "soft"])
-def test_two_rank_cuda_driver_matches_single_process(tmp_path, cuda_device, mode):
+@pytest.mark.parametrize("mode,strip", [("exact", False), ("soft", False), ("exact", True)])
+def test_two_rank_cuda_driver_matches_single_process(tmp_path, cuda_device, mode, strip,
+                                                     monkeypatch):
     import torch
     from paper_2407_11272_b200 import _lib as L, device
     from paper_2407_11272_b200.grad import device_loss_grad
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode), nprocs=2, join=True)
-    out = np.load(tmp_path / f"out_{mode}.npz")
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode, strip), nprocs=2, join=True)
+    out = np.load(tmp_path / f"out_{mode}_{int(strip)}.npz")
+    if strip:
+        monkeypatch.setattr(device, "STRIP_MIN_NODES", 0)
     v, f, grid, target = _problem()
     dm = device.DeviceMesh.from_numpy(v, f)
     sums, g = device_loss_grad(dm, grid, torch.from_numpy(target).cuda(), mode=mode,
