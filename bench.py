@@ -352,11 +352,9 @@ def run_ours(args):
     # (device.STRIP_MIN_NODES), whose split plans decide the optional launches.
     strip_path = cnt >= device.STRIP_MIN_NODES
     if strip_path:
-        grp = device.STRIP_GROUP
-        n_rows = int(dmesh.exact_pair_setup(grp)[0].shape[0])
+        n_rows = int(dmesh.exact_pair_setup()[0].shape[0])
         fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACTSTRIP_F32, F, cnt)
-        bws = getattr(L.lib(), f"wv_exact_{ {2: 'pair', 3: 'triple'}[grp] }_bwd_workspace_bytes")(
-            n_rows, cnt)
+        bws = L.lib().wv_exact_pair_bwd_workspace_bytes(n_rows, cnt)
     else:
         fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACT_F32, F, cnt)
         bws = L.lib().wv_bwd_workspace_bytes(L.PACK_EXACTGRAD_F32, active, cnt)

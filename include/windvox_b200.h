@@ -193,17 +193,6 @@ int wv_exact_pair_bwd_points_f32(const void *packed, int64_t n_faces, const floa
                                  int64_t count, const float *coefs, double coef_scale,
                                  double *face_grad, void *workspace, size_t workspace_bytes,
                                  void *stream);
-/* the same over strip TRIPLES: faces 3i, 3i+1, 3i+2 = (A,B,C), (B',C',D),
- * (C'',D',E); n_faces a multiple of 3 (see device.strip_groups). */
-size_t wv_exact_triple_bwd_workspace_bytes(int64_t n_faces, int64_t count);
-int wv_exact_triple_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid,
-                                 int64_t n0, int64_t count, const float *coefs,
-                                 double coef_scale, double *face_grad, void *workspace,
-                                 size_t workspace_bytes, void *stream);
-int wv_exact_triple_bwd_points_f32(const void *packed, int64_t n_faces, const float *points,
-                                   int64_t count, const float *coefs, double coef_scale,
-                                   double *face_grad, void *workspace, size_t workspace_bytes,
-                                   void *stream);
 int wv_soft_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float *coefs, double coef_scale,
                          double *face_grad, void *workspace, size_t workspace_bytes,

@@ -44,8 +44,7 @@ EXPORTED = (
     "wv_bwd_grid_f32_batch", "wv_strip_order", "wv_pack_exact_strip",
     "wv_exact_strip_fwd_grid_f32", "wv_exact_strip_fwd_points_f32",
     "wv_exact_pair_bwd_workspace_bytes", "wv_exact_pair_bwd_grid_f32",
-    "wv_exact_pair_bwd_points_f32", "wv_exact_triple_bwd_workspace_bytes",
-    "wv_exact_triple_bwd_grid_f32", "wv_exact_triple_bwd_points_f32",
+    "wv_exact_pair_bwd_points_f32",
 )
 
 
@@ -124,9 +123,6 @@ def _declare(lib):
         "wv_exact_pair_bwd_workspace_bytes": ([I64, I64], SZ),
         "wv_exact_pair_bwd_grid_f32": (bwd_grid, I),
         "wv_exact_pair_bwd_points_f32": (bwd_pts, I),
-        "wv_exact_triple_bwd_workspace_bytes": ([I64, I64], SZ),
-        "wv_exact_triple_bwd_grid_f32": (bwd_grid, I),
-        "wv_exact_triple_bwd_points_f32": (bwd_pts, I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

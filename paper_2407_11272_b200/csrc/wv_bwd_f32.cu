@@ -785,195 +785,6 @@ struct ExactEdgeBwdPair {
   }
 };
 
-// Exact backward over strip TRIPLES: F1 = (A, B, C), F2 = (B', C', D),
-// F3 = (C'', D', E) -- three consecutive strip faces.  Per point: 5 corner
-// distances and 7 edges for 3 faces (pairs: 4 and 5 for 2), 28 run sums (F2
-// shares BC with F1 and CD with F3).  Same conventions as ExactEdgeBwdPair:
-// unweighted sums, weights in the fp64 flush, per-face fallback when a weld
-// is broken, per-face redo of ill-conditioned runs.
-struct ExactTripleRec {
-  ExactGradRecF32 f[3];
-};
-struct ExactEdgeBwdTriple {
-  using One = ExactEdgeBwd;
-  using Rec = ExactTripleRec;
-  static constexpr int kFaces = 3;
-  static constexpr int kOut = 27;
-  static constexpr bool kScaled = true;
-  static constexpr bool kPairRuns = true;
-#ifndef WV_TRIPLE_STEP
-#define WV_TRIPLE_STEP 4
-#endif
-  static constexpr int kRowStep = WV_TRIPLE_STEP;
-  __device__ __forceinline__ static void scale(Rec& R, float s) {
-    One::scale(R.f[0], s);
-    One::scale(R.f[1], s);
-    One::scale(R.f[2], s);
-  }
-  static constexpr int kMinBlocks = 3;
-  static constexpr double kCoefScale = One::kCoefScale;
-  static constexpr int kAcc = 27;
-  static constexpr int kRowAcc = 28;
-  __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
-  template <bool kUnit>
-  __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
-                                                   float eps2, F2* g) {
-    uint32_t ill = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-      ill |= One::pair2<false>(R.f[k], qx, qy, qz, coef, eps2, g + k * One::kAcc) ? (1u << k)
-                                                                                  : 0u;
-    return ill;
-  }
-  __device__ __forceinline__ static void rare_pair(const Rec& R, float qx, float qy, float qz,
-                                                   float c, double (*acc)[kBwdThreads],
-                                                   uint32_t ill) {
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k)
-      if (ill & (1u << k)) exact_pair_f64(R.f[k], qx, qy, qz, c, acc + k * One::kAcc);
-  }
-  struct Row {
-    float a2, b2, c2, d2, e2;
-    float qx, qy;
-    bool welded;
-  };
-  __device__ __forceinline__ static bool same(float4 p, float4 q) {
-    return p.x == q.x && p.y == q.y && p.z == q.z;
-  }
-  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
-    const ExactGradRecF32 &F = R.f[0], &G = R.f[1], &H = R.f[2];
-    auto r2 = [&](float4 v) {
-      const float x = v.x - qx, y = v.y - qy;
-      return fmaf(y, y, x * x);
-    };
-    Row w;
-    w.a2 = r2(F.a);
-    w.b2 = r2(F.b);
-    w.c2 = r2(F.c);
-    w.d2 = r2(G.c);
-    w.e2 = r2(H.c);
-    w.qx = qx;
-    w.qy = qy;
-    w.welded = same(G.a, F.b) && same(G.b, F.c) && same(H.a, F.c) && same(H.b, G.c);
-    return w;
-  }
-  // sums (4 per edge PQ: t/|P-q|, t P_z/|P-q|, t/|Q-q|, t P_z/|Q-q|):
-  // AB 0-3, BC 4-7, CA 8-11, CD 12-15, DB 16-19, DE 20-23, EC 24-27
-  template <bool kUnit, int N>
-  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
-                                                  float, F2* z, F2* mr) {
-    if (!w.welded) return;
-    const ExactGradRecF32 &F = R.f[0], &G = R.f[1], &H = R.f[2];
-    const float u1p = F.u.x * F.u.y * F.u.z, u2p = G.u.y * G.u.z, u3p = H.u.y * H.u.z;
-    F2 ru[N];
-#pragma unroll
-    for (int u = 0; u < N; ++u) {
-      const F2 qz = f2(zc[u].x, zc[u].y), coef = f2(zc[u].z, zc[u].w);
-      const F2 az = sub2(f2s(F.a.z), qz), bz = sub2(f2s(F.b.z), qz), cz = sub2(f2s(F.c.z), qz);
-      const F2 dz = sub2(f2s(G.c.z), qz), ez = sub2(f2s(H.c.z), qz);
-      const F2 a2 = fma2(az, az, f2s(w.a2)), b2 = fma2(bz, bz, f2s(w.b2));
-      const F2 c2 = fma2(cz, cz, f2s(w.c2)), d2 = fma2(dz, dz, f2s(w.d2));
-      const F2 e2 = fma2(ez, ez, f2s(w.e2));
-      const F2 ia = rsqrt2(a2), ib = rsqrt2(b2), ic = rsqrt2(c2), id = rsqrt2(d2),
-               ie = rsqrt2(e2);
-      const F2 lb = mul2(b2, ib), lc = mul2(c2, ic), ld = mul2(d2, id);
-      const F2 dab = fma2(fma2(a2, ia, lb), fma2(a2, ia, lb), f2s(-F.u.x));
-      const F2 sbc = add2(lb, lc);
-      const F2 dbc = fma2(sbc, sbc, f2s(-F.u.y));
-      const F2 sca = fma2(a2, ia, lc);
-      const F2 dca = fma2(sca, sca, f2s(-F.u.z));
-      const F2 scd = add2(lc, ld);
-      const F2 dcd = fma2(scd, scd, f2s(-G.u.y));
-      const F2 sdb = fma2(d2, id, lb);
-      const F2 ddb = fma2(sdb, sdb, f2s(-G.u.z));
-      const F2 sde = fma2(e2, ie, ld);
-      const F2 dde = fma2(sde, sde, f2s(-H.u.y));
-      const F2 sec = fma2(e2, ie, lc);
-      const F2 dec = fma2(sec, sec, f2s(-H.u.z));
-      const F2 p1 = mul2(dbc, dca), rr1 = rcp2(mul2(dab, p1));
-      const F2 rr2 = rcp2(mul2(dcd, ddb)), rr3 = rcp2(mul2(dde, dec));
-      ru[u] = fma2(rr3, f2s(u3p), fma2(rr2, f2s(u2p), mul2(rr1, f2s(u1p))));
-      const F2 cr1 = mul2(coef, rr1), q0 = mul2(cr1, dab);
-      const F2 tab = mul2(cr1, p1), tbc = mul2(q0, dca), tca = mul2(q0, dbc);
-      const F2 cr2 = mul2(coef, rr2), cr3 = mul2(coef, rr3);
-      const F2 tcd = mul2(cr2, ddb), tdb = mul2(cr2, dcd);
-      const F2 tde = mul2(cr3, dec), tec = mul2(cr3, dde);
-      const F2 t[7] = {tab, tbc, tca, tcd, tdb, tde, tec};
-      const F2 pz[7] = {az, bz, cz, cz, dz, dz, ez};
-      const F2 ip[7] = {ia, ib, ic, ic, id, id, ie};
-      const F2 iq[7] = {ib, ic, ia, id, ib, ie, ic};
-#pragma unroll
-      for (int e = 0; e < 7; ++e) {
-        const F2 ue = mul2(t[e], pz[e]);
-        z[4 * e] = fma2(t[e], ip[e], z[4 * e]);
-        z[4 * e + 1] = fma2(ue, ip[e], z[4 * e + 1]);
-        z[4 * e + 2] = fma2(t[e], iq[e], z[4 * e + 2]);
-        z[4 * e + 3] = fma2(ue, iq[e], z[4 * e + 3]);
-      }
-    }
-#pragma unroll
-    for (int h = 1; h < N; h *= 2)
-#pragma unroll
-      for (int u = 0; u + h < N; u += 2 * h) ru[u] = add2(ru[u], ru[u + h]);
-    *mr = add2(*mr, ru[0]);
-  }
-  __device__ __noinline__ static void faces_one_by_one(const Rec& R, float qx, float qy,
-                                                       const float4* zcs, int j0, int e,
-                                                       float eps2, bool redo,
-                                                       double (*acc)[kBwdThreads]) {
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k) {
-      const ExactGradRecF32& Rk = R.f[k];
-      const One::Row rk = One::row(Rk, qx, qy);
-      F2 z[One::kRowAcc];
-      for (int i = 0; i < One::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
-      F2 mr = f2(0.0f, 0.0f);
-      if (!redo) {
-        for (int j = j0; j < e; ++j) {
-          const float4 zc = zcs[j];
-          if (!(zc.z == 0.0f && zc.w == 0.0f)) One::step_row<true, 1>(Rk, rk, &zc, eps2, z, &mr);
-        }
-      }
-      float m0, m1;
-      split(mr, m0, m1);
-      if (redo || !(m0 + m1 < One::kIllRatio))
-        One::redo_run<true>(Rk, rk, zcs, j0, e, eps2, z, acc + k * One::kAcc);
-      One::flush_row<true>(Rk, rk, z, acc + k * One::kAcc);
-    }
-  }
-  template <bool kUnit>
-  __device__ __forceinline__ static void run_end(const Rec& R, const Row& w, const float4* zcs,
-                                                 int j0, int e, float eps2, const F2* z, F2 mr,
-                                                 double (*acc)[kBwdThreads]) {
-    if (!w.welded) {
-      faces_one_by_one(R, w.qx, w.qy, zcs, j0, e, eps2, false, acc);
-      return;
-    }
-    float m0, m1;
-    split(mr, m0, m1);
-    if (!(m0 + m1 < One::kIllRatio)) {
-      faces_one_by_one(R, w.qx, w.qy, zcs, j0, e, eps2, true, acc);
-      return;
-    }
-    // F1: AB (01), BC (12), CA (20)
-    const F2 z1[12] = {z[0], z[1], z[10], z[11], z[2], z[3], z[4], z[5], z[6], z[7], z[8], z[9]};
-    // F2: BC (01), CD (12), DB (20)
-    const F2 z2[12] = {z[4], z[5], z[18], z[19], z[6], z[7], z[12], z[13], z[14], z[15],
-                       z[16], z[17]};
-    // F3: CD (01), DE (12), EC (20)
-    const F2 z3[12] = {z[12], z[13], z[26], z[27], z[14], z[15], z[20], z[21], z[22], z[23],
-                       z[24], z[25]};
-    One::flush_row<true>(R.f[0], One::row(R.f[0], w.qx, w.qy), z1, acc);
-    One::flush_row<true>(R.f[1], One::row(R.f[1], w.qx, w.qy), z2, acc + One::kAcc);
-    One::flush_row<true>(R.f[2], One::row(R.f[2], w.qx, w.qy), z3, acc + 2 * One::kAcc);
-  }
-  __device__ __forceinline__ static void finish(const Rec& R, const double* a, double* out) {
-    One::finish(R.f[0], a, out);
-    One::finish(R.f[1], a + One::kAcc, out + 9);
-    One::finish(R.f[2], a + 2 * One::kAcc, out + 18);
-  }
-};
-
 // Query points of a chunk, stored as packed PAIRS: xy[j] = {x_2j, x_2j+1,
 // y_2j, y_2j+1}, zc[j] = {z_2j, z_2j+1, coef_2j, coef_2j+1}; two LDS.128
 // deliver one point pair already in f32x2 register pairs.
@@ -1329,18 +1140,6 @@ int launch_exact_pair_bwd_f32(const void* packed, int64_t n_faces, const PointSo
   if (n_faces % 2 != 0) return kErrArg;
   return launch_bwd<ExactEdgeBwdPair>(packed, n_faces, ps, n_count, coefs, coef_scale, face_grad,
                                       ws, ws_bytes, num_sms, stream, Batch{});
-}
-int launch_exact_triple_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
-                                int64_t n_count, const float* coefs, double coef_scale,
-                                double* face_grad, void* ws, size_t ws_bytes, int num_sms,
-                                cudaStream_t stream) {
-  if (n_faces % 3 != 0) return kErrArg;
-  return launch_bwd<ExactEdgeBwdTriple>(packed, n_faces, ps, n_count, coefs, coef_scale,
-                                        face_grad, ws, ws_bytes, num_sms, stream, Batch{});
-}
-size_t exact_triple_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
-  return BwdPlan::make(n_faces / 3, n_count, num_sms, ExactEdgeBwdTriple::kMinBlocks)
-      .workspace(n_faces / 3, 1, ExactEdgeBwdTriple::kOut);
 }
 size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
   return BwdPlan::make(n_faces / 2, n_count, num_sms, ExactEdgeBwdPair::kMinBlocks)

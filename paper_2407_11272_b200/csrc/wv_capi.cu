@@ -296,34 +296,6 @@ int wv_exact_pair_bwd_points_f32(const void* packed, int64_t n_faces, const floa
                                        sm_count(), as_stream(stream));
 }
 
-size_t wv_exact_triple_bwd_workspace_bytes(int64_t n_faces, int64_t count) {
-  return n_faces > 0 && count > 0
-             ? wv::exact_triple_bwd_workspace_bytes(n_faces, count, sm_count())
-             : 0;
-}
-int wv_exact_triple_bwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid,
-                                 int64_t n0, int64_t count, const float* coefs,
-                                 double coef_scale, double* face_grad, void* workspace,
-                                 size_t workspace_bytes, void* stream) {
-  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) || !grid_ok(grid, n0, count) ||
-      n_faces % 3 != 0)
-    return WV_ERR_ARG;
-  return wv::launch_exact_triple_bwd_f32(packed, n_faces, grid_src(grid, n0), count, coefs,
-                                         coef_scale, face_grad, workspace, workspace_bytes,
-                                         sm_count(), as_stream(stream));
-}
-int wv_exact_triple_bwd_points_f32(const void* packed, int64_t n_faces, const float* points,
-                                   int64_t count, const float* coefs, double coef_scale,
-                                   double* face_grad, void* workspace, size_t workspace_bytes,
-                                   void* stream) {
-  if (!bwd_args_ok(packed, coefs, face_grad, n_faces, count) ||
-      (count > 0 && points == nullptr) || n_faces % 3 != 0)
-    return WV_ERR_ARG;
-  return wv::launch_exact_triple_bwd_f32(packed, n_faces, list_src(points, nullptr), count,
-                                         coefs, coef_scale, face_grad, workspace,
-                                         workspace_bytes, sm_count(), as_stream(stream));
-}
-
 int wv_soft_bwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float* coefs, double coef_scale,
                          double* face_grad, void* workspace, size_t workspace_bytes,

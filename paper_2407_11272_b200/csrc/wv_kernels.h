@@ -177,11 +177,6 @@ int launch_exact_pair_bwd_f32(const void* packed, int64_t n_faces, const PointSo
                               double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                               cudaStream_t stream);
 size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
-int launch_exact_triple_bwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
-                                int64_t n_count, const float* coefs, double coef_scale,
-                                double* face_grad, void* ws, size_t ws_bytes, int num_sms,
-                                cudaStream_t stream);
-size_t exact_triple_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
 // strip-ordered exact forward (wv_strip.cu builds and packs, wv_fwd_f32.cu runs)
 int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int64_t n_faces,
                 int64_t* perm, int64_t* win, uint8_t* flags);

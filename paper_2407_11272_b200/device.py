@@ -29,9 +29,6 @@ _DT = {"f32": torch.float32, "f64": torch.float64}
 # the strip-ordered records (wv_strip.cu): its host-side strip builder
 # (~0.5 us per face, once per DeviceMesh) pays off from ~2M nodes
 STRIP_MIN_NODES = 1 << 21
-# faces per thread of the exact f32 backward on such lattices (2: strip
-# pairs, 3: strip triples; 1 = the single-face kernel)
-STRIP_GROUP = 2
 
 
 def strip_order(vertices: np.ndarray, faces: np.ndarray):
@@ -123,14 +120,13 @@ def exact_edge_weights(faces: np.ndarray, dead: np.ndarray | None = None):
     return active, np.ascontiguousarray(w[active])
 
 
-def strip_groups(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray, k: int = 2):
-    """Group consecutive faces of each strip (strip_order) by k (2: pairs,
-    3: triples) for the exact backward's group kernels: returns (rows (kG,3)
-    int64 vertex ids with corners in window order, row weights (kG,3) f32,
-    valid (kG,) bool).  Rows kg .. kg+k-1 are consecutive strip faces
-    (A,B,C), (B',C',D), (C'',D',E); a missing member is a zero-weight
-    rotation of the previous row (valid False).  Window edge weights: edge
-    AB of a window is the face's directed edge between those corners,
+def strip_pairs(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray):
+    """Pair consecutive faces of each strip (strip_order) for the exact
+    backward's pair kernel: returns (rows (2P,3) int64 vertex ids with
+    corners in window order, row weights (2P,3) f32, valid (2P,) bool).
+    Rows 2i, 2i+1 are a pair F1 = (A,B,C), F2 = (B',C',D); an unpaired face
+    gets a zero-weight partner (B,C,A) (valid False).  Window edge weights:
+    edge AB of a window is the face's directed edge between those corners,
     negated when the window reflects the face's orientation."""
     f = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
     w = np.asarray(weights, dtype=np.float32).reshape(-1, 3)
@@ -148,29 +144,26 @@ def strip_groups(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray, k
         ww[:, e] = np.where(refl, -wo[ar, p1], wo[ar, p0])
     restart = (fl & 1) != 0
     start = np.maximum.accumulate(np.where(restart, ar, 0))
-    heads = np.flatnonzero((ar - start) % k == 0)  # group heads
-    G = len(heads)
-    rows = np.empty((k * G, 3), np.int64)
-    rw = np.zeros((k * G, 3), np.float32)
-    valid = np.zeros(k * G, bool)
-    rows[0::k] = win[heads]
-    rw[0::k] = ww[heads]
-    valid[0::k] = True
-    for j in range(1, k):
-        m = heads + j
-        real = m < A
-        real[real] = start[m[real]] == start[heads[real]]
-        real &= valid[j - 1::k]
-        prev = rows[j - 1::k]
-        rows[j::k] = np.where(real[:, None], win[np.minimum(m, A - 1)], prev[:, [1, 2, 0]])
-        rw[j::k] = np.where(real[:, None], ww[np.minimum(m, A - 1)], 0.0)
-        valid[j::k] = real
+    idx = ar - start                               # position within the strip
+    first = np.flatnonzero(idx % 2 == 0)           # pair heads
+    has2 = np.zeros(len(first), bool)
+    nxt = first + 1
+    ok = nxt < A
+    has2[ok] = ~restart[nxt[ok]]
+    P = len(first)
+    rows = np.empty((2 * P, 3), np.int64)
+    rw = np.zeros((2 * P, 3), np.float32)
+    valid = np.zeros(2 * P, bool)
+    rows[0::2] = win[first]
+    rw[0::2] = ww[first]
+    valid[0::2] = True
+    h = first[has2]
+    rows[1::2][has2] = win[h + 1]
+    rw[1::2][has2] = ww[h + 1]
+    valid[1::2][has2] = True
+    s = first[~has2]
+    rows[1::2][~has2] = win[s][:, [1, 2, 0]]       # zero-weight partner (B, C, A)
     return rows, rw, valid
-
-
-def strip_pairs(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray):
-    """strip_groups with k = 2 (the pair kernel)."""
-    return strip_groups(vertices, faces, weights, 2)
 
 
 def vertex_csr_rows(rows: np.ndarray, valid: np.ndarray, n_verts: int):
@@ -317,31 +310,30 @@ class DeviceMesh:
             self._exact_grad = eg
         return eg
 
-    def exact_pair_setup(self, k: int = 2):
+    def exact_pair_setup(self):
         """Strip pairs of the active faces for the exact f32 backward
         (wv_exact_pair_bwd_*): (faces (2P,3) int64 dev in pair order with
         window-ordered corners, weights (2P,3) f32 dev, CSR over the real
         rows, row ids 0..2P-1 for the packer).  Connectivity-only, built once from the setup-time positions
         (a pair whose welds later break is evaluated face by face)."""
-        cache = self.__dict__.setdefault("_exact_groups", {})
-        ps = cache.get(k)
+        ps = getattr(self, "_exact_pair", None)
         if ps is None:
             vnp = getattr(self, "_verts_np", None)
             if vnp is None:
                 vnp = self.vertices.detach().double().cpu().numpy()
             fnp = self.faces_np()
             active, w = exact_edge_weights(fnp, dead_faces(vnp, fnp))
-            rows_f, rows_w, valid = strip_groups(vnp, fnp[active], w, k)
+            rows_f, rows_w, valid = strip_pairs(vnp, fnp[active], w)
             off, slots = vertex_csr_rows(rows_f, valid, self.num_vertices)
             dev = self.vertices.device
             ps = (torch.from_numpy(rows_f).to(dev), torch.from_numpy(rows_w).to(dev),
                   (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev)),
                   torch.arange(len(rows_f), dtype=torch.int64, device=dev))
-            cache[k] = ps
+            self._exact_pair = ps
         return ps
 
-    def packed_exact_pair(self, k: int = 2) -> torch.Tensor:
-        key = f"exact_group{k}_f32"
+    def packed_exact_pair(self) -> torch.Tensor:
+        key = "exact_pair_f32"
         ver = (id(self.vertices), self.vertices._version)
         if ver != self._version:
             self._packs.clear()
@@ -349,7 +341,7 @@ class DeviceMesh:
         buf = self._packs.get(key)
         if buf is not None:
             return buf
-        rows_f, rows_w, _, idx = self.exact_pair_setup(k)
+        rows_f, rows_w, _, idx = self.exact_pair_setup()
         lib = L.lib()
         v = self.vertices.contiguous()
         n = int(rows_f.shape[0])
@@ -478,7 +470,7 @@ def exact_forward_f32(mesh: DeviceMesh, **kw):
 
 def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, *, grid=None,
               n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0,
-              pairs: bool | None = None, group: int | None = None):
+              pairs: bool | None = None):
     """Per-face corner gradients sum_p coef_scale*coefs[p]*dW_p/dv, f64.
     Returns (corner_grad (A,3,3), csr) where the rows are all faces (soft) or
     the active faces of the exact edge form (exact); feed both to
@@ -491,21 +483,14 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
         n_pts = int(torch.as_tensor(points).reshape(-1, 3).shape[0])
     else:
         n_pts = _grid_count(grid, n0, count)
-    if group is None:
-        if pairs is None:
-            auto = mode == "exact" and precision == "f32" and n_pts >= STRIP_MIN_NODES
-            group = STRIP_GROUP if auto else 1
-        else:
-            group = 2 if pairs else 1
-    if group not in (1, 2, 3):
-        raise ValueError("group must be 1, 2 or 3")
-    if group > 1 and not (mode == "exact" and precision == "f32"):
-        raise ValueError("strip groups exist for the exact f32 backward only")
-    pairs = group > 1
+    if pairs is None:
+        pairs = mode == "exact" and precision == "f32" and n_pts >= STRIP_MIN_NODES
+    if pairs and not (mode == "exact" and precision == "f32"):
+        raise ValueError("strip pairs exist for the exact f32 backward only")
     if pairs:
         kind = None
-        packed = mesh.packed_exact_pair(group)
-        rows_f, _, csr, _ = mesh.exact_pair_setup(group)
+        packed = mesh.packed_exact_pair()
+        rows_f, _, csr, _ = mesh.exact_pair_setup()
         F = int(rows_f.shape[0])
     elif mode == "exact":
         kind = _EXACTGRAD[precision]
@@ -529,16 +514,15 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     out = torch.empty((F, 3, 3), dtype=torch.float64, device=dev)
     if F == 0:
         return out, csr
-    gname = {2: "pair", 3: "triple"}.get(group)
     if pairs:
-        wsb = int(getattr(lib, f"wv_exact_{gname}_bwd_workspace_bytes")(F, count))
+        wsb = int(lib.wv_exact_pair_bwd_workspace_bytes(F, count))
     else:
         wsb = int(lib.wv_bwd_workspace_bytes(kind, F, count))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     st = _stream()
     name = f"wv_{mode}_bwd_{'points' if points is not None else 'grid'}_{precision}"
     if pairs:
-        name = f"wv_exact_{gname}_bwd_{'points' if points is not None else 'grid'}_f32"
+        name = f"wv_exact_pair_bwd_{'points' if points is not None else 'grid'}_f32"
     fn = getattr(lib, name)
     if points is not None:
         rc = fn(_ptr(packed), F, _ptr(pts), count, _ptr(cf), float(coef_scale), _ptr(out),
