@@ -618,9 +618,9 @@ def run_c4(args):
                          "flops_per_pair": SOFT_STEP_FLOPS, "traffic": None,
                          "note": "whole training step at the pinned soft fwd 15 + bwd 72 "
                                  "FLOP/pair (SURVEY 8d); MLP/Adam time included"},
-            # per mesh: 2 packs x (eps + pack), 2 loss kernels, 1 gather; per
-            # batch: 1 forward, 1 backward (+ split finalize / reduce)
-            "gpu_launches": args.steps * (per * 7 + 4),
+            # per batch: 2 packs x (eps + pack), 1 forward (+ split finalize),
+            # 2 loss kernels, 1 backward (+ split reduce), 1 gather
+            "gpu_launches": args.steps * 11,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

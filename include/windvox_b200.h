@@ -246,6 +246,28 @@ int wv_bwd_grid_f32_batch(int kind, const void *packed, size_t pack_stride, int6
                           wv_grid_t grid, int64_t n0, int64_t count, int64_t batch,
                           const float *coefs, double coef_scale, double *face_grad,
                           void *workspace, size_t workspace_bytes, void *stream);
+/* The per-mesh stages around them, batched the same way (two, two and one
+ * launches for the whole batch instead of per mesh):
+ *   wv_pack_faces_batch: vertices (batch, n_verts, 3) contiguous, one face
+ *     array; kinds 1-6; buffers pack_stride bytes apart (multiple of 16).
+ *   wv_loss_terms_f32_batch: values / flags / targets / coefs (batch, count),
+ *     weights NULL or (batch, count), sums (batch, 8); workspace
+ *     batch * wv_loss_workspace_bytes(count).
+ *   wv_face_to_vertex_batch: face_grad (batch, n_faces, 3, 3), one CSR,
+ *     scale NULL or scale[b * scale_stride], outputs (batch, n_verts, 3).
+ * Each mesh's results equal the single-mesh calls. */
+int wv_pack_faces_batch(int kind, const void *vertices, int vert_f64, int64_t n_verts,
+                        const void *faces, int faces_i64, int64_t n_faces, int64_t batch,
+                        void *packed, size_t pack_stride, void *stream);
+int wv_loss_terms_f32_batch(const float *values, const uint8_t *flags, const float *targets,
+                            const float *weights, int64_t count, int64_t batch, float *coefs,
+                            double *sums, void *workspace, size_t workspace_bytes,
+                            void *stream);
+int wv_face_to_vertex_batch(const double *face_grad, int64_t n_faces,
+                            const int64_t *csr_offsets, const int64_t *csr_slots,
+                            int64_t n_verts, int64_t batch, const double *scale,
+                            int64_t scale_stride, int accumulate, double *out64, float *out32,
+                            void *stream);
 
 /* ---- marching cubes on the device-resident grid (recon.py:39-108) --------
  * Four stream-ordered passes; the caller computes exclusive prefix sums

@@ -44,7 +44,8 @@ EXPORTED = (
     "wv_bwd_grid_f32_batch", "wv_strip_order", "wv_pack_exact_strip",
     "wv_exact_strip_fwd_grid_f32", "wv_exact_strip_fwd_points_f32",
     "wv_exact_pair_bwd_workspace_bytes", "wv_exact_pair_bwd_grid_f32",
-    "wv_exact_pair_bwd_points_f32",
+    "wv_exact_pair_bwd_points_f32", "wv_pack_faces_batch", "wv_loss_terms_f32_batch",
+    "wv_face_to_vertex_batch",
 )
 
 
@@ -123,6 +124,9 @@ def _declare(lib):
         "wv_exact_pair_bwd_workspace_bytes": ([I64, I64], SZ),
         "wv_exact_pair_bwd_grid_f32": (bwd_grid, I),
         "wv_exact_pair_bwd_points_f32": (bwd_pts, I),
+        "wv_pack_faces_batch": ([I, P, I, I64, P, I, I64, I64, P, SZ, P], I),
+        "wv_loss_terms_f32_batch": ([P, P, P, P, I64, I64, P, P, P, SZ, P], I),
+        "wv_face_to_vertex_batch": ([P, I64, P, P, I64, I64, P, I64, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

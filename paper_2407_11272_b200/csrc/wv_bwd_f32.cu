@@ -1156,7 +1156,14 @@ __global__ void face_to_vertex_kernel(const double* __restrict__ face_grad,
                                       const int64_t* __restrict__ off,
                                       const int64_t* __restrict__ slots, int64_t n_verts,
                                       const double* __restrict__ scale, int accumulate,
-                                      double* __restrict__ out64, float* __restrict__ out32) {
+                                      double* __restrict__ out64, float* __restrict__ out32,
+                                      int64_t fg_stride = 0, int64_t scale_stride = 0) {
+  // batched launches: blockIdx.y = mesh (face_grad fg_stride doubles apart,
+  // scale scale_stride apart, outputs n_verts x 3 apart)
+  face_grad += blockIdx.y * fg_stride;
+  if (scale) scale += blockIdx.y * scale_stride;
+  if (out64) out64 += blockIdx.y * 3 * n_verts;
+  if (out32) out32 += blockIdx.y * 3 * n_verts;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_verts;
        v += (int64_t)gridDim.x * blockDim.x) {
     double gx = 0.0, gy = 0.0, gz = 0.0;
@@ -1205,6 +1212,19 @@ int launch_face_to_vertex(const double* face_grad, const int64_t* off, const int
   if (blocks > num_sms * 16) blocks = num_sms * 16;
   face_to_vertex_kernel<<<blocks, 256, 0, stream>>>(face_grad, off, slots, n_verts, scale,
                                                     accumulate, out64, out32);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+int launch_face_to_vertex_batch(const double* face_grad, int64_t n_faces, const int64_t* off,
+                                const int64_t* slots, int64_t n_verts, int64_t batch,
+                                const double* scale, int64_t scale_stride, int accumulate,
+                                double* out64, float* out32, int num_sms, cudaStream_t stream) {
+  if (n_verts <= 0) return kOk;
+  if (batch < 1 || batch > 65535) return kErrArg;
+  int blocks = (int)((n_verts + 255) / 256);
+  if (blocks > num_sms * 16) blocks = num_sms * 16;
+  face_to_vertex_kernel<<<dim3((unsigned)blocks, (unsigned)batch), 256, 0, stream>>>(
+      face_grad, off, slots, n_verts, scale, accumulate, out64, out32, n_faces * 9, scale_stride);
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 

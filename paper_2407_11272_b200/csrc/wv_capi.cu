@@ -372,6 +372,38 @@ int wv_face_to_vertex(const double* face_grad, const int64_t* csr_offsets,
                                    out64, out32, sm_count(), as_stream(stream));
 }
 
+int wv_face_to_vertex_batch(const double* face_grad, int64_t n_faces, const int64_t* csr_offsets,
+                            const int64_t* csr_slots, int64_t n_verts, int64_t batch,
+                            const double* scale, int64_t scale_stride, int accumulate,
+                            double* out64, float* out32, void* stream) {
+  if (n_verts < 0 || n_faces < 0 || batch < 1) return WV_ERR_ARG;
+  if (n_verts > 0 && (csr_offsets == nullptr || (out64 == nullptr && out32 == nullptr)))
+    return WV_ERR_ARG;
+  return wv::launch_face_to_vertex_batch(face_grad, n_faces, csr_offsets, csr_slots, n_verts,
+                                         batch, scale, scale_stride, accumulate, out64, out32,
+                                         sm_count(), as_stream(stream));
+}
+int wv_pack_faces_batch(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                        const void* faces, int faces_i64, int64_t n_faces, int64_t batch,
+                        void* packed, size_t pack_stride, void* stream) {
+  if (packed == nullptr || n_verts < 0 || n_faces < 0 || batch < 1) return WV_ERR_ARG;
+  if ((n_verts > 0 && vertices == nullptr) || (n_faces > 0 && faces == nullptr))
+    return WV_ERR_ARG;
+  if (pack_stride < wv::packed_bytes(kind, n_faces)) return WV_ERR_ARG;
+  return wv::launch_pack_batch(kind, vertices, vert_f64, n_verts, faces, faces_i64, n_faces,
+                               batch, packed, pack_stride, as_stream(stream));
+}
+int wv_loss_terms_f32_batch(const float* values, const uint8_t* flags, const float* targets,
+                            const float* weights, int64_t count, int64_t batch, float* coefs,
+                            double* sums, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (count <= 0 || batch < 1 || values == nullptr || flags == nullptr || targets == nullptr ||
+      coefs == nullptr || sums == nullptr)
+    return WV_ERR_ARG;
+  return wv::launch_loss_f32_batch(values, flags, targets, weights, count, batch, coefs, sums,
+                                   workspace, workspace_bytes, as_stream(stream));
+}
+
 // ---- marching cubes ------------------------------------------------------------
 int wv_mc_classify(const void* values, int values_f64, wv_grid_t grid, double iso,
                    const int8_t* tri_count, uint8_t* cases, int32_t* counts, void* stream) {

@@ -96,7 +96,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 
     // one face against the thread's P points (rot: strip slot rotation)
     auto do_face = [&](const Rec& R, auto rot) {
-      constexpr int kRot = decltype(rot)::value;
+      [[maybe_unused]] constexpr int kRot = decltype(rot)::value;
       uint32_t rare;
       if constexpr (kRows) {
         const typename Pol::Row w = Pol::row(R, rx, ry);

@@ -223,6 +223,16 @@ int launch_soft_bwd_f64(const void* packed, int64_t n_faces, const PointSource& 
                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                         cudaStream_t stream);
 size_t bwd64_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+int launch_face_to_vertex_batch(const double* face_grad, int64_t n_faces, const int64_t* off,
+                                const int64_t* slots, int64_t n_verts, int64_t batch,
+                                const double* scale, int64_t scale_stride, int accumulate,
+                                double* out64, float* out32, int num_sms, cudaStream_t stream);
+int launch_pack_batch(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                      const void* faces, int faces_i64, int64_t n_faces, int64_t batch,
+                      void* packed, size_t pack_stride, cudaStream_t stream);
+int launch_loss_f32_batch(const float* values, const uint8_t* flags, const float* targets,
+                          const float* weights, int64_t n, int64_t batch, float* coefs,
+                          double* sums, void* ws, size_t ws_bytes, cudaStream_t stream);
 int launch_face_to_vertex(const double* face_grad, const int64_t* off, const int64_t* slots,
                           int64_t n_verts, const double* scale, int accumulate, double* out64,
                           float* out32, int num_sms, cudaStream_t stream);

@@ -17,6 +17,16 @@ template <typename T>
 __global__ void loss_terms_kernel(const T* __restrict__ values, const uint8_t* __restrict__ flags,
                                   const T* __restrict__ targets, const T* __restrict__ weights,
                                   int64_t n, T* __restrict__ coefs, double* __restrict__ part) {
+  // batched launches: blockIdx.y = mesh (arrays n apart, partials per mesh)
+  {
+    const int64_t o = (int64_t)blockIdx.y * n;
+    values += o;
+    flags += o;
+    targets += o;
+    if (weights) weights += o;
+    coefs += o;
+    part += (int64_t)blockIdx.y * 3 * gridDim.x;
+  }
   __shared__ double s0[kLossThreads], s1[kLossThreads], s2[kLossThreads];
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)kLossThreads + threadIdx.x; i < n;
@@ -50,6 +60,8 @@ __global__ void loss_terms_kernel(const T* __restrict__ values, const uint8_t* _
 
 __global__ void loss_final_kernel(const double* __restrict__ part, int nblocks,
                                   double* __restrict__ sums) {
+  part += (int64_t)blockIdx.x * 3 * nblocks;  // batched: block b = mesh b
+  sums += 8 * blockIdx.x;
   // fixed-order two-level sum (thread t takes partials t, t+256, ...; then a
   // shared-memory tree): deterministic, and ~30x faster than one thread
   __shared__ double s0[kLossThreads], s1[kLossThreads], s2[kLossThreads];
@@ -113,6 +125,19 @@ static int launch_loss(const T* values, const uint8_t* flags, const T* targets, 
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
+// (batch, n) arrays, sums (batch, 8): one terms and one final launch for all
+int launch_loss_f32_batch(const float* values, const uint8_t* flags, const float* targets,
+                          const float* weights, int64_t n, int64_t batch, float* coefs,
+                          double* sums, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const int nb = loss_blocks(n, 0);
+  if (batch < 1 || batch > 65535 || n <= 0) return kErrArg;
+  if (ws == nullptr || ws_bytes < (size_t)batch * loss_workspace_bytes(n)) return kErrWorkspace;
+  double* part = static_cast<double*>(ws);
+  loss_terms_kernel<float><<<dim3((unsigned)nb, (unsigned)batch), kLossThreads, 0, stream>>>(
+      values, flags, targets, weights, n, coefs, part);
+  loss_final_kernel<<<(unsigned)batch, kLossThreads, 0, stream>>>(part, nb, sums);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
 int launch_loss_f32(const float* values, const uint8_t* flags, const float* targets,
                     const float* weights, int64_t n, float* coefs, double* sums, void* ws,
                     size_t ws_bytes, cudaStream_t stream) {

@@ -22,7 +22,12 @@ __device__ __forceinline__ void load_vertex(const V* v, int64_t i, double* out) 
 
 template <typename V>
 __global__ void surface_eps_kernel(const V* __restrict__ verts, int64_t n_verts,
-                                   PackHeader* __restrict__ hdr) {
+                                   PackHeader* __restrict__ hdr, int64_t vstride = 0,
+                                   size_t hstride = 0) {
+  // batched launches: block b handles mesh b (vertices vstride elements,
+  // headers hstride bytes apart)
+  verts += blockIdx.x * vstride;
+  hdr = reinterpret_cast<PackHeader*>(reinterpret_cast<char*>(hdr) + blockIdx.x * hstride);
   __shared__ double smin[3][1024];
   __shared__ double smax[3][1024];
   double lo[3] = {INFINITY, INFINITY, INFINITY};
@@ -64,7 +69,13 @@ __global__ void surface_eps_kernel(const V* __restrict__ verts, int64_t n_verts,
 template <typename V, typename I>
 __global__ void pack_kernel(int kind, const V* __restrict__ verts,
                             const I* __restrict__ faces, int64_t n_faces,
-                            PackHeader* __restrict__ hdr, void* __restrict__ recs) {
+                            PackHeader* __restrict__ hdr, void* __restrict__ recs,
+                            int64_t vstride = 0, size_t pstride = 0) {
+  // batched launches: blockIdx.y = mesh (vertices vstride elements, packed
+  // buffers pstride bytes apart; one connectivity)
+  verts += blockIdx.y * vstride;
+  hdr = reinterpret_cast<PackHeader*>(reinterpret_cast<char*>(hdr) + blockIdx.y * pstride);
+  recs = static_cast<void*>(reinterpret_cast<char*>(recs) + blockIdx.y * pstride);
   const double eps = hdr->eps;
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_faces;
        f += (int64_t)gridDim.x * blockDim.x) {
@@ -324,6 +335,48 @@ int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
     else
       pack_kernel<float, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
           kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs);
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
+// One connectivity, `batch` vertex sets ((batch, n_verts, 3) contiguous): the
+// packed buffers lie pack_stride bytes apart (a multiple of 16).  Two
+// launches for the whole batch; each mesh's buffer equals launch_pack's.
+int launch_pack_batch(int kind, const void* vertices, int vert_f64, int64_t n_verts,
+                      const void* faces, int faces_i64, int64_t n_faces, int64_t batch,
+                      void* packed, size_t pack_stride, cudaStream_t stream) {
+  if (kind < 1 || kind > 6 || batch < 1 || batch > 65535 || pack_stride % 16 != 0)
+    return kErrArg;
+  PackHeader* hdr = static_cast<PackHeader*>(packed);
+  const int64_t vs = 3 * n_verts;
+  if (vert_f64)
+    surface_eps_kernel<double><<<(unsigned)batch, 1024, 0, stream>>>(
+        static_cast<const double*>(vertices), n_verts, hdr, vs, pack_stride);
+  else
+    surface_eps_kernel<float><<<(unsigned)batch, 1024, 0, stream>>>(
+        static_cast<const float*>(vertices), n_verts, hdr, vs, pack_stride);
+  void* recs = hdr + 1;
+  const int threads = 256;
+  int64_t blocks = (n_faces + threads - 1) / threads;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 4096) blocks = 4096;
+  const dim3 grid((unsigned)blocks, (unsigned)batch);
+  if (vert_f64) {
+    const double* v = static_cast<const double*>(vertices);
+    if (faces_i64)
+      pack_kernel<double, int64_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+    else
+      pack_kernel<double, int32_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+  } else {
+    const float* v = static_cast<const float*>(vertices);
+    if (faces_i64)
+      pack_kernel<float, int64_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+    else
+      pack_kernel<float, int32_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
