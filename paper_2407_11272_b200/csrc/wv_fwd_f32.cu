@@ -302,9 +302,6 @@ struct ExactPol {
 // operations on the same coordinates), so a face costs 1 square root + 1
 // reciprocal per pair instead of 3 + 1 -- the MUFU pipe bounds this kernel.
 // Records restart (recompute A and B) at strip starts and at every tile.
-#ifndef WV_STRIP_CARRY_S
-#define WV_STRIP_CARRY_S 1
-#endif
 #ifndef WV_STRIP_P
 #define WV_STRIP_P 8
 #endif
@@ -324,10 +321,7 @@ struct ExactStripPol : ExactPol {
   // s_A = |a| + |b| from the previous face) and writes C's distance to slot
   // (k+2) mod 3, so with the face loop unrolled by 3 nothing is moved.
   struct Slot {
-    F2 d;
-#if WV_STRIP_CARRY_S
-    F2 s;
-#endif
+    F2 d, s;
   };
   // alpha = N.(C - q) (any corner of the face gives alpha; C's z part is
   // needed for |c - q| anyway, so alpha costs one FFMA2 per point pair)
@@ -355,9 +349,7 @@ struct ExactStripPol : ExactPol {
         const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
         sA[pp].d = sqrt2(fma2(az, az, f2s(w.a2)));
         sB[pp].d = sqrt2(fma2(bz, bz, f2s(w.b2)));
-#if WV_STRIP_CARRY_S
         sA[pp].s = add2(sA[pp].d, sB[pp].d);
-#endif
       }
     }
     constexpr float kL = -16.0f / 7.0f;
@@ -374,12 +366,8 @@ struct ExactStripPol : ExactPol {
       const F2 la = sA[pp].d, lb = sB[pp].d;
       const F2 sbc = add2(lb, lc), sca = add2(lc, la);
       sC[pp].d = lc;
-#if WV_STRIP_CARRY_S
       sB[pp].s = sbc;
-      const F2 sab = sA[pp].s;
-#else
-      const F2 sab = add2(la, lb);
-#endif
+      const F2 sab = sA[pp].s;  // |a| + |b|, the previous face's |b| + |c|
       const F2 x = mul2(mul2(sab, sbc), sca);
       const F2 lp = fma2(lc, f2s(kab), fma2(lb, f2s(kca), mul2(la, f2s(kbc))));  // 16/7 (-L)
       const F2 beta2 = fma2(lp, f2s(0.875f), x);  // X - 2L
