@@ -48,11 +48,6 @@ __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
   return r;
 }
-__device__ __forceinline__ F2 abs2(F2 a) {
-  F2 r;
-  r.v = a.v & 0x7fffffff7fffffffull;
-  return r;
-}
 // (a.b) for packed 3-vectors
 __device__ __forceinline__ F2 dot2(F2 ax, F2 ay, F2 az, F2 bx, F2 by, F2 bz) {
   return fma2(az, bz, fma2(ay, by, mul2(ax, bx)));
