@@ -120,10 +120,11 @@ def exact_edge_weights(faces: np.ndarray, dead: np.ndarray | None = None):
     return active, np.ascontiguousarray(w[active])
 
 
-def strip_pairs(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray):
+def strip_pairs(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray, order=None):
     """Pair consecutive faces of each strip (strip_order) for the exact
     backward's pair kernel: returns (rows (2P,3) int64 vertex ids with
     corners in window order, row weights (2P,3) f32, valid (2P,) bool).
+    ``order``: a precomputed ``strip_order(vertices, faces)``.
     Rows 2i, 2i+1 are a pair F1 = (A,B,C), F2 = (B',C',D); an unpaired face
     gets a zero-weight partner (B,C,A) (valid False).  Window edge weights:
     edge AB of a window is the face's directed edge between those corners,
@@ -133,7 +134,7 @@ def strip_pairs(vertices: np.ndarray, faces: np.ndarray, weights: np.ndarray):
     A = len(f)
     if A == 0:
         return np.zeros((0, 3), np.int64), np.zeros((0, 3), np.float32), np.zeros(0, bool)
-    perm, win, fl = strip_order(vertices, f)
+    perm, win, fl = strip_order(vertices, f) if order is None else order
     fo, wo = f[perm], w[perm]
     pos = np.stack([np.argmax(fo == win[:, c:c + 1], axis=1) for c in range(3)], axis=1)
     refl = (fl & 2) != 0
@@ -276,6 +277,7 @@ class DeviceMesh:
             dev = self.vertices.device
             st = tuple(torch.from_numpy(a).to(dev) for a in (perm, win, fl))
             self._strip = st
+            self._strip_host = (perm, win, fl)
         return st
 
     def faces_np(self) -> np.ndarray:
@@ -323,7 +325,11 @@ class DeviceMesh:
                 vnp = self.vertices.detach().double().cpu().numpy()
             fnp = self.faces_np()
             active, w = exact_edge_weights(fnp, dead_faces(vnp, fnp))
-            rows_f, rows_w, valid = strip_pairs(vnp, fnp[active], w)
+            # every face active in face order (soups): the forward's strips apply
+            order = getattr(self, "_strip_host", None)
+            if order is not None and not np.array_equal(active, np.arange(len(fnp))):
+                order = None
+            rows_f, rows_w, valid = strip_pairs(vnp, fnp[active], w, order)
             off, slots = vertex_csr_rows(rows_f, valid, self.num_vertices)
             dev = self.vertices.device
             ps = (torch.from_numpy(rows_f).to(dev), torch.from_numpy(rows_w).to(dev),
