@@ -310,6 +310,7 @@ struct ExactPol {
 #endif
 struct ExactStripPol : ExactPol {
   static constexpr bool kStrip = true;
+  static_assert(kTile == 128, "pack_strip_kernel restarts a strip every 128 records");
   static constexpr int kP = WV_STRIP_P;
   static constexpr int kMinBlocksRow = WV_STRIP_MINB;
 #ifndef WV_STRIP_GROUP
