@@ -47,6 +47,7 @@ extern "C" {
 #define WV_PACK_EXACTGRAD_F32 7 /* wv_pack_exact_grad: active faces of the exact backward */
 #define WV_PACK_EXACTGRAD_F64 8
 #define WV_PACK_EXACTSTRIP_F32 9 /* wv_pack_exact_strip: exact f32 records in strip order */
+#define WV_PACK_EXACTSTRIP_F64 10 /* wv_pack_exact_strip_f64: f64 parity records in strip order */
 
 /* stored value for on-surface (flagged) nodes */
 #define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
@@ -154,6 +155,20 @@ int wv_exact_strip_fwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t g
 int wv_exact_strip_fwd_points_f32(const void *packed, int64_t n_faces, const float *points,
                                   int64_t count, int policy, float *out, uint8_t *flags,
                                   void *workspace, size_t workspace_bytes, void *stream);
+/* f64 parity twin (replaces _kernels.exact_batch on large lattices): each
+ * face term is the reference's bit for bit, the shared corners' |v - q| are
+ * carried along the strip (one DP square root per pair instead of three),
+ * and only the order of the face sum differs from wv_exact_fwd_*_f64. */
+int wv_pack_exact_strip_f64(const void *vertices, int vert_f64, int64_t n_verts,
+                            const void *faces, int faces_i64, int64_t n_faces,
+                            const int64_t *perm, const int64_t *window, const uint8_t *flags,
+                            void *packed, void *stream);
+int wv_exact_strip_fwd_grid_f64(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                                int64_t count, int use_atan2, int policy, double *out,
+                                uint8_t *flags, void *stream);
+int wv_exact_strip_fwd_points_f64(const void *packed, int64_t n_faces, const double *points,
+                                  int64_t count, int use_atan2, int policy, double *out,
+                                  uint8_t *flags, void *stream);
 
 /* ---- backward: per-face corner gradients reduced over query points ------
  * face_grad (F,3,3) f64 is OVERWRITTEN with

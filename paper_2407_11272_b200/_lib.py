@@ -24,6 +24,7 @@ PACK_SOFTGRAD_F64 = 6
 PACK_EXACTGRAD_F32 = 7
 PACK_EXACTGRAD_F64 = 8
 PACK_EXACTSTRIP_F32 = 9
+PACK_EXACTSTRIP_F64 = 10
 POLICY_RAW = 0
 POLICY_HALF = 1
 
@@ -45,7 +46,8 @@ EXPORTED = (
     "wv_exact_strip_fwd_grid_f32", "wv_exact_strip_fwd_points_f32",
     "wv_exact_pair_bwd_workspace_bytes", "wv_exact_pair_bwd_grid_f32",
     "wv_exact_pair_bwd_points_f32", "wv_pack_faces_batch", "wv_loss_terms_f32_batch",
-    "wv_face_to_vertex_batch",
+    "wv_face_to_vertex_batch", "wv_pack_exact_strip_f64", "wv_exact_strip_fwd_grid_f64",
+    "wv_exact_strip_fwd_points_f64",
 )
 
 
@@ -127,6 +129,9 @@ def _declare(lib):
         "wv_pack_faces_batch": ([I, P, I, I64, P, I, I64, I64, P, SZ, P], I),
         "wv_loss_terms_f32_batch": ([P, P, P, P, I64, I64, P, P, P, SZ, P], I),
         "wv_face_to_vertex_batch": ([P, I64, P, P, I64, I64, P, I64, I, P, P, P], I),
+        "wv_pack_exact_strip_f64": ([P, I, I64, P, I, I64, P, P, P, P, P], I),
+        "wv_exact_strip_fwd_grid_f64": ([P, I64, Grid, I64, I64, I, I, P, P, P], I),
+        "wv_exact_strip_fwd_points_f64": ([P, I64, P, I64, I, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -167,6 +167,33 @@ int wv_exact_strip_fwd_points_f32(const void* packed, int64_t n_faces, const flo
                                         as_stream(stream));
 }
 
+int wv_pack_exact_strip_f64(const void* vertices, int vert_f64, int64_t n_verts,
+                            const void* faces, int faces_i64, int64_t n_faces,
+                            const int64_t* perm, const int64_t* window, const uint8_t* flags,
+                            void* packed, void* stream) {
+  if (packed == nullptr || n_verts < 0 || n_faces < 0) return WV_ERR_ARG;
+  if (n_faces > 0 && (vertices == nullptr || faces == nullptr || perm == nullptr ||
+                      window == nullptr || flags == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_pack_strip_f64(vertices, vert_f64, n_verts, faces, faces_i64, n_faces, perm,
+                                   window, flags, packed, as_stream(stream));
+}
+int wv_exact_strip_fwd_grid_f64(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
+                                int64_t count, int use_atan2, int policy, double* out,
+                                uint8_t* flags, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || !grid_ok(grid, n0, count)) return WV_ERR_ARG;
+  return wv::launch_exact_strip_fwd_f64(packed, n_faces, grid_src(grid, n0), count, use_atan2,
+                                        policy, out, flags, as_stream(stream));
+}
+int wv_exact_strip_fwd_points_f64(const void* packed, int64_t n_faces, const double* points,
+                                  int64_t count, int use_atan2, int policy, double* out,
+                                  uint8_t* flags, void* stream) {
+  if (!fwd_args_ok(packed, out, n_faces, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_strip_fwd_f64(packed, n_faces, list_src(nullptr, points), count,
+                                        use_atan2, policy, out, flags, as_stream(stream));
+}
+
 int wv_exact_fwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                           int64_t count, int policy, float* out, uint8_t* flags,
                           void* workspace, size_t workspace_bytes, void* stream) {

@@ -181,6 +181,155 @@ static int launch_f64(const void* packed, int64_t n_faces, const PointSource& ps
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
+// ---------------------------------------------------------------------------
+// Strip-ordered f64 exact forward (records from pack_strip_f64_kernel): the
+// reference's per-face term, bit for bit (true vertex order for alpha, beta
+// and the on-surface tests), but the corner distances |v - q| of the strip's
+// shared corners are carried between consecutive faces -- the same
+// expression on the same coordinates, so the carried values are the ones the
+// reference computes -- and a face costs one DP square root instead of
+// three.  Only the order of the face sum differs from the index-order kernel
+// (~1e-16 relative).
+__device__ __forceinline__ double vdist(const double* v, double qx, double qy, double qz) {
+  const double x = v[0] - qx, y = v[1] - qy, z = v[2] - qz;
+  return sqrt(x * x + y * y + z * z);
+}
+template <int kRot>
+__device__ __forceinline__ void exact_f64_strip_face(const ExactRecF64& R, double qx, double qy,
+                                                     double qz, double eps, int use_atan2,
+                                                     double* d, double& acc, bool& hit) {
+  const int code = (int)R.pad[1];
+  const int iA = code % 3, iB = code / 3, iC = 3 - iA - iB;
+  const double* t = R.v;
+  if (R.pad[0] != 0.0) {
+    d[kRot] = vdist(t + 3 * iA, qx, qy, qz);
+    d[(kRot + 1) % 3] = vdist(t + 3 * iB, qx, qy, qz);
+  }
+  d[(kRot + 2) % 3] = vdist(t + 3 * iC, qx, qy, qz);
+  if (R.dead != 0.0) return;  // dropped by _prepare_exact (the carry still advances)
+  // |v_k - q| in true corner order
+  const double dA = d[kRot], dB = d[(kRot + 1) % 3], dC = d[(kRot + 2) % 3];
+  const double na = iA == 0 ? dA : iB == 0 ? dB : dC;
+  const double nb = iA == 1 ? dA : iB == 1 ? dB : dC;
+  const double nc = iA == 2 ? dA : iB == 2 ? dB : dC;
+  const double ax = t[0] - qx, ay = t[1] - qy, az = t[2] - qz;
+  const double bx = t[3] - qx, by = t[4] - qy, bz = t[5] - qz;
+  const double cx = t[6] - qx, cy = t[7] - qy, cz = t[8] - qz;
+  if (na < eps || nb < eps || nc < eps) {
+    hit = true;
+    return;
+  }
+  const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
+  if (-eps < pd && pd < eps) {
+    const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+    const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
+    const double d00 = ux * ux + uy * uy + uz * uz;
+    const double d01 = ux * wx + uy * wy + uz * wz;
+    const double d11 = wx * wx + wy * wy + wz * wz;
+    const double denom = d00 * d11 - d01 * d01;
+    const double ru = -(ax * ux + ay * uy + az * uz);
+    const double rw = -(ax * wx + ay * wy + az * wz);
+    const double b1 = (d11 * ru - d01 * rw) / denom;
+    const double b2 = (d00 * rw - d01 * ru) / denom;
+    if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) {
+      hit = true;
+      return;
+    }
+  }
+  const double alpha = (ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz)) +
+                       az * (bx * cy - by * cx);
+  const double beta = (na * (nb * nc) + (bx * cx + by * cy + bz * cz) * na) +
+                      ((ax * bx + ay * by + az * bz) * nc + (cx * ax + cy * ay + cz * az) * nb);
+  if (use_atan2) {
+    if (fabs(alpha) * 8.0 < beta) {  // as ExactF64Pol
+      const double tt = alpha / beta;
+      const double ss = tt * tt;
+      double p = 1.0 / 17.0;
+      p = fma(p, ss, -1.0 / 15.0);
+      p = fma(p, ss, 1.0 / 13.0);
+      p = fma(p, ss, -1.0 / 11.0);
+      p = fma(p, ss, 1.0 / 9.0);
+      p = fma(p, ss, -1.0 / 7.0);
+      p = fma(p, ss, 1.0 / 5.0);
+      p = fma(p, ss, -1.0 / 3.0);
+      p = fma(p * ss, tt, tt);
+      acc += 2.0 * p;
+    } else {
+      acc += 2.0 * atan2(alpha, beta);
+    }
+  } else {
+    if (beta != 0.0)
+      acc += 2.0 * atan(alpha / beta);
+    else if (alpha > 0.0)
+      acc += kPi;
+    else if (alpha < 0.0)
+      acc -= kPi;
+  }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kF64Threads, 6)
+fwd_f64_strip_kernel(const PackHeader* __restrict__ hdr, const ExactRecF64* __restrict__ recs,
+                     int64_t n_faces, Src src, int64_t n_count, int use_atan2, int policy,
+                     double* __restrict__ out, uint8_t* __restrict__ flags) {
+  static_assert(kF64Tile == 64, "pack_strip_f64_kernel restarts a strip every 64 records");
+  __shared__ FaceRing<ExactRecF64, kF64Tile, kF64Stages> ring;
+  const int64_t n_tiles = (n_faces + kF64Tile - 1) / kF64Tile;
+  ring_start(ring, recs, n_faces, 0, n_tiles);
+  const double eps = hdr->eps;
+  const int tid = threadIdx.x;
+  int64_t l = (int64_t)blockIdx.x * kF64NC + tid;
+  const int64_t lc = l < n_count ? l : n_count - 1;
+  double qx, qy, qz;
+  src.point(lc, qx, qy, qz);
+  double acc = 0.0, d[3] = {0.0, 0.0, 0.0};
+  bool hit = false;
+  for (int64_t t = 0; t < n_tiles; ++t) {
+    const int s = (int)(t % kF64Stages);
+    mbar_wait(&ring.full[s], (uint32_t)((t / kF64Stages) & 1));
+    const int64_t first = t * kF64Tile;
+    const int cnt = (int)((n_faces - first) < kF64Tile ? (n_faces - first) : kF64Tile);
+    const ExactRecF64* tile = ring.tiles[s];
+    int f = 0;
+#pragma unroll 1
+    for (; f + 3 <= cnt; f += 3) {
+      exact_f64_strip_face<0>(tile[f], qx, qy, qz, eps, use_atan2, d, acc, hit);
+      exact_f64_strip_face<1>(tile[f + 1], qx, qy, qz, eps, use_atan2, d, acc, hit);
+      exact_f64_strip_face<2>(tile[f + 2], qx, qy, qz, eps, use_atan2, d, acc, hit);
+    }
+    if (f < cnt) exact_f64_strip_face<0>(tile[f], qx, qy, qz, eps, use_atan2, d, acc, hit);
+    if (f + 1 < cnt)
+      exact_f64_strip_face<1>(tile[f + 1], qx, qy, qz, eps, use_atan2, d, acc, hit);
+    __syncwarp();
+    if ((tid & 31) == 0) ring_release(ring, s, kF64ConsumerWarps, recs, n_faces, t, n_tiles);
+  }
+  if (l < n_count) {
+    double w = acc / (4.0 * kPi);
+    if (hit && policy == kPolicyHalf) w = 0.5;
+    out[l] = w;
+    if (flags) flags[l] = hit ? 1 : 0;
+  }
+}
+
+int launch_exact_strip_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                               int64_t n_count, int use_atan2, int policy, double* out,
+                               uint8_t* flags, cudaStream_t stream) {
+  if (n_count <= 0) return kOk;
+  const PackHeader* hdr = static_cast<const PackHeader*>(packed);
+  const auto* recs = reinterpret_cast<const ExactRecF64*>(hdr + 1);
+  const unsigned blocks = (unsigned)((n_count + kF64NC - 1) / kF64NC);
+  if (ps.kind == PointSource::kGrid) {
+    GridSrc src{ps.grid, ps.n0};
+    fwd_f64_strip_kernel<GridSrc><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+  } else {
+    ListSrc64 src{ps.points64};
+    fwd_f64_strip_kernel<ListSrc64><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
 int launch_exact_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
                          int64_t n_count, int use_atan2, int policy, double* out, uint8_t* flags,
                          cudaStream_t stream) {

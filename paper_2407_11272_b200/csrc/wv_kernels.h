@@ -183,6 +183,13 @@ int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int6
 int launch_pack_strip(const void* verts, int vert_f64, int64_t n_verts, const void* faces,
                       int faces_i64, int64_t n_faces, const int64_t* perm, const int64_t* win,
                       const uint8_t* flags, void* packed, cudaStream_t stream);
+int launch_pack_strip_f64(const void* verts, int vert_f64, int64_t n_verts, const void* faces,
+                          int faces_i64, int64_t n_faces, const int64_t* perm,
+                          const int64_t* win, const uint8_t* flags, void* packed,
+                          cudaStream_t stream);
+int launch_exact_strip_fwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
+                               int64_t n_count, int use_atan2, int policy, double* out,
+                               uint8_t* flags, cudaStream_t stream);
 int launch_exact_strip_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                                int64_t n_count, int policy, float* out, uint8_t* flags,
                                void* workspace, size_t ws_bytes, int num_sms,

@@ -289,6 +289,7 @@ size_t packed_bytes(int kind, int64_t n_faces) {
     case 7: rec = sizeof(ExactGradRecF32); break;
     case 8: rec = sizeof(ExactGradRecF64); break;
     case 9: rec = sizeof(ExactRecF32); break;  // strip-ordered exact records (wv_strip.cu)
+    case 10: rec = sizeof(ExactRecF64); break;  // strip-ordered f64 parity records
     default: return 0;
   }
   return sizeof(PackHeader) + rec * (size_t)(n_faces > 0 ? n_faces : 0);

@@ -242,6 +242,94 @@ __global__ void pack_strip_kernel(const V* __restrict__ verts, const I* __restri
   }
 }
 
+// f64 parity records in strip order: the reference's own per-face arrays
+// (true vertex order, nhat, pld, dead -- bit-identical to pack_kernel kind 3)
+// plus pad[0] = strip restart (1.0 / 0.0) and pad[1] = the window as true
+// corner indices, iA + 3 iB (iC = 3 - iA - iB).  Restarts every kF64Tile (64)
+// records and wherever the window's A, B are not bitwise the previous B, C.
+template <typename V, typename I>
+__global__ void pack_strip_f64_kernel(const V* __restrict__ verts, const I* __restrict__ faces,
+                                      const int64_t* __restrict__ perm,
+                                      const int64_t* __restrict__ win,
+                                      const uint8_t* __restrict__ flags, int64_t n_faces,
+                                      ExactRecF64* __restrict__ recs) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_faces;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = perm[k];
+    int64_t vi[3];
+    double v[3][3];
+    for (int c = 0; c < 3; ++c) {
+      vi[c] = (int64_t)faces[3 * f + c];
+      for (int d = 0; d < 3; ++d) v[c][d] = (double)verts[3 * vi[c] + d];
+    }
+    const double ux = v[1][0] - v[0][0], uy = v[1][1] - v[0][1], uz = v[1][2] - v[0][2];
+    const double wx = v[2][0] - v[0][0], wy = v[2][1] - v[0][1], wz = v[2][2] - v[0][2];
+    const double nx = uy * wz - uz * wy;
+    const double ny = uz * wx - ux * wz;
+    const double nz = ux * wy - uy * wx;
+    const double norm = sqrt(nx * nx + ny * ny + nz * nz);
+    const bool dead = !(norm > 0.0);
+    ExactRecF64& r = recs[k];
+    for (int d = 0; d < 3; ++d) {
+      r.v[d] = v[0][d];
+      r.v[3 + d] = v[1][d];
+      r.v[6 + d] = v[2][d];
+    }
+    double hx = 0.0, hy = 0.0, hz = 0.0, pld = 0.0;
+    if (!dead) {
+      hx = nx / norm;
+      hy = ny / norm;
+      hz = nz / norm;
+      pld = hx * v[0][0] + hy * v[0][1] + hz * v[0][2];
+    }
+    r.nhat[0] = hx;
+    r.nhat[1] = hy;
+    r.nhat[2] = hz;
+    r.pld = pld;
+    r.dead = dead ? 1.0 : 0.0;
+    // window corners as true corner indices
+    int ic[3] = {0, 1, 2};
+    for (int c = 0; c < 3; ++c)
+      for (int t = 0; t < 3; ++t)
+        if (vi[t] == win[3 * k + c]) ic[c] = t;
+    bool restart = (flags[k] & 1) != 0 || (k % 64) == 0;
+    if (!restart) {
+      const int64_t* pw = win + 3 * (k - 1);
+      for (int d = 0; d < 3; ++d) {
+        restart |= (double)verts[3 * pw[1] + d] != v[ic[0]][d];
+        restart |= (double)verts[3 * pw[2] + d] != v[ic[1]][d];
+      }
+    }
+    r.pad[0] = restart ? 1.0 : 0.0;
+    r.pad[1] = (double)(ic[0] + 3 * ic[1]);
+  }
+}
+
+int launch_pack_strip_f64(const void* verts, int vert_f64, int64_t n_verts, const void* faces,
+                          int faces_i64, int64_t n_faces, const int64_t* perm,
+                          const int64_t* win, const uint8_t* flags, void* packed,
+                          cudaStream_t stream) {
+  PackHeader* hdr = static_cast<PackHeader*>(packed);
+  const int rc = launch_surface_eps(verts, vert_f64, n_verts, reinterpret_cast<double*>(hdr),
+                                    stream);
+  if (rc != kOk) return rc;
+  ExactRecF64* recs = reinterpret_cast<ExactRecF64*>(hdr + 1);
+  const int blocks = (int)((n_faces + 255) / 256 > 0 ? (n_faces + 255) / 256 : 1);
+#define WV_PSF(VT, IT)                                                                       \
+  pack_strip_f64_kernel<VT, IT><<<blocks, 256, 0, stream>>>(                                  \
+      static_cast<const VT*>(verts), static_cast<const IT*>(faces), perm, win, flags, n_faces, \
+      recs)
+  if (vert_f64) {
+    if (faces_i64) WV_PSF(double, int64_t);
+    else WV_PSF(double, int32_t);
+  } else {
+    if (faces_i64) WV_PSF(float, int64_t);
+    else WV_PSF(float, int32_t);
+  }
+#undef WV_PSF
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
 int launch_pack_strip(const void* verts, int vert_f64, int64_t n_verts, const void* faces,
                       int faces_i64, int64_t n_faces, const int64_t* perm, const int64_t* win,
                       const uint8_t* flags, void* packed, cudaStream_t stream) {

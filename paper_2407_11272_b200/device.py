@@ -250,7 +250,14 @@ class DeviceMesh:
         f = f.contiguous()
         nbytes = int(lib.wv_packed_bytes(kind, self.num_faces))
         buf = torch.empty(nbytes, dtype=torch.uint8, device=v.device)
-        if kind == L.PACK_EXACTSTRIP_F32:
+        if kind == L.PACK_EXACTSTRIP_F64:
+            perm, win, fl = self.strip_setup()
+            L.check(lib.wv_pack_exact_strip_f64(_ptr(v), int(v.dtype == torch.float64),
+                                                self.num_vertices, _ptr(f),
+                                                int(f.dtype == torch.int64), self.num_faces,
+                                                _ptr(perm), _ptr(win), _ptr(fl), _ptr(buf),
+                                                _stream()), "wv_pack_exact_strip_f64")
+        elif kind == L.PACK_EXACTSTRIP_F32:
             perm, win, fl = self.strip_setup()
             L.check(lib.wv_pack_exact_strip(_ptr(v), int(v.dtype == torch.float64),
                                             self.num_vertices, _ptr(f),
@@ -400,8 +407,8 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
             flags: torch.Tensor | None = None, strip: bool | None = None):
     """Winding numbers on the device.  ``grid=(lo, hi, res)`` with the node
     range [n0, n0+count), or ``points`` (n,3).  Returns (values, flags u8).
-    ``strip`` (exact f32 only): strip-ordered records; None = automatic
-    (lattice ranges of >= STRIP_MIN_NODES row-aligned nodes)."""
+    ``strip`` (exact only): strip-ordered records; None = automatic (lattice
+    ranges of >= STRIP_MIN_NODES nodes, row-aligned for f32)."""
     _check_precision(precision)
     if mode not in ("exact", "soft"):
         raise ValueError(f"mode must be 'exact' or 'soft', got {mode!r}")
@@ -449,8 +456,23 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
             rc = fn(_ptr(packed), F, L.make_grid(*grid), int(n0), count, policy, _ptr(out),
                     _ptr(flags), _ptr(ws), wsb, st)
     else:
+        if strip is None:
+            strip = (mode == "exact" and points is None and count >= STRIP_MIN_NODES)
+        if strip and mode != "exact":
+            raise ValueError("strip records exist for the exact forward only")
+        if strip:
+            kind = L.PACK_EXACTSTRIP_F64
         packed = mesh.packed(kind)
-        if mode == "exact":
+        if strip:
+            if points is not None:
+                rc = lib.wv_exact_strip_fwd_points_f64(_ptr(packed), F, _ptr(pts), count,
+                                                       int(bool(use_atan2)), policy, _ptr(out),
+                                                       _ptr(flags), st)
+            else:
+                rc = lib.wv_exact_strip_fwd_grid_f64(_ptr(packed), F, L.make_grid(*grid),
+                                                     int(n0), count, int(bool(use_atan2)),
+                                                     policy, _ptr(out), _ptr(flags), st)
+        elif mode == "exact":
             if points is not None:
                 rc = lib.wv_exact_fwd_points_f64(_ptr(packed), F, _ptr(pts), count,
                                                  int(bool(use_atan2)), policy, _ptr(out),

@@ -253,3 +253,59 @@ def test_pair_backward_closed_mesh_and_tiny_meshes(cuda_device):
                                                 grid=grid, pairs=True)).cpu().numpy()
     r = orc.exact_grad(v1, f1, p32, c32, threads=1)
     assert np.abs(g - r).max() <= 1e-4 * np.abs(r).max()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_f64_strip_forward_matches_reference_order(cuda_device, seed):
+    """The f64 parity forward over strip records: every face term is the
+    reference's (true-order alpha / beta / on-surface tests), only the order
+    of the face sum differs -- agreement with the index-order f64 kernel and
+    the oracle to 1e-12, identical flags (random meshes with degenerate and
+    duplicated faces; lattice-aligned vertices for on-vertex nodes; both
+    atan branches)."""
+    from paper_2407_11272_b200 import _lib as L, device
+    v, f, pts = random_case(seed)
+    scale = float(np.abs(v).max())
+    res = (10, 12, 32)
+    lo, hi = (-1.1 * scale,) * 3, (1.1 * scale,) * 3
+    if seed % 2 == 0:
+        ax = [orc.axis_nodes(lo[a], hi[a], res[a]) for a in range(3)]
+        v = np.stack([ax[a][np.abs(ax[a][None, :] - v[:, a:a + 1]).argmin(axis=1)]
+                      for a in range(3)], axis=1)
+    grid = (lo, hi, res)
+    dm = device.DeviceMesh.from_numpy(v, f)
+    nodes = orc.node_coordinates(*grid)
+    for use_atan2 in (True, False):
+        a, fa = device.forward(dm, "exact", "f64", grid=grid, policy=L.POLICY_RAW,
+                               use_atan2=use_atan2, strip=False)
+        b, fb = device.forward(dm, "exact", "f64", grid=grid, policy=L.POLICY_RAW,
+                               use_atan2=use_atan2, strip=True)
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.array_equal(fa.cpu().numpy(), fb.cpu().numpy()), seed
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(a).max()), seed
+        if use_atan2:
+            ref, rf = orc.winding_number_batch(v, f, nodes, mode="exact", threads=1)
+            assert np.array_equal(fb.cpu().numpy().astype(bool), rf), seed
+            assert np.abs(b - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), seed
+    got, gf = device.forward(dm, "exact", "f64", points=pts, strip=True)
+    ref, rf = orc.winding_number_batch(v, f, pts, mode="exact", threads=1)
+    assert np.array_equal(gf.cpu().numpy().astype(bool), rf)
+    assert np.abs(got.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+def test_f64_strip_forward_soup_and_broken_welds(cuda_device):
+    import torch
+    from paper_2407_11272_b200 import _lib as L, configs, device
+    v, f = configs.soup(*configs.torus(0.7, 0.3, 40, 30), seed=2)
+    grid = ((-1.0,) * 3, (1.0,) * 3, (16, 16, 32))
+    dm = device.DeviceMesh.from_numpy(v, f)
+    for step in range(2):
+        a, fa = device.forward(dm, "exact", "f64", grid=grid, policy=L.POLICY_HALF, strip=False)
+        b, fb = device.forward(dm, "exact", "f64", grid=grid, policy=L.POLICY_HALF, strip=True)
+        assert np.array_equal(fa.cpu().numpy(), fb.cpu().numpy())
+        assert float((a - b).abs().max()) <= 1e-12
+        v2 = v.copy()  # break half of the welds after the strips were built
+        rng = np.random.default_rng(1)
+        moved = rng.random(len(v)) < 0.5
+        v2[moved] += rng.normal(scale=1e-3, size=(int(moved.sum()), 3))
+        dm.set_vertices(torch.from_numpy(v2).to(dm.vertices.device))
