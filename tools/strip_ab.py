@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--bwd", action="store_true", help="A/B the exact backward (pairs)")
+    ap.add_argument("--f64", action="store_true", help="A/B the f64 parity forward")
     args = ap.parse_args()
     import time
     import torch
@@ -31,15 +32,16 @@ def main():
         return bwd_ab(args, w, grid, dm)
     res = {}
     outs = {}
+    prec = "f64" if args.f64 else "f32"
     for strip in (False, True, False, True):
-        v, f = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW, strip=strip)
+        v, f = device.forward(dm, "exact", prec, grid=grid, policy=L.POLICY_RAW, strip=strip)
         torch.cuda.synchronize()
         ts = []
         for _ in range(args.reps):
             dm.invalidate()  # include the re-pack, as a step does
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            v, f = device.forward(dm, "exact", "f32", grid=grid, policy=L.POLICY_RAW,
+            v, f = device.forward(dm, "exact", prec, grid=grid, policy=L.POLICY_RAW,
                                   strip=strip)
             b.record()
             torch.cuda.synchronize()
