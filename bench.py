@@ -10,7 +10,9 @@ the FP32 path: pack the (moved) mesh, exact forward over the rank's i-slab,
 fused loss terms against a fixed target occupancy, exact backward, vertex
 gather, and (N>1) one all-reduce of [grad numerator | loss sums].  Synthetic
 inputs (no network); the target is the binarized exact occupancy of the same
-soup scaled by 1.03, computed once before timing.
+soup scaled by 1.03, computed once before timing.  At this size both
+directions run over face strips (strip-ordered forward, strip-pair backward;
+DESIGN.md 3.1b / 3.3b).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
