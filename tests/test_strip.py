@@ -116,3 +116,17 @@ def test_strip_pairs_preserve_edge_weights(case):
         assert valid.mean() > 0.9  # nearly every row is a real pair member
     off, slots = device.vertex_csr_rows(rows, valid, len(v))
     assert off[-1] == 3 * valid.sum() and np.all(valid[slots // 3])
+
+
+def test_strip_pairs_reuse_the_forward_order():
+    """strip_pairs with a precomputed strip_order (the forward's, reused for
+    soups whose faces are all active) gives the same rows."""
+    from paper_2407_11272_b200 import device
+    _strips(np.zeros((3, 3)), np.zeros((0, 3), np.int64))
+    v, f = configs.soup(*configs.torus(0.7, 0.3, 20, 12), seed=5)
+    active, w = device.exact_edge_weights(f, device.dead_faces(v, f))
+    assert np.array_equal(active, np.arange(len(f)))
+    a = device.strip_pairs(v, f, w)
+    b = device.strip_pairs(v, f, w, device.strip_order(v, f))
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
