@@ -11,6 +11,7 @@ expressions are the same IEEE sequence as the numpy/numba reference.
 
 from __future__ import annotations
 
+import os
 import shutil
 import subprocess
 import sys
@@ -58,7 +59,9 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(obj)
         if not force and not _stale(obj, [src, *headers]):
             continue
-        cmd = [nvcc, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+        # WV_NVCC_DEFINES: extra -D flags for A/B builds of kernel variants
+        extra = os.environ.get("WV_NVCC_DEFINES", "").split()
+        cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", str(src), "-o", str(obj)]
         if src.name in NO_FMAD:
             cmd.insert(-4, "-fmad=false")
         if verbose:

@@ -82,6 +82,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   typename Pol::Ctx ctx = Pol::make_ctx(eps);
   uint32_t hits = 0;
   typename Pol::Slot slot[3][PP];  // strip policies: corner distances (ring of 3 slots)
+  [[maybe_unused]] float rrow[3] = {0.0f, 0.0f, 0.0f};  // strip policies: row parts of |v - q|^2
 
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int64_t it = t - t_begin;
@@ -94,36 +95,8 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) tacc[pp] = f2(0.0f, 0.0f);
 
-    // one face against the thread's P points (rot: strip slot rotation)
-    auto do_face = [&](const Rec& R, auto rot) {
-      [[maybe_unused]] constexpr int kRot = decltype(rot)::value;
-      uint32_t rare;
-      if constexpr (kRows) {
-        const typename Pol::Row w = Pol::row(R, rx, ry);
-        // groups of (at most) 4 point pairs: the per-face row constants are
-        // shared by all of a thread's points, the temporaries by one group
-        rare = 0;
-        if constexpr (Pol::kStrip) {
-          const bool restart = __float_as_int(R.v1.w) < 0;  // uniform per face
-#pragma unroll
-          for (int g0 = 0; g0 < PP; g0 += Pol::kGroup)
-            rare |= Pol::template face_strip<(PP < Pol::kGroup ? PP : Pol::kGroup)>(
-                        R, w, qz + g0, ctx, restart, slot[kRot] + g0, slot[(kRot + 1) % 3] + g0,
-                        slot[(kRot + 2) % 3] + g0, tacc + g0)
-                    << (2 * g0);
-        } else {
-#pragma unroll
-          for (int g0 = 0; g0 < PP; g0 += 4)
-            rare |= Pol::template face_row<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, tacc + g0)
-                    << (2 * g0);
-        }
-      } else {
-        rare = 0;
-#pragma unroll
-        for (int g0 = 0; g0 < PP; g0 += 4)
-          rare |= Pol::template face<(PP < 4 ? PP : 4)>(R, qx + g0, qy + g0, qz + g0, ctx,
-                                                          tacc + g0) << (2 * g0);
-      }
+    // lanes of one face that the fp32 paths left to the fp64 path
+    auto do_rare = [&](const Rec& R, uint32_t rare) {
       if (rare != 0u) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
@@ -141,18 +114,118 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         }
       }
     };
+    // one face against the thread's P points
+    auto do_face = [&](const Rec& R, auto) {
+      uint32_t rare;
+      if constexpr (kRows) {
+        // groups of (at most) 4 point pairs: the per-face row constants are
+        // shared by all of a thread's points, the temporaries by one group
+        rare = 0;
+        {
+          const typename Pol::Row w = Pol::row(R, rx, ry);
+#pragma unroll
+          for (int g0 = 0; g0 < PP; g0 += 4)
+            rare |= Pol::template face_row<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, tacc + g0)
+                    << (2 * g0);
+        }
+      } else {
+        rare = 0;
+#pragma unroll
+        for (int g0 = 0; g0 < PP; g0 += 4)
+          rare |= Pol::template face<(PP < 4 ? PP : 4)>(R, qx + g0, qy + g0, qz + g0, ctx,
+                                                          tacc + g0) << (2 * g0);
+      }
+      do_rare(R, rare);
+    };
     using R0 = std::integral_constant<int, 0>;
+    using R1 = std::integral_constant<int, 1>;
+    using R2 = std::integral_constant<int, 2>;
     if constexpr (Pol::kStrip && kRows) {
-      // strip records: unrolled by 3 so the slot rotation is static
+      static_assert(PP <= Pol::kGroup, "strip faces are decided for all point pairs at once");
+      // one strip face's common-path terms; the slots rotate by kRot
+      auto fast = [&](const Rec& R, auto rot, F2* tq, F2* tp) -> bool {
+        constexpr int kRot = decltype(rot)::value;
+        const bool restart = __float_as_int(R.v1.w) < 0;  // uniform per face
+        // the row parts of |A - q|^2, |B - q|^2 are the previous faces'
+        // |C - q|^2 row parts (ring of 3, like the distance slots)
+        typename Pol::Row w = Pol::row_c(R, rx, ry);
+        if (restart) Pol::row_ab(R, rx, ry, rrow[kRot], rrow[(kRot + 1) % 3]);
+        w.a2 = rrow[kRot];
+        w.b2 = rrow[(kRot + 1) % 3];
+        rrow[(kRot + 2) % 3] = w.c2;
+        return Pol::template strip_fast<PP>(R, w, qz, ctx, restart, slot[kRot],
+                                            slot[(kRot + 1) % 3], slot[(kRot + 2) % 3], tq, tp);
+      };
+      auto commit = [&](const Rec& R, bool ok, const F2* tq, const F2* tp) {
+        if (ok) {
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
+        } else {
+          do_rare(R, Pol::template strip_slow<PP>(R, rx, ry, qz, ctx, tacc));
+        }
+      };
+      // two faces per decision: face k's tail overlaps face k+1's square
+      // roots (one branch per two faces); terms are added in face order
+#ifndef WV_STRIP_PAIR_TERMS
+#define WV_STRIP_PAIR_TERMS 1  // 1287.6 ms vs 1290.7 (speculative tacc) on C3
+#endif
+      auto pair = [&](const Rec& Ra, const Rec& Rb, auto rota, auto rotb) {
+#if WV_STRIP_PAIR_TERMS
+        F2 tqa[PP], tpa[PP], tqb[PP], tpb[PP];  // both faces' terms
+        const bool oka = fast(Ra, rota, tqa, tpa);
+        const bool okb = fast(Rb, rotb, tqb, tpb);
+        if (oka && okb) {
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp)
+            tacc[pp] = fma2(tqb[pp], tpb[pp], fma2(tqa[pp], tpa[pp], tacc[pp]));
+        } else {
+          commit(Ra, oka, tqa, tpa);
+          commit(Rb, okb, tqb, tpb);
+        }
+#else
+        F2 ta[PP];  // tacc with face a's common terms (taken if face a is common)
+        bool oka;
+        {
+          F2 tq[PP], tp[PP];
+          oka = fast(Ra, rota, tq, tp);
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) ta[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
+        }
+        F2 tq[PP], tp[PP];
+        const bool okb = fast(Rb, rotb, tq, tp);
+        if (oka && okb) {
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], ta[pp]);
+        } else {
+          if (oka) {
+#pragma unroll
+            for (int pp = 0; pp < PP; ++pp) tacc[pp] = ta[pp];
+          } else {
+            do_rare(Ra, Pol::template strip_slow<PP>(Ra, rx, ry, qz, ctx, tacc));
+          }
+          commit(Rb, okb, tq, tp);
+        }
+#endif
+      };
+      auto one = [&](const Rec& R, auto rot) {
+        F2 tq[PP], tp[PP];
+        const bool ok = fast(R, rot, tq, tp);
+        commit(R, ok, tq, tp);
+      };
+      // unrolled by 6 so the slot rotation is static
       int f = 0;
 #pragma unroll 1
-      for (; f + 3 <= cnt; f += 3) {
-        do_face(tile[f], R0{});
-        do_face(tile[f + 1], std::integral_constant<int, 1>{});
-        do_face(tile[f + 2], std::integral_constant<int, 2>{});
+      for (; f + 6 <= cnt; f += 6) {
+        pair(tile[f], tile[f + 1], R0{}, R1{});
+        pair(tile[f + 2], tile[f + 3], R2{}, R0{});
+        pair(tile[f + 4], tile[f + 5], R1{}, R2{});
       }
-      if (f < cnt) do_face(tile[f], R0{});
-      if (f + 1 < cnt) do_face(tile[f + 1], std::integral_constant<int, 1>{});
+      const int r = cnt - f;  // 0..5 faces left, rotation 0
+      if (r >= 2) pair(tile[f], tile[f + 1], R0{}, R1{});
+      else if (r == 1) one(tile[f], R0{});
+      if (r >= 4) pair(tile[f + 2], tile[f + 3], R2{}, R0{});
+      else if (r == 3) one(tile[f + 2], R2{});
+      if (r == 5) one(tile[f + 4], R1{});
     } else {
 #pragma unroll 1
       for (int f = 0; f < cnt; ++f) do_face(tile[f], R0{});

@@ -326,10 +326,21 @@ struct ExactStripPol : ExactPol {
   };
   // alpha = N.(C - q) (any corner of the face gives alpha; C's z part is
   // needed for |c - q| anyway, so alpha costs one FFMA2 per point pair)
-  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
-    Row w = ExactPol::row(R, qx, qy);
-    w.alpha = fmaf(R.n.y, R.v2.y - qy, R.n.x * (R.v2.x - qx));
+  // Per face only C's row part is computed; A's and B's are carried from the
+  // previous faces (row_ab at strip starts), bitwise what ExactPol::row gives
+  __device__ __forceinline__ static Row row_c(const Rec& R, float qx, float qy) {
+    const float cx = R.v2.x - qx, cy = R.v2.y - qy;
+    Row w;
+    w.c2 = fmaf(cy, cy, cx * cx);
+    w.alpha = fmaf(R.n.y, cy, R.n.x * cx);
     return w;
+  }
+  __device__ __forceinline__ static void row_ab(const Rec& R, float qx, float qy, float& a2,
+                                                float& b2) {
+    const float ax = R.v0e.x - qx, ay = R.v0e.y - qy;
+    const float bx = R.v1.x - qx, by = R.v1.y - qy;
+    a2 = fmaf(ay, ay, ax * ax);
+    b2 = fmaf(by, by, bx * bx);
   }
   // beta without the three dot products (no squared distances needed):
   //   a.b = (|a|^2 + |b|^2)/2 - h_ab  gives
@@ -339,11 +350,15 @@ struct ExactStripPol : ExactPol {
   // beta > |a||b||c|/2), tested as L' > -X on the ALU with L' = 16/7 (-L);
   // angle: t^2 < 1/64 (max tree); no corner within eps (per-face scalar).
   // Lanes that fail take tail2 (recomputed from squared distances) or the
-  // fp64 path.
+  // fp64 path.  The kernel decides two faces at a time (one branch per two
+  // faces, so one face's tail overlaps the next face's square roots).
+  // The common-path terms of one face for PP point pairs (tq, tp: the
+  // accumulation is tacc = fma(tq, tp, tacc)); true when every pair is
+  // common.  Always updates the distance slots.
   template <int PP>
-  __device__ __forceinline__ static uint32_t face_strip(const Rec& R, const Row& w, const F2* qz,
-                                                        const Ctx& ctx, bool restart, Slot* sA,
-                                                        Slot* sB, Slot* sC, F2* tacc) {
+  __device__ __forceinline__ static bool strip_fast(const Rec& R, const Row& w, const F2* qz,
+                                                    const Ctx& ctx, bool restart, Slot* sA,
+                                                    Slot* sB, Slot* sC, F2* tq, F2* tp) {
     if (restart) {
 #pragma unroll
       for (int pp = 0; pp < PP; ++pp) {
@@ -355,14 +370,16 @@ struct ExactStripPol : ExactPol {
     }
     constexpr float kL = -16.0f / 7.0f;
     const float kab = kL * fabsf(R.v1.w), kbc = kL * fabsf(R.v2.w), kca = kL * R.n.w;
-    const float nz2 = 2.0f * R.n.z, wal2 = 2.0f * w.alpha;  // alpha from corner C (row())
-    F2 tq[PP], tp[PP];
+    // t/2 = alpha / (2 beta) is what the division gives; the series is taken
+    // in (t/2)^2 with its coefficients scaled by powers of 2, so
+    // (t/2) (2 p(t^2)) rounds exactly as t p(t^2) does, without doubling alpha
+    constexpr float kC2 = 32.0f * 0.19669890403747559f, kC1 = 8.0f * -0.33331409096717834f;
     float ms = 0.0f;
     bool cond = true;
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
       const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
-      const F2 alpha2 = fma2(f2s(nz2), cz, f2s(wal2));
+      const F2 alpha = fma2(f2s(R.n.z), cz, f2s(w.alpha));  // alpha from corner C (row_c())
       const F2 lc = sqrt2(fma2(cz, cz, f2s(w.c2)));
       const F2 la = sA[pp].d, lb = sB[pp].d;
       const F2 sbc = add2(lb, lc), sca = add2(lc, la);
@@ -376,21 +393,25 @@ struct ExactStripPol : ExactPol {
       split(x, x0, x1);
       split(lp, l0, l1);
       cond = cond && (l0 > -x0) && (l1 > -x1);
-      const F2 tt = mul2(alpha2, rcp2(beta2));
-      const F2 s = mul2(tt, tt);
+      const F2 th = mul2(alpha, rcp2(beta2));  // t/2
+      const F2 s4 = mul2(th, th);               // t^2/4
       float s0, s1;
-      split(s, s0, s1);
+      split(s4, s0, s1);
       ms = fmaxf(ms, fmaxf(s0, s1));
-      tq[pp] = tt;
-      tp[pp] = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
-                    f2s(1.0f));
+      tq[pp] = th;
+      tp[pp] = fma2(fma2(s4, f2s(kC2), f2s(kC1)), s4, f2s(2.0f));
     }
     const bool near = fminf(w.a2, fminf(w.b2, w.c2)) < ctx.eps2;
-    if (ms < 1.0f / 64.0f && cond && !near) {
-#pragma unroll
-      for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
-      return 0u;
-    }
+    return ms < 1.0f / 256.0f && cond && !near;  // t^2 < 1/64
+  }
+  // A face whose pairs are not all common: tail2 per lane, from squared
+  // distances recomputed from the record (the row parts bitwise the carried
+  // ones); returns the lanes for the fp64 path
+  template <int PP>
+  __device__ __forceinline__ static uint32_t strip_slow(const Rec& R, float qx, float qy,
+                                                        const F2* qz, const Ctx& ctx, F2* tacc) {
+    Row w = row_c(R, qx, qy);
+    row_ab(R, qx, qy, w.a2, w.b2);
     uint32_t rare = 0;
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
