@@ -28,6 +28,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", str(CSRC), "-I", str(INCLUDE)]
 # files whose f64 arithmetic must not be FMA-contracted
+# host code that runs on all cores (parallel sorts of the strip builder)
+OPENMP = {"wv_strip.cu"}
 NO_FMAD = {"wv_pack.cu", "wv_f64.cu", "wv_mc.cu", "wv_metrics.cu", "wv_strip.cu"}
 
 
@@ -64,13 +66,15 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", str(src), "-o", str(obj)]
         if src.name in NO_FMAD:
             cmd.insert(-4, "-fmad=false")
+        if src.name in OPENMP:
+            cmd[-4:-4] = ["-Xcompiler", "-fopenmp"]
         if verbose:
             cmd.insert(-4, "-Xptxas=-v")
         print("[windvox_b200] nvcc", src.name, flush=True)
         subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
         cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
-               "-lrt", "-lpthread", "-ldl"]
+               "-lrt", "-lpthread", "-ldl", "-lgomp"]
         subprocess.run(cmd, check=True)
     return LIB
 

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <parallel/algorithm>  // __gnu_parallel::sort (OpenMP: the host's cores)
 #include <vector>
 
 #include "wv_kernels.h"
@@ -47,7 +48,9 @@ int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int6
       std::memcpy(&o.z, verts + 3 * i + 2, 8);
       o.i = i;
     }
-    std::sort(ord.begin(), ord.end(), [](const VK& a, const VK& b) {
+    // both comparators are total orders (ties broken by index), so the
+    // parallel sort's result does not depend on the thread count
+    __gnu_parallel::sort(ord.begin(), ord.end(), [](const VK& a, const VK& b) {
       if (a.x != b.x) return a.x < b.x;
       if (a.y != b.y) return a.y < b.y;
       if (a.z != b.z) return a.z < b.z;
@@ -85,7 +88,7 @@ int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int6
     he.push_back({ekey(b, c), 3 * f + 1});
     he.push_back({ekey(c, a), 3 * f + 2});
   }
-  std::sort(he.begin(), he.end(), [](const HE& x, const HE& y) {
+  __gnu_parallel::sort(he.begin(), he.end(), [](const HE& x, const HE& y) {
     return x.key < y.key || (x.key == y.key && x.slot < y.slot);
   });
   std::vector<int64_t> run((size_t)n_faces * 3, -1);
