@@ -130,3 +130,24 @@ def test_strip_pairs_reuse_the_forward_order():
     b = device.strip_pairs(v, f, w, device.strip_order(v, f))
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_strip_order_independent_of_thread_count():
+    """The builder's sorts run on all host cores (__gnu_parallel::sort); both
+    comparators are total orders, so the strips must not depend on the
+    OpenMP thread count (wv_strip.cu)."""
+    import ctypes
+    v, f = configs.soup(*configs.torus(0.7, 0.3, 120, 80), seed=7)  # 19,200 faces
+    gomp = ctypes.CDLL("libgomp.so.1")
+    default = gomp.omp_get_max_threads()
+    ref = None
+    try:
+        for n in (1, 2, 3, 8):
+            gomp.omp_set_num_threads(n)
+            got = _strips(v, f)
+            if ref is None:
+                ref = got
+            for a, b in zip(ref, got):
+                assert np.array_equal(a, b), n
+    finally:
+        gomp.omp_set_num_threads(default)
