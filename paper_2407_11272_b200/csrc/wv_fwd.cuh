@@ -143,9 +143,12 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     if constexpr (Pol::kStrip && kRows) {
       static_assert(PP <= Pol::kGroup, "strip faces are decided for all point pairs at once");
       // one strip face's common-path terms; the slots rotate by kRot
-      auto fast = [&](const Rec& R, auto rot, F2* tq, F2* tp) -> bool {
+      // may_restart: false when the caller has checked that R continues its
+      // strip (then the block has no restart branch)
+      auto fast = [&](const Rec& R, auto rot, F2* tq, F2* tp, auto may_restart) -> bool {
         constexpr int kRot = decltype(rot)::value;
-        const bool restart = __float_as_int(R.v1.w) < 0;  // uniform per face
+        const bool restart =
+            decltype(may_restart)::value && __float_as_int(R.v1.w) < 0;  // uniform per face
         // the row parts of |A - q|^2, |B - q|^2 are the previous faces'
         // |C - q|^2 row parts (ring of 3, like the distance slots)
         typename Pol::Row w = Pol::row_c(R, rx, ry);
@@ -169,11 +172,13 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #ifndef WV_STRIP_PAIR_TERMS
 #define WV_STRIP_PAIR_TERMS 1  // 1287.6 ms vs 1290.7 (speculative tacc) on C3
 #endif
-      auto pair = [&](const Rec& Ra, const Rec& Rb, auto rota, auto rotb) {
+      using Yes = std::true_type;
+      using No = std::false_type;
+      auto pair_body = [&](const Rec& Ra, const Rec& Rb, auto rota, auto rotb, auto mr) {
 #if WV_STRIP_PAIR_TERMS
         F2 tqa[PP], tpa[PP], tqb[PP], tpb[PP];  // both faces' terms
-        const bool oka = fast(Ra, rota, tqa, tpa);
-        const bool okb = fast(Rb, rotb, tqb, tpb);
+        const bool oka = fast(Ra, rota, tqa, tpa, mr);
+        const bool okb = fast(Rb, rotb, tqb, tpb, mr);
         if (oka && okb) {
 #pragma unroll
           for (int pp = 0; pp < PP; ++pp)
@@ -187,12 +192,12 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         bool oka;
         {
           F2 tq[PP], tp[PP];
-          oka = fast(Ra, rota, tq, tp);
+          oka = fast(Ra, rota, tq, tp, mr);
 #pragma unroll
           for (int pp = 0; pp < PP; ++pp) ta[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
         }
         F2 tq[PP], tp[PP];
-        const bool okb = fast(Rb, rotb, tq, tp);
+        const bool okb = fast(Rb, rotb, tq, tp, mr);
         if (oka && okb) {
 #pragma unroll
           for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], ta[pp]);
@@ -207,9 +212,17 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         }
 #endif
       };
+      // one restart test per pair: the common case (both faces continue a
+      // strip) runs as one basic block up to the commit test
+      auto pair = [&](const Rec& Ra, const Rec& Rb, auto rota, auto rotb) {
+        if ((__float_as_int(Ra.v1.w) | __float_as_int(Rb.v1.w)) < 0)
+          pair_body(Ra, Rb, rota, rotb, Yes{});
+        else
+          pair_body(Ra, Rb, rota, rotb, No{});
+      };
       auto one = [&](const Rec& R, auto rot) {
         F2 tq[PP], tp[PP];
-        const bool ok = fast(R, rot, tq, tp);
+        const bool ok = fast(R, rot, tq, tp, Yes{});
         commit(R, ok, tq, tp);
       };
       // unrolled by 6 so the slot rotation is static
