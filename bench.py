@@ -50,14 +50,14 @@ EXACT_BWD_FLOPS = 170
 # algorithmic counts above: the algorithmic-FLOP rate can exceed the FP32
 # peak, and the executed-work fractions below are the pipe utilisation.
 # strip-ordered forward (the lattice default from 2M nodes): measured from the
-# ncu executed-instruction mix on c3s (tools/sass_exec_mix.py; 9.6% strip
-# restarts there, 4.3% on C3); the face-ordered kernel executed 42.25 / 4 MUFU
-EXACT_FWD_EXEC_FLOPS = 28.0    # fwd_f32_kernel<ExactStripPol,RowSrc> (profiles/r01_ncu_c3s_fwd_v64_summary.txt)
+# ncu executed-instruction mix on the full C3 lattice (tools/sass_exec_mix.py;
+# 4.3% strip restarts); the face-ordered kernel executed 42.25 / 4 MUFU
+EXACT_FWD_EXEC_FLOPS = 25.7    # fwd_f32_kernel<ExactStripPol,RowSrc> (profiles/r01_ncu_c3_fwd_v73_summary.txt)
 EXACT_FWD_FACE_ORDER_EXEC_FLOPS = 42.25  # fwd_f32_kernel<ExactPol,RowSrc>, all-common fast path
 # strip-pair backward (the lattice default from 2M nodes), ncu executed mix on
 # c3s; the single-face kernel executed 60.5 / 4 MUFU (static SASS count)
 EXACT_BWD_EXEC_FLOPS = 49.0    # bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>
-EXACT_FWD_MUFU = 2.2  # 1 sqrt (+2 per strip restart) + 1 rcp; face-ordered: 4
+EXACT_FWD_MUFU = 2.09  # 1 sqrt (+2 per strip restart) + 1 rcp; face-ordered: 4
 SOFT_STEP_FLOPS = 15 + 72  # soft forward + soft backward, pinned
 EXACT_BWD_MUFU = 3.1  # 2 rsqrt + 1 rcp per face and pair (+ rare paths)
 
@@ -77,7 +77,7 @@ def traffic(workload: str, kernel: str):
 # packed f32x2 op), from the same ncu executed-instruction mixes: the FMA
 # pipe issues 128 lane-ops per clock per SM whatever the op, so this (not the
 # FLOP count, where an add is half an FMA) is what bounds the kernels.
-EXACT_FWD_LANE_OPS = 19.2   # strip forward (c3s mix, alpha from corner C)
+EXACT_FWD_LANE_OPS = 17.4   # strip forward (C3 mix, v73: row parts carried, two faces per decision)
 EXACT_BWD_LANE_OPS = 31.7   # strip-pair backward (c3s mix)
 
 
