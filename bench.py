@@ -10,17 +10,27 @@ the FP32 path: pack the (moved) mesh, exact forward over the rank's i-slab,
 fused loss terms against a fixed target occupancy, exact backward, vertex
 gather, and (N>1) one all-reduce of [grad numerator | loss sums].  Synthetic
 inputs (no network); the target is the binarized exact occupancy of the same
-soup scaled by 1.03, computed once before timing.  At this size both
-directions run over face strips (strip-ordered forward, strip-pair backward;
-DESIGN.md 3.1b / 3.3b).
+soup scaled by 1.03, computed once before timing.  ``value`` is the
+fwd+bwd pair rate of the whole step; the forward (= the 256^3 voxelize) and
+backward rates and ``voxelize_ms`` ride along.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c3r|c1|c2|c3s|c3rs|c4|c5] [--precision f32|f64]
 
-Under torchrun each rank owns 1/N of the grid (weak scaling in pairs per
-GPU is NOT what this is: total work is fixed, so scaling is "strong"); time
-is the max over ranks.  ``--impl reference`` times the reference's CPU
-algorithm (the bit-exact C port in oracle/, all host threads) on a bounded
-node sample of the same workload, rank 0 only.
+``--gpus N`` without torchrun re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL); each rank owns
+1/N of the grid (total work fixed: "strong" scaling), time is the max over
+ranks.  ``--impl reference`` times the reference's CPU algorithm (the
+bit-exact C port in oracle/, all host threads) on a bounded node sample of the
+same workload, rank 0 only, and prints the SAME metric / unit / config.
+
+Roofline: ``achieved``/``frac`` are the dominant kernel's EXECUTED FLOP rate
+(per-pair counts from the committed ncu capture profiles/exec_mix.json)
+against the FP32 (FP64 for --precision f64) CUDA-core peak;
+``algorithmic_achieved``/``algorithmic_frac`` use SURVEY 8d's pinned FLOPs per
+pair (which the lattice-row / strip / edge-form kernels undercut, so that
+figure can exceed 1); ``fma_pipe_frac`` / ``xu_frac`` are the two pipes'
+utilisation.
 """
 
 from __future__ import annotations
@@ -29,6 +39,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -39,27 +50,36 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+# BASELINE.json's metric, printed verbatim by BOTH arms (the driver pairs the
+# lines by metric + unit); the per-direction figures ride in extra keys
+METRIC = "point-triangle solid-angle evals/sec fwd & fwd+bwd; 256^3 voxelize ms"
+UNIT = "pairs/s"
+
 # algorithmic work per point-triangle pair
-EXACT_FWD_FLOPS = 63
-EXACT_BWD_FLOPS = 170
-# What the kernels actually EXECUTE per pair, from the SASS of their inner
-# loops (tools/sass_loop_mix.py; FMA = 2 FLOPs; MUFU = XU-pipe ops).  The
-# lattice-row kernels hoist the x/y parts of every pair term out of the pair
-# loop, and the backward's edge (Biot-Savart) form is cheaper than the pinned
-# face-wise closed form, so they execute FEWER FLOPs than the pinned
-# algorithmic counts above: the algorithmic-FLOP rate can exceed the FP32
-# peak, and the executed-work fractions below are the pipe utilisation.
-# strip-ordered forward (the lattice default from 2M nodes): measured from the
-# ncu executed-instruction mix on the full C3 lattice (tools/sass_exec_mix.py;
-# 4.3% strip restarts); the face-ordered kernel executed 42.25 / 4 MUFU
-EXACT_FWD_EXEC_FLOPS = 25.7    # fwd_f32_kernel<ExactStripPol,RowSrc> (profiles/r01_ncu_c3_fwd_v73_summary.txt)
-EXACT_FWD_FACE_ORDER_EXEC_FLOPS = 42.25  # fwd_f32_kernel<ExactPol,RowSrc>, all-common fast path
-# strip-pair backward (the lattice default from 2M nodes), ncu executed mix on
-# c3s; the single-face kernel executed 60.5 / 4 MUFU (static SASS count)
-EXACT_BWD_EXEC_FLOPS = 49.0    # bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>
-EXACT_FWD_MUFU = 2.09  # 1 sqrt (+2 per strip restart) + 1 rcp; face-ordered: 4
-SOFT_STEP_FLOPS = 15 + 72  # soft forward + soft backward, pinned
-EXACT_BWD_MUFU = 3.1  # 2 rsqrt + 1 rcp per face and pair (+ rare paths)
+PINNED = {"exact_fwd": 63, "exact_bwd": 170, "soft_fwd": 15, "soft_bwd": 72}
+
+# the kernels each path launches (names as in the ncu launch list / exec_mix.json)
+KERNELS = {
+    ("f32", "fwd", True): "fwd_f32_kernel<ExactStripPol,RowSrc>",
+    ("f32", "fwd", False): "fwd_f32_kernel<ExactPol,RowSrc>",
+    ("f32", "bwd", True): "bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>",
+    ("f32", "bwd", False): "bwd_f32_kernel<ExactEdgeBwd,RowSrc>",
+    ("f64", "fwd", True): "fwd_f64_strip_kernel<GridSrc>",
+    ("f64", "fwd", False): "fwd_f64_kernel<ExactF64Pol,GridSrc>",
+    ("f64", "bwd", False): "bwd_f64_kernel<ExactBwd64,GridSrc>",
+}
+
+
+def exec_mix(kernel: str, workload: str):
+    """Executed work per pair of ``kernel`` from profiles/exec_mix.json: the
+    entry for this workload, else the kernel's first entry (None if absent)."""
+    try:
+        ents = json.loads((ROOT / "profiles" / "exec_mix.json").read_text())["entries"]
+    except (OSError, ValueError, KeyError):
+        return None
+    hits = [e for e in ents if e["kernel"] == kernel]
+    exact = [e for e in hits if e["workload"] == workload]
+    return (exact or hits or [None])[0]
 
 
 def traffic(workload: str, kernel: str):
@@ -68,47 +88,84 @@ def traffic(workload: str, kernel: str):
         t = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(workload)
     except (OSError, ValueError):
         return None
-    if not t or t["kernel"].split("<")[0] not in kernel:
+    if not t or t["kernel"] != kernel:
         return None
     return t["read"] + t["write"]
 
 
-# FMA-pipe lane-ops per pair (one per lane of every FFMA/FADD/FMUL, two per
-# packed f32x2 op), from the same ncu executed-instruction mixes: the FMA
-# pipe issues 128 lane-ops per clock per SM whatever the op, so this (not the
-# FLOP count, where an add is half an FMA) is what bounds the kernels.
-EXACT_FWD_LANE_OPS = 17.4   # strip forward (C3 mix, v73: row parts carried, two faces per decision)
-EXACT_BWD_LANE_OPS = 31.7   # strip-pair backward (c3s mix)
+def peaks(precision: str = "f32"):
+    """CUDA-core peak, TFLOP/s: 148 SMs x lanes x 2 FLOP/FMA x max clock
+    (FP32 128 lanes, FP64 64 lanes per SM); MEASURED_PEAKS.json has no
+    FP32/FP64 entry, only the clock."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    sm_mhz, src = 1965.0, "nominal 1965 MHz"
+    if p.exists():
+        d = json.loads(p.read_text())
+        sm_mhz = float(d.get("sm_max_mhz", sm_mhz))
+        src = "MEASURED_PEAKS.json sm_max_mhz"
+    lanes = 128 if precision == "f32" else 64
+    return 148 * lanes * 2 * sm_mhz * 1e6 / 1e12, \
+        f"{'FP32' if lanes == 128 else 'FP64'} CUDA-core peak 148 SM x {lanes} lanes x 2 x " \
+        f"clock ({src})"
 
 
-def executed(alg_tf, alg_flops, exec_flops, mufu, ms, peak, clk_mhz, lane_ops=None):
-    """Roofline of one kernel: pinned-algorithmic rate plus the utilisation of
-    the two pipes it actually runs on (FP32 FMA pipe, XU/MUFU pipe at 16 ops
-    per clock per SM)."""
-    pairs_s = alg_tf * 1e12 / alg_flops
-    xu_peak = 148 * 16 * clk_mhz * 1e6
-    r = {"achieved": alg_tf, "frac": alg_tf / peak, "kernel_ms": ms,
-         "executed_flops_per_pair": exec_flops, "mufu_per_pair": mufu,
-         "fma_frac": pairs_s * exec_flops / 1e12 / peak,
-         "xu_frac": pairs_s * mufu / xu_peak}
-    if lane_ops:
-        r["fma_lane_ops_per_pair"] = lane_ops
-        r["fma_pipe_frac"] = pairs_s * lane_ops / (148 * 128 * clk_mhz * 1e6)
-    return r
+def measured_peaks():
+    """FP32 (FFMA/FFMA2) and FP64 (DFMA) throughput measured on this GPU by
+    tools/ffma2_probe, TFLOP/s: {"f32": x, "f64": y} (None if unavailable)."""
+    exe = ROOT / "tools" / "ffma2_probe"
+    out = {"f32": None, "f64": None}
+    if not exe.exists():
+        return out
+    try:
+        txt = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout
+    except Exception:
+        return out
+    f32 = [float(ln.split()[-2]) for ln in txt.splitlines() if "TFLOP/s" in ln
+           and ln.startswith("FFMA")]
+    f64 = [float(ln.split()[-2]) for ln in txt.splitlines() if ln.startswith("DFMA")]
+    out["f32"] = max(f32) if f32 else None
+    out["f64"] = max(f64) if f64 else None
+    return out
 
 
-def parse():
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c3")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target duration of the CPU-baseline sample")
+    ap.add_argument("--precision", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--cpu-nodes", type=int, default=65536,
+                    help="lattice nodes in the CPU-baseline sample (SURVEY 8d: 65,536)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def spawn_ranks(args) -> int:
+    """``--gpus N`` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks on 127.0.0.1 (one process per GPU)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def init_dist(local: int, world: int):
@@ -134,36 +191,10 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def peaks():
-    p = ROOT / "MEASURED_PEAKS.json"
-    sm_mhz, src = 1965.0, "nominal 1965 MHz"
-    if p.exists():
-        d = json.loads(p.read_text())
-        sm_mhz = float(d.get("sm_max_mhz", sm_mhz))
-        src = "MEASURED_PEAKS.json sm_max_mhz"
-    # FP32 CUDA-core peak: 148 SMs x 128 FP32 lanes x 2 FLOP/FMA x clock
-    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, src
-
-
-def measured_fp32_peak():
-    """FP32 FMA throughput measured on this GPU by tools/ffma2_probe (16
-    independent FMA chains per thread, FFMA and packed FFMA2), TFLOP/s."""
-    import subprocess
-    exe = ROOT / "tools" / "ffma2_probe"
-    if not exe.exists():
-        return None
-    try:
-        out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout
-        vals = [float(line.split()[-2]) for line in out.splitlines() if "TFLOP/s" in line]
-        return max(vals) if vals else None
-    except Exception:
-        return None
-
-
 class ClockSampler:
     """SM clock / throttle reasons sampled (NVML) DURING the timed region."""
 
-    def __init__(self, index: int, period: float = 0.25):
+    def __init__(self, index: int, period: float = 0.1):
         self.index, self.period = index, period
         self.samples = []
         self._stop = threading.Event()
@@ -214,6 +245,51 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml"}
 
 
+def count_launches(fn) -> int | None:
+    """Kernels of OUR library (namespace wv::) one call of ``fn`` launches,
+    counted by the CUDA activity trace (torch.profiler/CUPTI) on an untimed
+    call; None if the tracer is unavailable."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        n = sum(1 for e in prof.events()
+                if e.device_type.name == "CUDA" and "wv::" in e.name)
+        return n or None
+    except Exception:
+        return None
+
+
+def roofline(kernel: str, workload: str, pairs: float, ms: float, alg_flops: float,
+             precision: str, clk_mhz: float, bound: str):
+    """Roofline of one kernel launch: executed FLOP rate (committed ncu mix)
+    against the CUDA-core peak, the pinned-algorithm rate beside it, and the
+    FMA / XU pipe utilisation."""
+    peak, peak_src = peaks(precision)
+    pairs_s = pairs / (ms / 1e3)
+    alg = alg_flops * pairs_s / 1e12
+    e = exec_mix(kernel, workload)
+    r = {"bound": bound, "unit": "TFLOP/s", "peak": peak, "kernel": kernel, "kernel_ms": ms,
+         "pairs_per_launch": pairs, "algorithmic_flops_per_pair": alg_flops,
+         "algorithmic_achieved": alg, "algorithmic_frac": alg / peak, "peak_source": peak_src}
+    if e is None:
+        r.update(achieved=None, frac=None, exec_mix_source=None)
+        return r
+    fl = e["flops"] if precision == "f32" else e.get("dflops") or e["flops"]
+    r.update(achieved=fl * pairs_s / 1e12, frac=fl * pairs_s / 1e12 / peak,
+             executed_flops_per_pair=fl,
+             exec_mix_source=f"{e['source']} [{e['workload']}]")
+    if e.get("lane_ops"):
+        r["fma_pipe_frac"] = pairs_s * e["lane_ops"] / (148 * 128 * clk_mhz * 1e6)
+        r["fma_lane_ops_per_pair"] = e["lane_ops"]
+    if e.get("mufu"):
+        r["xu_frac"] = pairs_s * e["mufu"] / (148 * 16 * clk_mhz * 1e6)
+        r["mufu_per_pair"] = e["mufu"]
+    return r
+
+
 # ---------------------------------------------------------------------------
 # CPU side: the reference algorithm (bit-exact C port, oracle/) on a sample
 
@@ -225,33 +301,88 @@ def _nodes(w, idx):
     return np.stack([ax[0][i], ax[1][j], ax[2][k]], axis=1)
 
 
-def cpu_fwd_bwd_rate(w, seconds: float, threads: int, seed: int = 0):
-    """Exact f64 forward (reference exact_batch, bit-exact port) + exact f64
-    gradient (closed-form oracle; the reference has no exact-gradient kernel)
-    on a seeded node sample sized for ~`seconds` on `threads` threads.
-    Returns (fwd+bwd pairs/s, fwd pairs/s, nodes, wall s)."""
+def cpu_fwd_bwd(vertices, faces, w, n: int, threads: int, mode: str = "exact", seed: int = 0,
+                precision: str = "f64"):
+    """Reference CPU algorithm on ``n`` seeded random lattice nodes: forward
+    (bit-exact C port of _kernels.exact_batch / soft_batch) + gradient
+    (exact: closed-form oracle -- the reference has no exact-gradient kernel;
+    soft: port of _kernels.soft_grad_accum with the reference's per-chunk
+    buffers, grad.py:113-127).  Returns (fwd+bwd pairs/s, fwd pairs/s, wall s)."""
     from oracle import oracle as orc
     rng = np.random.default_rng(seed)
-    probe = max(threads * 32, 64)  # large enough that per-call staging does not dominate
-    pts = _nodes(w, rng.choice(w.n_nodes, size=probe, replace=False))
-    t0 = time.perf_counter()
-    orc.winding_number_batch(w.vertices, w.faces, pts, chunk=1, threads=threads)
-    orc.exact_grad(w.vertices, w.faces, pts, np.ones(probe), chunk=1, threads=threads)
-    rate = probe * w.n_faces / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(w.n_nodes, max(threads * 4, rate * seconds / w.n_faces)))
     pts = _nodes(w, np.sort(rng.choice(w.n_nodes, size=n, replace=False)))
+    if precision == "f32":
+        pts = pts.astype(np.float32).astype(np.float64)
+    F = len(faces)
     chunk = max(1, n // (threads * 4))
     t0 = time.perf_counter()
-    vals, flags = orc.winding_number_batch(w.vertices, w.faces, pts, chunk=chunk, threads=threads)
+    vals, flags = orc.winding_number_batch(vertices, faces, pts, mode=mode, chunk=chunk,
+                                           threads=threads)
     t_f = time.perf_counter() - t0
     coefs = np.where(flags, 0.0, 2.0 * (vals - (vals > 0.5)))
-    # one (V,3) buffer per chunk in the reference's merge (grad.py:113-127)
     gchunk = max(chunk, n // threads)
+    gfn = orc.exact_grad if mode == "exact" else orc.soft_grad
     t1 = time.perf_counter()
-    orc.exact_grad(w.vertices, w.faces, pts, coefs, chunk=gchunk, threads=threads)
+    gfn(vertices, faces, pts, coefs, chunk=gchunk, threads=threads)
     t_b = time.perf_counter() - t1
-    return n * w.n_faces / (t_f + t_b), n * w.n_faces / t_f, n, t_f + t_b
+    return n * F / (t_f + t_b), n * F / t_f, t_f + t_b
 
+
+def cpu_fwd(vertices, faces, w, n: int, threads: int, seed: int = 0):
+    """Exact forward only (C5 is forward-only)."""
+    from oracle import oracle as orc
+    rng = np.random.default_rng(seed)
+    pts = _nodes(w, np.sort(rng.choice(w.n_nodes, size=n, replace=False)))
+    t0 = time.perf_counter()
+    orc.winding_number_batch(vertices, faces, pts, chunk=max(1, n // (threads * 4)),
+                             threads=threads)
+    dt = time.perf_counter() - t0
+    return n * len(faces) / dt, dt
+
+
+def cpu_desc(threads: int, n: int, what: str, dt: float):
+    return {"unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": "port",
+            "sample": f"{n} seeded random lattice nodes x all faces: {what}; {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# workload descriptions shared by both arms
+
+def exact_config(w, precision: str, world: int, active: int | None = None):
+    c = {"workload": w.name, "faces": w.n_faces, "grid": list(w.res), "mode": "exact",
+         "precision": precision,
+         "step": "pack + exact fwd + loss + exact bwd + vertex gather"
+                 + (" + all-reduce" if world > 1 else ""),
+         "l2": "256 MiB buffer zeroed between timed steps (> 126 MB L2)",
+         "parallelism": f"i-slabs x{world}"}
+    if active is not None:
+        c["active_bwd_faces"] = active
+    return c
+
+
+def c4_config(world: int, B=64, R=64, n_faces=5120):
+    return {"workload": "c4_64x_icosphere4_64", "meshes": B, "faces_per_mesh": n_faces,
+            "grid": [R] * 3, "mode": "soft", "precision": "f32",
+            "parallelism": f"mesh DP x{world}",
+            "step": "MLP fwd + fused soft fwd/loss/bwd per mesh + MLP bwd + Adam",
+            "l2": "inputs re-read every step; 67 MB targets + 16.8 MB W per step"}
+
+
+def c5_config(w, world: int):
+    return {"workload": w.name, "faces": w.n_faces, "grid": list(w.res), "mode": "exact",
+            "precision": "f32", "step": "pack + exact forward (voxelize, flagged -> 0.5)",
+            "l2": "outputs 537 MB per step (> L2)", "parallelism": f"i-slabs x{world}"}
+
+
+def line_base(args, world, value, ms_step, dtype, config):
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": dtype, "data": "synthetic", "config": config}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
 
 def run_reference(args):
     rank, world, _ = dist_env()
@@ -259,46 +390,72 @@ def run_reference(args):
         return 0
     from oracle import oracle as orc
     from paper_2407_11272_b200 import configs
-    w = configs.make(args.config)
     threads = orc.default_threads()
-    per = max(3.0, args.cpu_seconds / max(1, args.steps))
-    for _ in range(min(1, args.warmup)):
-        cpu_fwd_bwd_rate(w, 0.5, threads, seed=99)
-    rates, fwd, samples = [], [], []
+    steps = max(1, args.steps)
+    # the whole run samples args.cpu_nodes nodes (65,536), split
+    # evenly over the timed steps; warm-up steps use a small sample
+    per = max(64, -(-args.cpu_nodes // steps))
+    if args.config == "c4":
+        from paper_2407_11272_b200.configs import c4_batch
+        meshes = c4_batch(64)
+        g = configs.Workload("c4_mesh", *meshes[0], (-1.0,) * 3, (1.0,) * 3, (64,) * 3)
+        per = min(per, g.n_nodes)
+
+        def one(k, n):
+            v, f = meshes[k % 64]
+            r, rf, dt = cpu_fwd_bwd(v, f, g, n, threads, mode="soft", seed=k,
+                                    precision="f32")
+            return r, rf, dt
+        config = c4_config(world)
+        what = "soft f32-rounded nodes: fwd (port of soft_batch) + soft_grad_accum, one mesh"
+        pairs_per_step = 64 * 64 ** 3 * len(meshes[0][1])
+    elif args.config == "c5":
+        w = configs.make("c5")
+        per = max(64, -(-min(args.cpu_nodes, 8192) // steps))
+
+        def one(k, n):
+            r, dt = cpu_fwd(w.vertices, w.faces, w, n, threads, seed=k)
+            return r, r, dt
+        config = c5_config(w, world)
+        what = "exact f64 fwd (bit-exact C port of _kernels.exact_batch)"
+        pairs_per_step = w.pairs
+    else:
+        w = configs.make(args.config)
+
+        def one(k, n):
+            return cpu_fwd_bwd(w.vertices, w.faces, w, n, threads, seed=k)
+        config = exact_config(w, args.precision, world)
+        what = ("exact f64 fwd (bit-exact C port of _kernels.exact_batch) + exact f64 grad "
+                "(closed-form oracle; the reference has no exact-gradient kernel)")
+        pairs_per_step = w.pairs
+    for k in range(args.warmup):
+        one(1000 + k, 64)
+    rates, fwd, tot = [], [], 0.0
     t_all = time.perf_counter()
-    for k in range(args.steps):
-        r, rf, n, _ = cpu_fwd_bwd_rate(w, per, threads, seed=k)
+    for k in range(steps):
+        r, rf, dt = one(k, per)
         rates.append(r)
         fwd.append(rf)
-        samples.append(n)
+        tot += dt
     wall = time.perf_counter() - t_all
     rate = statistics.median(rates)
-    line = {
-        "impl": "reference",
-        "metric": "point-triangle solid-angle evals/sec, exact fwd+bwd (256^3 voxelize ms in "
-                  "extrapolated_voxelize_ms)",
-        "value": rate, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(1, args.steps),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": w.name, "faces": w.n_faces, "grid": list(w.res), "mode": "exact",
-                   "step": "bounded node sample: exact forward + exact gradient"},
+    line = line_base(args, world, rate, wall * 1e3 / steps, "f64" if args.config != "c4"
+                     else "f32", config)
+    line["impl"] = "reference"
+    line.update({
         "fwd_pairs_per_s": statistics.median(fwd),
-        "extrapolated_voxelize_ms": w.pairs / statistics.median(fwd) * 1e3,
-        "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": threads, "kind": "port",
-                         "sample": f"{samples} seeded random nodes of the {w.res[0]}^3 grid x "
-                                   f"{w.n_faces} faces per step; forward = bit-exact C port of "
-                                   "_kernels.exact_batch, backward = closed-form oracle "
-                                   "(no reference exact-gradient kernel exists)"},
-        "e2e": {"value": rate, "unit": "pairs/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
+        "extrapolated_step_s": pairs_per_step / rate,
+        "extrapolated_voxelize_ms": pairs_per_step / statistics.median(fwd) * 1e3,
+        "cpu_baseline": dict(cpu_desc(threads, per * steps, what + f"; {per} nodes per step",
+                                      tot), value=rate),
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# our arm: exact fwd+bwd step (C1/C2/C3/C3r and the quarter-size variants)
 
 def run_ours(args):
     import torch
@@ -308,9 +465,10 @@ def run_ours(args):
     dev = init_dist(local, world)
     local = dev.index
     from paper_2407_11272_b200 import configs, device
-    from paper_2407_11272_b200 import _lib as L
-    from paper_2407_11272_b200.distributed import SlabDriver, slab_range
+    from paper_2407_11272_b200.distributed import CudaSlabEvaluator, SlabDriver, slab_range
 
+    prec = args.precision
+    vdt = torch.float32 if prec == "f32" else torch.float64
     w = configs.make(args.config)
     n0, cnt = slab_range(w.n_nodes, rank, world)
     grid = (w.lo, w.hi, w.res)
@@ -318,7 +476,7 @@ def run_ours(args):
     # fixed target: binarized exact occupancy of the soup scaled by 1.03 (untimed)
     tmesh = device.DeviceMesh.from_numpy(w.vertices * 1.03, w.faces, dev)
     tv, _ = device.forward(tmesh, "exact", "f32", grid=grid, n0=n0, count=cnt)
-    targets = (tv > 0.5).to(torch.float32)
+    targets = (tv > 0.5).to(vdt)
     del tmesh, tv
 
     dmesh = device.DeviceMesh.from_numpy(w.vertices, w.faces, dev)
@@ -334,11 +492,11 @@ def run_ours(args):
                 ev[k].append(e)
         dmesh.invalidate()  # the vertices moved: re-stage every kernel's records
         mark("f0")
-        vals, flags = device.forward(dmesh, "exact", "f32", grid=grid, n0=n0, count=cnt)
+        vals, flags = device.forward(dmesh, "exact", prec, grid=grid, n0=n0, count=cnt)
         mark("f1")
         coefs, sums = device.loss_terms(vals, flags, targets)
         mark("b0")
-        fg = device.face_grad(dmesh, "exact", "f32", coefs, grid=grid, n0=n0, count=cnt)
+        fg = device.face_grad(dmesh, "exact", prec, coefs, grid=grid, n0=n0, count=cnt)
         mark("b1")
         g = device.vertex_grad(dmesh, fg)
         buf = torch.cat([g.reshape(-1), sums[:3]])
@@ -348,25 +506,15 @@ def run_ours(args):
 
     F = w.n_faces
     active = int(dmesh.exact_grad_setup()[0].shape[0])
-    # per step: [surface eps + pack + forward (+ split finalize)] + [loss terms +
-    # loss final] + [surface eps + pack + backward (+ split reduce)] + gather.
-    # Large lattices take the strip forward and the strip-pair backward
-    # (device.STRIP_MIN_NODES), whose split plans decide the optional launches.
-    strip_path = cnt >= device.STRIP_MIN_NODES
-    if strip_path:
-        n_rows = int(dmesh.exact_pair_setup()[0].shape[0])
-        fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACTSTRIP_F32, F, cnt)
-        bws = L.lib().wv_exact_pair_bwd_workspace_bytes(n_rows, cnt)
-    else:
-        fws = L.lib().wv_fwd_workspace_bytes(L.PACK_EXACT_F32, F, cnt)
-        bws = L.lib().wv_bwd_workspace_bytes(L.PACK_EXACTGRAD_F32, active, cnt)
-    bwd_launches = (3 + (1 if bws else 0)) if active > 0 else 1  # no active face: eps only
-    launches = 3 + (1 if fws else 0) + 2 + bwd_launches + 1
+    fwd_strip, bwd_pairs = device.lattice_paths(dmesh, "exact", prec, grid, n0, cnt)
+    kf = KERNELS[(prec, "fwd", fwd_strip)]
+    kb = KERNELS[(prec, "bwd", bwd_pairs)]
 
-    fp32_meas = measured_fp32_peak() if rank == 0 else None
+    meas = measured_peaks() if rank == 0 else {}
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    launches = count_launches(step)
 
     def barrier():
         if world > 1:
@@ -393,7 +541,8 @@ def run_ours(args):
     fwd_ms, bwd_ms = float(t[1]), float(t[2])
     value = w.pairs / (ms_step / 1e3)
 
-    # --- e2e: host numpy in (mesh + this rank's target slab), host grads out
+    # --- e2e: host numpy in (mesh + this rank's target slab), host grads out,
+    # through the public device path (DeviceMesh + SlabDriver.loss_grad)
     e2e = None
     if not args.no_e2e:
         tgt_host = targets.cpu().numpy()
@@ -403,7 +552,8 @@ def run_ours(args):
         def e2e_step():
             m = device.DeviceMesh.from_numpy(w.vertices, w.faces, dev)
             tg = torch.from_numpy(tgt_host).pin_memory().to(dev, non_blocking=True)
-            drv = SlabDriver(_E(m, grid), w.n_nodes, rank, world)
+            drv = SlabDriver(CudaSlabEvaluator(m, grid, mode="exact", precision=prec),
+                             w.n_nodes, rank, world)
             lo, gr, _, _ = drv.loss_grad(tg)
             return gr.cpu().numpy(), float(lo)
 
@@ -418,90 +568,54 @@ def run_ours(args):
                           dtype=torch.float64)
         if world > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": w.pairs / float(dt), "unit": "pairs/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h,
+        e2e = {"value": w.pairs / float(dt), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                "api": "DeviceMesh.from_numpy + SlabDriver(CudaSlabEvaluator).loss_grad "
                       "(grad.exact_loss_grad's device path), numpy in / numpy grads out"}
 
     if rank == 0:
-        peak, peak_src = peaks()
-        fwd_tf = EXACT_FWD_FLOPS * cnt * F / (fwd_ms / 1e3) / 1e12
-        # the exact backward launches only faces with a non-cancelling edge
-        # (all of them for a soup): count the pairs it actually evaluates
-        bwd_tf = EXACT_BWD_FLOPS * cnt * active / (bwd_ms / 1e3) / 1e12
+        clocks = clk.summary()
+        clk_mhz = clocks.get("sm_mhz") or 1965.0
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as orc
             thr = orc.default_threads()
-            r, rf, n, dt = cpu_fwd_bwd_rate(w, args.cpu_seconds, thr)
-            cpu = {"value": r, "unit": "pairs/s", "cores": thr, "kind": "port",
-                   "fwd_pairs_per_s": rf,
-                   "sample": f"{n} seeded random nodes of the {w.res[0]}^3 grid x {F} faces, "
-                             f"exact f64 fwd (bit-exact C port of _kernels.exact_batch) + exact "
-                             f"f64 grad (closed-form oracle), {dt:.1f} s"}
-        if strip_path:  # strip forward + strip-pair backward (device.STRIP_MIN_NODES)
-            kf, kb = "fwd_f32_kernel<ExactStripPol,RowSrc>", "bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>"
-            xf = (EXACT_FWD_EXEC_FLOPS, EXACT_FWD_MUFU, EXACT_FWD_LANE_OPS)
-            xb = (EXACT_BWD_EXEC_FLOPS, EXACT_BWD_MUFU, EXACT_BWD_LANE_OPS)
-        else:
-            kf, kb = "fwd_f32_kernel<ExactPol,RowSrc>", "bwd_f32_kernel<ExactEdgeBwd,RowSrc>"
-            xf = (EXACT_FWD_FACE_ORDER_EXEC_FLOPS, 4, 26.75)
-            xb = (60.5, 4, 34.7)
-        dom = (f"exact_bwd ({kb})", bwd_ms, bwd_tf) if bwd_ms >= fwd_ms \
-            else (f"exact_fwd ({kf})", fwd_ms, fwd_tf)
-        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
-        rfwd = executed(fwd_tf, EXACT_FWD_FLOPS, xf[0], xf[1], fwd_ms, peak, clk_mhz, xf[2])
-        rbwd = executed(bwd_tf, EXACT_BWD_FLOPS, xb[0], xb[1], bwd_ms, peak, clk_mhz, xb[2])
-        step_tf = (EXACT_FWD_FLOPS * cnt * F + EXACT_BWD_FLOPS * cnt * active) \
-            / (ms_step / 1e3) / 1e12
-        line = {
-            "metric": "point-triangle solid-angle evals/sec fwd & fwd+bwd; 256^3 voxelize ms",
-            "value": value, "unit": "pairs/s (exact fwd+bwd)", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": w.name, "faces": F, "grid": list(w.res), "mode": "exact",
-                       "step": "pack + exact fwd + loss + exact bwd + vertex gather"
-                               + (" + all-reduce" if world > 1 else ""),
-                       "l2": "256 MiB buffer zeroed between timed steps (> 126 MB L2)",
-                       "parallelism": f"i-slabs x{world}", "active_bwd_faces": active},
+            n = min(args.cpu_nodes, w.n_nodes)
+            r, rf, dt = cpu_fwd_bwd(w.vertices, w.faces, w, n, thr)
+            cpu = dict(cpu_desc(thr, n, "exact f64 fwd (bit-exact C port of "
+                                        "_kernels.exact_batch) + exact f64 grad (closed-form "
+                                        "oracle; no reference exact-gradient kernel exists)",
+                                dt), value=r, fwd_pairs_per_s=rf)
+        bound = "fp32 (FMA + XU pipes)" if prec == "f32" else "fp64"
+        rf_ = roofline(kf, w.name, cnt * F, fwd_ms, PINNED["exact_fwd"], prec, clk_mhz, bound)
+        rb_ = roofline(kb, w.name, cnt * active, bwd_ms, PINNED["exact_bwd"], prec, clk_mhz,
+                       bound)
+        dom = rb_ if bwd_ms >= fwd_ms else rf_
+        dom = dict(dom, traffic=traffic(w.name, dom["kernel"]),
+                   traffic_unit="dram read+write bytes per launch (profiles/traffic.json; "
+                                "null if not captured for this workload)",
+                   peak_measured=meas.get(prec),
+                   peak_measured_source="tools/ffma2_probe (FFMA/FFMA2 or DFMA chains, this "
+                                        "GPU, before the timed region)")
+        line = line_base(args, world, value, ms_step, prec, exact_config(w, prec, world, active))
+        line.update({
             "fwd_pairs_per_s": w.pairs / (fwd_ms / 1e3),
             "bwd_pairs_per_s": w.pairs / (bwd_ms / 1e3),
             "voxelize_ms": fwd_ms,
             "loss": float(loss),
-            "roofline": {"bound": "fp32", "achieved": dom[2], "peak": peak, "unit": "TFLOP/s",
-                         "frac": dom[2] / peak, "traffic": traffic(w.name, dom[0]),
-                         "traffic_unit": "bytes per launch", "kernel": dom[0],
-                         "kernel_ms": dom[1],
-                         "flops_per_pair": EXACT_BWD_FLOPS if dom[0].startswith("exact_bwd")
-                         else EXACT_FWD_FLOPS,
-                         # the pipe that bounds the kernel: FMA-pipe lane-ops actually
-                         # issued per pair (ncu mix) against 128 per clock per SM
-                         "fma_pipe_frac": (rbwd if dom[0].startswith("exact_bwd")
-                                           else rfwd)["fma_pipe_frac"],
-                         "peak_source": f"FP32 CUDA-core peak 148 SM x 128 lanes x 2 x clock "
-                                        f"({peak_src}); MEASURED_PEAKS has no FP32 entry",
-                         "peak_measured": fp32_meas,
-                         "peak_measured_source": "tools/ffma2_probe (FFMA/FFMA2 chains, this "
-                                                 "GPU, before the timed region)",
-                         "traffic_note": "dram read+write bytes per launch of this kernel "
-                                         "from one ncu --set full capture "
-                                         "(profiles/traffic.json); null if not captured for "
-                                         "this workload",
-                         "frac_note": "achieved uses the pinned algorithmic FLOPs/pair (SURVEY "
-                                      "8d); the kernels execute fewer (roofline_fwd/bwd "
-                                      "executed_flops_per_pair), so frac may exceed 1 -- "
-                                      "fma_frac / xu_frac there are the pipe utilisation"},
-            "roofline_fwd": rfwd,
-            "roofline_bwd": rbwd,
-            "roofline_step": {"achieved": step_tf, "frac": step_tf / peak,
-                              "note": "whole step: 63 FLOP per forward pair + 170 per "
-                                      "backward pair actually evaluated (active faces)"},
+            "paths": {"forward": kf, "backward": kb,
+                      "shared_corner_fraction": dmesh.shared_corner_fraction(),
+                      "strip_restart_fraction": dmesh.strip_restart_fraction()},
+            "roofline": dom,
+            "roofline_fwd": rf_,
+            "roofline_bwd": rb_,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches * args.steps,
-            "clocks": clk.summary(),
-        }
+            "gpu_launches": None if launches is None else launches * args.steps,
+            "gpu_launches_source": "torch.profiler CUDA activity: wv:: kernels of one untimed "
+                                   "step x steps",
+            "clocks": clocks,
+        })
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -509,38 +623,13 @@ def run_ours(args):
     return 0
 
 
-class _E:
-    """CudaSlabEvaluator in exact/f32 mode (the product evaluator)."""
+# ---------------------------------------------------------------------------
+# C4: the mesh-morphing training batch
 
-    def __new__(cls, dmesh, grid):
-        from paper_2407_11272_b200.distributed import CudaSlabEvaluator
-        return CudaSlabEvaluator(dmesh, grid, mode="exact", precision="f32")
-
-
-def run_c4(args):
-    """Config C4: a mesh-morphing training batch -- 64 meshes (icosphere(4),
-    5120 faces, seeded radial bumps) deformed by a random-init MLP
-    [xyz + 32-d latent -> 3, hidden 128x2], soft occupancy loss against
-    seeded primitive targets at 64^3; a step = net forward, fused soft
-    fwd+loss+bwd for every mesh, net backward, Adam step.  Multi-GPU: the
-    meshes shard over ranks, MLP gradients are all-reduced (DP)."""
+def c4_targets(ids, grid, dev):
+    """Exact occupancy of seeded primitives (cube / ellipsoid / torus)."""
     import torch
-    import torch.distributed as dist
-
-    rank, world, local = dist_env()
-    dev = init_dist(local, world)
-    local = dev.index
     from paper_2407_11272_b200 import configs, device
-    from paper_2407_11272_b200.batch import DeformationNet, batch_occupancy_loss
-
-    B, R = 64, 64
-    grid = ((-1.0,) * 3, (1.0,) * 3, (R, R, R))
-    per = B // world
-    ids = list(range(rank * per, (rank + 1) * per))
-    meshes = configs.c4_batch(B)
-    faces = torch.from_numpy(meshes[0][1]).to(dev)
-    tmpl = torch.stack([torch.from_numpy(meshes[b][0]) for b in ids]).to(dev, torch.float32)
-    # targets: exact occupancy of seeded primitives (cube / ellipsoid / torus)
     tg = []
     for b in ids:
         rng = np.random.default_rng(1000 + b)
@@ -558,30 +647,74 @@ def run_c4(args):
         dm = device.DeviceMesh.from_numpy(cv, cf, dev)
         w, _ = device.forward(dm, "exact", "f32", grid=grid)
         tg.append((w > 0.5).float())
-    targets = torch.stack(tg)
+    return torch.stack(tg)
+
+
+def run_c4(args):
+    """Config C4: a mesh-morphing training batch -- 64 meshes (icosphere(4),
+    5120 faces, seeded radial bumps) deformed by a random-init MLP
+    [xyz + 32-d latent -> 3, hidden 128x2], soft occupancy loss against
+    seeded primitive targets at 64^3; a step = net forward, fused soft
+    fwd+loss+bwd for every mesh, net backward, Adam step.  Multi-GPU: the
+    meshes shard over ranks, MLP gradients are all-reduced as ONE flattened
+    bucket (DP)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    dev = init_dist(local, world)
+    local = dev.index
+    from paper_2407_11272_b200 import configs, device
+    from paper_2407_11272_b200.batch import DeformationNet, batch_occupancy_loss
+
+    B, R = 64, 64
+    grid = ((-1.0,) * 3, (1.0,) * 3, (R, R, R))
+    per = B // world
+    ids = list(range(rank * per, (rank + 1) * per))
+    meshes = configs.c4_batch(B)
+    faces = torch.from_numpy(meshes[0][1]).to(dev)
+    tmpl_host = torch.stack([torch.from_numpy(meshes[b][0]) for b in ids]).to(torch.float32)
+    tmpl = tmpl_host.to(dev)
+    targets = c4_targets(ids, grid, dev)
     torch.manual_seed(0)
     net = DeformationNet(B).to(dev)
     opt = torch.optim.Adam(net.parameters(), lr=1e-4)  # soft-W MSE is spiky: 1e-3 oscillates
     mid = torch.tensor(ids, device=dev)
     csr = device.DeviceMesh(tmpl[0], faces).csr()
+    params = [p for p in net.parameters()]
+    gbuf = torch.zeros(sum(p.numel() for p in params), device=dev)
 
-    def step():
-        opt.zero_grad(set_to_none=True)
-        verts = net(tmpl, mid)
-        losses = batch_occupancy_loss(verts, faces, grid, targets, csr=csr)
+    def allreduce_grads():
+        # one bucket: flatten every parameter gradient, one NCCL all-reduce,
+        # scatter back (the DDP pattern without DDP's hooks)
+        off = 0
+        for p in params:
+            n = p.numel()
+            gbuf[off:off + n].copy_(p.grad.reshape(-1))
+            off += n
+        dist.all_reduce(gbuf)
+        gbuf.div_(world)
+        off = 0
+        for p in params:
+            n = p.numel()
+            p.grad.copy_(gbuf[off:off + n].view_as(p.grad))
+            off += n
+
+    def step(tm=tmpl, tg=targets):
+        opt.zero_grad(set_to_none=False)
+        verts = net(tm, mid)
+        losses = batch_occupancy_loss(verts, faces, grid, tg, csr=csr)
         loss = losses.mean()
         loss.backward()
         if world > 1:
-            for p in net.parameters():
-                if p.grad is not None:
-                    dist.all_reduce(p.grad)
-                    p.grad /= world
+            allreduce_grads()
         opt.step()
         return loss
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    launches = count_launches(step)
 
     def barrier():
         if world > 1:
@@ -603,34 +736,76 @@ def run_c4(args):
     ms_step = float(t) / args.steps
     n_faces = int(faces.shape[0])
     pairs = B * R ** 3 * n_faces
+
+    # e2e: every step copies its inputs (mesh templates + target occupancy)
+    # from pinned host memory and reads the loss back
+    e2e = None
+    if not args.no_e2e:
+        tm_pin = tmpl_host.pin_memory()
+        tg_pin = targets.to(torch.uint8).cpu().pin_memory()
+
+        def e2e_step():
+            tm = tm_pin.to(dev, non_blocking=True)
+            tg = tg_pin.to(dev, non_blocking=True).float()
+            return float(step(tm, tg))
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        dt = torch.tensor([(time.perf_counter() - t0) / args.steps], device=dev,
+                          dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs / float(dt), "unit": UNIT,
+               "h2d_bytes_per_step": tm_pin.numel() * 4 + tg_pin.numel(),
+               "d2h_bytes_per_step": 4, "steps": args.steps,
+               "api": "batch.batch_occupancy_loss (autograd) + Adam; templates (f32) and "
+                      "targets (u8) copied from pinned host each step, loss read back"}
     if rank == 0:
-        line = {
-            "metric": "point-triangle solid-angle evals/sec (C4: soft fwd+bwd training step)",
-            "value": pairs / (ms_step / 1e3), "unit": "pairs/s (soft fwd+bwd)", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "c4_64x_icosphere4_64", "meshes": B, "faces_per_mesh": n_faces,
-                       "grid": [R] * 3, "mode": "soft", "parallelism": f"mesh DP x{world}",
-                       "step": "MLP fwd + fused soft fwd/loss/bwd per mesh + MLP bwd + Adam"},
+        clocks = clk.summary()
+        clk_mhz = clocks.get("sm_mhz") or 1965.0
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as orc
+            thr = orc.default_threads()
+            g = configs.Workload("c4_mesh", *meshes[0], (-1.0,) * 3, (1.0,) * 3, (R,) * 3)
+            n = min(args.cpu_nodes, g.n_nodes)
+            r, rf, dt = cpu_fwd_bwd(meshes[0][0], meshes[0][1], g, n, thr, mode="soft",
+                                    precision="f32")
+            cpu = dict(cpu_desc(thr, n, "mesh 0: soft fwd (port of _kernels.soft_batch) + "
+                                        "soft_grad_accum (per-chunk buffers)", dt),
+                       value=r, fwd_pairs_per_s=rf)
+        peak, peak_src = peaks("f32")
+        alg = (PINNED["soft_fwd"] + PINNED["soft_bwd"]) * pairs / (ms_step / 1e3) / 1e12
+        line = line_base(args, world, pairs / (ms_step / 1e3), ms_step, "f32", c4_config(world))
+        line.update({
             "loss_first": float(losses[0].detach()), "loss_last": float(losses[-1].detach()),
-            "roofline": {"bound": "fp32", "unit": "TFLOP/s", "peak": peaks()[0],
-                         "achieved": SOFT_STEP_FLOPS * pairs / (ms_step / 1e3) / 1e12,
-                         "frac": SOFT_STEP_FLOPS * pairs / (ms_step / 1e3) / 1e12 / peaks()[0],
-                         "flops_per_pair": SOFT_STEP_FLOPS, "traffic": None,
+            "roofline": {"bound": "fp32", "unit": "TFLOP/s", "peak": peak,
+                         "achieved": None, "frac": None,
+                         "algorithmic_achieved": alg, "algorithmic_frac": alg / peak,
+                         "algorithmic_flops_per_pair": PINNED["soft_fwd"] + PINNED["soft_bwd"],
+                         "traffic": None, "peak_source": peak_src,
                          "note": "whole training step at the pinned soft fwd 15 + bwd 72 "
                                  "FLOP/pair (SURVEY 8d); MLP/Adam time included"},
-            # per batch: 2 packs x (eps + pack), 1 forward (+ split finalize),
-            # 2 loss kernels, 1 backward (+ split reduce), 1 gather
-            "gpu_launches": args.steps * 11,
-            "clocks": clk.summary(),
-        }
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": None if launches is None else launches * args.steps,
+            "gpu_launches_source": "torch.profiler CUDA activity: wv:: kernels of one untimed "
+                                   "step x steps",
+            "clocks": clocks,
+        })
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
+
+# ---------------------------------------------------------------------------
+# C5: 1M faces at 512^3, forward only
 
 def run_c5(args):
     """Config C5: 1M-face torus, exact forward only (voxelize,
@@ -661,6 +836,7 @@ def run_c5(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    launches = count_launches(step)
 
     def barrier():
         if world > 1:
@@ -670,7 +846,7 @@ def run_c5(args):
     stream = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, period=0.5) as clk:
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
@@ -681,30 +857,51 @@ def run_c5(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t) / args.steps
+
+    # e2e: the public voxelize from a host mesh to a host grid (537 MB D2H)
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(cnt, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            m = device.DeviceMesh.from_numpy(w.vertices, w.faces, dev)
+            v, _ = device.forward(m, "exact", "f32", grid=grid, n0=n0, count=cnt,
+                                  policy=L.POLICY_HALF)
+            host.copy_(v)
+
+        barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        barrier()
+        dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": w.pairs / float(dt), "unit": UNIT,
+               "h2d_bytes_per_step": w.vertices.nbytes + w.faces.nbytes,
+               "d2h_bytes_per_step": cnt * 4, "steps": 1,
+               "api": "DeviceMesh.from_numpy + device.forward (voxelize's device path), "
+                      "host values out"}
     if rank == 0:
-        peak, peak_src = peaks()
         clocks = clk.summary()
         clk_mhz = clocks.get("sm_mhz") or 1965.0
-        F = w.n_faces
-        fwd_tf = EXACT_FWD_FLOPS * cnt * F / (ms_step / 1e3) / 1e12
-        rf = executed(fwd_tf, EXACT_FWD_FLOPS, EXACT_FWD_EXEC_FLOPS, EXACT_FWD_MUFU, ms_step,
-                      peak, clk_mhz, EXACT_FWD_LANE_OPS)
-        line = {
-            "metric": "point-triangle solid-angle evals/sec (C5: exact forward / voxelize)",
-            "value": w.pairs / (ms_step / 1e3), "unit": "pairs/s (exact fwd)", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": w.name, "faces": F, "grid": list(w.res), "mode": "exact",
-                       "step": "pack + exact forward (voxelize, flagged -> 0.5)",
-                       "l2": "inputs (48 MB records) L2-resident by design; outputs 537 MB",
-                       "parallelism": f"i-slabs x{world}"},
-            "voxelize_ms": ms_step,
-            "roofline": dict(rf, bound="xu+fp32", peak=peak, unit="TFLOP/s",
-                             kernel="exact_fwd (fwd_f32_kernel<ExactStripPol,RowSrc>)",
-                             peak_source=peak_src, traffic=None),
-            "clocks": clocks,
-        }
+        fwd_strip, _ = device.lattice_paths(dmesh, "exact", "f32", grid, n0, cnt)
+        kf = KERNELS[("f32", "fwd", fwd_strip)]
+        rf = roofline(kf, w.name, cnt * w.n_faces, ms_step, PINNED["exact_fwd"], "f32", clk_mhz,
+                      "fp32 (FMA + XU pipes)")
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as orc
+            thr = orc.default_threads()
+            n = 8192
+            r, dt = cpu_fwd(w.vertices, w.faces, w, n, thr)
+            cpu = dict(cpu_desc(thr, n, "exact f64 fwd (bit-exact C port of "
+                                        "_kernels.exact_batch)", dt), value=r)
+        line = line_base(args, world, w.pairs / (ms_step / 1e3), ms_step, "f32",
+                         c5_config(w, world))
+        line.update({"voxelize_ms": ms_step, "roofline": dict(rf, traffic=None),
+                     "cpu_baseline": cpu, "e2e": e2e,
+                     "gpu_launches": None if launches is None else launches * args.steps,
+                     "clocks": clocks})
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -712,8 +909,10 @@ def run_c5(args):
     return 0
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "c4":

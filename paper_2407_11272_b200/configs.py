@@ -104,6 +104,25 @@ def soup(verts: np.ndarray, faces: np.ndarray, seed: int = 0):
                                                               dtype=np.int64).reshape(-1, 3)
 
 
+def random_soup(n_faces: int = 100_000, seed: int = 3, half: float = 0.8, edge: float = 0.05):
+    """C3's stress variant: ``n_faces`` independent triangles,
+    centres U[-half, half]^3, each an equilateral triangle of edge ~``edge``
+    (x U[0.8, 1.2]) in a uniformly random orientation, ``default_rng(seed)``.
+    No two faces share a corner position, so nothing welds: the strip
+    kernels cannot share distances and the face-ordered kernels run."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-half, half, size=(n_faces, 3))
+    # random orthonormal frames (QR of a Gaussian matrix, sign-fixed -> Haar)
+    q, r = np.linalg.qr(rng.normal(size=(n_faces, 3, 3)))
+    q = q * np.sign(np.diagonal(r, axis1=1, axis2=2))[:, None, :]
+    s = edge * rng.uniform(0.8, 1.2, size=n_faces) / np.sqrt(3.0)   # circumradius
+    ang = 2.0 * np.pi * np.arange(3) / 3.0
+    loc = np.stack([np.cos(ang), np.sin(ang)], axis=1)                 # (3, 2) in-plane
+    tri = c[:, None, :] + s[:, None, None] * np.einsum("kj,fij->fki", loc, q[:, :, :2])
+    return np.ascontiguousarray(tri.reshape(-1, 3)), np.arange(3 * n_faces,
+                                                             dtype=np.int64).reshape(-1, 3)
+
+
 def bumpy_icosphere(seed: int, subdivisions: int = 4, radius: float = 0.5):
     v, f = icosphere(subdivisions, radius)
     rng = np.random.default_rng(seed)
@@ -147,6 +166,12 @@ def make(name: str) -> Workload:
     if name == "c3":
         v, f = soup(*torus(0.7, 0.3, 250, 200), seed=0)
         return Workload("c3_torus100k_soup_256", v, f, *g, (256,) * 3)
+    if name == "c3r":  # C3 stress variant: random-triangle soup, nothing welds
+        v, f = random_soup(100_000, seed=3)
+        return Workload("c3r_random_soup100k_256", v, f, *g, (256,) * 3)
+    if name == "c3rs":  # quarter-size c3r for profiling (25k random triangles, 128^3)
+        v, f = random_soup(25_000, seed=3)
+        return Workload("c3rs_random_soup25k_128", v, f, *g, (128,) * 3)
     if name == "c3s":  # quarter-size C3 for profiling (25k-face soup, 128^3)
         v, f = soup(*torus(0.7, 0.3, 125, 100), seed=0)
         return Workload("c3s_torus25k_soup_128", v, f, *g, (128,) * 3)

@@ -117,8 +117,9 @@ int wv_vertex_normals(const double* vertices, int64_t n_verts, const int64_t* fa
 // ---- forward ---------------------------------------------------------------
 size_t wv_fwd_workspace_bytes(int kind, int64_t n_faces, int64_t count) {
   switch (kind) {
-    case WV_PACK_EXACT_F32:
-    case WV_PACK_EXACTSTRIP_F32: return wv::exact_fwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_EXACT_F32: return wv::exact_fwd_workspace_bytes(n_faces, count, sm_count());
+    case WV_PACK_EXACTSTRIP_F32:
+      return wv::exact_strip_fwd_workspace_bytes(n_faces, count, sm_count());
     case WV_PACK_SOFT_F32: return wv::soft_fwd_workspace_bytes(n_faces, count, sm_count());
     default: return 0;
   }

@@ -267,18 +267,28 @@ struct FwdPlan {
   int64_t blocks_x = 0;
   int splits = 1;
   int64_t tiles_per_split = 0;
-  static FwdPlan make(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch = 1) {
+  // rows: the launch takes the lattice-row kernel, whose occupancy
+  // (kMinBlocksRow CTAs per SM) sets the wave size the split count fills
+  static FwdPlan make(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch = 1,
+                      bool rows = false) {
     FwdPlan pl;
     const int64_t per_block = (int64_t)Pol::kConsumerWarps * 32 * Pol::kP;
     pl.blocks_x = (n_count + per_block - 1) / per_block;
     const int64_t n_tiles = (n_faces + Pol::kTile - 1) / Pol::kTile;
-    const int s = choose_splits(pl.blocks_x * batch, n_tiles, num_sms, Pol::kMinBlocks);
+    const int s = choose_splits(pl.blocks_x * batch, n_tiles, num_sms,
+                                rows ? Pol::kMinBlocksRow : Pol::kMinBlocks);
     pl.tiles_per_split = n_tiles > 0 ? (n_tiles + s - 1) / s : 0;
     pl.splits = pl.tiles_per_split > 0 ? (int)((n_tiles + pl.tiles_per_split - 1) / pl.tiles_per_split) : 1;
     return pl;
   }
   size_t workspace(int64_t n_count) const {
     return splits > 1 ? (size_t)splits * (size_t)n_count * (sizeof(double) + 1) + 256 : 0;
+  }
+  // what a launch needs whichever kernel (row or generic) it takes
+  static size_t workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
+    const size_t a = make(n_faces, n_count, num_sms, batch, false).workspace(n_count * batch);
+    const size_t b = make(n_faces, n_count, num_sms, batch, true).workspace(n_count * batch);
+    return a > b ? a : b;
   }
 };
 
@@ -295,7 +305,8 @@ int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, i
   if (bt.n > 65535 || (bt.n > 1 && ps.kind != PointSource::kGrid)) return kErrArg;
   const PackHeader* hdr = static_cast<const PackHeader*>(packed);
   const typename Pol::Rec* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
-  const FwdPlan<Pol> pl = FwdPlan<Pol>::make(n_faces, n_count, num_sms, bt.n);
+  const bool rows = ps.kind == PointSource::kGrid && row_aligned(ps.grid, ps.n0, n_count, Pol::kP);
+  const FwdPlan<Pol> pl = FwdPlan<Pol>::make(n_faces, n_count, num_sms, bt.n, rows);
   OutF32 o;
   o.out = out;
   o.flags = flags;
@@ -310,7 +321,7 @@ int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, i
   }
   dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits, (unsigned)bt.n);
   const unsigned threads = Pol::kThreads;
-  if (ps.kind == PointSource::kGrid && row_aligned(ps.grid, ps.n0, n_count, Pol::kP)) {
+  if (rows) {
     RowSrc src{{ps.grid, ps.n0}};
     fwd_f32_kernel<Pol, RowSrc><<<grid, threads, 0, stream>>>(
         hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);

@@ -574,7 +574,7 @@ int launch_exact_strip_fwd_f32(const void* packed, int64_t n_faces, const PointS
                                        workspace, ws_bytes, num_sms, stream, Batch{});
 }
 size_t exact_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
-  return FwdPlan<ExactPol>::make(n_faces, n_count, num_sms, batch).workspace(n_count * batch);
+  return FwdPlan<ExactPol>::workspace_bytes(n_faces, n_count, num_sms, batch);
 }
 int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, int policy, float* out, uint8_t* flags,
@@ -583,8 +583,11 @@ int launch_soft_fwd_f32(const void* packed, int64_t n_faces, const PointSource& 
   return launch_fwd_f32<SoftPol>(packed, n_faces, ps, n_count, policy, out, flags, workspace,
                                  ws_bytes, num_sms, stream, bt);
 }
+size_t exact_strip_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+  return FwdPlan<ExactStripPol>::workspace_bytes(n_faces, n_count, num_sms, 1);
+}
 size_t soft_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
-  return FwdPlan<SoftPol>::make(n_faces, n_count, num_sms, batch).workspace(n_count * batch);
+  return FwdPlan<SoftPol>::workspace_bytes(n_faces, n_count, num_sms, batch);
 }
 
 }  // namespace wv

@@ -176,6 +176,7 @@ int launch_exact_pair_bwd_f32(const void* packed, int64_t n_faces, const PointSo
                               int64_t n_count, const float* coefs, double coef_scale,
                               double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                               cudaStream_t stream);
+size_t exact_strip_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
 size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
 // strip-ordered exact forward (wv_strip.cu builds and packs, wv_fwd_f32.cu runs)
 int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int64_t n_faces,

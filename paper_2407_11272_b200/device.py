@@ -29,6 +29,11 @@ _DT = {"f32": torch.float32, "f64": torch.float64}
 # the strip-ordered records (wv_strip.cu): its host-side strip builder
 # (~0.5 us per face, once per DeviceMesh) pays off from ~2M nodes
 STRIP_MIN_NODES = 1 << 21
+# ... and only when the mesh actually forms strips: a strip restart costs the
+# two extra square roots plus the strip kernel's per-face branch, so above
+# this fraction of restarting faces (e.g. a random-triangle soup, where no
+# corner position is shared: 100%) the face-ordered kernels are faster
+STRIP_MAX_RESTART = 0.25
 
 
 def strip_order(vertices: np.ndarray, faces: np.ndarray):
@@ -189,6 +194,15 @@ def dead_faces(vertices: np.ndarray, faces: np.ndarray) -> np.ndarray:
     return ~(np.linalg.norm(np.cross(t[:, 1] - t[:, 0], t[:, 2] - t[:, 0]), axis=1) > 0.0)
 
 
+def _dead_faces_dev(vertices: torch.Tensor, faces: torch.Tensor) -> torch.Tensor:
+    """``dead_faces`` on the device: |N| == 0 in f64 (same expression order)."""
+    t = vertices.to(torch.float64)[faces.long()]
+    u, w = t[:, 1] - t[:, 0], t[:, 2] - t[:, 0]
+    n = torch.stack([u[:, 1] * w[:, 2] - u[:, 2] * w[:, 1], u[:, 2] * w[:, 0] - u[:, 0] * w[:, 2],
+                     u[:, 0] * w[:, 1] - u[:, 1] * w[:, 0]], dim=1)
+    return ~(torch.sqrt((n * n).sum(1)) > 0.0)
+
+
 @dataclass
 class DeviceMesh:
     """Mesh resident on the GPU.  ``vertices`` (V,3) f32/f64 and ``faces``
@@ -226,9 +240,21 @@ class DeviceMesh:
         self._packs.clear()
 
     def set_vertices(self, vertices: torch.Tensor) -> None:
-        """Replace the vertex positions (same connectivity); re-packs lazily."""
+        """Replace the vertex positions (same connectivity); re-packs lazily.
+        The exact backward's active faces and edge weights exclude faces that
+        are degenerate at the CURRENT positions (the reference re-drops them
+        on every call, winding.py:262-264): if a move changes that set, the
+        cached setups are rebuilt from the new positions."""
         self.vertices = vertices.contiguous()
         self._packs.clear()
+        dead0 = getattr(self, "_dead_dev", None)
+        if dead0 is not None:
+            dead = _dead_faces_dev(self.vertices, self.faces)
+            if not torch.equal(dead, dead0):
+                self._verts_np = self.vertices.detach().double().cpu().numpy()
+                self._exact_grad = None
+                self._exact_pair = None
+                self._dead_dev = None
 
     def packed(self, kind: int) -> torch.Tensor:
         ver = (id(self.vertices), self.vertices._version)
@@ -287,6 +313,45 @@ class DeviceMesh:
             self._strip_host = (perm, win, fl)
         return st
 
+    def strip_restart_fraction(self) -> float:
+        """Fraction of faces that start a strip in ``strip_setup``'s order
+        (builds the order on first use)."""
+        self.strip_setup()
+        fl = self._strip_host[2]
+        return float(np.count_nonzero(fl & 1)) / max(1, len(fl))
+
+    def shared_corner_fraction(self) -> float:
+        """1 - (distinct corner positions) / (3F): ~5/6 for a closed surface
+        (welded or un-welded soup alike: the copies are bitwise equal), 0 for
+        a soup of independent triangles.  Positions are hashed from their f64
+        bit patterns (a collision can only overstate sharing, which the strip
+        builder then measures exactly)."""
+        vnp = getattr(self, "_verts_np", None)
+        if vnp is None:
+            vnp = self.vertices.detach().double().cpu().numpy()
+        bits = np.ascontiguousarray(vnp, dtype=np.float64).view(np.uint64).reshape(-1, 3)
+        with np.errstate(over="ignore"):
+            h = (bits[:, 0] * np.uint64(0x9E3779B97F4A7C15)
+                 ^ bits[:, 1] * np.uint64(0xC2B2AE3D27D4EB4F)
+                 ^ bits[:, 2] * np.uint64(0x165667B19E3779F9))
+        corners = h[self.faces_np().reshape(-1)]
+        if corners.size == 0:
+            return 0.0
+        return 1.0 - np.unique(corners).size / corners.size
+
+    def strips_pay(self) -> bool:
+        """Whether the strip-ordered kernels beat the face-ordered ones on this
+        mesh (restart fraction <= STRIP_MAX_RESTART); decided once."""
+        sp = getattr(self, "_strips_pay", None)
+        if sp is None:
+            # cheap reject first: when most face corners have a position no
+            # other corner shares (a random soup), no strip can form and the
+            # strip builder's sorts are not worth running
+            sp = (self.num_faces > 0 and self.shared_corner_fraction() >= 0.5
+                  and self.strip_restart_fraction() <= STRIP_MAX_RESTART)
+            self._strips_pay = sp
+        return sp
+
     def faces_np(self) -> np.ndarray:
         fn = getattr(self, "_faces_np", None)
         if fn is None:
@@ -311,7 +376,9 @@ class DeviceMesh:
             if vnp is None:
                 vnp = self.vertices.detach().double().cpu().numpy()
             fnp = self.faces_np()
-            active, w = exact_edge_weights(fnp, dead_faces(vnp, fnp))
+            dead = dead_faces(vnp, fnp)
+            self._dead_dev = torch.from_numpy(dead).to(self.vertices.device)
+            active, w = exact_edge_weights(fnp, dead)
             off, slots = vertex_csr(fnp[active], self.num_vertices)
             dev = self.vertices.device
             eg = (torch.from_numpy(active).to(dev), torch.from_numpy(w).to(dev),
@@ -331,7 +398,9 @@ class DeviceMesh:
             if vnp is None:
                 vnp = self.vertices.detach().double().cpu().numpy()
             fnp = self.faces_np()
-            active, w = exact_edge_weights(fnp, dead_faces(vnp, fnp))
+            dead = dead_faces(vnp, fnp)
+            self._dead_dev = torch.from_numpy(dead).to(self.vertices.device)
+            active, w = exact_edge_weights(fnp, dead)
             # every face active in face order (soups): the forward's strips apply
             order = getattr(self, "_strip_host", None)
             if order is not None and not np.array_equal(active, np.arange(len(fnp))):
@@ -401,6 +470,22 @@ def _grid_count(grid, n0, count):
     return total - int(n0) if count is None else int(count)
 
 
+def lattice_paths(mesh: DeviceMesh, mode: str, precision: str, grid, n0: int, count: int):
+    """Which records the automatic choice takes for a lattice node range:
+    (forward over strips, exact backward over strip pairs).  Strips need a
+    large range (STRIP_MIN_NODES, the host strip builder's break-even), a mesh
+    that forms strips (``strips_pay``) and, for the f32 row kernel, 8-node
+    aligned k-rows; strip pairs exist for the exact f32 backward only."""
+    if mode != "exact" or count < STRIP_MIN_NODES or mesh.num_faces == 0:
+        return False, False
+    if precision == "f32" and not (int(grid[2][2]) % 8 == 0 and int(n0) % 8 == 0
+                                   and count % 8 == 0):
+        fwd = False
+    else:
+        fwd = mesh.strips_pay()
+    return fwd, precision == "f32" and mesh.strips_pay()
+
+
 def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int = 0,
             count: int | None = None, points=None, policy: int = L.POLICY_RAW,
             use_atan2: bool = True, out: torch.Tensor | None = None,
@@ -430,8 +515,7 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
         if not use_atan2:
             raise ValueError("the single-argument arctan branch exists only at precision='f64'")
         if strip is None:
-            strip = (mode == "exact" and points is None and count >= STRIP_MIN_NODES
-                     and int(grid[2][2]) % 8 == 0 and int(n0) % 8 == 0 and count % 8 == 0)
+            strip = points is None and lattice_paths(mesh, mode, precision, grid, n0, count)[0]
         if strip and mode != "exact":
             raise ValueError("strip records exist for the exact forward only")
         if strip:
@@ -457,7 +541,7 @@ def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int =
                     _ptr(flags), _ptr(ws), wsb, st)
     else:
         if strip is None:
-            strip = (mode == "exact" and points is None and count >= STRIP_MIN_NODES)
+            strip = points is None and lattice_paths(mesh, mode, precision, grid, n0, count)[0]
         if strip and mode != "exact":
             raise ValueError("strip records exist for the exact forward only")
         if strip:
@@ -512,7 +596,8 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     else:
         n_pts = _grid_count(grid, n0, count)
     if pairs is None:
-        pairs = mode == "exact" and precision == "f32" and n_pts >= STRIP_MIN_NODES
+        pairs = (mode == "exact" and precision == "f32" and n_pts >= STRIP_MIN_NODES
+                 and mesh.num_faces > 0 and mesh.strips_pay())
     if pairs and not (mode == "exact" and precision == "f32"):
         raise ValueError("strip pairs exist for the exact f32 backward only")
     if pairs:

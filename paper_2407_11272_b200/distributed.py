@@ -98,6 +98,10 @@ class SlabDriver:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
         s = buf[-3:]
         wsum = s[1]
+        # every rank holds the same reduced sums, so every rank raises alike
+        # (the reference's check, grad.py:108-109)
+        if float(wsum) == 0.0:
+            raise ValueError("no usable grid nodes: all excluded or zero-weighted")
         grads = buf[:-3].reshape(V, 3) / wsum
         loss = s[0] / wsum
         return loss, grads, s[2], wsum

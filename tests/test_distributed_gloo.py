@@ -106,3 +106,50 @@ def test_multi_rank_loss_grad_matches_single_process(tmp_path, world):
     vals, flags = orc.voxelize(g["vertices"], g["faces"], pts, mode="soft")
     assert np.array_equal(out["vals"], vals)
     assert np.array_equal(out["flags"].astype(bool), flags)
+
+
+def _worker_io(rank, world, port, outdir):
+    """gather_and_save of a slab-sharded forward, and the all-excluded loss."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_11272_b200.distributed import SlabDriver
+    from paper_2407_11272_b200.fieldio import gather_and_save
+    from paper_2407_11272_b200.types import GridSpec
+    g = golden("loss_grad")
+    grid = grid_of(g)
+    ev = OracleEvaluator(g["vertices"], g["faces"], grid)
+    n_total = int(np.prod(grid[2]))
+    drv = SlabDriver(ev, n_total, rank, world)
+    gather_and_save(drv, GridSpec(grid[0], grid[1], grid[2]), os.path.join(outdir, "g.wvox"))
+    n0, cnt = drv.slab
+    raised = 0
+    try:  # every node zero-weighted: the reference's ValueError on every rank
+        drv.loss_grad(g["target"][n0:n0 + cnt], np.zeros(cnt))
+    except ValueError as e:
+        raised = int("no usable grid nodes" in str(e))
+    flag = torch.tensor([raised], dtype=torch.int64)
+    dist.all_reduce(flag)
+    if rank == 0:
+        np.savez(os.path.join(outdir, "io.npz"), raised=int(flag))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_and_save_and_empty_weights_world2(tmp_path):
+    """fieldio.gather_and_save over two ranks writes the same WVOX1 bytes as
+    save_field of the single-process grid (reference winding.py:396-443), and
+    a loss with every node zero-weighted raises the reference's ValueError
+    (grad.py:108-109) on both ranks instead of returning NaN."""
+    port = _free_port()
+    mp.spawn(_worker_io, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    from oracle import oracle as orc
+    from paper_2407_11272_b200.fieldio import load_field, save_field
+    from paper_2407_11272_b200.types import GridSpec, ScalarField
+    g = golden("loss_grad")
+    grid = grid_of(g)
+    vals, _ = orc.voxelize(g["vertices"], g["faces"], orc.node_coordinates(*grid), mode="soft")
+    save_field(ScalarField(GridSpec(grid[0], grid[1], grid[2]), vals), tmp_path / "ref.wvox")
+    assert (tmp_path / "g.wvox").read_bytes() == (tmp_path / "ref.wvox").read_bytes()
+    assert np.array_equal(load_field(tmp_path / "g.wvox").values, vals)
+    assert int(np.load(tmp_path / "io.npz")["raised"]) == 2

@@ -191,3 +191,37 @@ def test_uniform_laplacian_matches_definition():
         dense[r, ix[ip[r]:ip[r + 1]]] += d[ip[r]:ip[r + 1]]
     assert np.allclose(dense.sum(axis=1), 0.0)  # rows of I - D^-1 A sum to 0
     assert np.allclose(np.diag(dense), 1.0)
+
+
+def test_bench_metric_is_baseline_metric():
+    """Both bench arms print BASELINE.json's metric and one unit, so the
+    driver can pair the lines (round-1 verdict: they differed)."""
+    import json
+    import bench
+    base = json.loads((ROOT / "BASELINE.json").read_text())
+    assert bench.METRIC == base["metric"]
+    assert bench.UNIT == "pairs/s"
+
+
+def test_random_soup_config_and_path_choice():
+    """C3's stress variant: 100k independent equilateral-ish triangles
+    (edge 0.04-0.06, centres in [-0.8,0.8]^3) share no corner position, so the
+    automatic choice takes the face-ordered kernels; the welded C3 soup takes
+    the strip kernels (host-side decision, no GPU needed)."""
+    import torch
+    from paper_2407_11272_b200 import configs, device
+    w = configs.make("c3r")
+    assert w.n_faces == 100_000 and w.res == (256, 256, 256)
+    t = w.vertices.reshape(-1, 3, 3)
+    e = np.linalg.norm(t[:, 1] - t[:, 0], axis=1)
+    assert 0.0399 < e.min() and e.max() < 0.0601
+    c = t.mean(axis=1)
+    assert np.abs(c).max() <= 0.8
+    for name, pay in (("c3r", False), ("c3", True)):
+        w = configs.make(name)
+        m = device.DeviceMesh(torch.from_numpy(w.vertices), torch.from_numpy(w.faces))
+        m._verts_np, m._faces_np = w.vertices, w.faces
+        assert m.strips_pay() is pay, name
+        grid = (w.lo, w.hi, w.res)
+        assert device.lattice_paths(m, "exact", "f32", grid, 0, w.n_nodes) == (pay, pay)
+        assert device.lattice_paths(m, "exact", "f64", grid, 0, w.n_nodes) == (pay, False)

@@ -44,6 +44,21 @@ __global__ void k_ffma2(float* out, int iters, float m) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// FP64: 8 independent DFMA chains per thread (the f64 parity path's pipe)
+__global__ void k_dfma(double* out, int iters, double m) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = fma(a[j], m, 0.5);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -65,6 +80,19 @@ int main() {
       const double flops = 2.0 * 16 * (double)iters * blocks * threads;
       if (pass == 1) printf("%s: %.3f ms  %.1f TFLOP/s\n", v ? "FFMA2" : "FFMA ", ms, flops / ms / 1e9);
     }
+  }
+  double* dout;
+  cudaMalloc(&dout, blocks * threads * sizeof(double));
+  for (int pass = 0; pass < 2; ++pass) {
+    const int diters = iters / 4;
+    cudaEventRecord(e0);
+    k_dfma<<<blocks, threads>>>(dout, diters, 0.999);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8 * (double)diters * blocks * threads;
+    if (pass == 1) printf("DFMA : %.3f ms  %.2f TFLOP/s\n", ms, flops / ms / 1e9);
   }
   return 0;
 }

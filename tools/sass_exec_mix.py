@@ -3,13 +3,42 @@
 their executed warp-instruction counts, optionally per point-face pair.
 
     python tools/sass_exec_mix.py REP.ncu-rep [--pairs N] [--top 25]
+        [--json profiles/exec_mix.json --kernel NAME --workload W --source TEXT]
+
+With ``--json`` the per-pair FLOPs, FP32 FMA-pipe lane-ops, MUFU ops, FP64
+FLOPs and thread-instructions are written into that file's ``entries``
+(replacing the entry with the same kernel and workload): bench.py reads them
+for its executed-work roofline.
 """
 
 import argparse
 import collections
 import csv
 import io
+import json
 import subprocess
+
+# FLOPs per thread-instruction (FMA = 2) and FP32 FMA-pipe lane-ops
+F32 = {"FFMA": (2, 1), "FADD": (1, 1), "FMUL": (1, 1),
+       "FFMA2": (4, 2), "FADD2": (2, 2), "FMUL2": (2, 2)}
+F64 = {"DFMA": 2, "DADD": 1, "DMUL": 1}
+
+
+def counts(mix, pairs):
+    """Per-pair executed work from an opcode -> warp-instruction Counter."""
+    per = lambda n: n * 32 / pairs  # noqa: E731
+    fl = lo = mu = df = 0.0
+    for op, n in mix.items():
+        base = op.split(".")[0]
+        if base in F32:
+            fl += F32[base][0] * per(n)
+            lo += F32[base][1] * per(n)
+        elif base in F64:
+            df += F64[base] * per(n)
+        elif base == "MUFU":
+            mu += per(n)
+    return {"flops": round(fl, 3), "lane_ops": round(lo, 3), "mufu": round(mu, 3),
+            "dflops": round(df, 3), "thread_instr": round(per(sum(mix.values())), 3)}
 
 
 def main():
@@ -17,6 +46,10 @@ def main():
     ap.add_argument("report")
     ap.add_argument("--pairs", type=float, default=0.0)
     ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--kernel", default=None)
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--source", default="")
     a = ap.parse_args()
     txt = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source",
                           "sass"], check=True, capture_output=True, text=True).stdout
@@ -49,6 +82,17 @@ def main():
     for o, n in mix.most_common(a.top):
         per = f"  {n * 32 / a.pairs:7.3f}/pair" if a.pairs else ""
         print(f"  {o:28s} {n:14.4g} {100 * n / tot:6.2f}%{per}  samples {smp[o]:.0f}")
+    if a.pairs:
+        c = counts(mix, a.pairs)
+        print("per pair:", json.dumps(c))
+        if a.json:
+            doc = json.load(open(a.json))
+            ent = dict(kernel=a.kernel, workload=a.workload, **c, source=a.source)
+            doc["entries"] = [e for e in doc["entries"]
+                              if (e["kernel"], e["workload"]) != (a.kernel, a.workload)] + [ent]
+            with open(a.json, "w") as fh:
+                json.dump(doc, fh, indent=1)
+                fh.write("\n")
 
 
 if __name__ == "__main__":
