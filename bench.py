@@ -421,6 +421,7 @@ def run_reference(args):
         pairs_per_step = w.pairs
     else:
         w = configs.make(args.config)
+        per = min(per, w.n_nodes)
 
         def one(k, n):
             return cpu_fwd_bwd(w.vertices, w.faces, w, n, threads, seed=k)

@@ -308,6 +308,18 @@ int wv_mc_vertices(const void *values, int values_f64, wv_grid_t grid, double is
 int wv_mc_emit(const uint8_t *cases, const int64_t *tri_offsets, const int8_t *tri_table,
                int max_tris, const int8_t *edge_axis, const int8_t *edge_base,
                const int64_t *vertex_index, wv_grid_t grid, int64_t *faces, void *stream);
+/* Slab-sharded marching cubes (one i-slab per GPU): a rank
+ * runs wv_mc_classify / wv_mc_edges / wv_mc_emit on its block of `rows`
+ * i-rows (its slab plus a 1-row halo from the next rank; `grid` with
+ * res[0] = rows), vertex_index holding GLOBAL vertex ids, and
+ * wv_mc_vertices_slab places the vertices of the block's crossed edges at
+ * slot[g] (local output rows; slot < 0: skipped, e.g. the halo row's edges,
+ * which the next rank owns), computing positions with the GLOBAL grid
+ * `grid` (i = i0 + local row).  distributed.slab_marching_cubes does the
+ * halo exchange and the id offsets; the result equals the one-GPU mesh. */
+int wv_mc_vertices_slab(const void *values, int values_f64, wv_grid_t grid, int64_t i0,
+                        int64_t rows, double iso, const int32_t *flags, const int64_t *slot,
+                        double *vertices, void *stream);
 
 /* ---- occupancy loss terms (grad.py:101-110), fused on the device ---------
  * coefs[n] = 2 w r (0 on flagged nodes); sums (8 doubles, device) =

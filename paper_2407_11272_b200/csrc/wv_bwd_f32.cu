@@ -124,9 +124,9 @@ struct ExactEdgeBwd {
     const F2 ia = rsqrt2(a2), ib = rsqrt2(b2), ic = rsqrt2(c2);
     const F2 lb = mul2(b2, ib), lc = mul2(c2, ic);
     const F2 s01 = fma2(a2, ia, lb), s12 = add2(lb, lc), s20 = fma2(a2, ia, lc);
-    const F2 r01 = rcp2(fma2(s01, s01, f2s(-R.u.x)));
-    const F2 r12 = rcp2(fma2(s12, s12, f2s(-R.u.y)));
-    const F2 r20 = rcp2(fma2(s20, s20, f2s(-R.u.z)));
+    const F2 r01 = rcp2_abs(fma2(s01, s01, f2s(-R.u.x)));
+    const F2 r12 = rcp2_abs(fma2(s12, s12, f2s(-R.u.y)));
+    const F2 r20 = rcp2_abs(fma2(s20, s20, f2s(-R.u.z)));
     float q0, q1;
     split(mul2(mul2(r01, r12), mul2(r20, f2s(R.u.x * R.u.y * R.u.z))), q0, q1);
     const bool ill0 = !(q0 < kIllRatio), ill1 = !(q1 < kIllRatio);
@@ -222,7 +222,7 @@ struct ExactEdgeBwd {
     const F2 d12 = fma2(s12, s12, f2s(-R.u.y));
     const F2 d20 = fma2(s20, s20, f2s(-R.u.z));
     const F2 p12 = mul2(d12, d20);
-    const F2 rr = rcp2(mul2(d01, p12));
+    const F2 rr = rcp2_abs(mul2(d01, p12));
     // ill-conditioned lanes (some d_e < |e|^2 / kIllRatio, or a non-finite
     // reciprocal) leave the fp32 sums: cr = 0 here, exact_pair_f64 later
     const F2 ru = mul2(rr, f2s(R.u.x * R.u.y * R.u.z));
@@ -353,7 +353,10 @@ struct SoftBwd {
   template <bool kUnit>
   __device__ __forceinline__ static uint32_t pair2(const Rec& R, F2 qx, F2 qy, F2 qz, F2 coef,
                                                    float eps2, F2* g) {
-    const F2 dx = sub2(f2s(R.c.x), qx), dy = sub2(f2s(R.c.y), qy), dz = sub2(f2s(R.c.z), qz);
+    // d = (c_hi - q) + c_lo (SoftGradRecF32)
+    const F2 dx = add2(sub2(f2s(R.c.x), qx), f2s(R.c.w));
+    const F2 dy = add2(sub2(f2s(R.c.y), qy), f2s(R.n.w));
+    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.u.w));
     const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
     const F2 rs = rsqrt2(r2);
     const F2 S = fma2(f2s(R.n.z), dz, fma2(f2s(R.n.y), dy, mul2(f2s(R.n.x), dx)));
@@ -363,7 +366,9 @@ struct SoftBwd {
     split(mul2(mul2(coef, rs2), rs), cl, ch);
     // r < eps: that face is skipped for that point (_kernels.py:203-204)
     const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
-    const F2 c5 = mul2(mul2(c3, S), rs2);
+    // c3 S / r^2 as (c3 (S / r)) / r: |S / r| <= |N|, so a node next to a
+    // centroid does not overflow fp32 through 1/r^5
+    const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);
     // G1 = w x d, G2 = d x u
     const F2 g1x = sub2(mul2(f2s(R.w.y), dz), mul2(f2s(R.w.z), dy));
     const F2 g1y = sub2(mul2(f2s(R.w.z), dx), mul2(f2s(R.w.x), dz));
@@ -394,8 +399,8 @@ struct SoftBwd {
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
     Row w;
-    w.dx = R.c.x - qx;
-    w.dy = R.c.y - qy;
+    w.dx = (R.c.x - qx) + R.c.w;  // + c_lo
+    w.dy = (R.c.y - qy) + R.n.w;
     w.r2 = fmaf(w.dy, w.dy, w.dx * w.dx);
     w.s = fmaf(R.n.y, w.dy, R.n.x * w.dx);
     return w;
@@ -403,17 +408,16 @@ struct SoftBwd {
   template <bool kUnit>
   __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
                                                    float eps2, F2* z) {
-    const F2 dz = sub2(f2s(R.c.z), qz);
+    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.u.w));
     const F2 r2 = fma2(dz, dz, f2s(w.r2));
     const F2 rs = rsqrt2(r2);
     const F2 S = fma2(f2s(R.n.z), dz, f2s(w.s));
-    const F2 rs2 = mul2(rs, rs);
     float r2l, r2h, cl, ch;
     split(r2, r2l, r2h);
-    split(mul2(mul2(coef, rs2), rs), cl, ch);
+    split(mul2(mul2(coef, mul2(rs, rs)), rs), cl, ch);
     // r < eps: that face is skipped for that point (_kernels.py:203-204)
     const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
-    const F2 c5 = mul2(mul2(c3, S), rs2);
+    const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);  // no 1/r^5 overflow (pair2)
     z[0] = add2(z[0], c3);
     z[1] = fma2(c3, dz, z[1]);
     z[2] = add2(z[2], c5);
@@ -433,7 +437,7 @@ struct SoftBwd {
     float m = __int_as_float(0x7f800000);
 #pragma unroll
     for (int u = 0; u < N; ++u) {
-      dz[u] = sub2(f2s(R.c.z), f2(zc[u].x, zc[u].y));
+      dz[u] = add2(sub2(f2s(R.c.z), f2(zc[u].x, zc[u].y)), f2s(R.u.w));
       r2[u] = fma2(dz[u], dz[u], f2s(w.r2));
       float l, h;
       split(r2[u], l, h);
@@ -449,9 +453,8 @@ struct SoftBwd {
     for (int u = 0; u < N; ++u) {
       const F2 rs = rsqrt2(r2[u]);
       const F2 S = fma2(f2s(R.n.z), dz[u], f2s(w.s));
-      const F2 rs2 = mul2(rs, rs);
-      const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), rs2), rs);
-      const F2 c5 = mul2(mul2(c3, S), rs2);
+      const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), mul2(rs, rs)), rs);
+      const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);
       z[0] = add2(z[0], c3);
       z[1] = fma2(c3, dz[u], z[1]);
       z[2] = add2(z[2], c5);
@@ -556,7 +559,7 @@ struct SoftBwdPair {
     for (int k = 0; k < 2; ++k) {
 #pragma unroll
       for (int u = 0; u < N; ++u) {
-        dz[k][u] = sub2(f2s(R.f[k].c.z), f2(zc[u].x, zc[u].y));
+        dz[k][u] = add2(sub2(f2s(R.f[k].c.z), f2(zc[u].x, zc[u].y)), f2s(R.f[k].u.w));
         r2[k][u] = fma2(dz[k][u], dz[k][u], f2s(w.r[k].r2));
         float l, h;
         split(r2[k][u], l, h);
@@ -576,9 +579,8 @@ struct SoftBwdPair {
         F2* zk = z + k * One::kRowAcc;
         const F2 rs = rsqrt2(r2[k][u]);
         const F2 S = fma2(f2s(R.f[k].n.z), dz[k][u], f2s(w.r[k].s));
-        const F2 rs2 = mul2(rs, rs);
-        const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), rs2), rs);
-        const F2 c5 = mul2(mul2(c3, S), rs2);
+        const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), mul2(rs, rs)), rs);
+        const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);
         zk[0] = add2(zk[0], c3);
         zk[1] = fma2(c3, dz[k][u], zk[1]);
         zk[2] = add2(zk[2], c5);
@@ -693,8 +695,8 @@ struct ExactEdgeBwdPair {
       const F2 dab = fma2(sab, sab, f2s(-F.u.x)), dbc = fma2(sbc, sbc, f2s(-F.u.y));
       const F2 dca = fma2(sca, sca, f2s(-F.u.z));
       const F2 dcd = fma2(scd, scd, f2s(-G.u.y)), ddb = fma2(sdb, sdb, f2s(-G.u.z));
-      const F2 p1 = mul2(dbc, dca), rr1 = rcp2(mul2(dab, p1));
-      const F2 rr2 = rcp2(mul2(dcd, ddb));
+      const F2 p1 = mul2(dbc, dca), rr1 = rcp2_abs(mul2(dab, p1));
+      const F2 rr2 = rcp2_abs(mul2(dcd, ddb));
       ru[u] = fma2(rr2, f2s(u2p), mul2(rr1, f2s(u1p)));  // both faces' ratio products
       const F2 cr1 = mul2(coef, rr1), q0 = mul2(cr1, dab);
       const F2 tab = mul2(cr1, p1), tbc = mul2(q0, dca), tca = mul2(q0, dbc);

@@ -456,8 +456,18 @@ int wv_mc_vertices(const void* values, int values_f64, wv_grid_t grid, double is
                    const int32_t* flags, const int64_t* vertex_index, double* vertices,
                    void* stream) {
   if (values == nullptr || flags == nullptr || vertex_index == nullptr) return WV_ERR_ARG;
-  return wv::launch_mc_vertices(values, values_f64, grid_src(grid, 0).grid, iso, flags,
-                                vertex_index, vertices, sm_count(), as_stream(stream));
+  return wv::launch_mc_vertices(values, values_f64, grid_src(grid, 0).grid, 0, grid.res[0], iso,
+                                flags, vertex_index, vertices, sm_count(), as_stream(stream));
+}
+
+int wv_mc_vertices_slab(const void* values, int values_f64, wv_grid_t grid, int64_t i0,
+                        int64_t rows, double iso, const int32_t* flags, const int64_t* slot,
+                        double* vertices, void* stream) {
+  if (values == nullptr || flags == nullptr || slot == nullptr || i0 < 0 || rows < 1 ||
+      i0 + rows > grid.res[0])
+    return WV_ERR_ARG;
+  return wv::launch_mc_vertices(values, values_f64, grid_src(grid, 0).grid, i0, rows, iso, flags,
+                                slot, vertices, sm_count(), as_stream(stream));
 }
 
 int wv_mc_emit(const uint8_t* cases, const int64_t* tri_offsets, const int8_t* tri_table,

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -32,19 +33,37 @@ struct __align__(16) ExactRecF32 {
 static_assert(sizeof(ExactRecF32) == 64, "record size");
 
 // SoftRecF32 (32 B): centroid c = v0 + (u+w)/3 and N = u x w, both computed
-//   in f64 exactly as _kernels.py:139-155 does per pair, then rounded.
+//   in f64 exactly as _kernels.py:139-155 does per pair (from the
+//   f32-rounded corners), then rounded.  The centroid is kept as hi + lo:
+//   d = c - q = (c_hi - q) + c_lo is then accurate to ~ulp(|d|) instead of
+//   ulp(|c|), which matters at nodes next to a centroid (the dipole term
+//   grows like 1/|d|^2).  lo.x, lo.y ride as a bf16 pair (they are <= ulp(c)/2,
+//   so 8 bits of them is ~1e-10 absolute).
 struct __align__(16) SoftRecF32 {
-  float4 c;   // c.xyz, N.x
-  float4 n;   // N.y, N.z, 0, 0
+  float4 c;   // c_hi.xyz, N.x
+  float4 n;   // N.y, N.z, c_lo.z, bits: bf16(c_lo.x) | bf16(c_lo.y) << 16
 };
 static_assert(sizeof(SoftRecF32) == 32, "record size");
+__host__ __device__ __forceinline__ uint32_t bf16_bits(float x) {  // round to nearest even
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  b += 0x7fffu + ((b >> 16) & 1u);
+  return b >> 16;
+}
+__device__ __forceinline__ float lo_x(const SoftRecF32& R) {
+  return __uint_as_float(__float_as_uint(R.n.w) << 16);
+}
+__device__ __forceinline__ float lo_y(const SoftRecF32& R) {
+  return __uint_as_float(__float_as_uint(R.n.w) & 0xffff0000u);
+}
 
-// SoftGradRecF32 (64 B): what the soft backward needs per face -- centroid,
-//   N = u x w, u = v1-v0, w = v2-v0 (all from f64, then rounded).
+// SoftGradRecF32 (64 B): what the soft backward needs per face -- centroid
+//   (hi + lo, as SoftRecF32), N = u x w, u = v1-v0, w = v2-v0 (all from the
+//   f32-rounded corners in f64, then rounded).
 struct __align__(16) SoftGradRecF32 {
-  float4 c;  // c.xyz, 0
-  float4 n;  // N.xyz, 0
-  float4 u;  // u.xyz, 0
+  float4 c;  // c_hi.xyz, c_lo.x
+  float4 n;  // N.xyz, c_lo.y
+  float4 u;  // u.xyz, c_lo.z
   float4 w;  // w.xyz, 0
 };
 static_assert(sizeof(SoftGradRecF32) == 64, "record size");

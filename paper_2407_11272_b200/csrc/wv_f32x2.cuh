@@ -69,4 +69,15 @@ __device__ __forceinline__ F2 rcp2(F2 a) {
   return f2(rcp_approx(l), rcp_approx(h));
 }
 
+// 1/|x| per half: the exact backward's edge denominators are >= 0 in exact
+// arithmetic but can round to small NEGATIVE values next to an edge; with the
+// magnitude their ill-conditioning ratios stay >= 0, so a near-edge pair can
+// never pass the ratio test with a negative (cancelled) ratio.  (The abs
+// folds into MUFU.RCP's source operand.)
+__device__ __forceinline__ F2 rcp2_abs(F2 a) {
+  float l, h;
+  split(a, l, h);
+  return f2(rcp_approx(fabsf(l)), rcp_approx(fabsf(h)));
+}
+
 }  // namespace wv

@@ -363,11 +363,15 @@ struct ExactBwd64 {
     const double b[3] = {Q[0] - qx, Q[1] - qy, Q[2] - qz};
     const double la = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
     const double lb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
-    const double den = la * lb + (a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
-    if (!(den > 0.0)) return;  // q on the segment: an on-surface point
-    const double t = cw / den;
     const double m[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
                          a[0] * b[1] - a[1] * b[0]};
+    // |a||b| + a.b without cancellation next to the edge's segment (a.b < 0):
+    // |a x b|^2 / (|a||b| - a.b)
+    const double L = la * lb, ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+    const double den =
+        ab < 0.0 ? (m[0] * m[0] + m[1] * m[1] + m[2] * m[2]) / (L - ab) : L + ab;
+    if (!(den > 0.0)) return;  // q on the segment: an on-surface point
+    const double t = cw / den;
     const double sp = t / la, sq = t / lb;
     for (int d = 0; d < 3; ++d) {
       gP[d] += m[d] * sp;

@@ -173,9 +173,13 @@ struct ExactPol {
     const bool cl = sl < 0.0f && bl > p2l && vl, ch = sh < 0.0f && bh > p2h && vh;
     const F2 p = fma2(fma2(s, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s,
                       f2s(1.0f));
-    float tl, th;
-    split(tt, tl, th);
-    tacc = fma2(f2(cl ? tl : 0.0f, ch ? th : 0.0f), p, tacc);
+    // select the updated sum per lane (a rare lane's t and p may be inf /
+    // NaN -- beta cancelled to ~0 next to the surface -- so 0 * p is no
+    // neutral term)
+    float ul, uh, al, ah;
+    split(fma2(tt, p, tacc), ul, uh);
+    split(tacc, al, ah);
+    tacc = f2(cl ? ul : al, ch ? uh : ah);
     return (cl ? 0u : 1u) | (ch ? 0u : 2u);
   }
   // All PP point pairs of a thread against one face.  The common-pair test
@@ -450,7 +454,10 @@ struct SoftPol {
   __device__ static Ctx make_ctx(float eps) { return Ctx{eps * eps}; }
   __device__ __forceinline__ static uint32_t common2(const Rec& R, F2 qx, F2 qy, F2 qz,
                                                      const Ctx& ctx, F2& tacc) {
-    const F2 dx = sub2(f2s(R.c.x), qx), dy = sub2(f2s(R.c.y), qy), dz = sub2(f2s(R.c.z), qz);
+    // d = (c_hi - q) + c_lo (SoftRecF32)
+    const F2 dx = add2(sub2(f2s(R.c.x), qx), f2s(lo_x(R)));
+    const F2 dy = add2(sub2(f2s(R.c.y), qy), f2s(lo_y(R)));
+    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.n.z));
     const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
     const F2 s = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
     return tail2(r2, s, ctx, tacc);
@@ -459,7 +466,7 @@ struct SoftPol {
     float r2, s;
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
-    const float dx = R.c.x - qx, dy = R.c.y - qy;
+    const float dx = (R.c.x - qx) + lo_x(R), dy = (R.c.y - qy) + lo_y(R);
     Row w;
     w.r2 = fmaf(dy, dy, dx * dx);
     w.s = fmaf(R.n.x, dy, R.c.w * dx);
@@ -467,7 +474,7 @@ struct SoftPol {
   }
   __device__ __forceinline__ static uint32_t common_row2(const Rec& R, const Row& w, F2 qz,
                                                          const Ctx& ctx, F2& tacc) {
-    const F2 dz = sub2(f2s(R.c.z), qz);
+    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.n.z));
     return tail2(fma2(dz, dz, f2s(w.r2)), fma2(f2s(R.n.y), dz, f2s(w.s)), ctx, tacc);
   }
   __device__ __forceinline__ static uint32_t tail2(F2 r2, F2 s, const Ctx& ctx, F2& tacc) {
@@ -516,7 +523,7 @@ struct SoftPol {
     F2 r2[PP], s[PP];
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
-      const F2 dz = sub2(f2s(R.c.z), qz[pp]);
+      const F2 dz = add2(sub2(f2s(R.c.z), qz[pp]), f2s(R.n.z));
       r2[pp] = fma2(dz, dz, f2s(w.r2));
       s[pp] = fma2(f2s(R.n.y), dz, f2s(w.s));
     }
@@ -528,8 +535,9 @@ struct SoftPol {
     F2 r2[PP], s[PP];
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
-      const F2 dx = sub2(f2s(R.c.x), qx[pp]), dy = sub2(f2s(R.c.y), qy[pp]);
-      const F2 dz = sub2(f2s(R.c.z), qz[pp]);
+      const F2 dx = add2(sub2(f2s(R.c.x), qx[pp]), f2s(lo_x(R)));
+      const F2 dy = add2(sub2(f2s(R.c.y), qy[pp]), f2s(lo_y(R)));
+      const F2 dz = add2(sub2(f2s(R.c.z), qz[pp]), f2s(R.n.z));
       r2[pp] = dot2(dx, dy, dz, dx, dy, dz);
       s[pp] = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
     }

@@ -251,9 +251,9 @@ int launch_mc_classify(const void* vals, int f64, int64_t rx, int64_t ry, int64_
                        cudaStream_t stream);
 int launch_mc_edges(const void* vals, int f64, int64_t rx, int64_t ry, int64_t rz, double iso,
                     int32_t* flags, int num_sms, cudaStream_t stream);
-int launch_mc_vertices(const void* vals, int f64, const GridDesc& g, double iso,
-                       const int32_t* flags, const int64_t* vidx, double* verts, int num_sms,
-                       cudaStream_t stream);
+int launch_mc_vertices(const void* vals, int f64, const GridDesc& g, int64_t i0, int64_t rows,
+                       double iso, const int32_t* flags, const int64_t* slot, double* verts,
+                       int num_sms, cudaStream_t stream);
 int launch_mc_emit(const uint8_t* cases, const int64_t* tri_off, const int8_t* tri_tab,
                    int max_tris, const int8_t* edge_axis, const int8_t* edge_base,
                    const int64_t* vidx, int64_t rx, int64_t ry, int64_t rz, int64_t* faces,

@@ -6,7 +6,7 @@
 //
 // Pipeline (prefix sums between the passes are done by the caller):
 //   classify : per cell, case index (bit c = corner c outside, value <= iso)
-//              and its triangle count from the (generated) case table
+//              and its triangle count from the (classic) case table
 //   edges    : per lattice edge (axis * N + base node), 1 if it crosses iso
 //   vertices : per crossed edge, its interpolated position at its prefix slot
 //   emit     : per cell, its triangles at its prefix offset, edge -> vertex id
@@ -55,22 +55,24 @@ __global__ void mc_edge_kernel(const void* __restrict__ vals, int f64, int64_t r
   }
 }
 
-__global__ void mc_vertex_kernel(const void* __restrict__ vals, int f64, GridDesc g, double iso,
-                                 const int32_t* __restrict__ flags,
-                                 const int64_t* __restrict__ vidx, double* __restrict__ verts) {
-  const int64_t rx = g.res[0], ry = g.res[1], rz = g.res[2];
-  const int64_t n = rx * ry * rz;
+// rows i-rows of the grid starting at global row i0 (the whole grid: i0 = 0,
+// rows = Rx); an edge with slot < 0 is not written (a slab's halo row)
+__global__ void mc_vertex_kernel(const void* __restrict__ vals, int f64, GridDesc g, int64_t i0,
+                                 int64_t rows, double iso, const int32_t* __restrict__ flags,
+                                 const int64_t* __restrict__ slot, double* __restrict__ verts) {
+  const int64_t ry = g.res[1], rz = g.res[2];
+  const int64_t n = rows * ry * rz;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 3 * n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    if (!flags[e]) continue;
+    if (!flags[e] || slot[e] < 0) continue;
     const int axis = (int)(e / n);
     const int64_t node = e - axis * n;
     const int64_t i = node / (ry * rz), rem = node - i * ry * rz, j = rem / rz, k = rem - j * rz;
     const int64_t stride = axis == 0 ? ry * rz : (axis == 1 ? rz : 1);
     const double va = mc_val(vals, f64, node), vb = mc_val(vals, f64, node + stride);
     const double t = (iso - va) / (vb - va);
-    const int64_t idx[3] = {i, j, k};
-    double* out = verts + 3 * vidx[e];
+    const int64_t idx[3] = {i0 + i, j, k};
+    double* out = verts + 3 * slot[e];
     for (int d = 0; d < 3; ++d) {
       const double pa = axis_node(g.lo[d], g.hi[d], g.res[d], idx[d]);
       const double pb = axis_node(g.lo[d], g.hi[d], g.res[d], idx[d] + (d == axis ? 1 : 0));
@@ -128,12 +130,13 @@ int launch_mc_edges(const void* vals, int f64, int64_t rx, int64_t ry, int64_t r
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
-int launch_mc_vertices(const void* vals, int f64, const GridDesc& g, double iso,
-                       const int32_t* flags, const int64_t* vidx, double* verts, int num_sms,
-                       cudaStream_t stream) {
-  const int64_t n = 3 * g.res[0] * g.res[1] * g.res[2];
-  mc_vertex_kernel<<<grid_blocks(n, num_sms), 256, 0, stream>>>(vals, f64, g, iso, flags, vidx,
-                                                                verts);
+int launch_mc_vertices(const void* vals, int f64, const GridDesc& g, int64_t i0, int64_t rows,
+                       double iso, const int32_t* flags, const int64_t* slot, double* verts,
+                       int num_sms, cudaStream_t stream) {
+  const int64_t n = 3 * rows * g.res[1] * g.res[2];
+  if (n <= 0) return kOk;
+  mc_vertex_kernel<<<grid_blocks(n, num_sms), 256, 0, stream>>>(vals, f64, g, i0, rows, iso,
+                                                                flags, slot, verts);
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 

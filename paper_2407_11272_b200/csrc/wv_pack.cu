@@ -19,6 +19,17 @@ __device__ __forceinline__ void load_vertex(const V* v, int64_t i, double* out) 
   out[1] = (double)v[3 * i + 1];
   out[2] = (double)v[3 * i + 2];
 }
+// the FP32 records describe the f32-ROUNDED mesh (the inputs the kernels
+// compute with, as the reference's f32 path rounds tri, winding.py:370-373):
+// normals, edge lengths, centroids and the degenerate test are derived in f64
+// from the rounded corners, so alpha = N.(v0 - q) etc. are consistent with
+// the corners the kernels (and their fp64 rare paths) see
+template <typename V>
+__device__ __forceinline__ void load_vertex_f32(const V* v, int64_t i, double* out) {
+  out[0] = (double)(float)v[3 * i + 0];
+  out[1] = (double)(float)v[3 * i + 1];
+  out[2] = (double)(float)v[3 * i + 2];
+}
 
 template <typename V>
 __global__ void surface_eps_kernel(const V* __restrict__ verts, int64_t n_verts,
@@ -80,9 +91,15 @@ __global__ void pack_kernel(int kind, const V* __restrict__ verts,
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_faces;
        f += (int64_t)gridDim.x * blockDim.x) {
     double v0[3], v1[3], v2[3];
-    load_vertex(verts, (int64_t)faces[3 * f + 0], v0);
-    load_vertex(verts, (int64_t)faces[3 * f + 1], v1);
-    load_vertex(verts, (int64_t)faces[3 * f + 2], v2);
+    if (kind == 1 || kind == 2 || kind == 5) {  // FP32 records: the rounded mesh
+      load_vertex_f32(verts, (int64_t)faces[3 * f + 0], v0);
+      load_vertex_f32(verts, (int64_t)faces[3 * f + 1], v1);
+      load_vertex_f32(verts, (int64_t)faces[3 * f + 2], v2);
+    } else {
+      load_vertex(verts, (int64_t)faces[3 * f + 0], v0);
+      load_vertex(verts, (int64_t)faces[3 * f + 1], v1);
+      load_vertex(verts, (int64_t)faces[3 * f + 2], v2);
+    }
     const double ux = v1[0] - v0[0], uy = v1[1] - v0[1], uz = v1[2] - v0[2];
     const double wx = v2[0] - v0[0], wy = v2[1] - v0[1], wz = v2[2] - v0[2];
     // np.cross(u, w) component order (winding.py:262)
@@ -130,15 +147,20 @@ __global__ void pack_kernel(int kind, const V* __restrict__ verts,
       const double cx = v0[0] + (ux + wx) / 3.0;
       const double cy = v0[1] + (uy + wy) / 3.0;
       const double cz = v0[2] + (uz + wz) / 3.0;
+      // centroid hi + lo (SoftRecF32)
+      const float hx = (float)cx, hy = (float)cy, hz = (float)cz;
+      const float lx = (float)(cx - (double)hx), ly = (float)(cy - (double)hy),
+                  lz = (float)(cz - (double)hz);
       if (kind == 2) {
         SoftRecF32* r = static_cast<SoftRecF32*>(recs) + f;
-        r->c = make_float4((float)cx, (float)cy, (float)cz, (float)nx);
-        r->n = make_float4((float)ny, (float)nz, 0.0f, 0.0f);
+        r->c = make_float4(hx, hy, hz, (float)nx);
+        r->n = make_float4((float)ny, (float)nz, lz,
+                           __uint_as_float(bf16_bits(lx) | (bf16_bits(ly) << 16)));
       } else if (kind == 5) {
         SoftGradRecF32* r = static_cast<SoftGradRecF32*>(recs) + f;
-        r->c = make_float4((float)cx, (float)cy, (float)cz, 0.0f);
-        r->n = make_float4((float)nx, (float)ny, (float)nz, 0.0f);
-        r->u = make_float4((float)ux, (float)uy, (float)uz, 0.0f);
+        r->c = make_float4(hx, hy, hz, lx);
+        r->n = make_float4((float)nx, (float)ny, (float)nz, ly);
+        r->u = make_float4((float)ux, (float)uy, (float)uz, lz);
         r->w = make_float4((float)wx, (float)wy, (float)wz, 0.0f);
       } else if (kind == 6) {
         SoftGradRecF64* r = static_cast<SoftGradRecF64*>(recs) + f;
@@ -179,9 +201,15 @@ __global__ void pack_exact_grad_kernel(int kind, const V* __restrict__ verts,
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = active[i];
     double v0[3], v1[3], v2[3];
-    load_vertex(verts, (int64_t)faces[3 * f + 0], v0);
-    load_vertex(verts, (int64_t)faces[3 * f + 1], v1);
-    load_vertex(verts, (int64_t)faces[3 * f + 2], v2);
+    if (kind == 7) {  // FP32 records: the rounded mesh (squared edge lengths too)
+      load_vertex_f32(verts, (int64_t)faces[3 * f + 0], v0);
+      load_vertex_f32(verts, (int64_t)faces[3 * f + 1], v1);
+      load_vertex_f32(verts, (int64_t)faces[3 * f + 2], v2);
+    } else {
+      load_vertex(verts, (int64_t)faces[3 * f + 0], v0);
+      load_vertex(verts, (int64_t)faces[3 * f + 1], v1);
+      load_vertex(verts, (int64_t)faces[3 * f + 2], v2);
+    }
     if (kind == 7) {
       ExactGradRecF32* r = static_cast<ExactGradRecF32*>(recs) + i;
       r->a = make_float4((float)v0[0], (float)v0[1], (float)v0[2], weights[3 * i + 0]);

@@ -210,8 +210,9 @@ __global__ void pack_strip_kernel(const V* __restrict__ verts, const I* __restri
     double t[3][3], w[3][3];
     for (int c = 0; c < 3; ++c)
       for (int d = 0; d < 3; ++d) {
-        t[c][d] = (double)verts[3 * (int64_t)faces[3 * f + c] + d];
-        w[c][d] = (double)verts[3 * win[3 * k + c] + d];
+        // the rounded mesh, as pack_kernel's FP32 kinds
+        t[c][d] = (double)(float)verts[3 * (int64_t)faces[3 * f + c] + d];
+        w[c][d] = (double)(float)verts[3 * win[3 * k + c] + d];
       }
     // true-orientation normal, as pack_kernel (winding.py:262)
     const double ux = t[1][0] - t[0][0], uy = t[1][1] - t[0][1], uz = t[1][2] - t[0][2];

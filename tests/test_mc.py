@@ -1,11 +1,9 @@
-"""Marching cubes: our generated case table and the device
-pipeline vs the reference's marching_cubes (golden fixtures).
-
-The reference uses the classic table; ours is generated from a face rule, so
-triangles may split the same crossing polygons differently.  What must agree
-exactly is the welded vertex array (same crossings, same interpolation, same
-global edge ids); the surfaces must be closed, consistently and outwardly
-oriented, and enclose the same volume to within the diagonal choices.
+"""Marching cubes: the case table (the reference's classic
+triangulation re-indexed into our cell conventions) and the device pipeline
+vs the reference's marching_cubes (recon.py:39-108, golden fixtures): the
+welded vertex array (same crossings, same interpolation, same global edge
+ids) AND the faces (same triangles, same order, same vertex order) are
+bit-identical.
 """
 
 import numpy as np
@@ -76,20 +74,33 @@ def numpy_mc(values, lo, hi, res, iso):
     return verts, np.array(faces, dtype=np.int64).reshape(-1, 3)
 
 
-def test_generated_table_vs_reference_mc():
+def test_table_vs_reference_mc():
+    """The table walked in our conventions reproduces the reference's meshes
+    exactly: a binary occupancy grid (iso 0.5) and a smooth field (iso 0.3)."""
     g = golden("marching_cubes")
     lo, hi, res = grid_of(g, "g16")
     v, f = numpy_mc(g["occ"], lo, hi, res, 0.5)
     assert v.tobytes() == g["m1_vertices"].tobytes()
-    assert_closed_oriented(f)
-    vol, vref = signed_volume(v, f), signed_volume(g["m1_vertices"], g["m1_faces"])
-    assert vol > 0 and abs(vol - vref) <= 1e-2 * vref  # diagonal choices on a 16^3 grid
+    assert np.array_equal(f, g["m1_faces"])
+    assert signed_volume(v, f) > 0
     lo, hi, res = grid_of(g, "g14")
     v2, f2 = numpy_mc(g["smooth"], lo, hi, res, 0.3)
     assert v2.tobytes() == g["m2_vertices"].tobytes()
-    assert_closed_oriented(f2)
-    vol2, vref2 = signed_volume(v2, f2), signed_volume(g["m2_vertices"], g["m2_faces"])
-    assert abs(vol2 - vref2) <= 2e-2 * abs(vref2)
+    assert np.array_equal(f2, g["m2_faces"])
+
+
+def test_table_structure():
+    """Every case lists each crossed cell edge, and only crossed edges; the
+    two trivial cases (all inside / all outside) emit nothing."""
+    from paper_2407_11272_b200.mc_table import EDGES, TRI_COUNT, TRI_TABLE
+    assert TRI_COUNT[0] == 0 and TRI_COUNT[255] == 0
+    for case in range(256):
+        out = [(case >> c) & 1 for c in range(8)]
+        crossed = {e for e, (_, a, b) in enumerate(EDGES) if out[a] != out[b]}
+        row = TRI_TABLE[case]
+        used = {int(e) for e in row if e >= 0}
+        assert used == crossed, case
+        assert (row >= 0).sum() == 3 * TRI_COUNT[case]
 
 
 @pytest.mark.gpu
@@ -101,9 +112,11 @@ def test_device_mc_matches(cuda_device):
     spec = wv.GridSpec(lo, hi, res)
     m = marching_cubes(wv.ScalarField(spec, g["occ"]), iso=0.5)
     assert m.vertices.tobytes() == g["m1_vertices"].tobytes()
-    nv, nf = numpy_mc(g["occ"], lo, hi, res, 0.5)
-    assert np.array_equal(m.faces, nf)
-    assert_closed_oriented(m.faces)
+    assert np.array_equal(m.faces, g["m1_faces"])
+    lo2, hi2, res2 = grid_of(g, "g14")
+    m2 = marching_cubes(wv.ScalarField(wv.GridSpec(lo2, hi2, res2), g["smooth"]), iso=0.3)
+    assert m2.vertices.tobytes() == g["m2_vertices"].tobytes()
+    assert np.array_equal(m2.faces, g["m2_faces"])
     # smoothing the reference's own mesh reproduces the reference's result
     s = laplacian_smooth(wv.TriangleMesh(g["m1_vertices"], g["m1_faces"]), lam=0.15,
                          iterations=10)
@@ -112,9 +125,10 @@ def test_device_mc_matches(cuda_device):
     # voxelize -> marching cubes entirely on the device
     from paper_2407_11272_b200 import configs
     occ = wv.voxelize(wv.TriangleMesh(*configs.icosphere(2, 0.7)), spec, precision="f32")
-    m2 = marching_cubes(occ, iso=0.5)
-    assert_closed_oriented(m2.faces)
-    assert abs(signed_volume(m2.vertices, m2.faces) - signed_volume(m.vertices, m.faces)) < 1e-3
+    m3 = marching_cubes(occ, iso=0.5)
+    v3, f3 = numpy_mc(occ.values, lo, hi, res, 0.5)
+    assert m3.vertices.tobytes() == v3.tobytes() and np.array_equal(m3.faces, f3)
+    assert signed_volume(m3.vertices, m3.faces) > 0
     empty = marching_cubes(wv.ScalarField(spec, np.zeros(spec.num_nodes)), iso=0.5)
     assert empty.num_faces == 0 and empty.num_vertices == 0
 
@@ -124,17 +138,19 @@ def test_reconstruction_pipeline_scores_match_reference(cuda_device):
     """Acceptance criterion 5's pipeline (test_acceptance.py:170-214) on a
     procedural torus: exact voxelize at 48^3 -> marching cubes -> Laplacian
     smoothing -> sampled Chamfer / Hausdorff against the input, all on the
-    device.  Our case table splits some crossing polygons along other
-    diagonals, so the scores match the reference's to a few percent."""
+    device.  The marching-cubes faces are the reference's; the only
+    difference left is the f64 forward's atan2 (CUDA's vs libm's, <= 1e-12
+    in W), so the scores match the reference's to 1e-6 relative and the face
+    count exactly."""
     import paper_2407_11272_b200 as wv
     g = golden("recon_pipeline")
     mesh = wv.TriangleMesh(g["vertices"], g["faces"])
     spec = wv.GridSpec(*grid_of(g))
     field = wv.voxelize(mesh, spec, mode="exact")
     recon = wv.laplacian_smooth(wv.marching_cubes(field, iso=0.5), lam=0.15, iterations=10)
-    assert_closed_oriented(recon.faces)
     sc = wv.evaluate_reconstruction(mesh, recon, n=20000, repeats=3, seed=0)
     ref = g["scores"]
-    assert abs(sc["chamfer_mean"] - ref[0]) <= 0.03 * ref[0]
-    assert abs(sc["hausdorff_mean"] - ref[2]) <= 0.10 * ref[2]
-    assert abs(recon.num_faces - int(g["recon_faces"])) <= 0.01 * int(g["recon_faces"])
+    print("recon scores", sc, "reference", ref)
+    assert recon.num_faces == int(g["recon_faces"])
+    assert abs(sc["chamfer_mean"] - ref[0]) <= 1e-6 * ref[0]
+    assert abs(sc["hausdorff_mean"] - ref[2]) <= 1e-6 * ref[2]
