@@ -250,6 +250,8 @@ def count_launches(fn) -> int | None:
     counted by the CUDA activity trace (torch.profiler/CUPTI) on an untimed
     call; None if the tracer is unavailable."""
     import torch
+    if os.environ.get("CUDA_INJECTION64_PATH"):  # under ncu: CUPTI has one subscriber
+        return None
     try:
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CUDA]) as prof:

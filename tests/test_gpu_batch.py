@@ -34,15 +34,16 @@ def test_batch_loss_matches_oracle_per_mesh(cuda_device):
         assert abs(float(losses[b]) - one.loss) <= 1e-6 * one.loss
         g = verts.grad[b].double().cpu().numpy()
         assert np.abs(g - one.grads.vectors).max() <= 1e-5 * np.abs(one.grads.vectors).max()
-        # and close to the f64 oracle; the soft (dipole) loss of this coarse
-        # grid has nodes within ~1e-2 of face centroids (loss ~1e2), where
-        # the fp32 rounding of the centroids alone is ~1e-4 relative
+        # and the f64 oracle on the same f32-rounded inputs (north_star: 1e-4
+        # relative for gradients); the centroid rides as hi + lo in the
+        # records, so nodes ~1e-2 from a centroid (loss ~1e2) keep full fp32
+        # accuracy
         v32 = meshes[b][0].astype(np.float32).astype(np.float64)
         loss, grads, _ = orc.occupancy_loss_grad(v32, meshes[b][1], pts.astype(np.float32)
                                                  .astype(np.float64),
                                                  targets[b].double().cpu().numpy())
-        assert abs(float(losses[b]) - loss) <= 2e-3 * loss
-        assert np.abs(g - grads).max() <= 2e-3 * np.abs(grads).max()
+        assert abs(float(losses[b]) - loss) <= 1e-5 * loss
+        assert np.abs(g - grads).max() <= 1e-4 * np.abs(grads).max()
     # the deformation net trains through it
     torch.manual_seed(0)
     net = DeformationNet(3).cuda()

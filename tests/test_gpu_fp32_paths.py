@@ -52,9 +52,24 @@ def test_soft_forward_flags_on_centroid(torch_):
     mesh = wv.TriangleMesh(g["vertices"], g["faces"])
     cen = mesh.vertices[mesh.faces].mean(axis=1)
     pts = np.concatenate([cen[:3], [[3.0, 0.0, 0.0]]])
-    w, f = wv.winding_number_batch(mesh, pts, mode="soft", precision="f32")
+    # f64 (the reference's default): exact centroids are on-centroid hits
+    w, f = wv.winding_number_batch(mesh, pts, mode="soft", precision="f64")
     ref, rf = orc.winding_number_batch(g["vertices"], g["faces"], pts, mode="soft")
     assert np.array_equal(f, rf) and f[:3].all() and not f[3]
+    # f32: the kernels see f32-rounded points and corners (winding.py:362-373);
+    # with the centroid carried as hi + lo a rounded centroid is ~1e-8 off
+    # the true one, i.e. farther than eps = 1e-9 * diag: flags and values as
+    # the oracle's on the same rounded inputs
+    from test_gpu_fuzz import r32
+    w, f = wv.winding_number_batch(mesh, pts, mode="soft", precision="f32")
+    ref, rf = orc.winding_number_batch(r32(g["vertices"]), g["faces"], r32(pts), mode="soft")
+    assert np.array_equal(f, rf)
+    assert np.abs(w[~rf] - ref[~rf]).max() <= 1e-5 * np.abs(ref[~rf]).max()
+    # a point that IS the centroid in f32 arithmetic (a dyadic triangle) is hit
+    v = np.array([[0.0, 0.0, 0.0], [0.75, 0.0, 0.0], [0.0, 0.75, 0.0]])
+    w, f = wv.winding_number_batch(wv.TriangleMesh(v, [[0, 1, 2]]), [[0.25, 0.25, 0.0]],
+                                   mode="soft", precision="f32")
+    assert f[0]
 
 
 def _subset(w, n, seed):
