@@ -239,6 +239,40 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       if (r >= 4) pair(tile[f + 2], tile[f + 3], R2{}, R0{});
       else if (r == 3) one(tile[f + 2], R2{});
       if (r == 5) one(tile[f + 4], R1{});
+    } else if constexpr (Pol::kPairFaces) {
+      // two faces per angle evaluation (Pol::pair_fast); a pair that is not
+      // common everywhere goes face by face
+      // (groups of 2 point pairs: a group whose pair is not common
+      // everywhere goes face by face, the others keep the pair's terms)
+      auto do_pair = [&](const Rec& Ra, const Rec& Rb) {
+        uint32_t rare_a = 0, rare_b = 0;
+        if constexpr (kRows) {
+          const typename Pol::Row wa = Pol::row(Ra, rx, ry), wb = Pol::row(Rb, rx, ry);
+#pragma unroll
+          for (int g0 = 0; g0 < PP; g0 += 2) {
+            if (!Pol::template face_row_pair<2>(Ra, wa, Rb, wb, qz + g0, ctx, tacc + g0)) {
+              rare_a |= Pol::template face_row<2>(Ra, wa, qz + g0, ctx, tacc + g0) << (2 * g0);
+              rare_b |= Pol::template face_row<2>(Rb, wb, qz + g0, ctx, tacc + g0) << (2 * g0);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int g0 = 0; g0 < PP; g0 += 2) {
+            if (!Pol::template face_pair<2>(Ra, Rb, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)) {
+              rare_a |= Pol::template face<2>(Ra, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)
+                        << (2 * g0);
+              rare_b |= Pol::template face<2>(Rb, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)
+                        << (2 * g0);
+            }
+          }
+        }
+        do_rare(Ra, rare_a);
+        do_rare(Rb, rare_b);
+      };
+      int f = 0;
+#pragma unroll 1
+      for (; f + 2 <= cnt; f += 2) do_pair(tile[f], tile[f + 1]);
+      if (f < cnt) do_face(tile[f], R0{});
     } else {
 #pragma unroll 1
       for (int f = 0; f < cnt; ++f) do_face(tile[f], R0{});

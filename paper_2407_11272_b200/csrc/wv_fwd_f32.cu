@@ -249,6 +249,116 @@ struct ExactPol {
       rare |= tail2(R, alpha[pp], la2[pp], lb2[pp], lc2[pp], ctx, tacc[pp]) << (2 * pp);
     return rare;
   }
+  // ---- two faces per angle (kPairFaces) --------------------------------
+  // theta_a + theta_b = atan(T), T = tan(theta_a + theta_b)
+  //   = (alpha_a beta_b + alpha_b beta_a) / (beta_a beta_b - alpha_a alpha_b),
+  // so a PAIR of common faces needs one reciprocal and one polynomial instead
+  // of two: 3.5 MUFU per pair instead of 4 (this kernel is bound by the MUFU
+  // pipe).  Valid whenever |T| < 1/8 and both betas are well conditioned
+  // (beta > |a||b||c|/2, as tail2): then |t_i| = |alpha_i|/beta_i < 2
+  // (|alpha| <= |a||b||c|), so beta_a beta_b - alpha_a alpha_b <= 0 -- a sum
+  // past pi/2 -- cannot come with |T| < 1/8, and num = den = 0 cannot
+  // happen.  Accuracy: num and den are well conditioned when |T| < 1/8
+  // (cancellation in num costs only ulp(t_i) absolute), so the pair's term
+  // has the single-face error.  A pair that fails takes both faces through
+  // the single-face path (nothing of the pair was added).
+  static constexpr bool kPairFaces = true;
+  __device__ __forceinline__ static void beta_ee(const Rec& R, F2 la2, F2 lb2, F2 lc2, F2& beta,
+                                                 F2& ee) {
+    const F2 la = sqrt2(la2), lb = sqrt2(lb2), lc = sqrt2(lc2);
+    const F2 half = f2s(0.5f);
+    const F2 ab = fma2(add2(la2, lb2), half, f2s(-fabsf(R.v1.w)));
+    const F2 bc = fma2(add2(lb2, lc2), half, f2s(-fabsf(R.v2.w)));
+    const F2 ca = fma2(add2(lc2, la2), half, f2s(-R.n.w));
+    const F2 labc = mul2(la, mul2(lb, lc));
+    beta = fma2(ca, lb, fma2(ab, lc, fma2(bc, la, labc)));
+    ee = fma2(beta, f2s(-2.0f), labc);  // < 0: well conditioned (finish_len)
+  }
+  // geo(k, pp, alpha, la2, lb2, lc2): the pair quantities of face k (0: Ra,
+  // 1: Rb) and point pair pp (row or generic form, same operations as
+  // face_row / face)
+  template <int PP, class Geo>
+  __device__ __forceinline__ static bool pair_fast(const Rec& Ra, const Rec& Rb, Geo geo,
+                                                   bool near, F2* tacc) {
+    F2 tq[PP], tp[PP];
+    float m = -1.0f;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      F2 aa, la2, lb2, lc2, ba, ea, ab_, bb, eb;
+      geo(0, pp, aa, la2, lb2, lc2);
+      beta_ee(Ra, la2, lb2, lc2, ba, ea);
+      geo(1, pp, ab_, la2, lb2, lc2);
+      beta_ee(Rb, la2, lb2, lc2, bb, eb);
+      const F2 num = fma2(aa, bb, mul2(ab_, ba));
+      const F2 den = fma2(mul2(aa, ab_), f2s(-1.0f), mul2(ba, bb));
+      const F2 tt = mul2(num, rcp2(den));
+      const F2 s2 = mul2(tt, tt);
+      const F2 dd = add2(s2, f2s(-1.0f / 64.0f));
+      float d0, d1, a0, a1, b0, b1;
+      split(dd, d0, d1);
+      split(ea, a0, a1);
+      split(eb, b0, b1);
+      m = fmaxf(m, fmaxf(fmaxf(d0, d1), fmaxf(fmaxf(a0, a1), fmaxf(b0, b1))));
+      tq[pp] = tt;
+      tp[pp] = fma2(fma2(s2, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s2,
+                    f2s(1.0f));
+    }
+    if (m < 0.0f && !near) {
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
+      return true;
+    }
+    return false;
+  }
+  template <int PP>
+  __device__ __forceinline__ static bool face_row_pair(const Rec& Ra, const Row& wa,
+                                                       const Rec& Rb, const Row& wb,
+                                                       const F2* qz, const Ctx& ctx, F2* tacc) {
+    const bool near = fminf(fminf(wa.a2, fminf(wa.b2, wa.c2)),
+                            fminf(wb.a2, fminf(wb.b2, wb.c2))) < ctx.eps2;
+    auto geo = [&](int k, int pp, F2& alpha, F2& la2, F2& lb2, F2& lc2) {
+      const Rec& R = k ? Rb : Ra;
+      const Row& w = k ? wb : wa;
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
+      const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
+      alpha = fma2(f2s(R.n.z), az, f2s(w.alpha));
+      la2 = fma2(az, az, f2s(w.a2));
+      lb2 = fma2(bz, bz, f2s(w.b2));
+      lc2 = fma2(cz, cz, f2s(w.c2));
+    };
+    return pair_fast<PP>(Ra, Rb, geo, near, tacc);
+  }
+  template <int PP>
+  __device__ __forceinline__ static bool face_pair(const Rec& Ra, const Rec& Rb, const F2* qx,
+                                                   const F2* qy, const F2* qz, const Ctx& ctx,
+                                                   F2* tacc) {
+    float mn = __int_as_float(0x7f800000);
+    auto geo = [&](int k, int pp, F2& alpha, F2& la2, F2& lb2, F2& lc2) {
+      const Rec& R = k ? Rb : Ra;
+      const F2 ax = sub2(f2s(R.v0e.x), qx[pp]), ay = sub2(f2s(R.v0e.y), qy[pp]);
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]);
+      const F2 bx = sub2(f2s(R.v1.x), qx[pp]), by = sub2(f2s(R.v1.y), qy[pp]);
+      const F2 bz = sub2(f2s(R.v1.z), qz[pp]);
+      const F2 cx = sub2(f2s(R.v2.x), qx[pp]), cy = sub2(f2s(R.v2.y), qy[pp]);
+      const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
+      alpha = fma2(f2s(R.n.z), az, fma2(f2s(R.n.y), ay, mul2(f2s(R.n.x), ax)));
+      la2 = dot2(ax, ay, az, ax, ay, az);
+      lb2 = dot2(bx, by, bz, bx, by, bz);
+      lc2 = dot2(cx, cy, cz, cx, cy, cz);
+      float a0, a1, b0, b1, c0, c1;
+      split(la2, a0, a1);
+      split(lb2, b0, b1);
+      split(lc2, c0, c1);
+      mn = fminf(mn, fminf(fminf(a0, a1), fminf(fminf(b0, b1), fminf(c0, c1))));
+    };
+    // the vertex-hit test needs every lane's distances: evaluate, then decide
+    F2 tq[PP];
+    for (int pp = 0; pp < PP; ++pp) tq[pp] = tacc[pp];
+    const bool ok = pair_fast<PP>(Ra, Rb, geo, false, tq);
+    if (!ok || mn < ctx.eps2) return false;
+    for (int pp = 0; pp < PP; ++pp) tacc[pp] = tq[pp];
+    return true;
+  }
   template <int PP>
   __device__ __forceinline__ static uint32_t face_row(const Rec& R, const Row& w, const F2* qz,
                                                       const Ctx& ctx, F2* tacc) {
@@ -314,6 +424,7 @@ struct ExactPol {
 #endif
 struct ExactStripPol : ExactPol {
   static constexpr bool kStrip = true;
+  static constexpr bool kPairFaces = false;  // strips pair their faces themselves
   static_assert(kTile == 128, "pack_strip_kernel restarts a strip every 128 records");
   static constexpr int kP = WV_STRIP_P;
   static constexpr int kMinBlocksRow = WV_STRIP_MINB;
@@ -447,6 +558,7 @@ struct SoftPol {
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (8.0 * kPi);
   static constexpr bool kStrip = false;
+  static constexpr bool kPairFaces = false;
   struct Slot {};
   struct Ctx {
     float eps2;
