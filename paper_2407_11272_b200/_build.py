@@ -51,13 +51,19 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, objdir: Path | None = None,
+          lib: Path | None = None) -> Path:
+    """Compile every csrc/*.cu (stale ones only) and link the library.
+    ``objdir`` / ``lib``: another object directory and output (A/B variant
+    builds, tools/build_variant.py)."""
     nvcc = _nvcc()
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+    OBJDIR_ = objdir or OBJDIR
+    LIB_ = lib or LIB
+    OBJDIR_.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list(INCLUDE.glob("*.h"))
     objs = []
     for src in sources():
-        obj = OBJDIR / (src.stem + ".o")
+        obj = OBJDIR_ / (src.stem + ".o")
         objs.append(obj)
         if not force and not _stale(obj, [src, *headers]):
             continue
@@ -72,11 +78,11 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             cmd.insert(-4, "-Xptxas=-v")
         print("[windvox_b200] nvcc", src.name, flush=True)
         subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+    if force or _stale(LIB_, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB_), *map(str, objs), "-lcudart_static",
                "-lrt", "-lpthread", "-ldl", "-lgomp"]
         subprocess.run(cmd, check=True)
-    return LIB
+    return LIB_
 
 
 def build_probe() -> Path:

@@ -9,10 +9,14 @@ the library is missing or no CUDA device is visible, every entry point raises
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_lib" / "libwindvox_b200.so"
+# A/B builds of kernel variants (tools/build_variant.py) load another copy
+if os.environ.get("WV_LIB_PATH"):
+    LIB_PATH = Path(os.environ["WV_LIB_PATH"])
 
 WV_OK = 0
 PACK_EXACT_F32 = 1

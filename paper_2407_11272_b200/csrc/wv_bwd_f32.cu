@@ -203,9 +203,13 @@ struct ExactEdgeBwd {
     w.qy = qy;
     return w;
   }
-  // kMask = false (hot path): no masking; the |e|^2/d-products are summed
-  //   into *mr; a run whose sum reaches kIllRatio (an ill pair, or several
-  //   moderately close ones) is discarded and redone with kMask = true.
+  // kMask = false (hot path): no masking; the pair's reciprocal edge product
+  //   rr = 1/(d01 d12 d20) goes to *mr, whose running max over the run (ALU
+  //   pipe, NaN-propagating) times |e01|^2 |e12|^2 |e20|^2 is the run's worst
+  //   ill-conditioning ratio product (ill_run); a run that reaches kIllRatio
+  //   is discarded and redone with kMask = true.  (Each pair's fp32 terms
+  //   carry a relative error ~1e-7 x its ratio, so the worst pair bounds the
+  //   run sum's relative error.)
   // kMask = true: ill lanes contribute nothing here (bits returned; the
   //   caller adds them with exact_pair_f64).
   template <bool kUnit, bool kMask = true>
@@ -225,10 +229,10 @@ struct ExactEdgeBwd {
     const F2 rr = rcp2_abs(mul2(d01, p12));
     // ill-conditioned lanes (some d_e < |e|^2 / kIllRatio, or a non-finite
     // reciprocal) leave the fp32 sums: cr = 0 here, exact_pair_f64 later
-    const F2 ru = mul2(rr, f2s(R.u.x * R.u.y * R.u.z));
     bool ill0 = false, ill1 = false;
     F2 cr;  // coef / (d01 d12 d20)
     if constexpr (kMask) {
+      const F2 ru = mul2(rr, f2s(R.u.x * R.u.y * R.u.z));
       float ru0, ru1;
       split(ru, ru0, ru1);
       ill0 = !(ru0 < kIllRatio);
@@ -237,10 +241,7 @@ struct ExactEdgeBwd {
       split(mul2(coef, rr), r0, r1);
       cr = f2(ill0 ? 0.0f : r0, ill1 ? 0.0f : r1);
     } else {
-      // the pair's ratios go out; step_row sums them (>= 0; inf / NaN
-      // propagate), so any single ill pair pushes the run's sum past
-      // kIllRatio
-      *mr = ru;
+      *mr = rr;  // (>= 0: rcp2_abs; inf / NaN propagate through maxnan)
       cr = mul2(coef, rr);
     }
     const F2 q0 = mul2(cr, d01);
@@ -271,12 +272,18 @@ struct ExactEdgeBwd {
 #pragma unroll
     for (int u = 0; u < N; ++u)
       pair_row2<kUnit, false>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z, &ru[u]);
-    // pairwise sum (short dependency chain), then one add into the run's sum
+    // pairwise max (short dependency chain), then one max into the run's
 #pragma unroll
     for (int h = 1; h < N; h *= 2)
 #pragma unroll
-      for (int u = 0; u + h < N; u += 2 * h) ru[u] = add2(ru[u], ru[u + h]);
-    *mr = add2(*mr, ru[0]);
+      for (int u = 0; u + h < N; u += 2 * h) ru[u] = maxnan2(ru[u], ru[u + h]);
+    *mr = maxnan2(*mr, ru[0]);
+  }
+  // the run's worst ratio product reached kIllRatio (or is NaN)
+  __device__ __forceinline__ static bool ill_run(const Rec& R, F2 mr) {
+    float m0, m1;
+    split(mr, m0, m1);
+    return !(maxnan(m0, m1) * (R.u.x * R.u.y * R.u.z) < kIllRatio);
   }
   __device__ __forceinline__ static void rare_pair(const Rec& R, float qx, float qy, float qz,
                                                    float c, double (*acc)[kBwdThreads],
@@ -430,6 +437,7 @@ struct SoftBwd {
   template <bool kUnit, class W>
   __device__ __forceinline__ static void redo_run(const Rec&, const W&, const float4*, int, int,
                                                   float, F2*, double (*)[kBwdThreads]) {}
+  __device__ __forceinline__ static bool ill_run(const Rec&, F2) { return false; }
   template <bool kUnit, int N>
   __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
                                                   float eps2, F2* z, F2*) {
@@ -534,6 +542,7 @@ struct SoftBwdPair {
   template <bool kUnit, class W>
   __device__ __forceinline__ static void redo_run(const Rec&, const W&, const float4*, int, int,
                                                   float, F2*, double (*)[kBwdThreads]) {}
+  __device__ __forceinline__ static bool ill_run(const Rec&, F2) { return false; }
   struct Row {
     One::Row r[2];
   };
@@ -679,7 +688,6 @@ struct ExactEdgeBwdPair {
     if (!w.paired) return;  // run_end evaluates the faces one by one
     const ExactGradRecF32& F = R.f[0];
     const ExactGradRecF32& G = R.f[1];
-    const float u1p = F.u.x * F.u.y * F.u.z, u2p = G.u.y * G.u.z;
     F2 ru[N];
 #pragma unroll
     for (int u = 0; u < N; ++u) {
@@ -697,7 +705,10 @@ struct ExactEdgeBwdPair {
       const F2 dcd = fma2(scd, scd, f2s(-G.u.y)), ddb = fma2(sdb, sdb, f2s(-G.u.z));
       const F2 p1 = mul2(dbc, dca), rr1 = rcp2_abs(mul2(dab, p1));
       const F2 rr2 = rcp2_abs(mul2(dcd, ddb));
-      ru[u] = fma2(rr2, f2s(u2p), mul2(rr1, f2s(u1p)));  // both faces' ratio products
+      float r10, r11, r20, r21;  // lane max per face (ALU): F1's lo, F2's hi
+      split(rr1, r10, r11);
+      split(rr2, r20, r21);
+      ru[u] = f2(maxnan(r10, r11), maxnan(r20, r21));
       const F2 cr1 = mul2(coef, rr1), q0 = mul2(cr1, dab);
       const F2 tab = mul2(cr1, p1), tbc = mul2(q0, dca), tca = mul2(q0, dbc);
       const F2 cr2 = mul2(coef, rr2);
@@ -728,8 +739,8 @@ struct ExactEdgeBwdPair {
 #pragma unroll
     for (int h = 1; h < N; h *= 2)
 #pragma unroll
-      for (int u = 0; u + h < N; u += 2 * h) ru[u] = add2(ru[u], ru[u + h]);
-    *mr = add2(*mr, ru[0]);
+      for (int u = 0; u + h < N; u += 2 * h) ru[u] = maxnan2(ru[u], ru[u + h]);
+    *mr = maxnan2(*mr, ru[0]);
   }
   // one face over a run with the single-face row code (broken welds), flushed
   __device__ __noinline__ static void single_run(const ExactGradRecF32& Rk, float qx, float qy,
@@ -744,9 +755,7 @@ struct ExactEdgeBwdPair {
       const float4 zc = zcs[j];
       if (!(zc.z == 0.0f && zc.w == 0.0f)) One::step_row<true, 1>(Rk, rk, &zc, eps2, z, &mr);
     }
-    float m0, m1;
-    split(mr, m0, m1);
-    if (!(m0 + m1 < One::kIllRatio)) One::redo_run<true>(Rk, rk, zcs, j0, e, eps2, z, acc);
+    if (One::ill_run(Rk, mr)) One::redo_run<true>(Rk, rk, zcs, j0, e, eps2, z, acc);
     One::flush_row<true>(Rk, rk, z, acc);
   }
   __device__ __noinline__ static void redo_pair(const Rec& R, float qx, float qy,
@@ -770,9 +779,12 @@ struct ExactEdgeBwdPair {
       single_run(R.f[1], w.qx, w.qy, zcs, j0, e, eps2, acc + One::kAcc);
       return;
     }
+    // mr = (max rr of F1, max rr of F2): ratio products with each face's
+    // squared edge lengths (F2's shared edge BC is F1's)
     float m0, m1;
     split(mr, m0, m1);
-    if (!(m0 + m1 < One::kIllRatio)) {  // rare: an ill-conditioned pair in the run
+    const float u1p = R.f[0].u.x * R.f[0].u.y * R.f[0].u.z, u2p = R.f[1].u.y * R.f[1].u.z;
+    if (!(m0 * u1p < One::kIllRatio) || !(m1 * u2p < One::kIllRatio)) {  // rare: ill pair
       redo_pair(R, w.qx, w.qy, zcs, j0, e, eps2, acc);
       return;
     }
@@ -834,7 +846,7 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
 #pragma unroll
     for (int i = 0; i < Pol::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
     const int e = j + run, j0 = j;
-    F2 mr = f2(0.0f, 0.0f);  // summed ill-conditioning ratios of the run (exact only)
+    F2 mr = f2(0.0f, 0.0f);  // running max of the ill-conditioning screen (exact only)
     // Pol::kRowStep point pairs per step under one (warp-uniform)
     // zero-coefficient test, so their dependency chains share a basic block
     // and interleave (a zero-coefficient pair next to a live one adds
@@ -861,9 +873,7 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
     if constexpr (Pol::kPairRuns) {
       Pol::template run_end<kUnit>(R, w, ch.zc, j0, e, eps2, z, mr, acc);
     } else {
-      float m0, m1;
-      split(mr, m0, m1);
-      if (!(m0 + m1 < ExactEdgeBwd::kIllRatio))  // rare: an ill-conditioned pair in the run
+      if (Pol::ill_run(R, mr))  // rare: an ill-conditioned pair in the run
         Pol::template redo_run<kUnit>(R, w, ch.zc, j0, e, eps2, z, acc);
       Pol::flush_row(R, w, z, acc);
     }

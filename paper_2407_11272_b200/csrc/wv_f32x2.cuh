@@ -80,4 +80,20 @@ __device__ __forceinline__ F2 rcp2_abs(F2 a) {
   return f2(rcp_approx(fabsf(l)), rcp_approx(fabsf(h)));
 }
 
+// NaN-propagating max (max.NaN.f32, ALU pipe): the exact backward screens a
+// row run for ill-conditioned pairs with a running max of their reciprocal
+// edge products; a NaN (a point ON a vertex) must poison the run, so the run
+// is redone with per-lane masking
+__device__ __forceinline__ float maxnan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ F2 maxnan2(F2 a, F2 b) {
+  float al, ah, bl, bh;
+  split(a, al, ah);
+  split(b, bl, bh);
+  return f2(maxnan(al, bl), maxnan(ah, bh));
+}
+
 }  // namespace wv

@@ -244,24 +244,26 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       // common everywhere goes face by face
       // (groups of 2 point pairs: a group whose pair is not common
       // everywhere goes face by face, the others keep the pair's terms)
+      constexpr int G = Pol::kPairGroup;
+      static_assert(PP % G == 0, "point pairs split into whole decision groups");
       auto do_pair = [&](const Rec& Ra, const Rec& Rb) {
         uint32_t rare_a = 0, rare_b = 0;
         if constexpr (kRows) {
           const typename Pol::Row wa = Pol::row(Ra, rx, ry), wb = Pol::row(Rb, rx, ry);
 #pragma unroll
-          for (int g0 = 0; g0 < PP; g0 += 2) {
-            if (!Pol::template face_row_pair<2>(Ra, wa, Rb, wb, qz + g0, ctx, tacc + g0)) {
-              rare_a |= Pol::template face_row<2>(Ra, wa, qz + g0, ctx, tacc + g0) << (2 * g0);
-              rare_b |= Pol::template face_row<2>(Rb, wb, qz + g0, ctx, tacc + g0) << (2 * g0);
+          for (int g0 = 0; g0 < PP; g0 += G) {
+            if (!Pol::template face_row_pair<G>(Ra, wa, Rb, wb, qz + g0, ctx, tacc + g0)) {
+              rare_a |= Pol::template face_row<G>(Ra, wa, qz + g0, ctx, tacc + g0) << (2 * g0);
+              rare_b |= Pol::template face_row<G>(Rb, wb, qz + g0, ctx, tacc + g0) << (2 * g0);
             }
           }
         } else {
 #pragma unroll
-          for (int g0 = 0; g0 < PP; g0 += 2) {
-            if (!Pol::template face_pair<2>(Ra, Rb, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)) {
-              rare_a |= Pol::template face<2>(Ra, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)
+          for (int g0 = 0; g0 < PP; g0 += G) {
+            if (!Pol::template face_pair<G>(Ra, Rb, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)) {
+              rare_a |= Pol::template face<G>(Ra, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)
                         << (2 * g0);
-              rare_b |= Pol::template face<2>(Rb, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)
+              rare_b |= Pol::template face<G>(Rb, qx + g0, qy + g0, qz + g0, ctx, tacc + g0)
                         << (2 * g0);
             }
           }

@@ -73,8 +73,14 @@ struct ExactPol {
   static constexpr int kStages = 4;
   static constexpr int kConsumerWarps = 4;
   static constexpr int kThreads = kConsumerWarps * 32;
-  static constexpr int kMinBlocks = 4;
-  static constexpr int kMinBlocksRow = 4;  // 5 (96 regs) spills and measured 2% slower
+#ifndef WV_EXACT_MINB
+#define WV_EXACT_MINB 4
+#endif
+#ifndef WV_EXACT_MINB_ROW
+#define WV_EXACT_MINB_ROW 4  // 5 (96 regs) spills and measured 2% slower (single faces)
+#endif
+  static constexpr int kMinBlocks = WV_EXACT_MINB;
+  static constexpr int kMinBlocksRow = WV_EXACT_MINB_ROW;
   static constexpr int kP = 8;
   static constexpr double kScale = 1.0 / (2.0 * kPi);
   static constexpr bool kStrip = false;
@@ -263,6 +269,10 @@ struct ExactPol {
   // has the single-face error.  A pair that fails takes both faces through
   // the single-face path (nothing of the pair was added).
   static constexpr bool kPairFaces = true;
+#ifndef WV_PAIR_GROUP
+#define WV_PAIR_GROUP 2
+#endif
+  static constexpr int kPairGroup = WV_PAIR_GROUP;  // point pairs per pair decision
   __device__ __forceinline__ static void beta_ee(const Rec& R, F2 la2, F2 lb2, F2 lc2, F2& beta,
                                                  F2& ee) {
     const F2 la = sqrt2(la2), lb = sqrt2(lb2), lc = sqrt2(lc2);

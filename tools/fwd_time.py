@@ -1,0 +1,53 @@
+"""CUDA-event time of one kernel path on a BASELINE config's full lattice
+(re-pack included, as a step does), min over reps -- for A/B variant builds:
+
+    WV_LIB_PATH=scratch/variants/X/lib.so python tools/fwd_time.py --config c3r [--bwd]
+"""
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3r")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--bwd", action="store_true")
+    a = ap.parse_args()
+    import torch
+    from paper_2407_11272_b200 import configs, device
+    w = configs.make(a.config)
+    grid = (w.lo, w.hi, w.res)
+    dm = device.DeviceMesh.from_numpy(w.vertices, w.faces)
+    v, f = device.forward(dm, "exact", "f32", grid=grid)
+    coefs = torch.where(f.bool(), 0.0, 2.0 * (v - (v > 0.5).float()))
+
+    def run():
+        dm.invalidate()
+        if a.bwd:
+            device.face_grad(dm, "exact", "f32", coefs, grid=grid)
+        else:
+            device.forward(dm, "exact", "f32", grid=grid)
+
+    run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(json.dumps({"lib": os.environ.get("WV_LIB_PATH", "default"), "config": a.config,
+                      "bwd": a.bwd, "ms": min(ts), "all": ts}))
+
+
+if __name__ == "__main__":
+    main()
