@@ -174,7 +174,45 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #endif
       using Yes = std::true_type;
       using No = std::false_type;
+      // the row part of a face: C's computed, A's and B's carried (ring of 3)
+      auto row_of = [&](const Rec& R, auto rot, auto may_restart, bool& restart) {
+        constexpr int kRot = decltype(rot)::value;
+        restart = decltype(may_restart)::value && __float_as_int(R.v1.w) < 0;
+        typename Pol::Row w = Pol::row_c(R, rx, ry);
+        if (restart) Pol::row_ab(R, rx, ry, rrow[kRot], rrow[(kRot + 1) % 3]);
+        w.a2 = rrow[kRot];
+        w.b2 = rrow[(kRot + 1) % 3];
+        rrow[(kRot + 2) % 3] = w.c2;
+        return w;
+      };
       auto pair_body = [&](const Rec& Ra, const Rec& Rb, auto rota, auto rotb, auto mr) {
+       if constexpr (Pol::kPairAngle && !decltype(mr)::value) {
+        // both faces continue their strip: one angle evaluation for the pair
+        constexpr int ka = decltype(rota)::value, kb = decltype(rotb)::value;
+        bool ra, rb;
+        const typename Pol::Row wa = row_of(Ra, rota, mr, ra);
+        const typename Pol::Row wb = row_of(Rb, rotb, mr, rb);
+        {
+          F2 tq[PP], tp[PP];
+          if (Pol::template strip_pair_fast<PP>(Ra, wa, Rb, wb, qz, ctx, slot[ka],
+                                                slot[(ka + 1) % 3], slot[(ka + 2) % 3],
+                                                slot[(kb + 2) % 3], tq, tp)) {
+#pragma unroll
+            for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
+            return;
+          }
+        }
+        // rare: face by face (face a restarts: its A slot now holds b's C)
+        F2 tqa[PP], tpa[PP], tqb[PP], tpb[PP];
+        const bool oka = Pol::template strip_fast<PP>(Ra, wa, qz, ctx, true, slot[ka],
+                                                      slot[(ka + 1) % 3], slot[(ka + 2) % 3],
+                                                      tqa, tpa);
+        const bool okb = Pol::template strip_fast<PP>(Rb, wb, qz, ctx, false, slot[kb],
+                                                      slot[(kb + 1) % 3], slot[(kb + 2) % 3],
+                                                      tqb, tpb);
+        commit(Ra, oka, tqa, tpa);
+        commit(Rb, okb, tqb, tpb);
+       } else {
 #if WV_STRIP_PAIR_TERMS
         F2 tqa[PP], tpa[PP], tqb[PP], tpb[PP];  // both faces' terms
         const bool oka = fast(Ra, rota, tqa, tpa, mr);
@@ -211,6 +249,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
           commit(Rb, okb, tq, tp);
         }
 #endif
+       }
       };
       // one restart test per pair: the common case (both faces continue a
       // strip) runs as one basic block up to the commit test

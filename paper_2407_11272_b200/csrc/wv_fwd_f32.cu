@@ -529,6 +529,80 @@ struct ExactStripPol : ExactPol {
     const bool near = fminf(w.a2, fminf(w.b2, w.c2)) < ctx.eps2;
     return ms < 1.0f / 256.0f && cond && !near;  // t^2 < 1/64
   }
+  // Two consecutive strip faces for ONE angle evaluation (tan addition, see
+  // ExactPol::pair_fast): with B = 2 beta, the pair's t/2 is
+  //   (alpha_a B_b + alpha_b B_a) / (B_a B_b - 4 alpha_a alpha_b),
+  // one reciprocal and one polynomial for two faces (MUFU 2 -> 1.5 per pair).
+  // Both faces' conditioning tests and vertex-hit screens must pass, and the
+  // pair's angle test; the distance slots are updated exactly as two
+  // strip_fast calls do (so a failed pair can redo the faces one by one).
+#ifndef WV_STRIP_PAIR_ANGLE
+#define WV_STRIP_PAIR_ANGLE 1
+#endif
+  static constexpr bool kPairAngle = WV_STRIP_PAIR_ANGLE;
+  template <int PP>
+  __device__ __forceinline__ static void restart_ab(const Rec& R, const Row& w, const F2* qz,
+                                                    Slot* sA, Slot* sB) {
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
+      sA[pp].d = sqrt2(fma2(az, az, f2s(w.a2)));
+      sB[pp].d = sqrt2(fma2(bz, bz, f2s(w.b2)));
+      sA[pp].s = add2(sA[pp].d, sB[pp].d);
+    }
+  }
+  // one face's alpha and 2 beta at point pair pp (strip_fast's operations)
+  __device__ __forceinline__ static void ab_pp(const Rec& R, const Row& w, F2 qz, float kab,
+                                               float kbc, float kca, Slot& sA, Slot& sB,
+                                               Slot& sC, F2& alpha, F2& beta2, bool& cond) {
+    const F2 cz = sub2(f2s(R.v2.z), qz);
+    alpha = fma2(f2s(R.n.z), cz, f2s(w.alpha));
+    const F2 lc = sqrt2(fma2(cz, cz, f2s(w.c2)));
+    const F2 la = sA.d, lb = sB.d;
+    const F2 sbc = add2(lb, lc), sca = add2(lc, la);
+    const F2 x = mul2(mul2(sA.s, sbc), sca);
+    sC.d = lc;
+    sB.s = sbc;
+    const F2 lp = fma2(lc, f2s(kab), fma2(lb, f2s(kca), mul2(la, f2s(kbc))));
+    beta2 = fma2(lp, f2s(0.875f), x);
+    float x0, x1, l0, l1;
+    split(x, x0, x1);
+    split(lp, l0, l1);
+    cond = cond && (l0 > -x0) && (l1 > -x1);
+  }
+  template <int PP>
+  __device__ __forceinline__ static bool strip_pair_fast(const Rec& Ra, const Row& wa,
+                                                         const Rec& Rb, const Row& wb,
+                                                         const F2* qz, const Ctx& ctx,
+                                                         Slot* s0, Slot* s1,
+                                                         Slot* s2, Slot* s3, F2* tq, F2* tp) {
+    // face a: slots (s0, s1) -> s2; face b: (s1, s2) -> s3 (= s0's storage).
+    // Only for pairs that continue their strip (a restart takes strip_fast).
+    constexpr float kL = -16.0f / 7.0f;
+    const float kab_a = kL * fabsf(Ra.v1.w), kbc_a = kL * fabsf(Ra.v2.w), kca_a = kL * Ra.n.w;
+    const float kab_b = kL * fabsf(Rb.v1.w), kbc_b = kL * fabsf(Rb.v2.w), kca_b = kL * Rb.n.w;
+    constexpr float kC2 = 32.0f * 0.19669890403747559f, kC1 = 8.0f * -0.33331409096717834f;
+    float ms = 0.0f;
+    bool cond = true;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      F2 aa, ba, ab, bb;
+      ab_pp(Ra, wa, qz[pp], kab_a, kbc_a, kca_a, s0[pp], s1[pp], s2[pp], aa, ba, cond);
+      ab_pp(Rb, wb, qz[pp], kab_b, kbc_b, kca_b, s1[pp], s2[pp], s3[pp], ab, bb, cond);
+      const F2 num = fma2(aa, bb, mul2(ab, ba));
+      const F2 den = fma2(mul2(aa, ab), f2s(-4.0f), mul2(ba, bb));
+      const F2 th = mul2(num, rcp2(den));  // T/2, T = tan(theta_a + theta_b)
+      const F2 s4 = mul2(th, th);
+      float u0, u1;
+      split(s4, u0, u1);
+      ms = fmaxf(ms, fmaxf(u0, u1));
+      tq[pp] = th;
+      tp[pp] = fma2(fma2(s4, f2s(kC2), f2s(kC1)), s4, f2s(2.0f));
+    }
+    const bool near = fminf(fminf(wa.a2, fminf(wa.b2, wa.c2)),
+                            fminf(wb.a2, fminf(wb.b2, wb.c2))) < ctx.eps2;
+    return ms < 1.0f / 256.0f && cond && !near;
+  }
   // A face whose pairs are not all common: tail2 per lane, from squared
   // distances recomputed from the record (the row parts bitwise the carried
   // ones); returns the lanes for the fp64 path
