@@ -373,9 +373,7 @@ struct SoftBwd {
     split(mul2(mul2(coef, rs2), rs), cl, ch);
     // r < eps: that face is skipped for that point (_kernels.py:203-204)
     const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
-    // c3 S / r^2 as (c3 (S / r)) / r: |S / r| <= |N|, so a node next to a
-    // centroid does not overflow fp32 through 1/r^5
-    const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);
+    const F2 c5 = mul2(mul2(c3, S), rs2);
     // G1 = w x d, G2 = d x u
     const F2 g1x = sub2(mul2(f2s(R.w.y), dz), mul2(f2s(R.w.z), dy));
     const F2 g1y = sub2(mul2(f2s(R.w.z), dx), mul2(f2s(R.w.x), dz));
@@ -421,10 +419,11 @@ struct SoftBwd {
     const F2 S = fma2(f2s(R.n.z), dz, f2s(w.s));
     float r2l, r2h, cl, ch;
     split(r2, r2l, r2h);
-    split(mul2(mul2(coef, mul2(rs, rs)), rs), cl, ch);
+    const F2 rs2 = mul2(rs, rs);
+    split(mul2(mul2(coef, rs2), rs), cl, ch);
     // r < eps: that face is skipped for that point (_kernels.py:203-204)
     const F2 c3 = f2(r2l < eps2 ? 0.0f : cl, r2h < eps2 ? 0.0f : ch);
-    const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);  // no 1/r^5 overflow (pair2)
+    const F2 c5 = mul2(mul2(c3, S), rs2);
     z[0] = add2(z[0], c3);
     z[1] = fma2(c3, dz, z[1]);
     z[2] = add2(z[2], c5);
@@ -461,8 +460,9 @@ struct SoftBwd {
     for (int u = 0; u < N; ++u) {
       const F2 rs = rsqrt2(r2[u]);
       const F2 S = fma2(f2s(R.n.z), dz[u], f2s(w.s));
-      const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), mul2(rs, rs)), rs);
-      const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);
+      const F2 rs2 = mul2(rs, rs);
+      const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), rs2), rs);
+      const F2 c5 = mul2(mul2(c3, S), rs2);
       z[0] = add2(z[0], c3);
       z[1] = fma2(c3, dz[u], z[1]);
       z[2] = add2(z[2], c5);
@@ -588,8 +588,9 @@ struct SoftBwdPair {
         F2* zk = z + k * One::kRowAcc;
         const F2 rs = rsqrt2(r2[k][u]);
         const F2 S = fma2(f2s(R.f[k].n.z), dz[k][u], f2s(w.r[k].s));
-        const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), mul2(rs, rs)), rs);
-        const F2 c5 = mul2(mul2(c3, mul2(S, rs)), rs);
+        const F2 rs2 = mul2(rs, rs);
+        const F2 c3 = mul2(mul2(f2(zc[u].z, zc[u].w), rs2), rs);
+        const F2 c5 = mul2(mul2(c3, S), rs2);
         zk[0] = add2(zk[0], c3);
         zk[1] = fma2(c3, dz[k][u], zk[1]);
         zk[2] = add2(zk[2], c5);

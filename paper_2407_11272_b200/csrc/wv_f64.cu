@@ -354,25 +354,21 @@ constexpr double kEightPi = 8.0 * kPi;
 struct ExactBwd64 {
   using Rec = ExactGradRecF64;
   // edge (Biot-Savart) form of d(Omega)/dv, see ExactEdgeBwd in wv_bwd_f32.cu;
-  // coef carries the -1/(4 pi) factor
-  __device__ __forceinline__ static void edge(const double* P, const double* Q, double qx,
-                                              double qy, double qz, double cw, double* gP,
-                                              double* gQ) {
+  // coef carries the -1/(4 pi) factor.  Per pair: the three corner lengths
+  // and their reciprocals once (3 sqrt + 3 div), one division per edge.
+  __device__ __forceinline__ static void edge(const double* a, const double* b, double la,
+                                              double lb, double ia, double ib, double cw,
+                                              double* gP, double* gQ) {
     if (cw == 0.0) return;
-    const double a[3] = {P[0] - qx, P[1] - qy, P[2] - qz};
-    const double b[3] = {Q[0] - qx, Q[1] - qy, Q[2] - qz};
-    const double la = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-    const double lb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     const double m[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
                          a[0] * b[1] - a[1] * b[0]};
     // |a||b| + a.b without cancellation next to the edge's segment (a.b < 0):
-    // |a x b|^2 / (|a||b| - a.b)
+    // |a x b|^2 / (|a||b| - a.b), so cw / (|a||b| + a.b) = cw (|a||b| - a.b) / |a x b|^2
     const double L = la * lb, ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
-    const double den =
-        ab < 0.0 ? (m[0] * m[0] + m[1] * m[1] + m[2] * m[2]) / (L - ab) : L + ab;
-    if (!(den > 0.0)) return;  // q on the segment: an on-surface point
-    const double t = cw / den;
-    const double sp = t / la, sq = t / lb;
+    const double t = ab < 0.0 ? cw * (L - ab) / (m[0] * m[0] + m[1] * m[1] + m[2] * m[2])
+                              : cw / (L + ab);
+    if (!(fabs(t) < INFINITY)) return;  // q on the segment: an on-surface point
+    const double sp = t * ia, sq = t * ib;
     for (int d = 0; d < 3; ++d) {
       gP[d] += m[d] * sp;
       gQ[d] += m[d] * sq;
@@ -380,9 +376,17 @@ struct ExactBwd64 {
   }
   __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
                                               double coef, double, double* g) {
-    edge(R.v + 0, R.v + 3, qx, qy, qz, coef * R.w[0], g + 0, g + 3);
-    edge(R.v + 3, R.v + 6, qx, qy, qz, coef * R.w[1], g + 3, g + 6);
-    edge(R.v + 6, R.v + 0, qx, qy, qz, coef * R.w[2], g + 6, g + 0);
+    const double a[3] = {R.v[0] - qx, R.v[1] - qy, R.v[2] - qz};
+    const double b[3] = {R.v[3] - qx, R.v[4] - qy, R.v[5] - qz};
+    const double c[3] = {R.v[6] - qx, R.v[7] - qy, R.v[8] - qz};
+    const double la = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    const double lb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    const double lc = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    if (!(la > 0.0 && lb > 0.0 && lc > 0.0)) return;  // q on a vertex (flagged)
+    const double ia = 1.0 / la, ib = 1.0 / lb, ic = 1.0 / lc;
+    edge(a, b, la, lb, ia, ib, coef * R.w[0], g + 0, g + 3);
+    edge(b, c, lb, lc, ib, ic, coef * R.w[1], g + 3, g + 6);
+    edge(c, a, lc, la, ic, ia, coef * R.w[2], g + 6, g + 0);
   }
 };
 struct SoftBwd64 {

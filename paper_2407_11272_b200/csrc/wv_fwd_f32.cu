@@ -446,9 +446,28 @@ struct ExactStripPol : ExactPol {
   // slot's d.  Face k of a strip reads A, B from slots (k, k+1) mod 3 (and
   // s_A = |a| + |b| from the previous face) and writes C's distance to slot
   // (k+2) mod 3, so with the face loop unrolled by 3 nothing is moved.
+#ifndef WV_STRIP_CARRY_S
+#define WV_STRIP_CARRY_S 1
+#endif
   struct Slot {
-    F2 d, s;
+    F2 d;
+#if WV_STRIP_CARRY_S
+    F2 s;
+#endif
   };
+  // |a| + |b| of a face: carried from the previous face (s) or recomputed
+  __device__ __forceinline__ static F2 sum_ab(const Slot& A, const Slot& B) {
+#if WV_STRIP_CARRY_S
+    return A.s;
+#else
+    return add2(A.d, B.d);
+#endif
+  }
+  __device__ __forceinline__ static void set_s(Slot& S, F2 v) {
+#if WV_STRIP_CARRY_S
+    S.s = v;
+#endif
+  }
   // alpha = N.(C - q) (any corner of the face gives alpha; C's z part is
   // needed for |c - q| anyway, so alpha costs one FFMA2 per point pair)
   // Per face only C's row part is computed; A's and B's are carried from the
@@ -490,7 +509,7 @@ struct ExactStripPol : ExactPol {
         const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
         sA[pp].d = sqrt2(fma2(az, az, f2s(w.a2)));
         sB[pp].d = sqrt2(fma2(bz, bz, f2s(w.b2)));
-        sA[pp].s = add2(sA[pp].d, sB[pp].d);
+        set_s(sA[pp], add2(sA[pp].d, sB[pp].d));
       }
     }
     constexpr float kL = -16.0f / 7.0f;
@@ -509,8 +528,8 @@ struct ExactStripPol : ExactPol {
       const F2 la = sA[pp].d, lb = sB[pp].d;
       const F2 sbc = add2(lb, lc), sca = add2(lc, la);
       sC[pp].d = lc;
-      sB[pp].s = sbc;
-      const F2 sab = sA[pp].s;  // |a| + |b|, the previous face's |b| + |c|
+      const F2 sab = sum_ab(sA[pp], sB[pp]);  // |a| + |b|, the previous face's |b| + |c|
+      set_s(sB[pp], sbc);
       const F2 x = mul2(mul2(sab, sbc), sca);
       const F2 lp = fma2(lc, f2s(kab), fma2(lb, f2s(kca), mul2(la, f2s(kbc))));  // 16/7 (-L)
       const F2 beta2 = fma2(lp, f2s(0.875f), x);  // X - 2L
@@ -548,7 +567,7 @@ struct ExactStripPol : ExactPol {
       const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
       sA[pp].d = sqrt2(fma2(az, az, f2s(w.a2)));
       sB[pp].d = sqrt2(fma2(bz, bz, f2s(w.b2)));
-      sA[pp].s = add2(sA[pp].d, sB[pp].d);
+      set_s(sA[pp], add2(sA[pp].d, sB[pp].d));
     }
   }
   // one face's alpha and 2 beta at point pair pp (strip_fast's operations)
@@ -560,9 +579,9 @@ struct ExactStripPol : ExactPol {
     const F2 lc = sqrt2(fma2(cz, cz, f2s(w.c2)));
     const F2 la = sA.d, lb = sB.d;
     const F2 sbc = add2(lb, lc), sca = add2(lc, la);
-    const F2 x = mul2(mul2(sA.s, sbc), sca);
+    const F2 x = mul2(mul2(sum_ab(sA, sB), sbc), sca);
     sC.d = lc;
-    sB.s = sbc;
+    set_s(sB, sbc);
     const F2 lp = fma2(lc, f2s(kab), fma2(lb, f2s(kca), mul2(la, f2s(kbc))));
     beta2 = fma2(lp, f2s(0.875f), x);
     float x0, x1, l0, l1;
