@@ -399,24 +399,33 @@ struct SoftBwd {
   // sums (c3, c3 d_z, c5, c5 d_z); flush_row forms the 10 face sums per run.
   // Per pair: 12 FP32 lane-ops + 1 MUFU (was 22 + 1).
   static constexpr int kRowAcc = 4;
+  // Row: d's x/y parts from c_hi + c_lo (dx, dy: the flush, and r2c, sc: the
+  // near steps) and from c_hi alone (r2, s: the far steps, which drop c_lo in
+  // the nonlinear factors c3, c5 -- < 2e-8 relative change beyond the
+  // face's near threshold K2 on |d|^6, SoftRecF32).  The run sums of c*dz
+  // always use dz from c_hi; flush_row adds c_lo.z * (sum c).
   struct Row {
-    float dx, dy, r2, s;
+    float dxh, dyh, r2, s;  // d's x/y from c_hi; r^2, S x/y parts from c_hi
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
     Row w;
-    w.dx = (R.c.x - qx) + R.c.w;  // + c_lo
-    w.dy = (R.c.y - qy) + R.n.w;
-    w.r2 = fmaf(w.dy, w.dy, w.dx * w.dx);
-    w.s = fmaf(R.n.y, w.dy, R.n.x * w.dx);
+    w.dxh = R.c.x - qx;
+    w.dyh = R.c.y - qy;
+    w.r2 = fmaf(w.dyh, w.dyh, w.dxh * w.dxh);
+    w.s = fmaf(R.n.y, w.dyh, R.n.x * w.dxh);
     return w;
   }
+  // one point pair with the corrected d (near steps)
   template <bool kUnit>
   __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
                                                    float eps2, F2* z) {
-    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.u.w));
-    const F2 r2 = fma2(dz, dz, f2s(w.r2));
+    const float dx = w.dxh + R.c.w, dy = w.dyh + R.n.w;  // + c_lo (c3, c5)
+    const float r2c = fmaf(dy, dy, dx * dx), sc = fmaf(R.n.y, dy, R.n.x * dx);
+    const F2 dz = sub2(f2s(R.c.z), qz);            // c_hi (run sums)
+    const F2 dzc = add2(dz, f2s(R.u.w));
+    const F2 r2 = fma2(dzc, dzc, f2s(r2c));
     const F2 rs = rsqrt2(r2);
-    const F2 S = fma2(f2s(R.n.z), dz, f2s(w.s));
+    const F2 S = fma2(f2s(R.n.z), dzc, f2s(sc));
     float r2l, r2h, cl, ch;
     split(r2, r2l, r2h);
     const F2 rs2 = mul2(rs, rs);
@@ -444,13 +453,14 @@ struct SoftBwd {
     float m = __int_as_float(0x7f800000);
 #pragma unroll
     for (int u = 0; u < N; ++u) {
-      dz[u] = add2(sub2(f2s(R.c.z), f2(zc[u].x, zc[u].y)), f2s(R.u.w));
+      dz[u] = sub2(f2s(R.c.z), f2(zc[u].x, zc[u].y));
       r2[u] = fma2(dz[u], dz[u], f2s(w.r2));
       float l, h;
       split(r2[u], l, h);
       m = fminf(m, fminf(l, h));
     }
-    if (m < eps2) {  // some point of the step sits on this face's centroid
+    // some point of the step near this face's centroid (or on it)
+    if (m < eps2 || m * m * m < R.w.w) {
 #pragma unroll
       for (int u = 0; u < N; ++u)
         pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);
@@ -478,8 +488,10 @@ struct SoftBwd {
       split(z[j], lo, hi);
       S[j] = (double)lo + (double)hi;
     }
-    const double C = S[0], A = S[1], D = S[2], E = S[3];
-    const double dx = w.dx, dy = w.dy;
+    // the run sums of c * dz used dz from c_hi: add c_lo.z * sum c
+    const double lz = (double)R.u.w;
+    const double C = S[0], A = S[1] + lz * S[0], D = S[2], E = S[3] + lz * S[2];
+    const double dx = (double)w.dxh + (double)R.c.w, dy = (double)w.dyh + (double)R.n.w;
     const int t = threadIdx.x;
     // G1 = w x d, G2 = d x u with d = (dx, dy, dz): sum c3 G = row part * C + dz part * A
     acc[0][t] += (double)R.w.y * A - (double)R.w.z * dy * C;
@@ -521,11 +533,17 @@ struct SoftBwdPair {
   using Rec = SoftPairRec;
   static constexpr int kFaces = 2;
   static constexpr int kOut = 18;
-  static constexpr int kRowStep = 4;
+#ifndef WV_SOFT_PAIR_STEP
+#define WV_SOFT_PAIR_STEP 4
+#endif
+#ifndef WV_SOFT_PAIR_MINB
+#define WV_SOFT_PAIR_MINB 4  // two faces' state: up to 128 registers
+#endif
+  static constexpr int kRowStep = WV_SOFT_PAIR_STEP;
   static constexpr bool kScaled = false;
   static constexpr bool kPairRuns = false;
   __device__ __forceinline__ static void scale(Rec&, float) {}
-  static constexpr int kMinBlocks = 4;  // two faces' state: up to 128 registers
+  static constexpr int kMinBlocks = WV_SOFT_PAIR_MINB;
   static constexpr double kCoefScale = One::kCoefScale;
   static constexpr int kAcc = 2 * One::kAcc;
   static constexpr int kRowAcc = 2 * One::kRowAcc;
@@ -568,14 +586,14 @@ struct SoftBwdPair {
     for (int k = 0; k < 2; ++k) {
 #pragma unroll
       for (int u = 0; u < N; ++u) {
-        dz[k][u] = add2(sub2(f2s(R.f[k].c.z), f2(zc[u].x, zc[u].y)), f2s(R.f[k].u.w));
+        dz[k][u] = sub2(f2s(R.f[k].c.z), f2(zc[u].x, zc[u].y));
         r2[k][u] = fma2(dz[k][u], dz[k][u], f2s(w.r[k].r2));
         float l, h;
         split(r2[k][u], l, h);
         m = fminf(m, fminf(l, h));
       }
     }
-    if (m < eps2) {
+    if (m < eps2 || m * m * m < fmaxf(R.f[0].w.w, R.f[1].w.w)) {
 #pragma unroll
       for (int u = 0; u < N; ++u)
         pair_row2<kUnit>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), eps2, z);

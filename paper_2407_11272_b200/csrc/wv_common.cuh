@@ -37,11 +37,14 @@ static_assert(sizeof(ExactRecF32) == 64, "record size");
 //   f32-rounded corners), then rounded.  The centroid is kept as hi + lo:
 //   d = c - q = (c_hi - q) + c_lo is then accurate to ~ulp(|d|) instead of
 //   ulp(|c|), which matters at nodes next to a centroid (the dipole term
-//   grows like 1/|d|^2).  lo.x, lo.y ride as a bf16 pair (they are <= ulp(c)/2,
-//   so 8 bits of them is ~1e-10 absolute).
+//   grows like 1/|d|^2).  The lo parts ride as bf16 (they are <= ulp(c)/2,
+//   so 8 bits of them is ~1e-10 absolute) with K2 = (8e6 |N| |c_lo|)^2, the
+//   "near" threshold on |d|^6: a pair with |d|^6 >= K2 changes by less than
+//   2e-8 (in W) when c_lo is dropped, so far pairs skip the lo arithmetic.
 struct __align__(16) SoftRecF32 {
   float4 c;   // c_hi.xyz, N.x
-  float4 n;   // N.y, N.z, c_lo.z, bits: bf16(c_lo.x) | bf16(c_lo.y) << 16
+  float4 n;   // N.y, N.z, bits: bf16(c_lo.x) | bf16(c_lo.y) << 16,
+              //           bits: bf16(c_lo.z) | bf16(K2) << 16
 };
 static_assert(sizeof(SoftRecF32) == 32, "record size");
 __host__ __device__ __forceinline__ uint32_t bf16_bits(float x) {  // round to nearest even
@@ -51,9 +54,15 @@ __host__ __device__ __forceinline__ uint32_t bf16_bits(float x) {  // round to n
   return b >> 16;
 }
 __device__ __forceinline__ float lo_x(const SoftRecF32& R) {
-  return __uint_as_float(__float_as_uint(R.n.w) << 16);
+  return __uint_as_float(__float_as_uint(R.n.z) << 16);
 }
 __device__ __forceinline__ float lo_y(const SoftRecF32& R) {
+  return __uint_as_float(__float_as_uint(R.n.z) & 0xffff0000u);
+}
+__device__ __forceinline__ float lo_z(const SoftRecF32& R) {
+  return __uint_as_float(__float_as_uint(R.n.w) << 16);
+}
+__device__ __forceinline__ float near_k2(const SoftRecF32& R) {
   return __uint_as_float(__float_as_uint(R.n.w) & 0xffff0000u);
 }
 
@@ -64,7 +73,7 @@ struct __align__(16) SoftGradRecF32 {
   float4 c;  // c_hi.xyz, c_lo.x
   float4 n;  // N.xyz, c_lo.y
   float4 u;  // u.xyz, c_lo.z
-  float4 w;  // w.xyz, 0
+  float4 w;  // w.xyz, K2 (SoftRecF32)
 };
 static_assert(sizeof(SoftGradRecF32) == 64, "record size");
 

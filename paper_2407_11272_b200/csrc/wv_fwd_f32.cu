@@ -672,25 +672,35 @@ struct SoftPol {
     // d = (c_hi - q) + c_lo (SoftRecF32)
     const F2 dx = add2(sub2(f2s(R.c.x), qx), f2s(lo_x(R)));
     const F2 dy = add2(sub2(f2s(R.c.y), qy), f2s(lo_y(R)));
-    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.n.z));
+    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(lo_z(R)));
     const F2 r2 = dot2(dx, dy, dz, dx, dy, dz);
     const F2 s = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
     return tail2(r2, s, ctx, tacc);
   }
+  // Lattice rows: the x/y parts per face and row, from c_hi (r2, s) and from
+  // c_hi + c_lo (r2c, sc).  A step whose points are all beyond the face's
+  // near threshold (|d|^6 >= K2, SoftRecF32) takes the hi-only arithmetic
+  // (the centroid's lo part changes such a term by < 2e-8); the rare steps
+  // with a point nearer use the corrected d.
   struct Row {
-    float r2, s;
+    float dxh, dyh, r2, s, k2;
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
-    const float dx = (R.c.x - qx) + lo_x(R), dy = (R.c.y - qy) + lo_y(R);
     Row w;
-    w.r2 = fmaf(dy, dy, dx * dx);
-    w.s = fmaf(R.n.x, dy, R.c.w * dx);
+    w.dxh = R.c.x - qx;
+    w.dyh = R.c.y - qy;
+    w.r2 = fmaf(w.dyh, w.dyh, w.dxh * w.dxh);
+    w.s = fmaf(R.n.x, w.dyh, R.c.w * w.dxh);
+    w.k2 = near_k2(R);
     return w;
   }
+  // the corrected d (rare steps near a centroid)
   __device__ __forceinline__ static uint32_t common_row2(const Rec& R, const Row& w, F2 qz,
                                                          const Ctx& ctx, F2& tacc) {
-    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(R.n.z));
-    return tail2(fma2(dz, dz, f2s(w.r2)), fma2(f2s(R.n.y), dz, f2s(w.s)), ctx, tacc);
+    const float dx = w.dxh + lo_x(R), dy = w.dyh + lo_y(R);
+    const float r2c = fmaf(dy, dy, dx * dx), sc = fmaf(R.n.x, dy, R.c.w * dx);
+    const F2 dz = add2(sub2(f2s(R.c.z), qz), f2s(lo_z(R)));
+    return tail2(fma2(dz, dz, f2s(r2c)), fma2(f2s(R.n.y), dz, f2s(sc)), ctx, tacc);
   }
   __device__ __forceinline__ static uint32_t tail2(F2 r2, F2 s, const Ctx& ctx, F2& tacc) {
     float r2l, r2h;
@@ -736,13 +746,29 @@ struct SoftPol {
   __device__ __forceinline__ static uint32_t face_row(const Rec& R, const Row& w, const F2* qz,
                                                       const Ctx& ctx, F2* tacc) {
     F2 r2[PP], s[PP];
+    float m = __int_as_float(0x7f800000);
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) {
-      const F2 dz = add2(sub2(f2s(R.c.z), qz[pp]), f2s(R.n.z));
+      const F2 dz = sub2(f2s(R.c.z), qz[pp]);
       r2[pp] = fma2(dz, dz, f2s(w.r2));
       s[pp] = fma2(f2s(R.n.y), dz, f2s(w.s));
+      float l, h;
+      split(r2[pp], l, h);
+      m = fminf(m, fminf(l, h));
     }
-    return finish<PP>(r2, s, ctx, tacc);
+    if (m * m * m >= w.k2 && m >= ctx.eps2) {  // every point far from the centroid
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) {
+        const F2 rs = rsqrt2(r2[pp]);
+        tacc[pp] = fma2(s[pp], mul2(rs, mul2(rs, rs)), tacc[pp]);
+      }
+      return 0u;
+    }
+    // rare: d with the centroid's lo part, per-lane on-centroid test
+    uint32_t rare = 0;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) rare |= common_row2(R, w, qz[pp], ctx, tacc[pp]) << (2 * pp);
+    return rare;
   }
   template <int PP>
   __device__ __forceinline__ static uint32_t face(const Rec& R, const F2* qx, const F2* qy,
@@ -752,7 +778,7 @@ struct SoftPol {
     for (int pp = 0; pp < PP; ++pp) {
       const F2 dx = add2(sub2(f2s(R.c.x), qx[pp]), f2s(lo_x(R)));
       const F2 dy = add2(sub2(f2s(R.c.y), qy[pp]), f2s(lo_y(R)));
-      const F2 dz = add2(sub2(f2s(R.c.z), qz[pp]), f2s(R.n.z));
+      const F2 dz = add2(sub2(f2s(R.c.z), qz[pp]), f2s(lo_z(R)));
       r2[pp] = dot2(dx, dy, dz, dx, dy, dz);
       s[pp] = fma2(f2s(R.n.y), dz, fma2(f2s(R.n.x), dy, mul2(f2s(R.c.w), dx)));
     }

@@ -149,19 +149,26 @@ __global__ void pack_kernel(int kind, const V* __restrict__ verts,
       const double cz = v0[2] + (uz + wz) / 3.0;
       // centroid hi + lo (SoftRecF32)
       const float hx = (float)cx, hy = (float)cy, hz = (float)cz;
-      const float lx = (float)(cx - (double)hx), ly = (float)(cy - (double)hy),
-                  lz = (float)(cz - (double)hz);
+      const double dlx = cx - (double)hx, dly = cy - (double)hy, dlz = cz - (double)hz;
+      const float lx = (float)dlx, ly = (float)dly, lz = (float)dlz;
+      // near threshold on |d|^6 (SoftRecF32): (8e6 |N| |c_lo|)^2, rounded up
+      const double kk = 8e6 * sqrt(nx * nx + ny * ny + nz * nz) *
+                        sqrt(dlx * dlx + dly * dly + dlz * dlz);
+      const float k2 = (float)(kk * kk * 1.01);
       if (kind == 2) {
         SoftRecF32* r = static_cast<SoftRecF32*>(recs) + f;
         r->c = make_float4(hx, hy, hz, (float)nx);
-        r->n = make_float4((float)ny, (float)nz, lz,
-                           __uint_as_float(bf16_bits(lx) | (bf16_bits(ly) << 16)));
+        // bf16 of K2 rounded UP (a larger threshold is only more careful)
+        const uint32_t kb = (__float_as_uint(k2) + 0xffffu) >> 16;
+        r->n = make_float4((float)ny, (float)nz,
+                           __uint_as_float(bf16_bits(lx) | (bf16_bits(ly) << 16)),
+                           __uint_as_float(bf16_bits(lz) | (kb << 16)));
       } else if (kind == 5) {
         SoftGradRecF32* r = static_cast<SoftGradRecF32*>(recs) + f;
         r->c = make_float4(hx, hy, hz, lx);
         r->n = make_float4((float)nx, (float)ny, (float)nz, ly);
         r->u = make_float4((float)ux, (float)uy, (float)uz, lz);
-        r->w = make_float4((float)wx, (float)wy, (float)wz, 0.0f);
+        r->w = make_float4((float)wx, (float)wy, (float)wz, k2);
       } else if (kind == 6) {
         SoftGradRecF64* r = static_cast<SoftGradRecF64*>(recs) + f;
         r->c[0] = cx; r->c[1] = cy; r->c[2] = cz;

@@ -194,12 +194,13 @@ def test_autograd_matches_device_kernels(torch_):
 def test_row_kernels_match_generic_bitwise(torch_, c2, mode):
     """Row-aligned grid ranges run the lattice-row kernels (x/y parts hoisted
     per face); they must reproduce the generic point kernels on the same f32
-    coordinates, flags included: bit for bit in soft mode; in exact mode to
-    fp32 rounding (both pair faces for one angle evaluation, but the row
-    kernel's vertex-hit screen is the per-face row bound and the generic
-    one's the per-lane distances, so a pair can go face by face in one and
-    not the other).  rz=40 (row mode), rz=36 (generic grid), and an
-    unaligned slab start."""
+    coordinates, flags included; values to fp32 rounding.  Exact: both pair
+    faces for one angle evaluation, but the row kernel's vertex-hit screen is
+    the per-face row bound and the generic one's the per-lane distances, so a
+    pair can go face by face in one and not the other.  Soft: the row kernel
+    drops the centroid's lo part for pairs beyond the face's near threshold
+    (< 2e-8 per term), the generic kernel always adds it.  rz=40 (row mode),
+    rz=36 (generic grid), and an unaligned slab start."""
     from paper_2407_11272_b200 import device as D
     dm = D.DeviceMesh.from_numpy(c2.vertices, c2.faces)
     for res, n0, count in [((24, 20, 40), 0, None), ((24, 20, 40), 40 * 20 * 5, 40 * 20 * 7),
@@ -211,10 +212,8 @@ def test_row_kernels_match_generic_bitwise(torch_, c2, mode):
         pts = orc.node_coordinates(*grid)[n0:n0 + count].astype(np.float32)
         wp, fp = D.forward(dm, mode, "f32", points=torch_.from_numpy(pts).cuda())
         assert np.array_equal(fg.cpu().numpy(), fp.cpu().numpy())
-        if mode == "soft":
-            assert wg.cpu().numpy().tobytes() == wp.cpu().numpy().tobytes()
-        else:
-            assert (wg - wp).abs().max().item() <= 2e-7
+        scale = max(1.0, wp.abs().max().item())
+        assert (wg - wp).abs().max().item() <= (2e-7 if mode == "exact" else 1e-6) * scale
 
 
 @pytest.mark.parametrize("mode", ["exact", "soft"])
