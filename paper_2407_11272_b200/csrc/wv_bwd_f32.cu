@@ -406,6 +406,7 @@ struct SoftBwd {
   // always use dz from c_hi; flush_row adds c_lo.z * (sum c).
   struct Row {
     float dxh, dyh, r2, s;  // d's x/y from c_hi; r^2, S x/y parts from c_hi
+    float dx, dy;           // d's x/y with c_lo (the flush's moments)
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
     Row w;
@@ -413,13 +414,15 @@ struct SoftBwd {
     w.dyh = R.c.y - qy;
     w.r2 = fmaf(w.dyh, w.dyh, w.dxh * w.dxh);
     w.s = fmaf(R.n.y, w.dyh, R.n.x * w.dxh);
+    w.dx = w.dxh + R.c.w;
+    w.dy = w.dyh + R.n.w;
     return w;
   }
   // one point pair with the corrected d (near steps)
   template <bool kUnit>
   __device__ __forceinline__ static void pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
                                                    float eps2, F2* z) {
-    const float dx = w.dxh + R.c.w, dy = w.dyh + R.n.w;  // + c_lo (c3, c5)
+    const float dx = w.dx, dy = w.dy;  // + c_lo (c3, c5)
     const float r2c = fmaf(dy, dy, dx * dx), sc = fmaf(R.n.y, dy, R.n.x * dx);
     const F2 dz = sub2(f2s(R.c.z), qz);            // c_hi (run sums)
     const F2 dzc = add2(dz, f2s(R.u.w));
@@ -481,17 +484,18 @@ struct SoftBwd {
   }
   __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
                                                    double (*acc)[kBwdThreads]) {
+    // the run sums of c * dz used dz from c_hi: add c_lo.z * sum c
+    const F2 zz[kRowAcc] = {z[0], fma2(z[0], f2s(R.u.w), z[1]), z[2],
+                            fma2(z[2], f2s(R.u.w), z[3])};
     double S[kRowAcc];
 #pragma unroll
     for (int j = 0; j < kRowAcc; ++j) {
       float lo, hi;
-      split(z[j], lo, hi);
+      split(zz[j], lo, hi);
       S[j] = (double)lo + (double)hi;
     }
-    // the run sums of c * dz used dz from c_hi: add c_lo.z * sum c
-    const double lz = (double)R.u.w;
-    const double C = S[0], A = S[1] + lz * S[0], D = S[2], E = S[3] + lz * S[2];
-    const double dx = (double)w.dxh + (double)R.c.w, dy = (double)w.dyh + (double)R.n.w;
+    const double C = S[0], A = S[1], D = S[2], E = S[3];
+    const double dx = w.dx, dy = w.dy;
     const int t = threadIdx.x;
     // G1 = w x d, G2 = d x u with d = (dx, dy, dz): sum c3 G = row part * C + dz part * A
     acc[0][t] += (double)R.w.y * A - (double)R.w.z * dy * C;
