@@ -89,14 +89,20 @@ struct ExactEdgeBwd {
   static constexpr int kOut = 9;
   static constexpr bool kScaled = true;
   static constexpr bool kPairRuns = false;
-  static constexpr int kRowStep = wv::kRowStep;
+  #ifndef WV_EDGE_STEP
+#define WV_EDGE_STEP 4
+#endif
+#ifndef WV_EDGE_MINB
+#define WV_EDGE_MINB 5
+#endif
+  static constexpr int kRowStep = WV_EDGE_STEP;
   __device__ __forceinline__ static void scale(Rec& R, float s) {
     R.a.x *= s; R.a.y *= s; R.a.z *= s;
     R.b.x *= s; R.b.y *= s; R.b.z *= s;
     R.c.x *= s; R.c.y *= s; R.c.z *= s;
     R.u.x *= s * s; R.u.y *= s * s; R.u.z *= s * s;
   }
-  static constexpr int kMinBlocks = kBwdMinBlocks;
+  static constexpr int kMinBlocks = WV_EDGE_MINB;
   // -1/(4 pi) and the factor 2 of d = 2 (|a||b| + a.b) below
   static constexpr double kCoefScale = -2.0 / (4.0 * kPi);
   static constexpr int kAcc = 9;
@@ -1181,7 +1187,12 @@ size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_
       .workspace(n_faces / 2, 1, ExactEdgeBwdPair::kOut);
 }
 size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
-  return BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);
+  // the larger of the two single-face plans (exact and soft occupancies differ)
+  const size_t a =
+      BwdPlan::make(n_faces, n_count, num_sms, kBwdMinBlocks, batch).workspace(n_faces, batch);
+  const size_t b = BwdPlan::make(n_faces, n_count, num_sms, ExactEdgeBwd::kMinBlocks, batch)
+                       .workspace(n_faces, batch);
+  return a > b ? a : b;
 }
 
 // ---------------------------------------------------------------------------

@@ -22,6 +22,34 @@ constexpr int kF64Threads = kF64NC;
 constexpr int kF64P = 1;
 constexpr double kBaryTol = 1e-12;  // _kernels.py:31
 
+// FP64 reciprocal / reciprocal square root without the IEEE slow-path
+// branches of '/' and sqrt: the MUFU seed (rcp.approx.ftz.f64 /
+// rsqrt.approx.ftz.f64, ~2^-22 relative) and two Newton steps (error ~2^-88
+// before rounding: full f64 accuracy, within an ulp or two -- the parity
+// tolerance is 1e-9).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  // y <- y (3 - x y^2) / 2, twice
+  double h = x * y;
+  y = fma(y, fma(-h, y, 1.0) * 0.5, y);
+  h = x * y;
+  return fma(y, fma(-h, y, 1.0) * 0.5, y);
+}
+
+// |v| = v2 rsqrt(v2), 0 at the origin (the vertex-hit test needs the 0)
+__device__ __forceinline__ double norm_nr(double v2) {
+  return v2 > 0.0 ? v2 * rsqrt_nr(v2) : 0.0;
+}
+
 struct ExactF64Pol {
   using Rec = ExactRecF64;
   static constexpr double kDiv = 4.0 * kPi;  // out = acc / _FOUR_PI
@@ -33,9 +61,9 @@ struct ExactF64Pol {
     const double ax = t[0] - qx, ay = t[1] - qy, az = t[2] - qz;
     const double bx = t[3] - qx, by = t[4] - qy, bz = t[5] - qz;
     const double cx = t[6] - qx, cy = t[7] - qy, cz = t[8] - qz;
-    const double na = sqrt(ax * ax + ay * ay + az * az);
-    const double nb = sqrt(bx * bx + by * by + bz * bz);
-    const double nc = sqrt(cx * cx + cy * cy + cz * cz);
+    const double na = norm_nr(ax * ax + ay * ay + az * az);
+    const double nb = norm_nr(bx * bx + by * by + bz * bz);
+    const double nc = norm_nr(cx * cx + cy * cy + cz * cz);
     if (na < eps || nb < eps || nc < eps) {
       hit = true;
       return;
@@ -69,7 +97,7 @@ struct ExactF64Pol {
       // libm's atan2 and exactly odd, so flipped faces still negate exactly.
       // Other pairs take atan2.
       if (fabs(alpha) * 8.0 < beta) {
-        const double t = alpha / beta;
+        const double t = alpha * rcp_nr(beta);  // (odd in alpha: flips negate exactly)
         const double s = t * t;
         double p = 1.0 / 17.0;
         p = fma(p, s, -1.0 / 15.0);
@@ -192,7 +220,7 @@ static int launch_f64(const void* packed, int64_t n_faces, const PointSource& ps
 // (~1e-16 relative).
 __device__ __forceinline__ double vdist(const double* v, double qx, double qy, double qz) {
   const double x = v[0] - qx, y = v[1] - qy, z = v[2] - qz;
-  return sqrt(x * x + y * y + z * z);
+  return norm_nr(x * x + y * y + z * z);
 }
 template <int kRot>
 __device__ __forceinline__ void exact_f64_strip_face(const ExactRecF64& R, double qx, double qy,
@@ -242,7 +270,7 @@ __device__ __forceinline__ void exact_f64_strip_face(const ExactRecF64& R, doubl
                       ((ax * bx + ay * by + az * bz) * nc + (cx * ax + cy * ay + cz * az) * nb);
   if (use_atan2) {
     if (fabs(alpha) * 8.0 < beta) {  // as ExactF64Pol
-      const double tt = alpha / beta;
+      const double tt = alpha * rcp_nr(beta);
       const double ss = tt * tt;
       double p = 1.0 / 17.0;
       p = fma(p, ss, -1.0 / 15.0);
@@ -354,20 +382,21 @@ constexpr double kEightPi = 8.0 * kPi;
 struct ExactBwd64 {
   using Rec = ExactGradRecF64;
   // edge (Biot-Savart) form of d(Omega)/dv, see ExactEdgeBwd in wv_bwd_f32.cu;
-  // coef carries the -1/(4 pi) factor.  Per pair: the three corner lengths
-  // and their reciprocals once (3 sqrt + 3 div), one division per edge.
+  // coef carries the -1/(4 pi) factor.  Per pair: the three reciprocal corner
+  // lengths once (Newton rsqrt), one Newton reciprocal per edge, no branches.
   __device__ __forceinline__ static void edge(const double* a, const double* b, double la,
                                               double lb, double ia, double ib, double cw,
                                               double* gP, double* gQ) {
-    if (cw == 0.0) return;
     const double m[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
                          a[0] * b[1] - a[1] * b[0]};
     // |a||b| + a.b without cancellation next to the edge's segment (a.b < 0):
     // |a x b|^2 / (|a||b| - a.b), so cw / (|a||b| + a.b) = cw (|a||b| - a.b) / |a x b|^2
     const double L = la * lb, ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
-    const double t = ab < 0.0 ? cw * (L - ab) / (m[0] * m[0] + m[1] * m[1] + m[2] * m[2])
-                              : cw / (L + ab);
-    if (!(fabs(t) < INFINITY)) return;  // q on the segment: an on-surface point
+    const bool neg = ab < 0.0;
+    const double num = neg ? cw * (L - ab) : cw;
+    const double den = neg ? m[0] * m[0] + m[1] * m[1] + m[2] * m[2] : L + ab;
+    const double t = num * rcp_nr(den);
+    if (cw == 0.0 || !(fabs(t) < INFINITY)) return;  // q on the segment: on-surface
     const double sp = t * ia, sq = t * ib;
     for (int d = 0; d < 3; ++d) {
       gP[d] += m[d] * sp;
@@ -379,11 +408,12 @@ struct ExactBwd64 {
     const double a[3] = {R.v[0] - qx, R.v[1] - qy, R.v[2] - qz};
     const double b[3] = {R.v[3] - qx, R.v[4] - qy, R.v[5] - qz};
     const double c[3] = {R.v[6] - qx, R.v[7] - qy, R.v[8] - qz};
-    const double la = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-    const double lb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
-    const double lc = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
-    if (!(la > 0.0 && lb > 0.0 && lc > 0.0)) return;  // q on a vertex (flagged)
-    const double ia = 1.0 / la, ib = 1.0 / lb, ic = 1.0 / lc;
+    const double a2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+    const double b2 = b[0] * b[0] + b[1] * b[1] + b[2] * b[2];
+    const double c2 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+    if (!(a2 > 0.0 && b2 > 0.0 && c2 > 0.0)) return;  // q on a vertex (flagged)
+    const double ia = rsqrt_nr(a2), ib = rsqrt_nr(b2), ic = rsqrt_nr(c2);
+    const double la = a2 * ia, lb = b2 * ib, lc = c2 * ic;
     edge(a, b, la, lb, ia, ib, coef * R.w[0], g + 0, g + 3);
     edge(b, c, lb, lc, ib, ic, coef * R.w[1], g + 3, g + 6);
     edge(c, a, lc, la, ic, ia, coef * R.w[2], g + 6, g + 0);

@@ -50,11 +50,16 @@ def main():
     ap.add_argument("--kernel", default=None)
     ap.add_argument("--workload", default=None)
     ap.add_argument("--source", default="")
+    ap.add_argument("--nth", type=int, default=0, help="which kernel of the report (0 = first)")
     a = ap.parse_args()
     txt = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source",
                           "sass"], check=True, capture_output=True, text=True).stdout
     lines = txt.splitlines()
     rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
+    # the report holds one table per profiled kernel, each starting with a
+    # header row: keep the nth
+    starts = [i for i, r in enumerate(rows) if "Source" in r and "Instructions Executed" in r]
+    rows = rows[starts[a.nth]:]
     head = rows[0]
     isrc, iex, ism = head.index("Source"), head.index("Instructions Executed"), head.index(
         "Warp Stall Sampling (All Samples)")
