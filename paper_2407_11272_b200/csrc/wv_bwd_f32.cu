@@ -84,6 +84,7 @@ __device__ __noinline__ void exact_pair_f64(const ExactGradRecF32& R, double qx,
 }
 
 struct ExactEdgeBwd {
+  static constexpr bool kPrefetch = false;  // next chunk's coefficients in registers
   using Rec = ExactGradRecF32;
   static constexpr int kFaces = 1;  // faces per thread (per record)
   static constexpr int kOut = 9;
@@ -352,6 +353,7 @@ struct ExactEdgeBwd {
 };
 
 struct SoftBwd {
+  static constexpr bool kPrefetch = false;  // next chunk's coefficients in registers
   using Rec = SoftGradRecF32;
   static constexpr int kFaces = 1;
   static constexpr int kOut = 9;
@@ -539,6 +541,7 @@ struct SoftPairRec {
   SoftGradRecF32 f[2];
 };
 struct SoftBwdPair {
+  static constexpr bool kPrefetch = false;  // next chunk's coefficients in registers
   using One = SoftBwd;
   using Rec = SoftPairRec;
   static constexpr int kFaces = 2;
@@ -652,6 +655,7 @@ struct ExactPairRec {
   ExactGradRecF32 f[2];
 };
 struct ExactEdgeBwdPair {
+  static constexpr bool kPrefetch = true;  // next chunk's coefficients in registers
   using One = ExactEdgeBwd;
   using Rec = ExactPairRec;
   static constexpr int kFaces = 2;
@@ -962,15 +966,30 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     }
   }
 
+  // the coefficients of the NEXT chunk are loaded into registers while the
+  // current chunk is evaluated (their global-load latency had stalled the
+  // chunk fill; kPre per thread cover a chunk)
+  constexpr int kPre = kBwdChunk / kBwdThreads;
+  static_assert(kPre * kBwdThreads == kBwdChunk, "whole chunk per prefetch");
+  // (the strip-pair kernel only: the others' register budgets spill with it)
+  float cpre[kPre];
+  if constexpr (Pol::kPrefetch) {
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int64_t gi = p_begin + threadIdx.x + k * kBwdThreads;
+      cpre[k] = gi < p_end ? coefs[gi] : 0.0f;
+    }
+  }
   for (int64_t c0 = p_begin; c0 < p_end; c0 += kBwdChunk) {
     const int n = (int)((p_end - c0) < kBwdChunk ? (p_end - c0) : kBwdChunk);
     const int n_pairs = (n + 1) / 2;
     __syncthreads();
     int zero = 0;  // some coefficient of this chunk is zero (or padding)
-    for (int i = threadIdx.x; i < 2 * n_pairs; i += kBwdThreads) {
+    // one point of the chunk: coordinates (or parked), coefficient
+    auto fill = [&](int i, float cv) {
       float x = 1.0e6f, y = 1.0e6f, z = 1.0e6f, c = 0.0f;
       if (i < n) {
-        c = coefs[c0 + i] * coef_scale;
+        c = cv * coef_scale;
         // zero-coefficient points contribute nothing; park them far away so
         // the other half of their pair never sees an on-segment 0 * inf
         // (row mode keeps the row's x/y and parks z only)
@@ -1002,6 +1021,19 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       zc[i & 1] = z;
       zc[2 + (i & 1)] = c;
       zero |= c == 0.0f;
+    };
+    if constexpr (Pol::kPrefetch) {
+#pragma unroll
+      for (int k = 0; k < kPre; ++k) {
+        const float cv = cpre[k];
+        const int64_t gi = c0 + kBwdChunk + threadIdx.x + k * kBwdThreads;
+        cpre[k] = gi < p_end ? coefs[gi] : 0.0f;
+        const int i = threadIdx.x + k * kBwdThreads;
+        if (i < 2 * n_pairs) fill(i, cv);
+      }
+    } else {
+      for (int i = threadIdx.x; i < 2 * n_pairs; i += kBwdThreads)
+        fill(i, i < n ? coefs[c0 + i] : 0.0f);
     }
     // a chunk without zero coefficients (the common case of a loss over a
     // grid) skips the per-step zero tests
