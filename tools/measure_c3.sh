@@ -9,5 +9,5 @@ python bench.py --steps 5 --warmup 3 > $O/bench_c3_$T.json 2> $O/bench_c3_$T.err
 python bench.py --impl reference --steps 5 --warmup 3 > $O/ref_c3_$T.json 2>&1; tail -c 200 $O/ref_c3_$T.json
 C="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $C > $O/plain_$T.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3_$T.csv $C > $O/ncu_launch_$T.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:fwd_f32_kernel -s 1 -c 1 -o $O/ncu_c3_fwd_$T $C > $O/ncu_fwd_$T.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:bwd_f32_kernel -s 0 -c 1 -o $O/ncu_c3_bwd_$T $C > $O/ncu_bwd_$T.log 2>&1
 ls $O | tail -20
