@@ -151,6 +151,9 @@ def parse(argv=None):
                     help="lattice nodes in the CPU-baseline sample (SURVEY 8d: 65,536)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay the step as a CUDA graph (auto: one rank and < 2^20 nodes, "
+                         "where launch overhead matters)")
     return ap.parse_args(argv)
 
 
@@ -355,7 +358,8 @@ def exact_config(w, precision: str, world: int, active: int | None = None):
          "precision": precision,
          "step": "pack + exact fwd + loss + exact bwd + vertex gather"
                  + (" + all-reduce" if world > 1 else ""),
-         "l2": "256 MiB buffer zeroed between timed steps (> 126 MB L2)",
+         "l2": "256 MiB buffer zeroed between timed steps (> 126 MB L2; outside the "
+               "per-step CUDA events)",
          "parallelism": f"i-slabs x{world}"}
     if active is not None:
         c["active_bwd_faces"] = active
@@ -518,23 +522,48 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     launches = count_launches(step)
+    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and w.n_nodes < 1 << 20)
+    graph = None
+    if use_graph:
+        # the whole step (pack, forward, loss, backward, gather) as one CUDA
+        # graph: every kernel still runs on every replay, only the host-side
+        # launch overhead goes (C1 is launch-bound); phase times below come
+        # from un-graphed steps
+        for _ in range(args.steps):
+            step(record=True)
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            g_out = step()
+        torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    e_start = torch.cuda.Event(enable_timing=True)
-    e_stop = torch.cuda.Event(enable_timing=True)
+    # per-step CUDA events around each step (the L2 flush between steps is
+    # outside them)
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
-        e_start.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             flush.zero_()
-            grads, loss = step(record=True)
-        e_stop.record(stream)
+            ev_s[i].record(stream)
+            if graph is not None:
+                graph.replay()
+                grads, loss = g_out
+            else:
+                grads, loss = step(record=True)
+            ev_e[i].record(stream)
         barrier()
-    ms = e_start.elapsed_time(e_stop)
+    ms = sum(a.elapsed_time(b) for a, b in zip(ev_s, ev_e))
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["f0"], ev["f1"]))
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["b0"], ev["b1"]))
     t = torch.tensor([ms, fwd_ms, bwd_ms], device=dev, dtype=torch.float64)
@@ -606,6 +635,7 @@ def run_ours(args):
             "bwd_pairs_per_s": w.pairs / (bwd_ms / 1e3),
             "voxelize_ms": fwd_ms,
             "loss": float(loss),
+            "cuda_graph": use_graph,
             "paths": {"forward": kf, "backward": kb,
                       "shared_corner_fraction": dmesh.shared_corner_fraction(),
                       "strip_restart_fraction": dmesh.strip_restart_fraction()},
