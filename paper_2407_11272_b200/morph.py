@@ -88,11 +88,60 @@ def uniform_laplacian(faces: np.ndarray, n_verts: int):
             lap.data.astype(np.float64))
 
 
+def _padded(ip: np.ndarray, ix: np.ndarray, dv: np.ndarray, n: int):
+    """CSR rows as padded (n, width) column / value arrays; padding points at
+    the extra zero row n, so a row product is a fixed-order gather + sum."""
+    cnt = np.diff(ip)
+    width = max(1, int(cnt.max()) if n else 1)
+    cols = np.full((n, width), n, dtype=np.int64)
+    vals = np.zeros((n, width), dtype=np.float64)
+    r = np.repeat(np.arange(n), cnt)
+    k = np.arange(len(ix)) - np.repeat(ip[:-1], cnt)
+    cols[r, k] = ix
+    vals[r, k] = dv
+    return cols, vals
+
+
+class _Laplacian:
+    """y = L x and y = L^T x for the uniform Laplacian as padded gathers
+    (each row's CSR entries in column order, then a sum over the row): the
+    same terms as the sparse CSR product, in a fixed order, and capturable
+    in a CUDA graph (the sparse-library path is not)."""
+
+    def __init__(self, faces, n_verts: int, dev, dt):
+        import scipy.sparse as sp
+        ip, ix, dv = uniform_laplacian(faces, n_verts)
+        lt = sp.csr_matrix((dv, ix, ip), shape=(n_verts, n_verts)).T.tocsr()
+        lt.sort_indices()
+        self.n = n_verts
+        c, v = _padded(ip, ix, dv, n_verts)
+        self.cols, self.vals = torch.from_numpy(c).to(dev), torch.from_numpy(v).to(dev, dt)
+        c, v = _padded(lt.indptr.astype(np.int64), lt.indices.astype(np.int64),
+                       lt.data.astype(np.float64), n_verts)
+        self.tcols, self.tvals = torch.from_numpy(c).to(dev), torch.from_numpy(v).to(dev, dt)
+
+    def _apply(self, cols, vals, x):
+        xe = torch.cat([x, torch.zeros_like(x[:1])])
+        return (vals.unsqueeze(-1) * xe[cols]).sum(dim=1)
+
+    def mv(self, x):
+        return self._apply(self.cols, self.vals, x)
+
+    def tmv(self, x):
+        return self._apply(self.tcols, self.tvals, x)
+
+
 class _DeviceProblem:
-    """Everything the loop touches, resident on the GPU."""
+    """Everything the loop touches, resident on the GPU.  With ``graphs`` the
+    two evaluations (a trial's loss; the accepted step's loss + gradient) are
+    captured once as CUDA graphs over a static vertex buffer and replayed:
+    every kernel still runs per evaluation (pack, forward, loss terms,
+    backward, gather, smoothing), only the per-launch host overhead goes --
+    at the reference's own morph sizes (hundreds of faces, 32^3) that
+    overhead, not the kernels, is the evaluation's cost."""
 
     def __init__(self, template: TriangleMesh, target: ScalarField, cfg: MorphConfig,
-                 precision: str):
+                 precision: str, graphs: bool = True):
         self.prec = precision
         self.dt = torch.float64 if precision == "f64" else torch.float32
         self.cfg = cfg
@@ -103,12 +152,9 @@ class _DeviceProblem:
         self.grid = (spec.bounds_min, spec.bounds_max, spec.resolution)
         self.targets = torch.as_tensor(np.asarray(target.values, dtype=np.float64),
                                        dtype=self.dt).to(dev)
-        ip, ix, dv = uniform_laplacian(template.faces, template.num_vertices)
-        V = template.num_vertices
-        self.L = torch.sparse_csr_tensor(torch.from_numpy(ip), torch.from_numpy(ix),
-                                         torch.from_numpy(dv), size=(V, V),
-                                         check_invariants=True).to(dev, self.dt)
-        self.LT = self.L.to_sparse_coo().t().coalesce().to_sparse_csr()
+        self.lap = _Laplacian(template.faces, template.num_vertices, dev, self.dt)
+        self.graphs = graphs
+        self._g = None
 
     def _occupancy(self, verts: torch.Tensor):
         self.mesh.set_vertices(verts)
@@ -117,32 +163,69 @@ class _DeviceProblem:
         return coefs, sums
 
     def _smooth(self, verts):
-        lv = self.L @ verts
+        lv = self.lap.mv(verts)
         return (lv * lv).sum(), lv
 
-    def loss_only(self, verts: torch.Tensor) -> float:
+    def _loss_body(self, verts):
         _, sums = self._occupancy(verts)
         e, _ = self._smooth(verts)
-        s = torch.stack([sums[1], sums[4], e.to(torch.float64)]).cpu().numpy()
-        if s[0] == 0.0:
-            return float("inf")
-        return float(s[1] + self.cfg.smooth_weight * s[2])
+        return torch.stack([sums[1], sums[4], e.to(torch.float64)])
 
-    def full_eval(self, verts: torch.Tensor):
+    def _full_body(self, verts):
         coefs, sums = self._occupancy(verts)
         fg = face_grad(self.mesh, "soft", self.prec, coefs, grid=self.grid)
         g = vertex_grad(self.mesh, fg, scale=sums[3:4], dtype=self.dt)
         e, lv = self._smooth(verts)
-        g = g + self.cfg.smooth_weight * 2.0 * (self.LT @ lv)
-        s = torch.stack([sums[1], sums[4], e.to(torch.float64)]).cpu().numpy()
-        loss = float("inf") if s[0] == 0.0 else float(s[1] + self.cfg.smooth_weight * s[2])
-        return loss, g
+        g = g + self.cfg.smooth_weight * 2.0 * self.lap.tmv(lv)
+        return torch.stack([sums[1], sums[4], e.to(torch.float64)]), g
+
+    def _capture(self):
+        v0 = self.mesh.vertices
+        self.v_in = v0.clone()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up on a side stream before capture
+            self._loss_body(self.v_in)
+            self._full_body(self.v_in)
+        torch.cuda.current_stream().wait_stream(side)
+        self._gl, self._gf = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._gl):
+            self._out_l = self._loss_body(self.v_in)
+        with torch.cuda.graph(self._gf):
+            self._out_f = self._full_body(self.v_in)
+        self._g = True
+
+    def _loss_value(self, s) -> float:
+        s = s.cpu().numpy()
+        if s[0] == 0.0:
+            return float("inf")
+        return float(s[1] + self.cfg.smooth_weight * s[2])
+
+    def loss_only(self, verts: torch.Tensor) -> float:
+        if not self.graphs:
+            return self._loss_value(self._loss_body(verts))
+        if self._g is None:
+            self._capture()
+        self.v_in.copy_(verts)
+        self._gl.replay()
+        return self._loss_value(self._out_l)
+
+    def full_eval(self, verts: torch.Tensor):
+        if not self.graphs:
+            s, g = self._full_body(verts)
+            return self._loss_value(s), g
+        if self._g is None:
+            self._capture()
+        self.v_in.copy_(verts)
+        self._gf.replay()
+        return self._loss_value(self._out_f[0]), self._out_f[1].clone()
 
 
 def morph(template: TriangleMesh, target: ScalarField, cfg: MorphConfig | None = None, *,
-          precision: str = "f64") -> tuple[TriangleMesh, MorphReport]:
+          precision: str = "f64", graphs: bool = True) -> tuple[TriangleMesh, MorphReport]:
     """Fit ``template``'s soft occupancy to ``target``; returns (mesh, report).
-    Raises DivergedError if the loss turns non-finite."""
+    Raises DivergedError if the loss turns non-finite.  ``graphs``: replay
+    the evaluations as CUDA graphs (same kernels, same results)."""
     cfg = cfg or MorphConfig()
     if template.num_faces == 0:
         raise ValueError("template mesh has no faces")
@@ -152,7 +235,7 @@ def morph(template: TriangleMesh, target: ScalarField, cfg: MorphConfig | None =
     if np.any(lo < target.spec.bounds_min) or np.any(hi > target.spec.bounds_max):
         raise ValueError("target grid bounds must contain the template bounding box")
 
-    P = _DeviceProblem(template, target, cfg, precision)
+    P = _DeviceProblem(template, target, cfg, precision, graphs=graphs)
     verts = P.mesh.vertices.clone()
     report = MorphReport()
     loss, grad = P.full_eval(verts)

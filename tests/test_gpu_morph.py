@@ -95,3 +95,35 @@ def test_criterion_8_morph_demo(cuda_device, precision):
     print(f"criterion 8 ({precision}): chamfer {initial:.4f} -> {final:.4f}, {elapsed:.2f} s")
     assert all(b <= a for a, b in zip(losses, losses[1:]))
     assert final <= 0.5 * initial and elapsed < 300.0
+
+
+def test_morph_graphs_equal_eager_and_faster(wv):
+    """The CUDA-graph replay of the evaluations (default) runs the same
+    kernels as eager launches: identical traces and vertices, bit for bit;
+    and at the reference's acceptance size (icosphere(2) -> cube, 32^3) the
+    graphed loop is faster."""
+    import time
+    from paper_2407_11272_b200 import configs
+    from paper_2407_11272_b200.morph import MorphConfig, morph
+    g = golden("morph_traces")
+    tmpl = wv.TriangleMesh(g["tmpl_vertices"], g["tmpl_faces"])
+    target = wv.ScalarField(wv.GridSpec(*grid_of(g)), g["target"])
+    for prec in ("f64", "f32"):
+        a, ra = morph(tmpl, target, MorphConfig(iterations=8), precision=prec, graphs=True)
+        b, rb = morph(tmpl, target, MorphConfig(iterations=8), precision=prec, graphs=False)
+        assert a.vertices.tobytes() == b.vertices.tobytes(), prec
+        assert [e["loss"] for e in ra.entries] == [e["loss"] for e in rb.entries], prec
+    v, f = configs.icosphere(2, 0.5)
+    spec = wv.GridSpec((-1.0,) * 3, (1.0,) * 3, 32)
+    nodes = spec.node_coordinates()
+    cube = wv.ScalarField(spec, (np.abs(nodes).max(axis=1) < 0.45).astype(np.float64))
+    times = {}
+    for graphs in (True, False):
+        morph(wv.TriangleMesh(v, f), cube, MorphConfig(iterations=3), precision="f32",
+              graphs=graphs)
+        t0 = time.perf_counter()
+        morph(wv.TriangleMesh(v, f), cube, MorphConfig(iterations=60), precision="f32",
+              graphs=graphs)
+        times[graphs] = time.perf_counter() - t0
+    print("morph 60 iterations: graphs %.3f s, eager %.3f s" % (times[True], times[False]))
+    assert times[True] < times[False]
