@@ -73,6 +73,10 @@ int wv_set_device(int device);
  * (faces_i64=0) or int64.  `packed` must hold wv_packed_bytes(kind, F).
  * Exact kinds keep degenerate faces in place, marked dead (the reference
  * drops them; results are identical). */
+/* Kernels launched by this library since load (all entry points, all
+ * threads): bench.py's count of its own launches in a timed region. */
+long long wv_launch_count(void);
+
 size_t wv_packed_bytes(int kind, int64_t n_faces);
 int wv_pack_faces(int kind, const void *vertices, int vert_f64, int64_t n_verts,
                   const void *faces, int faces_i64, int64_t n_faces, void *packed,

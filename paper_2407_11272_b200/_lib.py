@@ -43,7 +43,7 @@ EXPORTED = (
     "wv_exact_bwd_points_f64", "wv_soft_bwd_grid_f64", "wv_soft_bwd_points_f64",
     "wv_face_to_vertex", "wv_loss_workspace_bytes", "wv_loss_terms_f32", "wv_loss_terms_f64",
     "wv_loss_finalize", "wv_mc_classify", "wv_mc_edges", "wv_mc_vertices", "wv_mc_emit",
-    "wv_mc_vertices_slab",
+    "wv_mc_vertices_slab", "wv_launch_count",
     "wv_splitmix64_uniform", "wv_pairwise_sum_workspace_bytes", "wv_pairwise_sum",
     "wv_surface_cdf", "wv_sample_surface", "wv_nearest_distances",
     "wv_fwd_workspace_bytes_batch", "wv_fwd_grid_f32_batch", "wv_bwd_workspace_bytes_batch",
@@ -115,6 +115,7 @@ def _declare(lib):
         "wv_mc_vertices": ([P, I, Grid, D, P, P, P, P], I),
         "wv_mc_emit": ([P, P, P, I, P, P, P, Grid, P, P], I),
         "wv_mc_vertices_slab": ([P, I, Grid, I64, I64, D, P, P, P, P], I),
+        "wv_launch_count": ([], ctypes.c_longlong),
         "wv_splitmix64_uniform": ([ctypes.c_uint64, I64, P, P], I),
         "wv_pairwise_sum_workspace_bytes": ([I64], SZ),
         "wv_pairwise_sum": ([P, I64, P, P, SZ, P], I),

@@ -1161,23 +1161,23 @@ static int launch_bwd(const void* packed, int64_t n_faces, const PointSource& ps
   if (ps.kind == PointSource::kGrid && ps.grid.res[2] >= 16 &&
       row_aligned(ps.grid, ps.n0, 2 * ((n_count + 1) / 2), 2)) {
     RowSrc src{{ps.grid, ps.n0}};
-    bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
+    { bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
         hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst,
-        Pol::kScaled ? grid_scale(ps.grid) : 1.0f);
+        Pol::kScaled ? grid_scale(ps.grid) : 1.0f); wv::note_launch(); }
   } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
-    bwd_f32_kernel<Pol, GridSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
+    { bwd_f32_kernel<Pol, GridSrc><<<grid, kBwdThreads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f); wv::note_launch(); }
   } else {
     ListSrc src{ps.points};
-    bwd_f32_kernel<Pol, ListSrc><<<grid, kBwdThreads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f);
+    { bwd_f32_kernel<Pol, ListSrc><<<grid, kBwdThreads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_rec, src, coefs, n_count, pl.pts_per_split, cs, dst, 1.0f); wv::note_launch(); }
   }
   if (pl.splits > 1) {
     const int64_t n = n_rec * Pol::kOut;
     int blocks = (int)((n * bt.n + 255) / 256);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
-    reduce_splits_kernel<<<blocks, 256, 0, stream>>>(dst, pl.splits, n, bt.n, face_grad);
+    { reduce_splits_kernel<<<blocks, 256, 0, stream>>>(dst, pl.splits, n, bt.n, face_grad); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -1288,8 +1288,8 @@ int launch_face_to_vertex(const double* face_grad, const int64_t* off, const int
   if (n_verts <= 0) return kOk;
   int blocks = (int)((n_verts + 255) / 256);
   if (blocks > num_sms * 16) blocks = num_sms * 16;
-  face_to_vertex_kernel<<<blocks, 256, 0, stream>>>(face_grad, off, slots, n_verts, scale,
-                                                    accumulate, out64, out32);
+  { face_to_vertex_kernel<<<blocks, 256, 0, stream>>>(face_grad, off, slots, n_verts, scale,
+                                                    accumulate, out64, out32); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -1301,8 +1301,8 @@ int launch_face_to_vertex_batch(const double* face_grad, int64_t n_faces, const 
   if (batch < 1 || batch > 65535) return kErrArg;
   int blocks = (int)((n_verts + 255) / 256);
   if (blocks > num_sms * 16) blocks = num_sms * 16;
-  face_to_vertex_kernel<<<dim3((unsigned)blocks, (unsigned)batch), 256, 0, stream>>>(
-      face_grad, off, slots, n_verts, scale, accumulate, out64, out32, n_faces * 9, scale_stride);
+  { face_to_vertex_kernel<<<dim3((unsigned)blocks, (unsigned)batch), 256, 0, stream>>>(
+      face_grad, off, slots, n_verts, scale, accumulate, out64, out32, n_faces * 9, scale_stride); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 

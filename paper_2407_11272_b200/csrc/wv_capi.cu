@@ -1,8 +1,15 @@
 // wv_capi.cu -- extern "C" boundary (include/windvox_b200.h).  Argument
 // validation, device-attribute caching, launch dispatch.  No exceptions cross
 // the ABI; every entry point returns a status code.
+#include <atomic>
 #include "../../include/windvox_b200.h"
 #include "wv_kernels.h"
+
+namespace wv {
+static std::atomic<long long> g_launch_count{0};
+void note_launch() { g_launch_count.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launch_count.load(std::memory_order_relaxed); }
+}  // namespace wv
 
 namespace {
 
@@ -79,6 +86,8 @@ const char* wv_status_string(int status) {
 int wv_set_device(int device) {
   return cudaSetDevice(device) == cudaSuccess ? WV_OK : WV_ERR_CUDA;
 }
+
+long long wv_launch_count(void) { return wv::launch_count(); }
 
 size_t wv_packed_bytes(int kind, int64_t n_faces) { return wv::packed_bytes(kind, n_faces); }
 

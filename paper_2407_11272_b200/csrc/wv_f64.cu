@@ -199,12 +199,12 @@ static int launch_f64(const void* packed, int64_t n_faces, const PointSource& ps
   const unsigned blocks = (unsigned)((n_count + per_block - 1) / per_block);
   if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
-    fwd_f64_kernel<Pol, GridSrc><<<blocks, kF64Threads, 0, stream>>>(
-        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+    { fwd_f64_kernel<Pol, GridSrc><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags); wv::note_launch(); }
   } else {
     ListSrc64 src{ps.points64};
-    fwd_f64_kernel<Pol, ListSrc64><<<blocks, kF64Threads, 0, stream>>>(
-        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+    { fwd_f64_kernel<Pol, ListSrc64><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -348,12 +348,12 @@ int launch_exact_strip_fwd_f64(const void* packed, int64_t n_faces, const PointS
   const unsigned blocks = (unsigned)((n_count + kF64NC - 1) / kF64NC);
   if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
-    fwd_f64_strip_kernel<GridSrc><<<blocks, kF64Threads, 0, stream>>>(
-        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+    { fwd_f64_strip_kernel<GridSrc><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags); wv::note_launch(); }
   } else {
     ListSrc64 src{ps.points64};
-    fwd_f64_strip_kernel<ListSrc64><<<blocks, kF64Threads, 0, stream>>>(
-        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags);
+    { fwd_f64_strip_kernel<ListSrc64><<<blocks, kF64Threads, 0, stream>>>(
+        hdr, recs, n_faces, src, n_count, use_atan2, policy, out, flags); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -540,20 +540,20 @@ static int launch_bwd64(const void* packed, int64_t n_faces, const PointSource& 
   dim3 grid((unsigned)bx, (unsigned)splits);
   if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
-    bwd_f64_kernel<Pol, GridSrc><<<grid, kBwd64Threads, 0, stream>>>(hdr, recs, n_faces, src,
+    { bwd_f64_kernel<Pol, GridSrc><<<grid, kBwd64Threads, 0, stream>>>(hdr, recs, n_faces, src,
                                                                      coefs, n_count, pps,
-                                                                     coef_scale, dst);
+                                                                     coef_scale, dst); wv::note_launch(); }
   } else {
     ListSrc64 src{ps.points64};
-    bwd_f64_kernel<Pol, ListSrc64><<<grid, kBwd64Threads, 0, stream>>>(hdr, recs, n_faces, src,
+    { bwd_f64_kernel<Pol, ListSrc64><<<grid, kBwd64Threads, 0, stream>>>(hdr, recs, n_faces, src,
                                                                        coefs, n_count, pps,
-                                                                       coef_scale, dst);
+                                                                       coef_scale, dst); wv::note_launch(); }
   }
   if (splits > 1) {
     const int64_t n = n_faces * 9;
     int blocks = (int)((n + 255) / 256);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
-    reduce_splits64_kernel<<<blocks, 256, 0, stream>>>(dst, splits, n, face_grad);
+    { reduce_splits64_kernel<<<blocks, 256, 0, stream>>>(dst, splits, n, face_grad); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }

@@ -398,23 +398,23 @@ int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, i
   const unsigned threads = Pol::kThreads;
   if (rows) {
     RowSrc src{{ps.grid, ps.n0}};
-    fwd_f32_kernel<Pol, RowSrc><<<grid, threads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
+    { fwd_f32_kernel<Pol, RowSrc><<<grid, threads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o); wv::note_launch(); }
   } else if (ps.kind == PointSource::kGrid) {
     GridSrc src{ps.grid, ps.n0};
-    fwd_f32_kernel<Pol, GridSrc><<<grid, threads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
+    { fwd_f32_kernel<Pol, GridSrc><<<grid, threads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o); wv::note_launch(); }
   } else {
     ListSrc src{ps.points};
-    fwd_f32_kernel<Pol, ListSrc><<<grid, threads, 0, stream>>>(
-        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
+    { fwd_f32_kernel<Pol, ListSrc><<<grid, threads, 0, stream>>>(
+        hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o); wv::note_launch(); }
   }
   if (pl.splits > 1) {
     const int t = 256;
     int blocks = (int)((total + t - 1) / t);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
-    finalize_theta_kernel<<<blocks, t, 0, stream>>>(o.part, o.part_flags, pl.splits, total,
-                                                    policy, out, flags, o.scale);
+    { finalize_theta_kernel<<<blocks, t, 0, stream>>>(o.part, o.part_flags, pl.splits, total,
+                                                    policy, out, flags, o.scale); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }

@@ -10,6 +10,12 @@
 
 namespace wv {
 
+// every kernel launch of the library bumps a process-wide counter
+// (wv_launch_count): bench.py reports the launches of its timed region from
+// it -- a count of OUR kernels that needs no profiler
+void note_launch();
+long long launch_count();
+
 // status codes (mirrored in include/windvox_b200.h)
 constexpr int kOk = 0;
 constexpr int kErrArg = 1;

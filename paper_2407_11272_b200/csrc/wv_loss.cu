@@ -117,11 +117,11 @@ static int launch_loss(const T* values, const uint8_t* flags, const T* targets, 
   if (ws == nullptr || ws_bytes < loss_workspace_bytes(n)) return kErrWorkspace;
   double* part = static_cast<double*>(ws);
   if (n > 0)
-    loss_terms_kernel<T><<<nb, kLossThreads, 0, stream>>>(values, flags, targets, weights, n,
-                                                          coefs, part);
+    { loss_terms_kernel<T><<<nb, kLossThreads, 0, stream>>>(values, flags, targets, weights, n,
+                                                          coefs, part); wv::note_launch(); }
   else
     cudaMemsetAsync(part, 0, 3 * sizeof(double), stream);
-  loss_final_kernel<<<1, kLossThreads, 0, stream>>>(part, n > 0 ? nb : 1, sums);
+  { loss_final_kernel<<<1, kLossThreads, 0, stream>>>(part, n > 0 ? nb : 1, sums); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -133,9 +133,9 @@ int launch_loss_f32_batch(const float* values, const uint8_t* flags, const float
   if (batch < 1 || batch > 65535 || n <= 0) return kErrArg;
   if (ws == nullptr || ws_bytes < (size_t)batch * loss_workspace_bytes(n)) return kErrWorkspace;
   double* part = static_cast<double*>(ws);
-  loss_terms_kernel<float><<<dim3((unsigned)nb, (unsigned)batch), kLossThreads, 0, stream>>>(
-      values, flags, targets, weights, n, coefs, part);
-  loss_final_kernel<<<(unsigned)batch, kLossThreads, 0, stream>>>(part, nb, sums);
+  { loss_terms_kernel<float><<<dim3((unsigned)nb, (unsigned)batch), kLossThreads, 0, stream>>>(
+      values, flags, targets, weights, n, coefs, part); wv::note_launch(); }
+  { loss_final_kernel<<<(unsigned)batch, kLossThreads, 0, stream>>>(part, nb, sums); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 int launch_loss_f32(const float* values, const uint8_t* flags, const float* targets,
@@ -151,7 +151,7 @@ int launch_loss_f64(const double* values, const uint8_t* flags, const double* ta
                              stream);
 }
 int launch_loss_finalize(double* sums, cudaStream_t stream) {
-  loss_finalize_kernel<<<1, 32, 0, stream>>>(sums);
+  { loss_finalize_kernel<<<1, 32, 0, stream>>>(sums); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 

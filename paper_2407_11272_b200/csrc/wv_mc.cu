@@ -118,15 +118,15 @@ int launch_mc_classify(const void* vals, int f64, int64_t rx, int64_t ry, int64_
                        cudaStream_t stream) {
   const int64_t cells = (rx - 1) * (ry - 1) * (rz - 1);
   if (cells <= 0) return kOk;
-  mc_classify_kernel<<<grid_blocks(cells, num_sms), 256, 0, stream>>>(vals, f64, rx, ry, rz, iso,
-                                                                      count_tab, cases, counts);
+  { mc_classify_kernel<<<grid_blocks(cells, num_sms), 256, 0, stream>>>(vals, f64, rx, ry, rz, iso,
+                                                                      count_tab, cases, counts); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
 int launch_mc_edges(const void* vals, int f64, int64_t rx, int64_t ry, int64_t rz, double iso,
                     int32_t* flags, int num_sms, cudaStream_t stream) {
   const int64_t n = 3 * rx * ry * rz;
-  mc_edge_kernel<<<grid_blocks(n, num_sms), 256, 0, stream>>>(vals, f64, rx, ry, rz, iso, flags);
+  { mc_edge_kernel<<<grid_blocks(n, num_sms), 256, 0, stream>>>(vals, f64, rx, ry, rz, iso, flags); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -135,8 +135,8 @@ int launch_mc_vertices(const void* vals, int f64, const GridDesc& g, int64_t i0,
                        int num_sms, cudaStream_t stream) {
   const int64_t n = 3 * rows * g.res[1] * g.res[2];
   if (n <= 0) return kOk;
-  mc_vertex_kernel<<<grid_blocks(n, num_sms), 256, 0, stream>>>(vals, f64, g, i0, rows, iso,
-                                                                flags, slot, verts);
+  { mc_vertex_kernel<<<grid_blocks(n, num_sms), 256, 0, stream>>>(vals, f64, g, i0, rows, iso,
+                                                                flags, slot, verts); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -146,8 +146,8 @@ int launch_mc_emit(const uint8_t* cases, const int64_t* tri_off, const int8_t* t
                    int num_sms, cudaStream_t stream) {
   const int64_t cells = (rx - 1) * (ry - 1) * (rz - 1);
   if (cells <= 0) return kOk;
-  mc_emit_kernel<<<grid_blocks(cells, num_sms), 256, 0, stream>>>(
-      cases, tri_off, tri_tab, max_tris, edge_axis, edge_base, vidx, rx, ry, rz, faces);
+  { mc_emit_kernel<<<grid_blocks(cells, num_sms), 256, 0, stream>>>(
+      cases, tri_off, tri_tab, max_tris, edge_axis, edge_base, vidx, rx, ry, rz, faces); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 

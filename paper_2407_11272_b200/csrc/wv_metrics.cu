@@ -232,7 +232,7 @@ static int grid_for(int64_t n, int threads, int num_sms) {
 
 int launch_splitmix(uint64_t seed, int64_t count, double* out, int num_sms, cudaStream_t s) {
   if (count <= 0) return kOk;
-  splitmix_kernel<<<grid_for(count, 256, num_sms), 256, 0, s>>>(seed, count, out);
+  { splitmix_kernel<<<grid_for(count, 256, num_sms), 256, 0, s>>>(seed, count, out); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -252,7 +252,7 @@ int launch_pairwise_sum(const double* x, int64_t n, double* out, void* ws, size_
   int64_t* len = lo + leaves;
   double* leaf = reinterpret_cast<double*>(len + leaves);
   int* status = reinterpret_cast<int*>(leaf + leaves);
-  pairwise_sum_kernel<<<1, 256, 0, s>>>(x, n, out, lo, len, leaf, (int)leaves, status);
+  { pairwise_sum_kernel<<<1, 256, 0, s>>>(x, n, out, lo, len, leaf, (int)leaves, status); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -260,8 +260,8 @@ int launch_surface_cdf(const double* v, const int64_t* f, int64_t n_faces, doubl
                        double* cdf, double* total, void* ws, size_t ws_bytes, int num_sms,
                        cudaStream_t s) {
   if (n_faces <= 0) return kErrArg;
-  face_area_kernel<<<grid_for(n_faces, 256, num_sms), 256, 0, s>>>(v, f, n_faces, areas);
-  cumsum_kernel<<<1, 1, 0, s>>>(areas, n_faces, cdf);
+  { face_area_kernel<<<grid_for(n_faces, 256, num_sms), 256, 0, s>>>(v, f, n_faces, areas); wv::note_launch(); }
+  { cumsum_kernel<<<1, 1, 0, s>>>(areas, n_faces, cdf); wv::note_launch(); }
   if (cudaGetLastError() != cudaSuccess) return kErrLaunch;
   return launch_pairwise_sum(areas, n_faces, total, ws, ws_bytes, s);
 }
@@ -270,7 +270,7 @@ int launch_sample_surface(const double* v, const int64_t* f, int64_t n_faces, co
                           const double* total, uint64_t seed, int64_t n, double* out, int num_sms,
                           cudaStream_t s) {
   if (n <= 0) return kOk;
-  sample_kernel<<<grid_for(n, 256, num_sms), 256, 0, s>>>(v, f, n_faces, cdf, total, seed, n, out);
+  { sample_kernel<<<grid_for(n, 256, num_sms), 256, 0, s>>>(v, f, n_faces, cdf, total, seed, n, out); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -279,7 +279,7 @@ int launch_nearest(const double* q, int64_t nq, const double* t, int64_t nt, dou
   if (nq <= 0) return kOk;
   if (nt <= 0) return kErrArg;
   const int64_t blocks = (nq + kNnThreads - 1) / kNnThreads;
-  nearest_kernel<<<(unsigned)blocks, kNnThreads, 0, s>>>(q, nq, t, nt, out);
+  { nearest_kernel<<<(unsigned)blocks, kNnThreads, 0, s>>>(q, nq, t, nt, out); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 

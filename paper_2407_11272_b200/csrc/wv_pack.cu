@@ -265,6 +265,7 @@ int launch_pack_exact_grad(int kind, const void* vertices, int vert_f64, int64_t
     if (faces_i64) WV_PACK_EG(float, int64_t);
     else WV_PACK_EG(float, int32_t);
   }
+  wv::note_launch();
 #undef WV_PACK_EG
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -307,8 +308,8 @@ int launch_vertex_normals(const double* verts, const int64_t* faces, int64_t n_f
   if (n_verts <= 0) return kOk;
   int64_t blocks = (n_verts + 255) / 256;
   if (blocks > 4096) blocks = 4096;
-  vertex_normals_kernel<<<(unsigned)blocks, 256, 0, stream>>>(verts, faces, n_faces > 0 ? n_faces : 1,
-                                                              off, slots, n_verts, normals, zero);
+  { vertex_normals_kernel<<<(unsigned)blocks, 256, 0, stream>>>(verts, faces, n_faces > 0 ? n_faces : 1,
+                                                              off, slots, n_verts, normals, zero); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -334,11 +335,11 @@ int launch_surface_eps(const void* vertices, int vert_f64, int64_t n_verts, doub
                        cudaStream_t stream) {
   PackHeader* hdr = reinterpret_cast<PackHeader*>(eps_dev);
   if (vert_f64)
-    surface_eps_kernel<double><<<1, 1024, 0, stream>>>(static_cast<const double*>(vertices),
-                                                       n_verts, hdr);
+    { surface_eps_kernel<double><<<1, 1024, 0, stream>>>(static_cast<const double*>(vertices),
+                                                       n_verts, hdr); wv::note_launch(); }
   else
-    surface_eps_kernel<float><<<1, 1024, 0, stream>>>(static_cast<const float*>(vertices),
-                                                      n_verts, hdr);
+    { surface_eps_kernel<float><<<1, 1024, 0, stream>>>(static_cast<const float*>(vertices),
+                                                      n_verts, hdr); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
@@ -358,19 +359,19 @@ int launch_pack(int kind, const void* vertices, int vert_f64, int64_t n_verts,
   if (vert_f64) {
     const double* v = static_cast<const double*>(vertices);
     if (faces_i64)
-      pack_kernel<double, int64_t><<<(unsigned)blocks, threads, 0, stream>>>(
-          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs);
+      { pack_kernel<double, int64_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs); wv::note_launch(); }
     else
-      pack_kernel<double, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
-          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs);
+      { pack_kernel<double, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs); wv::note_launch(); }
   } else {
     const float* v = static_cast<const float*>(vertices);
     if (faces_i64)
-      pack_kernel<float, int64_t><<<(unsigned)blocks, threads, 0, stream>>>(
-          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs);
+      { pack_kernel<float, int64_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs); wv::note_launch(); }
     else
-      pack_kernel<float, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
-          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs);
+      { pack_kernel<float, int32_t><<<(unsigned)blocks, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -386,11 +387,11 @@ int launch_pack_batch(int kind, const void* vertices, int vert_f64, int64_t n_ve
   PackHeader* hdr = static_cast<PackHeader*>(packed);
   const int64_t vs = 3 * n_verts;
   if (vert_f64)
-    surface_eps_kernel<double><<<(unsigned)batch, 1024, 0, stream>>>(
-        static_cast<const double*>(vertices), n_verts, hdr, vs, pack_stride);
+    { surface_eps_kernel<double><<<(unsigned)batch, 1024, 0, stream>>>(
+        static_cast<const double*>(vertices), n_verts, hdr, vs, pack_stride); wv::note_launch(); }
   else
-    surface_eps_kernel<float><<<(unsigned)batch, 1024, 0, stream>>>(
-        static_cast<const float*>(vertices), n_verts, hdr, vs, pack_stride);
+    { surface_eps_kernel<float><<<(unsigned)batch, 1024, 0, stream>>>(
+        static_cast<const float*>(vertices), n_verts, hdr, vs, pack_stride); wv::note_launch(); }
   void* recs = hdr + 1;
   const int threads = 256;
   int64_t blocks = (n_faces + threads - 1) / threads;
@@ -400,19 +401,19 @@ int launch_pack_batch(int kind, const void* vertices, int vert_f64, int64_t n_ve
   if (vert_f64) {
     const double* v = static_cast<const double*>(vertices);
     if (faces_i64)
-      pack_kernel<double, int64_t><<<grid, threads, 0, stream>>>(
-          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+      { pack_kernel<double, int64_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs, vs, pack_stride); wv::note_launch(); }
     else
-      pack_kernel<double, int32_t><<<grid, threads, 0, stream>>>(
-          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+      { pack_kernel<double, int32_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs, vs, pack_stride); wv::note_launch(); }
   } else {
     const float* v = static_cast<const float*>(vertices);
     if (faces_i64)
-      pack_kernel<float, int64_t><<<grid, threads, 0, stream>>>(
-          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+      { pack_kernel<float, int64_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int64_t*>(faces), n_faces, hdr, recs, vs, pack_stride); wv::note_launch(); }
     else
-      pack_kernel<float, int32_t><<<grid, threads, 0, stream>>>(
-          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs, vs, pack_stride);
+      { pack_kernel<float, int32_t><<<grid, threads, 0, stream>>>(
+          kind, v, static_cast<const int32_t*>(faces), n_faces, hdr, recs, vs, pack_stride); wv::note_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }

@@ -330,6 +330,7 @@ int launch_pack_strip_f64(const void* verts, int vert_f64, int64_t n_verts, cons
     if (faces_i64) WV_PSF(float, int64_t);
     else WV_PSF(float, int32_t);
   }
+  wv::note_launch();
 #undef WV_PSF
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
@@ -343,21 +344,21 @@ int launch_pack_strip(const void* verts, int vert_f64, int64_t n_verts, const vo
   ExactRecF32* recs = reinterpret_cast<ExactRecF32*>(hdr + 1);
   const int blocks = (int)((n_faces + 255) / 256 > 0 ? (n_faces + 255) / 256 : 1);
   if (vert_f64 && faces_i64)
-    pack_strip_kernel<double, int64_t><<<blocks, 256, 0, stream>>>(
+    { pack_strip_kernel<double, int64_t><<<blocks, 256, 0, stream>>>(
         static_cast<const double*>(verts), static_cast<const int64_t*>(faces), perm, win, flags,
-        n_faces, hdr, recs);
+        n_faces, hdr, recs); wv::note_launch(); }
   else if (vert_f64)
-    pack_strip_kernel<double, int32_t><<<blocks, 256, 0, stream>>>(
+    { pack_strip_kernel<double, int32_t><<<blocks, 256, 0, stream>>>(
         static_cast<const double*>(verts), static_cast<const int32_t*>(faces), perm, win, flags,
-        n_faces, hdr, recs);
+        n_faces, hdr, recs); wv::note_launch(); }
   else if (faces_i64)
-    pack_strip_kernel<float, int64_t><<<blocks, 256, 0, stream>>>(
+    { pack_strip_kernel<float, int64_t><<<blocks, 256, 0, stream>>>(
         static_cast<const float*>(verts), static_cast<const int64_t*>(faces), perm, win, flags,
-        n_faces, hdr, recs);
+        n_faces, hdr, recs); wv::note_launch(); }
   else
-    pack_strip_kernel<float, int32_t><<<blocks, 256, 0, stream>>>(
+    { pack_strip_kernel<float, int32_t><<<blocks, 256, 0, stream>>>(
         static_cast<const float*>(verts), static_cast<const int32_t*>(faces), perm, win, flags,
-        n_faces, hdr, recs);
+        n_faces, hdr, recs); wv::note_launch(); }
   return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
 }
 
