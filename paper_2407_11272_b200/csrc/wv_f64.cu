@@ -384,23 +384,27 @@ struct ExactBwd64 {
   // edge (Biot-Savart) form of d(Omega)/dv, see ExactEdgeBwd in wv_bwd_f32.cu;
   // coef carries the -1/(4 pi) factor.  Per pair: the three reciprocal corner
   // lengths once (Newton rsqrt), one Newton reciprocal per edge, no branches.
+  // The reference has no exact gradient, so no operation order is pinned:
+  // products and sums are fused explicitly (this file is built with
+  // -fmad=false for the forwards' reference order).
   __device__ __forceinline__ static void edge(const double* a, const double* b, double la,
                                               double lb, double ia, double ib, double cw,
                                               double* gP, double* gQ) {
-    const double m[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
-                         a[0] * b[1] - a[1] * b[0]};
+    const double m[3] = {fma(a[1], b[2], -a[2] * b[1]), fma(a[2], b[0], -a[0] * b[2]),
+                         fma(a[0], b[1], -a[1] * b[0])};
     // |a||b| + a.b without cancellation next to the edge's segment (a.b < 0):
     // |a x b|^2 / (|a||b| - a.b), so cw / (|a||b| + a.b) = cw (|a||b| - a.b) / |a x b|^2
-    const double L = la * lb, ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+    const double L = la * lb, ab = fma(a[0], b[0], fma(a[1], b[1], a[2] * b[2]));
     const bool neg = ab < 0.0;
     const double num = neg ? cw * (L - ab) : cw;
-    const double den = neg ? m[0] * m[0] + m[1] * m[1] + m[2] * m[2] : L + ab;
+    const double den = neg ? fma(m[0], m[0], fma(m[1], m[1], m[2] * m[2])) : L + ab;
     const double t = num * rcp_nr(den);
     if (cw == 0.0 || !(fabs(t) < INFINITY)) return;  // q on the segment: on-surface
     const double sp = t * ia, sq = t * ib;
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
-      gP[d] += m[d] * sp;
-      gQ[d] += m[d] * sq;
+      gP[d] = fma(m[d], sp, gP[d]);
+      gQ[d] = fma(m[d], sq, gQ[d]);
     }
   }
   __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
@@ -408,9 +412,9 @@ struct ExactBwd64 {
     const double a[3] = {R.v[0] - qx, R.v[1] - qy, R.v[2] - qz};
     const double b[3] = {R.v[3] - qx, R.v[4] - qy, R.v[5] - qz};
     const double c[3] = {R.v[6] - qx, R.v[7] - qy, R.v[8] - qz};
-    const double a2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
-    const double b2 = b[0] * b[0] + b[1] * b[1] + b[2] * b[2];
-    const double c2 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+    const double a2 = fma(a[0], a[0], fma(a[1], a[1], a[2] * a[2]));
+    const double b2 = fma(b[0], b[0], fma(b[1], b[1], b[2] * b[2]));
+    const double c2 = fma(c[0], c[0], fma(c[1], c[1], c[2] * c[2]));
     if (!(a2 > 0.0 && b2 > 0.0 && c2 > 0.0)) return;  // q on a vertex (flagged)
     const double ia = rsqrt_nr(a2), ib = rsqrt_nr(b2), ic = rsqrt_nr(c2);
     const double la = a2 * ia, lb = b2 * ib, lc = c2 * ic;
