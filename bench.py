@@ -571,6 +571,10 @@ def run_ours(args):
     # (a replayed graph launches the kernels its capture counted)
     n_timed = (graph_launches * args.steps if graph is not None
                else lib.wv_launch_count() - n_before)
+    if world > 1:  # all ranks' launches
+        nt = torch.tensor([n_timed], device=dev, dtype=torch.int64)
+        dist.all_reduce(nt)
+        n_timed = int(nt)
     ms = sum(a.elapsed_time(b) for a, b in zip(ev_s, ev_e))
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["f0"], ev["f1"]))
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["b0"], ev["b1"]))
@@ -654,7 +658,8 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": n_timed,
             "gpu_launches_source": "the library's launch counter (wv_launch_count) over the "
-                                   "timed region; CUDA-activity cross-check: "
+                                   "timed region, summed over ranks; CUDA-activity cross-check "
+                                   "(rank 0): "
                                    + (f"{launches * args.steps} wv:: kernels (torch.profiler, "
                                       "one untimed step x steps)" if launches else "unavailable"),
             "clocks": clocks,
@@ -776,6 +781,10 @@ def run_c4(args):
         e1.record(stream)
         barrier()
         n_timed = L.lib().wv_launch_count() - n_before
+    if world > 1:  # all ranks' launches
+        nt = torch.tensor([n_timed], device=dev, dtype=torch.int64)
+        dist.all_reduce(nt)
+        n_timed = int(nt)
     t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -840,7 +849,8 @@ def run_c4(args):
             "e2e": e2e,
             "gpu_launches": n_timed,
             "gpu_launches_source": "the library's launch counter (wv_launch_count) over the "
-                                   "timed region; CUDA-activity cross-check: "
+                                   "timed region, summed over ranks; CUDA-activity cross-check "
+                                   "(rank 0): "
                                    + (f"{launches * args.steps} wv:: kernels (torch.profiler)"
                                       if launches else "unavailable"),
             "clocks": clocks,
@@ -903,6 +913,10 @@ def run_c5(args):
         e1.record(stream)
         barrier()
         n_timed = L.lib().wv_launch_count() - n_before
+    if world > 1:  # all ranks' launches
+        nt = torch.tensor([n_timed], device=dev, dtype=torch.int64)
+        dist.all_reduce(nt)
+        n_timed = int(nt)
     t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
