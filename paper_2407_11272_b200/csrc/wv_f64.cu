@@ -50,13 +50,92 @@ __device__ __forceinline__ double norm_nr(double v2) {
   return v2 > 0.0 ? v2 * rsqrt_nr(v2) : 0.0;
 }
 
+// One exact face term in the reference's operation order
+// (_kernels.py:52-115).  The common pair -- a live face, no corner within
+// eps, q off the face's plane band, |alpha| < beta/8 -- is decided by ONE
+// predicate and evaluated branch-free (polynomial); everything else takes
+// exact_f64_slow, the reference's tests in order.  Same results as the
+// nested-branch form; far fewer divergent branches per pair.
+__device__ __noinline__ void exact_f64_slow(const ExactRecF64& R, double ax, double ay,
+                                            double az, double na, double nb, double nc,
+                                            double pd, double alpha, double beta, double eps,
+                                            int use_atan2, double& acc, bool& hit) {
+  if (R.dead != 0.0) return;  // dropped by _prepare_exact
+  if (na < eps || nb < eps || nc < eps) {
+    hit = true;
+    return;
+  }
+  const double* t = R.v;
+  if (-eps < pd && pd < eps) {
+    const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+    const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
+    const double d00 = ux * ux + uy * uy + uz * uz;
+    const double d01 = ux * wx + uy * wy + uz * wz;
+    const double d11 = wx * wx + wy * wy + wz * wz;
+    const double denom = d00 * d11 - d01 * d01;
+    const double ru = -(ax * ux + ay * uy + az * uz);
+    const double rw = -(ax * wx + ay * wy + az * wz);
+    const double b1 = (d11 * ru - d01 * rw) / denom;
+    const double b2 = (d00 * rw - d01 * ru) / denom;
+    if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) {
+      hit = true;
+      return;
+    }
+  }
+  if (use_atan2) {
+    acc += 2.0 * atan2(alpha, beta);
+  } else {  // regression-demonstration branch, _kernels.py:106-114
+    if (beta != 0.0)
+      acc += 2.0 * atan(alpha / beta);
+    else if (alpha > 0.0)
+      acc += kPi;
+    else if (alpha < 0.0)
+      acc -= kPi;
+  }
+}
+
+__device__ __forceinline__ void exact_f64_term(const ExactRecF64& R, double ax, double ay,
+                                               double az, double bx, double by, double bz,
+                                               double cx, double cy, double cz, double na,
+                                               double nb, double nc, double qx, double qy,
+                                               double qz, double eps, int use_atan2,
+                                               double& acc, bool& hit) {
+  const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
+  const double alpha = (ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz)) +
+                       az * (bx * cy - by * cx);
+  const double beta = (na * (nb * nc) + (bx * cx + by * cy + bz * cz) * na) +
+                      ((ax * bx + ay * by + az * bz) * nc + (cx * ax + cy * ay + cz * az) * nb);
+  // atan2(alpha, beta) for |alpha| < beta/8 (nearly every pair of a fine
+  // mesh): t = alpha/beta and the odd Taylor polynomial t (1 - s/3 + s^2/5
+  // - ... + s^8/17), s = t^2 <= 1/64 (truncation < 2e-18 relative;
+  // explicit fmas), a few ulp like libm's atan2 and exactly odd, so flipped
+  // faces still negate exactly
+  const bool common = use_atan2 && R.dead == 0.0 && na >= eps && nb >= eps && nc >= eps &&
+                      !(-eps < pd && pd < eps) && fabs(alpha) * 8.0 < beta;
+  if (common) {
+    const double tt = alpha * rcp_nr(beta);  // (odd in alpha: flips negate exactly)
+    const double ss = tt * tt;
+    double p = 1.0 / 17.0;
+    p = fma(p, ss, -1.0 / 15.0);
+    p = fma(p, ss, 1.0 / 13.0);
+    p = fma(p, ss, -1.0 / 11.0);
+    p = fma(p, ss, 1.0 / 9.0);
+    p = fma(p, ss, -1.0 / 7.0);
+    p = fma(p, ss, 1.0 / 5.0);
+    p = fma(p, ss, -1.0 / 3.0);
+    p = fma(p * ss, tt, tt);  // t + t s P(s)
+    acc += 2.0 * p;
+  } else {
+    exact_f64_slow(R, ax, ay, az, na, nb, nc, pd, alpha, beta, eps, use_atan2, acc, hit);
+  }
+}
+
 struct ExactF64Pol {
   using Rec = ExactRecF64;
   static constexpr double kDiv = 4.0 * kPi;  // out = acc / _FOUR_PI
   __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
                                               double eps, int use_atan2, double& acc,
                                               bool& hit) {
-    if (R.dead != 0.0) return;  // dropped by _prepare_exact
     const double* t = R.v;
     const double ax = t[0] - qx, ay = t[1] - qy, az = t[2] - qz;
     const double bx = t[3] - qx, by = t[4] - qy, bz = t[5] - qz;
@@ -64,62 +143,8 @@ struct ExactF64Pol {
     const double na = norm_nr(ax * ax + ay * ay + az * az);
     const double nb = norm_nr(bx * bx + by * by + bz * bz);
     const double nc = norm_nr(cx * cx + cy * cy + cz * cz);
-    if (na < eps || nb < eps || nc < eps) {
-      hit = true;
-      return;
-    }
-    const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
-    if (-eps < pd && pd < eps) {
-      const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
-      const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
-      const double d00 = ux * ux + uy * uy + uz * uz;
-      const double d01 = ux * wx + uy * wy + uz * wz;
-      const double d11 = wx * wx + wy * wy + wz * wz;
-      const double denom = d00 * d11 - d01 * d01;
-      const double ru = -(ax * ux + ay * uy + az * uz);
-      const double rw = -(ax * wx + ay * wy + az * wz);
-      const double b1 = (d11 * ru - d01 * rw) / denom;
-      const double b2 = (d00 * rw - d01 * ru) / denom;
-      if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) {
-        hit = true;
-        return;
-      }
-    }
-    const double alpha = (ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz)) +
-                         az * (bx * cy - by * cx);
-    const double beta = (na * (nb * nc) + (bx * cx + by * cy + bz * cz) * na) +
-                        ((ax * bx + ay * by + az * bz) * nc + (cx * ax + cy * ay + cz * az) * nb);
-    if (use_atan2) {
-      // atan2(alpha, beta) for |alpha| < beta/8 (nearly every pair of a fine
-      // mesh): t = alpha/beta (IEEE division) and the odd Taylor polynomial
-      // t (1 - s/3 + s^2/5 - ... + s^8/17), s = t^2 <= 1/64 (truncation
-      // < 2e-18 relative; evaluated with explicit fmas), a few ulp like
-      // libm's atan2 and exactly odd, so flipped faces still negate exactly.
-      // Other pairs take atan2.
-      if (fabs(alpha) * 8.0 < beta) {
-        const double t = alpha * rcp_nr(beta);  // (odd in alpha: flips negate exactly)
-        const double s = t * t;
-        double p = 1.0 / 17.0;
-        p = fma(p, s, -1.0 / 15.0);
-        p = fma(p, s, 1.0 / 13.0);
-        p = fma(p, s, -1.0 / 11.0);
-        p = fma(p, s, 1.0 / 9.0);
-        p = fma(p, s, -1.0 / 7.0);
-        p = fma(p, s, 1.0 / 5.0);
-        p = fma(p, s, -1.0 / 3.0);
-        p = fma(p * s, t, t);  // t + t s P(s)
-        acc += 2.0 * p;
-      } else {
-        acc += 2.0 * atan2(alpha, beta);
-      }
-    } else {  // regression-demonstration branch, _kernels.py:106-114
-      if (beta != 0.0)
-        acc += 2.0 * atan(alpha / beta);
-      else if (alpha > 0.0)
-        acc += kPi;
-      else if (alpha < 0.0)
-        acc -= kPi;
-    }
+    exact_f64_term(R, ax, ay, az, bx, by, bz, cx, cy, cz, na, nb, nc, qx, qy, qz, eps,
+                   use_atan2, acc, hit);
   }
 };
 
@@ -234,7 +259,6 @@ __device__ __forceinline__ void exact_f64_strip_face(const ExactRecF64& R, doubl
     d[(kRot + 1) % 3] = vdist(t + 3 * iB, qx, qy, qz);
   }
   d[(kRot + 2) % 3] = vdist(t + 3 * iC, qx, qy, qz);
-  if (R.dead != 0.0) return;  // dropped by _prepare_exact (the carry still advances)
   // |v_k - q| in true corner order
   const double dA = d[kRot], dB = d[(kRot + 1) % 3], dC = d[(kRot + 2) % 3];
   const double na = iA == 0 ? dA : iB == 0 ? dB : dC;
@@ -243,56 +267,9 @@ __device__ __forceinline__ void exact_f64_strip_face(const ExactRecF64& R, doubl
   const double ax = t[0] - qx, ay = t[1] - qy, az = t[2] - qz;
   const double bx = t[3] - qx, by = t[4] - qy, bz = t[5] - qz;
   const double cx = t[6] - qx, cy = t[7] - qy, cz = t[8] - qz;
-  if (na < eps || nb < eps || nc < eps) {
-    hit = true;
-    return;
-  }
-  const double pd = R.nhat[0] * qx + R.nhat[1] * qy + R.nhat[2] * qz - R.pld;
-  if (-eps < pd && pd < eps) {
-    const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
-    const double wx = t[6] - t[0], wy = t[7] - t[1], wz = t[8] - t[2];
-    const double d00 = ux * ux + uy * uy + uz * uz;
-    const double d01 = ux * wx + uy * wy + uz * wz;
-    const double d11 = wx * wx + wy * wy + wz * wz;
-    const double denom = d00 * d11 - d01 * d01;
-    const double ru = -(ax * ux + ay * uy + az * uz);
-    const double rw = -(ax * wx + ay * wy + az * wz);
-    const double b1 = (d11 * ru - d01 * rw) / denom;
-    const double b2 = (d00 * rw - d01 * ru) / denom;
-    if (b1 >= -kBaryTol && b2 >= -kBaryTol && b1 + b2 <= 1.0 + kBaryTol) {
-      hit = true;
-      return;
-    }
-  }
-  const double alpha = (ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz)) +
-                       az * (bx * cy - by * cx);
-  const double beta = (na * (nb * nc) + (bx * cx + by * cy + bz * cz) * na) +
-                      ((ax * bx + ay * by + az * bz) * nc + (cx * ax + cy * ay + cz * az) * nb);
-  if (use_atan2) {
-    if (fabs(alpha) * 8.0 < beta) {  // as ExactF64Pol
-      const double tt = alpha * rcp_nr(beta);
-      const double ss = tt * tt;
-      double p = 1.0 / 17.0;
-      p = fma(p, ss, -1.0 / 15.0);
-      p = fma(p, ss, 1.0 / 13.0);
-      p = fma(p, ss, -1.0 / 11.0);
-      p = fma(p, ss, 1.0 / 9.0);
-      p = fma(p, ss, -1.0 / 7.0);
-      p = fma(p, ss, 1.0 / 5.0);
-      p = fma(p, ss, -1.0 / 3.0);
-      p = fma(p * ss, tt, tt);
-      acc += 2.0 * p;
-    } else {
-      acc += 2.0 * atan2(alpha, beta);
-    }
-  } else {
-    if (beta != 0.0)
-      acc += 2.0 * atan(alpha / beta);
-    else if (alpha > 0.0)
-      acc += kPi;
-    else if (alpha < 0.0)
-      acc -= kPi;
-  }
+  // (a dead face is dropped by _prepare_exact; the carry still advanced)
+  exact_f64_term(R, ax, ay, az, bx, by, bz, cx, cy, cz, na, nb, nc, qx, qy, qz, eps, use_atan2,
+                 acc, hit);
 }
 
 template <class Src>
