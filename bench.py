@@ -62,11 +62,12 @@ PINNED = {"exact_fwd": 63, "exact_bwd": 170, "soft_fwd": 15, "soft_bwd": 72}
 KERNELS = {
     ("f32", "fwd", True): "fwd_f32_kernel<ExactStripPol,RowSrc>",
     ("f32", "fwd", False): "fwd_f32_kernel<ExactPol,RowSrc>",
-    ("f32", "bwd", True): "bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>",
-    ("f32", "bwd", False): "bwd_f32_kernel<ExactEdgeBwd,RowSrc>",
+    ("f32", "bwd", "trails"): "bwd_f32_kernel<ExactEdgeBwdTrail,RowSrc>",
+    ("f32", "bwd", "pairs"): "bwd_f32_kernel<ExactEdgeBwdPair,RowSrc>",
+    ("f32", "bwd", "faces"): "bwd_f32_kernel<ExactEdgeBwd,RowSrc>",
     ("f64", "fwd", True): "fwd_f64_strip_kernel<GridSrc>",
     ("f64", "fwd", False): "fwd_f64_kernel<ExactF64Pol,GridSrc>",
-    ("f64", "bwd", False): "bwd_f64_kernel<ExactBwd64,GridSrc>",
+    ("f64", "bwd", "faces"): "bwd_f64_kernel<ExactBwd64,GridSrc>",
 }
 
 
@@ -513,9 +514,10 @@ def run_ours(args):
 
     F = w.n_faces
     active = int(dmesh.exact_grad_setup()[0].shape[0])
-    fwd_strip, bwd_pairs = device.lattice_paths(dmesh, "exact", prec, grid, n0, cnt)
+    fwd_strip, _ = device.lattice_paths(dmesh, "exact", prec, grid, n0, cnt)
+    bpath = device.backward_path(dmesh, "exact", prec, grid, n0, cnt)
     kf = KERNELS[(prec, "fwd", fwd_strip)]
-    kb = KERNELS[(prec, "bwd", bwd_pairs)]
+    kb = KERNELS[(prec, "bwd", bpath)]
 
     meas = measured_peaks() if rank == 0 else {}
     for _ in range(args.warmup):
@@ -648,7 +650,7 @@ def run_ours(args):
             "voxelize_ms": fwd_ms,
             "loss": float(loss),
             "cuda_graph": use_graph,
-            "paths": {"forward": kf, "backward": kb,
+            "paths": {"forward": kf, "backward": kb, "backward_records": bpath,
                       "shared_corner_fraction": dmesh.shared_corner_fraction(),
                       "strip_restart_fraction": dmesh.strip_restart_fraction()},
             "roofline": dom,

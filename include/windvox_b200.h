@@ -212,6 +212,35 @@ int wv_exact_pair_bwd_points_f32(const void *packed, int64_t n_faces, const floa
                                  int64_t count, const float *coefs, double coef_scale,
                                  double *face_grad, void *workspace, size_t workspace_bytes,
                                  void *stream);
+/* exact f32 over EDGE TRAILS (same gradients, one evaluation per distinct
+ * edge; lattice rows only):
+ * wv_edge_trails (HOST memory, CPU): welds vertices by bitwise-equal
+ *   position, nets each vertex id's signed edge terms over its live faces
+ *   (dead: NULL or n_faces flags of faces the reference drops, winding.py:
+ *   262-264), drops edges whose net weights all vanish, and covers the rest
+ *   with trails (Hierholzer) cut into windows of three consecutive edges:
+ *   windows (capacity 12 n_faces int64) = 4 vertex ids per window (one per
+ *   position p0..p3), csr_off (n_verts + 1), csr_slots (capacity 6 n_faces)
+ *   = signed output slots per vertex id (6 w + 2 e + end, or -slot-1 to
+ *   subtract).  Sizes written to *n_windows, *n_slots.  vrep (NULL or
+ *   n_verts): the representative vertex id of each vertex's position.
+ * wv_pack_exact_trail: the window records (wv_packed_bytes(
+ *   WV_PACK_EXACTGRAD_F32, n_windows) bytes).
+ * wv_exact_trail_bwd_grid_f32: out (n_windows, 6, 3) doubles = the two end
+ *   vectors of each window edge; row-aligned lattice ranges only (res_z >= 16
+ *   and even, n0 even), else WV_ERR_ARG.  wv_face_to_vertex with the trail
+ *   CSR turns them into vertex gradients (replaces the reference's FD-only
+ *   exact gradient, grad.py:9-12; equal to wv_exact_bwd_* + gather). */
+int wv_edge_trails(const double *vertices, int64_t n_verts, const int64_t *faces,
+                   int64_t n_faces, const uint8_t *dead, int64_t *windows, int64_t *n_windows,
+                   int64_t *csr_off, int64_t *csr_slots, int64_t *n_slots, int64_t *vrep);
+int wv_pack_exact_trail(const void *vertices, int vert_f64, int64_t n_verts,
+                        const int64_t *windows, int64_t n_windows, void *packed, void *stream);
+size_t wv_exact_trail_bwd_workspace_bytes(int64_t n_windows, int64_t count);
+int wv_exact_trail_bwd_grid_f32(const void *packed, int64_t n_windows, wv_grid_t grid,
+                                int64_t n0, int64_t count, const float *coefs,
+                                double coef_scale, double *out, void *workspace,
+                                size_t workspace_bytes, void *stream);
 int wv_soft_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float *coefs, double coef_scale,
                          double *face_grad, void *workspace, size_t workspace_bytes,
@@ -240,7 +269,7 @@ int wv_soft_bwd_points_f64(const void *packed, int64_t n_faces, const double *po
 /* Vertex gradients from face-corner sums, in CSR order (deterministic):
  *   out[v] (+)= scale * sum_{e in [off[v], off[v+1])} face_grad[slots[e]]
  * slots[e] = 3*f + k for every corner k of face f incident to v, sorted by v
- * (stable).  `scale` is a DEVICE pointer (NULL = 1).  out64 / out32 may each
+ * (stable); a negative entry -s-1 SUBTRACTS slot s (edge-trail CSRs).  `scale` is a DEVICE pointer (NULL = 1).  out64 / out32 may each
  * be NULL.  Replaces the chunk-ordered buffer merge of grad.py:113-127. */
 int wv_face_to_vertex(const double *face_grad, const int64_t *csr_offsets,
                       const int64_t *csr_slots, int64_t n_verts, const double *scale,

@@ -29,8 +29,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I", str(CSRC), "-I", str(INCLUDE)]
 # files whose f64 arithmetic must not be FMA-contracted
 # host code that runs on all cores (parallel sorts of the strip builder)
-OPENMP = {"wv_strip.cu"}
-NO_FMAD = {"wv_pack.cu", "wv_f64.cu", "wv_mc.cu", "wv_metrics.cu", "wv_strip.cu"}
+OPENMP = {"wv_strip.cu", "wv_trail.cu"}
+NO_FMAD = {"wv_pack.cu", "wv_f64.cu", "wv_mc.cu", "wv_metrics.cu", "wv_strip.cu", "wv_trail.cu"}
 
 
 def _nvcc() -> str:

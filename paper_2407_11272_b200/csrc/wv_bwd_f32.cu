@@ -24,6 +24,7 @@
 //   corners, so they are accumulated once per face.
 // fp32 partials (per chunk or per run) are folded into fp64 accumulators.
 #include <cmath>
+#include <type_traits>
 
 #include "wv_f32x2.cuh"
 #include "wv_kernels.h"
@@ -832,6 +833,238 @@ struct ExactEdgeBwdPair {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Exact backward over edge TRAILS (wv_trail.cu): one thread owns a window of
+// three consecutive edges of a trail through the position-welded edge graph,
+// p0 -> p1 -> p2 -> p3.  Every distinct edge of the mesh is evaluated once
+// (closed surface: 1.5 per face, strip pairs 2.5) and each position's
+// distance serves both window edges at it: per point pair 4 MUFU.RSQ
+// (distances and their reciprocals) + 1 MUFU.RCP (the three denominators
+// share it) and ~40 FP32 lane-ops for 3 edges = 2 faces' worth, against 56 +
+// 6 MUFU for a strip pair.  The terms are those of ExactEdgeBwd (edge form,
+// row running sums, moments m = a_P x e formed once per row run in fp64);
+// the kernel writes the 2 end vectors of each window edge (18 doubles per
+// window) and the signed CSR gather (face_to_vertex_kernel) gives every
+// vertex id its terms with the signs of its faces' edge directions.
+
+// One ill-conditioned (window, point) pair in FP64 (ExactEdgeBwd's
+// exact_pair_f64 for the window's three edges): acc[6e + 3 end + axis].
+__device__ __noinline__ void trail_pair_f64(const ExactGradRecF32& R, double qx, double qy,
+                                            double qz, double c, double (*acc)[kBwdThreads]) {
+  if (c == 0.0) return;
+  const float4 p4[4] = {R.a, R.b, R.c, R.u};
+  double P[4][3], len[4];
+  for (int k = 0; k < 4; ++k) {
+    P[k][0] = (double)p4[k].x - qx;
+    P[k][1] = (double)p4[k].y - qy;
+    P[k][2] = (double)p4[k].z - qz;
+    len[k] = sqrt(P[k][0] * P[k][0] + P[k][1] * P[k][1] + P[k][2] * P[k][2]);
+  }
+  const int t = threadIdx.x;
+  for (int e = 0; e < 3; ++e) {
+    const double* A = P[e];
+    const double* B = P[e + 1];
+    const double m[3] = {A[1] * B[2] - A[2] * B[1], A[2] * B[0] - A[0] * B[2],
+                         A[0] * B[1] - A[1] * B[0]};
+    const double L = len[e] * len[e + 1], ab = A[0] * B[0] + A[1] * B[1] + A[2] * B[2];
+    const double mm = m[0] * m[0] + m[1] * m[1] + m[2] * m[2];
+    const double den = (L - ab) > 0.0 ? mm / (L - ab) : L + ab;  // |a||b| + a.b
+    if (!(den > 0.0) || !(len[e] > 0.0) || !(len[e + 1] > 0.0)) continue;  // on the edge
+    const double f = c / (2.0 * den);
+    for (int x = 0; x < 3; ++x) {
+      acc[6 * e + x][t] += m[x] * (f / len[e]);
+      acc[6 * e + 3 + x][t] += m[x] * (f / len[e + 1]);
+    }
+  }
+}
+
+struct ExactEdgeBwdTrail {
+  static constexpr bool kPrefetch = true;
+  using Rec = ExactGradRecF32;  // a, b, c, u = p0..p3; a.w, b.w, c.w = |e0|^2, |e1|^2, |e2|^2
+  static constexpr int kFaces = 1;
+  static constexpr int kOut = 18;  // (edge, end, axis)
+  static constexpr bool kScaled = true;
+  static constexpr bool kPairRuns = false;
+#ifndef WV_TRAIL_STEP
+#define WV_TRAIL_STEP 4
+#endif
+#ifndef WV_TRAIL_MINB
+#define WV_TRAIL_MINB 4
+#endif
+  static constexpr int kRowStep = WV_TRAIL_STEP;
+  static constexpr int kMinBlocks = WV_TRAIL_MINB;
+  static constexpr double kCoefScale = ExactEdgeBwd::kCoefScale;
+  static constexpr int kAcc = 18;
+  static constexpr int kRowAcc = 12;  // per edge: sum t/|P|, t a_z/|P|, t/|Q|, t a_z/|Q|
+  static constexpr float kIllRatio = ExactEdgeBwd::kIllRatio;
+  __device__ __forceinline__ static void scale(Rec& R, float s) {
+    const float s2 = s * s;
+    R.a.x *= s; R.a.y *= s; R.a.z *= s; R.a.w *= s2;
+    R.b.x *= s; R.b.y *= s; R.b.z *= s; R.b.w *= s2;
+    R.c.x *= s; R.c.y *= s; R.c.z *= s; R.c.w *= s2;
+    R.u.x *= s; R.u.y *= s; R.u.z *= s;
+  }
+  __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
+  struct Row {
+    float a2[4];  // x/y parts of |p_k - q|^2
+    float qx, qy;
+  };
+  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+    Row w;
+    const float4 p[4] = {R.a, R.b, R.c, R.u};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float dx = p[k].x - qx, dy = p[k].y - qy;
+      w.a2[k] = fmaf(dy, dy, dx * dx);
+    }
+    w.qx = qx;
+    w.qy = qy;
+    return w;
+  }
+  // Ill-conditioning screen, per EDGE: a pair is ill when some window edge
+  // has d_e <= |e|^2 / kIllRatio (fp32 keeps ~1e-7 kIllRatio relative
+  // accuracy above that), or d_e is NaN.  (ExactEdgeBwd screens the PRODUCT
+  // of its face's three ratios, sound there because the other two edges of
+  // a triangle bound their ratios from below for a point near one edge; a
+  // window's third edge can be a whole edge length away, so the trail
+  // screen keeps each edge's own minimum of d_e over the run -- NaN-
+  // propagating mins on the ALU pipe.)
+  struct Screen {
+    F2 d[3];
+  };
+  __device__ __forceinline__ static Screen screen_init() {
+    const F2 inf = f2s(__int_as_float(0x7f800000));
+    return Screen{{inf, inf, inf}};
+  }
+  // one point pair (packed f32x2).  kMask = false: the hot path, the edge
+  // denominators go to dd[3] for the run's screen; kMask = true: ill lanes
+  // leave the fp32 sums (bits returned, trail_pair_f64 adds them)
+  template <bool kMask>
+  __device__ __forceinline__ static uint32_t pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
+                                                       F2* z, F2* dd = nullptr) {
+    const F2 az0 = sub2(f2s(R.a.z), qz), az1 = sub2(f2s(R.b.z), qz);
+    const F2 az2 = sub2(f2s(R.c.z), qz), az3 = sub2(f2s(R.u.z), qz);
+    const F2 s0 = fma2(az0, az0, f2s(w.a2[0])), s1 = fma2(az1, az1, f2s(w.a2[1]));
+    const F2 s2 = fma2(az2, az2, f2s(w.a2[2])), s3 = fma2(az3, az3, f2s(w.a2[3]));
+    const F2 i0 = rsqrt2(s0), i1 = rsqrt2(s1), i2 = rsqrt2(s2), i3 = rsqrt2(s3);
+    const F2 l0 = mul2(s0, i0), l1 = mul2(s1, i1), l2 = mul2(s2, i2), l3 = mul2(s3, i3);
+    // 2 (|a||b| + a.b) = (|a| + |b|)^2 - |e|^2 per edge
+    const F2 e0 = add2(l0, l1), e1 = add2(l1, l2), e2 = add2(l2, l3);
+    const F2 d0 = fma2(e0, e0, f2s(-R.a.w));
+    const F2 d1 = fma2(e1, e1, f2s(-R.b.w));
+    const F2 d2 = fma2(e2, e2, f2s(-R.c.w));
+    const F2 p12 = mul2(d1, d2);
+    const F2 rr = rcp2_abs(mul2(d0, p12));
+    bool ill0 = false, ill1 = false;
+    F2 cr;
+    if constexpr (kMask) {
+      const float k0 = R.a.w * (1.0f / kIllRatio), k1 = R.b.w * (1.0f / kIllRatio);
+      const float k2 = R.c.w * (1.0f / kIllRatio);
+      float a0, a1, b0, b1, c0, c1;
+      split(d0, a0, a1);
+      split(d1, b0, b1);
+      split(d2, c0, c1);
+      ill0 = !(a0 > k0) || !(b0 > k1) || !(c0 > k2);
+      ill1 = !(a1 > k0) || !(b1 > k1) || !(c1 > k2);
+      float r0, r1;
+      split(mul2(coef, rr), r0, r1);
+      cr = f2(ill0 ? 0.0f : r0, ill1 ? 0.0f : r1);
+    } else {
+      dd[0] = d0;
+      dd[1] = d1;
+      dd[2] = d2;
+      cr = mul2(coef, rr);
+    }
+    const F2 q0 = mul2(cr, d0);
+    const F2 t0 = mul2(cr, p12), t1 = mul2(q0, d2), t2 = mul2(q0, d1);  // coef / d_e
+    const F2 u0 = mul2(t0, az0), u1 = mul2(t1, az1), u2 = mul2(t2, az2);
+    z[0] = fma2(t0, i0, z[0]);
+    z[1] = fma2(u0, i0, z[1]);
+    z[2] = fma2(t0, i1, z[2]);
+    z[3] = fma2(u0, i1, z[3]);
+    z[4] = fma2(t1, i1, z[4]);
+    z[5] = fma2(u1, i1, z[5]);
+    z[6] = fma2(t1, i2, z[6]);
+    z[7] = fma2(u1, i2, z[7]);
+    z[8] = fma2(t2, i2, z[8]);
+    z[9] = fma2(u2, i2, z[9]);
+    z[10] = fma2(t2, i3, z[10]);
+    z[11] = fma2(u2, i3, z[11]);
+    return (ill0 ? 1u : 0u) | (ill1 ? 2u : 0u);
+  }
+  template <bool kUnit, int N>
+  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
+                                                  float, F2* z, Screen* mr) {
+    // the step's own minima first (short chains), then one min into the run's
+    F2 m[3];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      F2 dd[3];
+      pair_row2<false>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), z, dd);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) m[e] = u == 0 ? dd[e] : minnan2(m[e], dd[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 3; ++e) mr->d[e] = minnan2(mr->d[e], m[e]);
+  }
+  __device__ __forceinline__ static bool ill_run(const Rec& R, const Screen& mr) {
+    const float k[3] = {R.a.w * (1.0f / kIllRatio), R.b.w * (1.0f / kIllRatio),
+                        R.c.w * (1.0f / kIllRatio)};
+    bool ill = false;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      float lo, hi;
+      split(mr.d[e], lo, hi);
+      ill |= !(minnan(lo, hi) > k[e]);
+    }
+    return ill;
+  }
+  template <bool kUnit>
+  __device__ __noinline__ static void redo_run(const Rec& R, const Row& w, const float4* zcs,
+                                               int j, int e, float, F2* z,
+                                               double (*acc)[kBwdThreads]) {
+    for (int i = 0; i < kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
+    for (; j < e; ++j) {
+      const float4 zc = zcs[j];
+      if (zc.z == 0.0f && zc.w == 0.0f) continue;
+      const uint32_t ill = pair_row2<true>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), z);
+      if (ill & 1u) trail_pair_f64(R, w.qx, w.qy, zc.x, zc.z, acc);
+      if (ill & 2u) trail_pair_f64(R, w.qx, w.qy, zc.y, zc.w, acc);
+    }
+  }
+  // the run's sums -> sum_q m s per (edge, end) into the fp64 accumulators
+  // (m = a_P x e: x/y affine in a_z of the edge's first position, z constant)
+  __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
+                                                   double (*acc)[kBwdThreads]) {
+    double S[kRowAcc];
+#pragma unroll
+    for (int j = 0; j < kRowAcc; ++j) {
+      float lo, hi;
+      split(z[j], lo, hi);
+      S[j] = (double)lo + (double)hi;
+    }
+    const float4 p[4] = {R.a, R.b, R.c, R.u};
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      const float ax = p[e].x - w.qx, ay = p[e].y - w.qy;
+      const float ex = p[e + 1].x - p[e].x, ey = p[e + 1].y - p[e].y, ez = p[e + 1].z - p[e].z;
+      const float kx = ay * ez, ky = -(ax * ez), mz = fmaf(ax, ey, -(ay * ex));
+      const double dex = (double)ex, dey = (double)ey;
+      const double* s = S + 4 * e;
+      acc[6 * e + 0][t] += kx * s[0] - dey * s[1];
+      acc[6 * e + 1][t] += ky * s[0] + dex * s[1];
+      acc[6 * e + 2][t] += mz * s[0];
+      acc[6 * e + 3][t] += kx * s[2] - dey * s[3];
+      acc[6 * e + 4][t] += ky * s[2] + dex * s[3];
+      acc[6 * e + 5][t] += mz * s[2];
+    }
+  }
+  __device__ __forceinline__ static void finish(const Rec&, const double* acc, double* out) {
+    for (int j = 0; j < kOut; ++j) out[j] = acc[j];
+  }
+};
+
 // Query points of a chunk, stored as packed PAIRS: xy[j] = {x_2j, x_2j+1,
 // y_2j, y_2j+1}, zc[j] = {z_2j, z_2j+1, coef_2j, coef_2j+1}; two LDS.128
 // deliver one point pair already in f32x2 register pairs.
@@ -864,6 +1097,19 @@ __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const Poi
 // Row mode: the chunk is cut at k-row boundaries (warp-uniform), each run of
 // pairs shares the row's x/y, and the per-face row constants are computed
 // once per run.  Needs rz and the range start even (pairs never straddle).
+// the row loop's screen state: Pol::Screen when the policy defines one, else
+// one F2 (a running max, 0 = clean)
+template <class Pol, class = void>
+struct ScreenOf {
+  using T = F2;
+  __device__ __forceinline__ static F2 init() { return f2(0.0f, 0.0f); }
+};
+template <class Pol>
+struct ScreenOf<Pol, std::void_t<typename Pol::Screen>> {
+  using T = typename Pol::Screen;
+  __device__ __forceinline__ static T init() { return Pol::screen_init(); }
+};
+
 template <class Pol, bool kUnit>
 __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const PointChunk& ch,
                                            int n_pairs, int64_t flat0, int64_t rz, float eps2,
@@ -879,7 +1125,8 @@ __device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const Poi
 #pragma unroll
     for (int i = 0; i < Pol::kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
     const int e = j + run, j0 = j;
-    F2 mr = f2(0.0f, 0.0f);  // running max of the ill-conditioning screen (exact only)
+    // running state of the ill-conditioning screen (exact only)
+    typename ScreenOf<Pol>::T mr = ScreenOf<Pol>::init();
     // Pol::kRowStep point pairs per step under one (warp-uniform)
     // zero-coefficient test, so their dependency chains share a basic block
     // and interleave (a zero-coefficient pair next to a live one adds
@@ -1218,6 +1465,49 @@ size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_
   return BwdPlan::make(n_faces / 2, n_count, num_sms, ExactEdgeBwdPair::kMinBlocks)
       .workspace(n_faces / 2, 1, ExactEdgeBwdPair::kOut);
 }
+// edge trails (ExactEdgeBwdTrail): lattice rows only (the trail records are
+// chosen for row-aligned lattice ranges); out = (n_windows, 18) doubles
+int launch_exact_trail_bwd_f32(const void* packed, int64_t n_windows, const PointSource& ps,
+                               int64_t n_count, const float* coefs, double coef_scale,
+                               double* out, void* workspace, size_t ws_bytes, int num_sms,
+                               cudaStream_t stream) {
+  using Pol = ExactEdgeBwdTrail;
+  if (n_windows <= 0) return kOk;
+  if (n_count <= 0)
+    return cudaMemsetAsync(out, 0, (size_t)n_windows * Pol::kOut * sizeof(double), stream) ==
+                   cudaSuccess ? kOk : kErrCuda;
+  if (!(ps.kind == PointSource::kGrid && ps.grid.res[2] >= 16 &&
+        row_aligned(ps.grid, ps.n0, 2 * ((n_count + 1) / 2), 2)))
+    return kErrArg;
+  const PackHeader* hdr = static_cast<const PackHeader*>(packed);
+  const auto* recs = reinterpret_cast<const Pol::Rec*>(hdr + 1);
+  const BwdPlan pl = BwdPlan::make(n_windows, n_count, num_sms, Pol::kMinBlocks);
+  double* dst = out;
+  if (pl.splits > 1) {
+    if (workspace == nullptr || ws_bytes < pl.workspace(n_windows, 1, Pol::kOut))
+      return kErrWorkspace;
+    dst = static_cast<double*>(workspace);
+  }
+  const float cs = (float)(coef_scale * Pol::kCoefScale);
+  dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits, 1u);
+  RowSrc src{{ps.grid, ps.n0}};
+  bwd_f32_kernel<Pol, RowSrc><<<grid, kBwdThreads, 0, stream>>>(
+      hdr, recs, 0, n_windows, src, coefs, n_count, pl.pts_per_split, cs, dst,
+      grid_scale(ps.grid));
+  wv::note_launch();
+  if (pl.splits > 1) {
+    const int64_t n = n_windows * Pol::kOut;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > num_sms * 8) blocks = num_sms * 8;
+    reduce_splits_kernel<<<blocks, 256, 0, stream>>>(dst, pl.splits, n, 1, out);
+    wv::note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+size_t exact_trail_bwd_workspace_bytes(int64_t n_windows, int64_t n_count, int num_sms) {
+  return BwdPlan::make(n_windows, n_count, num_sms, ExactEdgeBwdTrail::kMinBlocks)
+      .workspace(n_windows, 1, ExactEdgeBwdTrail::kOut);
+}
 size_t bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms, int64_t batch) {
   // the larger of the two single-face plans (exact and soft occupancies differ)
   const size_t a =
@@ -1246,10 +1536,20 @@ __global__ void face_to_vertex_kernel(const double* __restrict__ face_grad,
        v += (int64_t)gridDim.x * blockDim.x) {
     double gx = 0.0, gy = 0.0, gz = 0.0;
     for (int64_t e = off[v]; e < off[v + 1]; ++e) {
-      const double* src = face_grad + slots[e] * 3;  // slot = f*3 + corner
-      gx += src[0];
-      gy += src[1];
-      gz += src[2];
+      // slot = f*3 + corner (faces) or 6 w + 2 e + end (edge trails); a
+      // negative entry -s-1 subtracts slot s (a trail edge walked against
+      // the face's direction)
+      const int64_t s = slots[e];
+      const double* src = face_grad + (s >= 0 ? s : -s - 1) * 3;
+      if (s >= 0) {
+        gx += src[0];
+        gy += src[1];
+        gz += src[2];
+      } else {
+        gx -= src[0];
+        gy -= src[1];
+        gz -= src[2];
+      }
     }
     if (scale) {
       const double s = *scale;

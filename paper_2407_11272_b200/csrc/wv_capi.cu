@@ -333,6 +333,42 @@ int wv_exact_pair_bwd_points_f32(const void* packed, int64_t n_faces, const floa
                                        sm_count(), as_stream(stream));
 }
 
+int wv_edge_trails(const double* vertices, int64_t n_verts, const int64_t* faces,
+                   int64_t n_faces, const uint8_t* dead, int64_t* windows, int64_t* n_windows,
+                   int64_t* csr_off, int64_t* csr_slots, int64_t* n_slots, int64_t* vrep) {
+  if (n_verts < 0 || n_faces < 0 || n_windows == nullptr || n_slots == nullptr ||
+      csr_off == nullptr || (n_verts > 0 && vertices == nullptr) ||
+      (n_faces > 0 && (faces == nullptr || windows == nullptr || csr_slots == nullptr)))
+    return WV_ERR_ARG;
+  for (int64_t i = 0; i < 3 * n_faces; ++i)
+    if (faces[i] < 0 || faces[i] >= n_verts) return WV_ERR_ARG;
+  return wv::edge_trails(vertices, n_verts, faces, n_faces, dead, windows, n_windows, csr_off,
+                         csr_slots, n_slots, vrep);
+}
+int wv_pack_exact_trail(const void* vertices, int vert_f64, int64_t n_verts,
+                        const int64_t* windows, int64_t n_windows, void* packed, void* stream) {
+  if (packed == nullptr || n_verts < 0 || n_windows < 0 ||
+      (n_windows > 0 && (windows == nullptr || vertices == nullptr)))
+    return WV_ERR_ARG;
+  return wv::launch_pack_trail(vertices, vert_f64, n_verts, windows, n_windows, packed,
+                               as_stream(stream));
+}
+size_t wv_exact_trail_bwd_workspace_bytes(int64_t n_windows, int64_t count) {
+  return n_windows > 0 && count > 0
+             ? wv::exact_trail_bwd_workspace_bytes(n_windows, count, sm_count())
+             : 0;
+}
+int wv_exact_trail_bwd_grid_f32(const void* packed, int64_t n_windows, wv_grid_t grid,
+                                int64_t n0, int64_t count, const float* coefs,
+                                double coef_scale, double* out, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (!bwd_args_ok(packed, coefs, out, n_windows, count) || !grid_ok(grid, n0, count))
+    return WV_ERR_ARG;
+  return wv::launch_exact_trail_bwd_f32(packed, n_windows, grid_src(grid, n0), count, coefs,
+                                        coef_scale, out, workspace, workspace_bytes, sm_count(),
+                                        as_stream(stream));
+}
+
 int wv_soft_bwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float* coefs, double coef_scale,
                          double* face_grad, void* workspace, size_t workspace_bytes,

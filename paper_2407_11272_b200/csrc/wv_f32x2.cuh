@@ -89,6 +89,19 @@ __device__ __forceinline__ float maxnan(float a, float b) {
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
   return r;
 }
+// NaN-propagating min (min.NaN.f32, ALU pipe): the trail backward's per-edge
+// screen keeps the run's smallest edge denominator (a NaN poisons the run)
+__device__ __forceinline__ float minnan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ F2 minnan2(F2 a, F2 b) {
+  float al, ah, bl, bh;
+  split(a, al, ah);
+  split(b, bl, bh);
+  return f2(minnan(al, bl), minnan(ah, bh));
+}
 __device__ __forceinline__ F2 maxnan2(F2 a, F2 b) {
   float al, ah, bl, bh;
   split(a, al, ah);

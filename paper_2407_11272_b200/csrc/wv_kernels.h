@@ -184,6 +184,18 @@ int launch_exact_pair_bwd_f32(const void* packed, int64_t n_faces, const PointSo
                               cudaStream_t stream);
 size_t exact_strip_fwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
 size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms);
+// edge trails (wv_trail.cu builds and packs, wv_bwd_f32.cu runs)
+int64_t weld_positions(const double* verts, int64_t n_verts, int64_t* canon);
+int edge_trails(const double* verts, int64_t n_verts, const int64_t* faces, int64_t n_faces,
+                const uint8_t* dead, int64_t* windows, int64_t* n_windows, int64_t* csr_off,
+                int64_t* csr_slots, int64_t* n_slots, int64_t* vrep);
+int launch_pack_trail(const void* verts, int vert_f64, int64_t n_verts, const int64_t* windows,
+                      int64_t n_windows, void* packed, cudaStream_t stream);
+int launch_exact_trail_bwd_f32(const void* packed, int64_t n_windows, const PointSource& ps,
+                               int64_t n_count, const float* coefs, double coef_scale,
+                               double* out, void* workspace, size_t ws_bytes, int num_sms,
+                               cudaStream_t stream);
+size_t exact_trail_bwd_workspace_bytes(int64_t n_windows, int64_t n_count, int num_sms);
 // strip-ordered exact forward (wv_strip.cu builds and packs, wv_fwd_f32.cu runs)
 int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int64_t n_faces,
                 int64_t* perm, int64_t* win, uint8_t* flags);

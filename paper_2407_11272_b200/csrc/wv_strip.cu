@@ -28,6 +28,39 @@
 
 namespace wv {
 
+// Canonical position id per vertex (bitwise-equal f64 coordinates weld):
+// ids are dense, in ascending order of the coordinate bit patterns; returns
+// the number of distinct positions.  Total orders on both sides, so the
+// parallel sort's result is independent of the thread count.
+int64_t weld_positions(const double* verts, int64_t n_verts, int64_t* canon) {
+  struct VK {
+    uint64_t x, y, z;
+    int64_t i;
+  };
+  std::vector<VK> ord((size_t)n_verts);
+  for (int64_t i = 0; i < n_verts; ++i) {
+    VK& o = ord[(size_t)i];
+    std::memcpy(&o.x, verts + 3 * i, 8);
+    std::memcpy(&o.y, verts + 3 * i + 1, 8);
+    std::memcpy(&o.z, verts + 3 * i + 2, 8);
+    o.i = i;
+  }
+  __gnu_parallel::sort(ord.begin(), ord.end(), [](const VK& a, const VK& b) {
+    if (a.x != b.x) return a.x < b.x;
+    if (a.y != b.y) return a.y < b.y;
+    if (a.z != b.z) return a.z < b.z;
+    return a.i < b.i;
+  });
+  int64_t id = -1;
+  for (size_t r = 0; r < ord.size(); ++r) {
+    if (r == 0 || ord[r].x != ord[r - 1].x || ord[r].y != ord[r - 1].y ||
+        ord[r].z != ord[r - 1].z)
+      ++id;
+    canon[ord[r].i] = id;
+  }
+  return id + 1;
+}
+
 // perm[k]: face of strip position k; win[3k..3k+2]: its vertex indices in
 // window order; flags[k]: bit0 restart, bit1 reflected window.
 // Sort-based (no hash maps): ~20 ms per 100k faces on one core.
@@ -35,35 +68,7 @@ int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int6
                 int64_t* perm, int64_t* win, uint8_t* flags) {
   // canonical position id per vertex: sort by the coordinate bit patterns
   std::vector<int64_t> canon((size_t)n_verts);
-  {
-    struct VK {
-      uint64_t x, y, z;
-      int64_t i;
-    };
-    std::vector<VK> ord((size_t)n_verts);
-    for (int64_t i = 0; i < n_verts; ++i) {
-      VK& o = ord[(size_t)i];
-      std::memcpy(&o.x, verts + 3 * i, 8);
-      std::memcpy(&o.y, verts + 3 * i + 1, 8);
-      std::memcpy(&o.z, verts + 3 * i + 2, 8);
-      o.i = i;
-    }
-    // both comparators are total orders (ties broken by index), so the
-    // parallel sort's result does not depend on the thread count
-    __gnu_parallel::sort(ord.begin(), ord.end(), [](const VK& a, const VK& b) {
-      if (a.x != b.x) return a.x < b.x;
-      if (a.y != b.y) return a.y < b.y;
-      if (a.z != b.z) return a.z < b.z;
-      return a.i < b.i;
-    });
-    int64_t id = -1;
-    for (size_t r = 0; r < ord.size(); ++r) {
-      if (r == 0 || ord[r].x != ord[r - 1].x || ord[r].y != ord[r - 1].y ||
-          ord[r].z != ord[r - 1].z)
-        ++id;
-      canon[(size_t)ord[r].i] = id;
-    }
-  }
+  weld_positions(verts, n_verts, canon.data());
   auto cid = [&](int64_t f, int c) { return canon[(size_t)faces[3 * f + c]]; };
   // half-edges (canonical undirected key, face, local edge) sorted by key;
   // run[3f+e] = start of the run of face f's edge e (corners e, e+1)

@@ -51,6 +51,28 @@ def strip_order(vertices: np.ndarray, faces: np.ndarray):
     return perm, win, fl
 
 
+def edge_trails(vertices: np.ndarray, faces: np.ndarray, dead: np.ndarray | None = None):
+    """Edge trails of a mesh for the exact backward (wv_edge_trails, host code:
+    no GPU needed): (windows (W,4) int64 vertex ids, CSR offsets (V+1,),
+    signed CSR slots (S,), representative vertex id per vertex (V,)) -- see
+    include/windvox_b200.h and csrc/wv_trail.cu."""
+    import ctypes
+    v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+    f = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
+    F, V = len(f), len(v)
+    win = np.empty((max(1, 3 * F), 4), dtype=np.int64)
+    off = np.empty(V + 1, dtype=np.int64)
+    slots = np.empty(max(1, 6 * F), dtype=np.int64)
+    vrep = np.empty(max(1, V), dtype=np.int64)
+    d = None if dead is None else np.ascontiguousarray(dead, dtype=np.uint8).reshape(-1)
+    nw, ns = ctypes.c_int64(0), ctypes.c_int64(0)
+    L.check(L.load_library().wv_edge_trails(
+        v.ctypes.data, V, f.ctypes.data, F, None if d is None else d.ctypes.data,
+        win.ctypes.data, ctypes.addressof(nw), off.ctypes.data, slots.ctypes.data,
+        ctypes.addressof(ns), vrep.ctypes.data), "wv_edge_trails")
+    return win[:nw.value].copy(), off, slots[:ns.value].copy(), vrep[:V].copy()
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -247,6 +269,16 @@ class DeviceMesh:
         cached setups are rebuilt from the new positions."""
         self.vertices = vertices.contiguous()
         self._packs.clear()
+        tr = getattr(self, "_exact_trail", None)
+        if tr is not None:
+            # the trail records evaluate every vertex of a welded position at
+            # its representative's coordinates: rebuild when a move splits a weld
+            ids, reps = tr[3]
+            if ids.numel():
+                v32 = self.vertices.detach().float()
+                if not torch.equal(v32[ids], v32[reps]):
+                    self._verts_np = self.vertices.detach().double().cpu().numpy()
+                    self._exact_trail = None
         dead0 = getattr(self, "_dead_dev", None)
         if dead0 is not None:
             dead = _dead_faces_dev(self.vertices, self.faces)
@@ -254,6 +286,7 @@ class DeviceMesh:
                 self._verts_np = self.vertices.detach().double().cpu().numpy()
                 self._exact_grad = None
                 self._exact_pair = None
+                self._exact_trail = None
                 self._dead_dev = None
 
     def packed(self, kind: int) -> torch.Tensor:
@@ -436,6 +469,60 @@ class DeviceMesh:
         self._packs[key] = buf
         return buf
 
+    def trails_pay(self) -> bool:
+        """Whether the edge-trail backward beats the face kernels: corner
+        positions must be shared (a closed surface, welded or a soup); a
+        random soup of independent triangles has nothing to share."""
+        tp = getattr(self, "_trails_pay", None)
+        if tp is None:
+            tp = self.num_faces > 0 and self.shared_corner_fraction() >= 0.5
+            self._trails_pay = tp
+        return tp
+
+    def exact_trail_setup(self):
+        """Edge trails for the exact f32 backward (wv_exact_trail_bwd_*):
+        (windows (W,4) int64 dev, CSR (off, signed slots) dev, W, (ids, reps)
+        dev: vertices that share a representative's position).  Built from
+        the positions at setup time; ``set_vertices`` rebuilds it when a move
+        splits a weld."""
+        ts = getattr(self, "_exact_trail", None)
+        if ts is None:
+            vnp = getattr(self, "_verts_np", None)
+            if vnp is None:
+                vnp = self.vertices.detach().double().cpu().numpy()
+            fnp = self.faces_np()
+            dead = dead_faces(vnp, fnp)
+            self._dead_dev = torch.from_numpy(dead).to(self.vertices.device)
+            win, off, slots, vrep = edge_trails(vnp, fnp, dead)
+            dev = self.vertices.device
+            ids = np.flatnonzero(vrep != np.arange(len(vrep))).astype(np.int64)
+            ts = (torch.from_numpy(win).to(dev),
+                  (torch.from_numpy(off).to(dev), torch.from_numpy(slots).to(dev)),
+                  len(win),
+                  (torch.from_numpy(ids).to(dev), torch.from_numpy(vrep[ids]).to(dev)))
+            self._exact_trail = ts
+        return ts
+
+    def packed_exact_trail(self) -> torch.Tensor:
+        key = "exact_trail_f32"
+        ver = (id(self.vertices), self.vertices._version)
+        if ver != self._version:
+            self._packs.clear()
+            self._version = ver
+        buf = self._packs.get(key)
+        if buf is not None:
+            return buf
+        win, _, W, _ = self.exact_trail_setup()
+        lib = L.lib()
+        v = self.vertices.contiguous()
+        buf = torch.empty(int(lib.wv_packed_bytes(L.PACK_EXACTGRAD_F32, W)), dtype=torch.uint8,
+                          device=v.device)
+        L.check(lib.wv_pack_exact_trail(_ptr(v), int(v.dtype == torch.float64), self.num_vertices,
+                                        _ptr(win), W, _ptr(buf), _stream()),
+                "wv_pack_exact_trail")
+        self._packs[key] = buf
+        return buf
+
     def packed_exact_grad(self, precision: str) -> torch.Tensor:
         kind = _EXACTGRAD[precision]
         ver = (id(self.vertices), self.vertices._version)
@@ -484,6 +571,19 @@ def lattice_paths(mesh: DeviceMesh, mode: str, precision: str, grid, n0: int, co
     else:
         fwd = mesh.strips_pay()
     return fwd, precision == "f32" and mesh.strips_pay()
+
+
+def backward_path(mesh: DeviceMesh, mode: str, precision: str, grid, n0: int, count: int) -> str:
+    """The records face_grad's automatic choice takes for a lattice range:
+    "trails", "pairs", "faces" (exact) or "soft"."""
+    if mode != "exact":
+        return "soft"
+    big = precision == "f32" and count >= STRIP_MIN_NODES and mesh.num_faces > 0
+    if big and trail_rows_ok(grid, n0) and mesh.trails_pay():
+        return "trails"
+    if big and mesh.strips_pay():
+        return "pairs"
+    return "faces"
 
 
 def forward(mesh: DeviceMesh, mode: str, precision: str, *, grid=None, n0: int = 0,
@@ -580,13 +680,24 @@ def exact_forward_f32(mesh: DeviceMesh, **kw):
     return forward(mesh, "exact", "f32", **kw)
 
 
+def trail_rows_ok(grid, n0: int) -> bool:
+    """The edge-trail backward runs on lattice rows only: k-rows of >= 16
+    nodes, an even row length and an even range start."""
+    rz = int(grid[2][2])
+    return rz >= 16 and rz % 2 == 0 and int(n0) % 2 == 0
+
+
 def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, *, grid=None,
               n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0,
-              pairs: bool | None = None):
+              pairs: bool | None = None, trails: bool | None = None):
     """Per-face corner gradients sum_p coef_scale*coefs[p]*dW_p/dv, f64.
     Returns (corner_grad (A,3,3), csr) where the rows are all faces (soft) or
-    the active faces of the exact edge form (exact); feed both to
-    ``vertex_grad``.  Exact mode expects coefs == 0 at flagged points."""
+    the active faces of the exact edge form (exact) -- or, for the edge-trail
+    backward, the (2W,3,3) end vectors of the trail windows' edges with a
+    signed CSR; feed both to ``vertex_grad``.  Exact mode expects coefs == 0
+    at flagged points.  ``trails`` / ``pairs``: force (True) or forbid (False)
+    those records; None = automatic (large row-aligned lattice ranges of a
+    mesh whose corner positions are shared take the trails)."""
     _check_precision(precision)
     lib = L.lib()
     dev = mesh.vertices.device
@@ -595,10 +706,18 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
         n_pts = int(torch.as_tensor(points).reshape(-1, 3).shape[0])
     else:
         n_pts = _grid_count(grid, n0, count)
+    exact32 = mode == "exact" and precision == "f32"
+    if trails is None:
+        trails = (exact32 and pairs is None and points is None and n_pts >= STRIP_MIN_NODES
+                  and trail_rows_ok(grid, n0) and mesh.trails_pay())
+    if trails:
+        if not exact32 or points is not None or not trail_rows_ok(grid, n0):
+            raise ValueError("edge trails exist for the exact f32 backward on lattice rows only")
+        return _trail_grad(mesh, coefs, grid, n0, n_pts, coef_scale)
     if pairs is None:
-        pairs = (mode == "exact" and precision == "f32" and n_pts >= STRIP_MIN_NODES
-                 and mesh.num_faces > 0 and mesh.strips_pay())
-    if pairs and not (mode == "exact" and precision == "f32"):
+        pairs = (exact32 and n_pts >= STRIP_MIN_NODES and mesh.num_faces > 0
+                 and mesh.strips_pay())
+    if pairs and not exact32:
         raise ValueError("strip pairs exist for the exact f32 backward only")
     if pairs:
         kind = None
@@ -644,6 +763,27 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
         rc = fn(_ptr(packed), F, L.make_grid(*grid), int(n0), count, _ptr(cf), float(coef_scale),
                 _ptr(out), _ptr(ws), wsb, st)
     L.check(rc, name)
+    return out, csr
+
+
+def _trail_grad(mesh: DeviceMesh, coefs: torch.Tensor, grid, n0: int, count: int,
+                coef_scale: float):
+    """face_grad over edge trails: (end vectors (2W,3,3) f64, signed CSR)."""
+    lib = L.lib()
+    dev = mesh.vertices.device
+    packed = mesh.packed_exact_trail()
+    _, csr, W, _ = mesh.exact_trail_setup()
+    cf = coefs.to(device=dev, dtype=torch.float32).contiguous().reshape(-1)
+    if cf.numel() != count:
+        raise ValueError(f"coefs has {cf.numel()} entries for {count} query points")
+    out = torch.empty((2 * W, 3, 3), dtype=torch.float64, device=dev)
+    if W == 0:
+        return out, csr
+    wsb = int(lib.wv_exact_trail_bwd_workspace_bytes(W, count))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
+    L.check(lib.wv_exact_trail_bwd_grid_f32(_ptr(packed), W, L.make_grid(*grid), int(n0), count,
+                                            _ptr(cf), float(coef_scale), _ptr(out), _ptr(ws),
+                                            wsb, _stream()), "wv_exact_trail_bwd_grid_f32")
     return out, csr
 
 

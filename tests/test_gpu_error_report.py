@@ -1,6 +1,6 @@
 """Accuracy report of the FP32 hot path against the f64 oracle on the
 BASELINE configs, through the lattice kernels the bench runs (strip-ordered
-forward, strip-pair row backward): a seeded set of whole k-rows of each grid is
+forward, edge-trail row backward): a seeded set of whole k-rows of each grid is
 evaluated with grid launches (node range = one row) and compared with the
 oracle on the same f32-rounded nodes.
 
@@ -65,11 +65,12 @@ def test_error_report(cuda_device):
             g = torch.zeros((dm.num_vertices, 3), dtype=torch.float64, device="cuda")
             for i, r in enumerate(rows):
                 cr = torch.from_numpy(c32[i * rz:(i + 1) * rz]).float().cuda()
+                kw = {"pairs": False} if name == "c3r" else {"trails": True}
                 fg = device.face_grad(dm, "exact", "f32", cr, grid=grid, n0=int(r) * rz,
-                                      count=rz, pairs=name != "c3r")
+                                      count=rz, **kw)
                 device.vertex_grad(dm, fg, out=g, accumulate=True)
             gr = orc.exact_grad(v32, w.faces, p32, c32)
-            if int(dm.exact_grad_setup()[0].shape[0]) == 0:
+            if dm.exact_trail_setup()[2] == 0:
                 # closed mesh: the exact gradient is identically zero (every edge
                 # cancels); the oracle's face-wise sum shows its rounding noise
                 rep["exact_grad_abs"] = float(np.abs(g.cpu().numpy()).max())

@@ -99,6 +99,7 @@ def test_c3r_lattice_rows_auto_path(cuda_device):
     dm = device.DeviceMesh.from_numpy(w.vertices, w.faces)
     n0, cnt = 128 * 256 * 256, 32 * 256 * 256       # 2M nodes: the strip threshold
     assert device.lattice_paths(dm, "exact", "f32", grid, n0, cnt) == (False, False)
+    assert device.backward_path(dm, "exact", "f32", grid, n0, cnt) == "faces"
     vals, flags = device.forward(dm, "exact", "f32", grid=grid, n0=n0, count=cnt)
     rows = np.sort(np.random.default_rng(9).choice(cnt // rz, size=8, replace=False))
     idx = (n0 + rows[:, None] * rz + np.arange(rz)[None, :]).reshape(-1)

@@ -207,7 +207,8 @@ def test_random_soup_config_and_path_choice():
     """C3's stress variant: 100k independent equilateral-ish triangles
     (edge 0.04-0.06, centres in [-0.8,0.8]^3) share no corner position, so the
     automatic choice takes the face-ordered kernels; the welded C3 soup takes
-    the strip kernels (host-side decision, no GPU needed)."""
+    the strip forward and the edge-trail backward (host-side decision, no GPU
+    needed)."""
     import torch
     from paper_2407_11272_b200 import configs, device
     w = configs.make("c3r")
@@ -225,3 +226,8 @@ def test_random_soup_config_and_path_choice():
         grid = (w.lo, w.hi, w.res)
         assert device.lattice_paths(m, "exact", "f32", grid, 0, w.n_nodes) == (pay, pay)
         assert device.lattice_paths(m, "exact", "f64", grid, 0, w.n_nodes) == (pay, False)
+        # the exact f32 backward: edge trails where corner positions are shared
+        assert device.backward_path(m, "exact", "f32", grid, 0, w.n_nodes) == \
+            ("trails" if pay else "faces")
+        assert device.backward_path(m, "exact", "f64", grid, 0, w.n_nodes) == "faces"
+        assert device.backward_path(m, "soft", "f32", grid, 0, w.n_nodes) == "soft"

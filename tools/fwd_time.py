@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--config", default="c3r")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--bwd", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "trails", "pairs", "faces"],
+                    help="backward records (--bwd)")
     a = ap.parse_args()
     import torch
     from paper_2407_11272_b200 import configs, device
@@ -31,7 +33,9 @@ def main():
     def run():
         dm.invalidate()
         if a.bwd:
-            device.face_grad(dm, "exact", "f32", coefs, grid=grid)
+            kw = {"auto": {}, "trails": {"trails": True}, "pairs": {"pairs": True},
+                  "faces": {"pairs": False}}[a.path]
+            device.face_grad(dm, "exact", "f32", coefs, grid=grid, **kw)
         else:
             device.forward(dm, "exact", "f32", grid=grid)
 
@@ -46,7 +50,7 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     print(json.dumps({"lib": os.environ.get("WV_LIB_PATH", "default"), "config": a.config,
-                      "bwd": a.bwd, "ms": min(ts), "all": ts}))
+                      "bwd": a.bwd, "path": a.path, "ms": min(ts), "all": ts}))
 
 
 if __name__ == "__main__":
