@@ -48,6 +48,7 @@ extern "C" {
 #define WV_PACK_EXACTGRAD_F64 8
 #define WV_PACK_EXACTSTRIP_F32 9 /* wv_pack_exact_strip: exact f32 records in strip order */
 #define WV_PACK_EXACTSTRIP_F64 10 /* wv_pack_exact_strip_f64: f64 parity records in strip order */
+#define WV_PACK_EXACTTRAIL_F32 11 /* wv_pack_exact_trail: edge-trail windows of the exact backward */
 
 /* stored value for on-surface (flagged) nodes */
 #define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
@@ -218,19 +219,20 @@ int wv_exact_pair_bwd_points_f32(const void *packed, int64_t n_faces, const floa
  *   position, nets each vertex id's signed edge terms over its live faces
  *   (dead: NULL or n_faces flags of faces the reference drops, winding.py:
  *   262-264), drops edges whose net weights all vanish, and covers the rest
- *   with trails (Hierholzer) cut into windows of three consecutive edges:
- *   windows (capacity 12 n_faces int64) = 4 vertex ids per window (one per
- *   position p0..p3), csr_off (n_verts + 1), csr_slots (capacity 6 n_faces)
- *   = signed output slots per vertex id (6 w + 2 e + end, or -slot-1 to
- *   subtract).  Sizes written to *n_windows, *n_slots.  vrep (NULL or
+ *   with trails (Hierholzer) cut into windows of K = wv_trail_edges()
+ *   consecutive edges: windows (capacity 3 n_faces (K+1) int64) = K+1 vertex
+ *   ids per window (one per position p0..pK), csr_off (n_verts + 1),
+ *   csr_slots (capacity 6 n_faces) = signed output slots per vertex id
+ *   (2K w + 2 e + end, or -slot-1 to subtract).  Sizes written to *n_windows, *n_slots.  vrep (NULL or
  *   n_verts): the representative vertex id of each vertex's position.
  * wv_pack_exact_trail: the window records (wv_packed_bytes(
- *   WV_PACK_EXACTGRAD_F32, n_windows) bytes).
- * wv_exact_trail_bwd_grid_f32: out (n_windows, 6, 3) doubles = the two end
+ *   WV_PACK_EXACTTRAIL_F32, n_windows) bytes).
+ * wv_exact_trail_bwd_grid_f32: out (n_windows, 2K, 3) doubles = the two end
  *   vectors of each window edge; row-aligned lattice ranges only (res_z >= 16
  *   and even, n0 even), else WV_ERR_ARG.  wv_face_to_vertex with the trail
  *   CSR turns them into vertex gradients (replaces the reference's FD-only
  *   exact gradient, grad.py:9-12; equal to wv_exact_bwd_* + gather). */
+int wv_trail_edges(void); /* K, the edges per trail window of this build */
 int wv_edge_trails(const double *vertices, int64_t n_verts, const int64_t *faces,
                    int64_t n_faces, const uint8_t *dead, int64_t *windows, int64_t *n_windows,
                    int64_t *csr_off, int64_t *csr_slots, int64_t *n_slots, int64_t *vrep);

@@ -29,6 +29,7 @@ PACK_EXACTGRAD_F32 = 7
 PACK_EXACTGRAD_F64 = 8
 PACK_EXACTSTRIP_F32 = 9
 PACK_EXACTSTRIP_F64 = 10
+PACK_EXACTTRAIL_F32 = 11
 POLICY_RAW = 0
 POLICY_HALF = 1
 
@@ -52,7 +53,7 @@ EXPORTED = (
     "wv_exact_pair_bwd_workspace_bytes", "wv_exact_pair_bwd_grid_f32",
     "wv_exact_pair_bwd_points_f32", "wv_pack_faces_batch", "wv_loss_terms_f32_batch",
     "wv_face_to_vertex_batch", "wv_pack_exact_strip_f64", "wv_exact_strip_fwd_grid_f64",
-    "wv_exact_strip_fwd_points_f64", "wv_edge_trails", "wv_pack_exact_trail",
+    "wv_exact_strip_fwd_points_f64", "wv_trail_edges", "wv_edge_trails", "wv_pack_exact_trail",
     "wv_exact_trail_bwd_workspace_bytes", "wv_exact_trail_bwd_grid_f32",
 )
 
@@ -140,6 +141,7 @@ def _declare(lib):
         "wv_pack_exact_strip_f64": ([P, I, I64, P, I, I64, P, P, P, P, P], I),
         "wv_exact_strip_fwd_grid_f64": ([P, I64, Grid, I64, I64, I, I, P, P, P], I),
         "wv_exact_strip_fwd_points_f64": ([P, I64, P, I64, I, I, P, P, P], I),
+        "wv_trail_edges": ([], I),
         "wv_edge_trails": ([P, I64, P, I64, P, P, P, P, P, P, P], I),
         "wv_pack_exact_trail": ([P, I, I64, P, I64, P, P], I),
         "wv_exact_trail_bwd_workspace_bytes": ([I64, I64], SZ),

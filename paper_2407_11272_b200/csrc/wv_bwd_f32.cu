@@ -835,33 +835,34 @@ struct ExactEdgeBwdPair {
 
 // ---------------------------------------------------------------------------
 // Exact backward over edge TRAILS (wv_trail.cu): one thread owns a window of
-// three consecutive edges of a trail through the position-welded edge graph,
-// p0 -> p1 -> p2 -> p3.  Every distinct edge of the mesh is evaluated once
-// (closed surface: 1.5 per face, strip pairs 2.5) and each position's
-// distance serves both window edges at it: per point pair 4 MUFU.RSQ
-// (distances and their reciprocals) + 1 MUFU.RCP (the three denominators
-// share it) and ~40 FP32 lane-ops for 3 edges = 2 faces' worth, against 56 +
-// 6 MUFU for a strip pair.  The terms are those of ExactEdgeBwd (edge form,
-// row running sums, moments m = a_P x e formed once per row run in fp64);
-// the kernel writes the 2 end vectors of each window edge (18 doubles per
-// window) and the signed CSR gather (face_to_vertex_kernel) gives every
-// vertex id its terms with the signs of its faces' edge directions.
+// K = kTrailK (4) consecutive edges of a trail through the position-welded
+// edge graph, p0 -> p1 -> ... -> pK.  Every distinct edge of the mesh is
+// evaluated once (closed surface: 1.5 per face, strip pairs 2.5) and each
+// position's distance serves both window edges at it: per point pair K+1
+// MUFU.RSQ (distances and their reciprocals) + 1 MUFU.RCP (the K edge
+// denominators share it) and ~13 FP32 lane-ops per edge, i.e. per face of a
+// closed surface ~19.5 lane-ops + 2.25 MUFU (strip pairs: 28 + 3).  The
+// terms are those of ExactEdgeBwd (edge form, row running sums, moments
+// m = a_P x e formed once per row run in fp64); the kernel writes the 2 end
+// vectors of each window edge (6K doubles per window) and the signed CSR
+// gather (face_to_vertex_kernel) gives every vertex id its terms with the
+// signs of its faces' edge directions.
 
 // One ill-conditioned (window, point) pair in FP64 (ExactEdgeBwd's
-// exact_pair_f64 for the window's three edges): acc[6e + 3 end + axis].
-__device__ __noinline__ void trail_pair_f64(const ExactGradRecF32& R, double qx, double qy,
+// exact_pair_f64 for the window's edges): acc[6e + 3 end + axis].
+__device__ __noinline__ void trail_pair_f64(const TrailRecF32& R, double qx, double qy,
                                             double qz, double c, double (*acc)[kBwdThreads]) {
+  constexpr int K = kTrailK;
   if (c == 0.0) return;
-  const float4 p4[4] = {R.a, R.b, R.c, R.u};
-  double P[4][3], len[4];
-  for (int k = 0; k < 4; ++k) {
-    P[k][0] = (double)p4[k].x - qx;
-    P[k][1] = (double)p4[k].y - qy;
-    P[k][2] = (double)p4[k].z - qz;
+  double P[K + 1][3], len[K + 1];
+  for (int k = 0; k <= K; ++k) {
+    P[k][0] = (double)R.p[k].x - qx;
+    P[k][1] = (double)R.p[k].y - qy;
+    P[k][2] = (double)R.p[k].z - qz;
     len[k] = sqrt(P[k][0] * P[k][0] + P[k][1] * P[k][1] + P[k][2] * P[k][2]);
   }
   const int t = threadIdx.x;
-  for (int e = 0; e < 3; ++e) {
+  for (int e = 0; e < K; ++e) {
     const double* A = P[e];
     const double* B = P[e + 1];
     const double m[3] = {A[1] * B[2] - A[2] * B[1], A[2] * B[0] - A[0] * B[2],
@@ -879,14 +880,15 @@ __device__ __noinline__ void trail_pair_f64(const ExactGradRecF32& R, double qx,
 }
 
 struct ExactEdgeBwdTrail {
+  static constexpr int K = kTrailK;
   static constexpr bool kPrefetch = true;
-  using Rec = ExactGradRecF32;  // a, b, c, u = p0..p3; a.w, b.w, c.w = |e0|^2, |e1|^2, |e2|^2
+  using Rec = TrailRecF32;
   static constexpr int kFaces = 1;
-  static constexpr int kOut = 18;  // (edge, end, axis)
+  static constexpr int kOut = 6 * K;  // (edge, end, axis)
   static constexpr bool kScaled = true;
   static constexpr bool kPairRuns = false;
 #ifndef WV_TRAIL_STEP
-#define WV_TRAIL_STEP 4
+#define WV_TRAIL_STEP 2  // C3: 1249 ms (2) vs 1275 (4), 1252 (6, 3 CTAs/SM), 1282 (K = 3, step 4)
 #endif
 #ifndef WV_TRAIL_MINB
 #define WV_TRAIL_MINB 4
@@ -894,27 +896,29 @@ struct ExactEdgeBwdTrail {
   static constexpr int kRowStep = WV_TRAIL_STEP;
   static constexpr int kMinBlocks = WV_TRAIL_MINB;
   static constexpr double kCoefScale = ExactEdgeBwd::kCoefScale;
-  static constexpr int kAcc = 18;
-  static constexpr int kRowAcc = 12;  // per edge: sum t/|P|, t a_z/|P|, t/|Q|, t a_z/|Q|
+  static constexpr int kAcc = 6 * K;
+  static constexpr int kRowAcc = 4 * K;  // per edge: sum t/|P|, t a_z/|P|, t/|Q|, t a_z/|Q|
   static constexpr float kIllRatio = ExactEdgeBwd::kIllRatio;
   __device__ __forceinline__ static void scale(Rec& R, float s) {
     const float s2 = s * s;
-    R.a.x *= s; R.a.y *= s; R.a.z *= s; R.a.w *= s2;
-    R.b.x *= s; R.b.y *= s; R.b.z *= s; R.b.w *= s2;
-    R.c.x *= s; R.c.y *= s; R.c.z *= s; R.c.w *= s2;
-    R.u.x *= s; R.u.y *= s; R.u.z *= s;
+#pragma unroll
+    for (int k = 0; k <= K; ++k) {
+      R.p[k].x *= s;
+      R.p[k].y *= s;
+      R.p[k].z *= s;
+      R.p[k].w *= s2;
+    }
   }
   __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
   struct Row {
-    float a2[4];  // x/y parts of |p_k - q|^2
+    float a2[K + 1];  // x/y parts of |p_k - q|^2
     float qx, qy;
   };
   __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
     Row w;
-    const float4 p[4] = {R.a, R.b, R.c, R.u};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float dx = p[k].x - qx, dy = p[k].y - qy;
+    for (int k = 0; k <= K; ++k) {
+      const float dx = R.p[k].x - qx, dy = R.p[k].y - qy;
       w.a2[k] = fmaf(dy, dy, dx * dx);
     }
     w.qx = qx;
@@ -926,96 +930,113 @@ struct ExactEdgeBwdTrail {
   // accuracy above that), or d_e is NaN.  (ExactEdgeBwd screens the PRODUCT
   // of its face's three ratios, sound there because the other two edges of
   // a triangle bound their ratios from below for a point near one edge; a
-  // window's third edge can be a whole edge length away, so the trail
+  // window's far edges can be several edge lengths away, so the trail
   // screen keeps each edge's own minimum of d_e over the run -- NaN-
   // propagating mins on the ALU pipe.)
   struct Screen {
-    F2 d[3];
+    F2 d[K];
   };
   __device__ __forceinline__ static Screen screen_init() {
-    const F2 inf = f2s(__int_as_float(0x7f800000));
-    return Screen{{inf, inf, inf}};
+    Screen s;
+#pragma unroll
+    for (int e = 0; e < K; ++e) s.d[e] = f2s(__int_as_float(0x7f800000));
+    return s;
   }
   // one point pair (packed f32x2).  kMask = false: the hot path, the edge
-  // denominators go to dd[3] for the run's screen; kMask = true: ill lanes
+  // denominators go to dd[K] for the run's screen; kMask = true: ill lanes
   // leave the fp32 sums (bits returned, trail_pair_f64 adds them)
   template <bool kMask>
   __device__ __forceinline__ static uint32_t pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
                                                        F2* z, F2* dd = nullptr) {
-    const F2 az0 = sub2(f2s(R.a.z), qz), az1 = sub2(f2s(R.b.z), qz);
-    const F2 az2 = sub2(f2s(R.c.z), qz), az3 = sub2(f2s(R.u.z), qz);
-    const F2 s0 = fma2(az0, az0, f2s(w.a2[0])), s1 = fma2(az1, az1, f2s(w.a2[1]));
-    const F2 s2 = fma2(az2, az2, f2s(w.a2[2])), s3 = fma2(az3, az3, f2s(w.a2[3]));
-    const F2 i0 = rsqrt2(s0), i1 = rsqrt2(s1), i2 = rsqrt2(s2), i3 = rsqrt2(s3);
-    const F2 l0 = mul2(s0, i0), l1 = mul2(s1, i1), l2 = mul2(s2, i2), l3 = mul2(s3, i3);
+    F2 az[K + 1], ip[K + 1], lp[K + 1];
+#pragma unroll
+    for (int k = 0; k <= K; ++k) {
+      az[k] = sub2(f2s(R.p[k].z), qz);
+      const F2 s2 = fma2(az[k], az[k], f2s(w.a2[k]));
+      ip[k] = rsqrt2(s2);
+      lp[k] = mul2(s2, ip[k]);
+    }
     // 2 (|a||b| + a.b) = (|a| + |b|)^2 - |e|^2 per edge
-    const F2 e0 = add2(l0, l1), e1 = add2(l1, l2), e2 = add2(l2, l3);
-    const F2 d0 = fma2(e0, e0, f2s(-R.a.w));
-    const F2 d1 = fma2(e1, e1, f2s(-R.b.w));
-    const F2 d2 = fma2(e2, e2, f2s(-R.c.w));
-    const F2 p12 = mul2(d1, d2);
-    const F2 rr = rcp2_abs(mul2(d0, p12));
+    F2 d[K];
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const F2 se = add2(lp[e], lp[e + 1]);
+      d[e] = fma2(se, se, f2s(-R.p[e].w));
+    }
+    // one reciprocal for the K denominators
+    F2 t[K];
+    F2 rr, cr;
+    F2 p01, p23;
+    if constexpr (K == 3) {
+      p23 = mul2(d[1], d[2]);
+      rr = rcp2_abs(mul2(d[0], p23));
+    } else {
+      p01 = mul2(d[0], d[1]);
+      p23 = mul2(d[2], d[3]);
+      rr = rcp2_abs(mul2(p01, p23));
+    }
     bool ill0 = false, ill1 = false;
-    F2 cr;
     if constexpr (kMask) {
-      const float k0 = R.a.w * (1.0f / kIllRatio), k1 = R.b.w * (1.0f / kIllRatio);
-      const float k2 = R.c.w * (1.0f / kIllRatio);
-      float a0, a1, b0, b1, c0, c1;
-      split(d0, a0, a1);
-      split(d1, b0, b1);
-      split(d2, c0, c1);
-      ill0 = !(a0 > k0) || !(b0 > k1) || !(c0 > k2);
-      ill1 = !(a1 > k0) || !(b1 > k1) || !(c1 > k2);
+#pragma unroll
+      for (int e = 0; e < K; ++e) {
+        const float k = R.p[e].w * (1.0f / kIllRatio);
+        float lo, hi;
+        split(d[e], lo, hi);
+        ill0 |= !(lo > k);
+        ill1 |= !(hi > k);
+      }
       float r0, r1;
       split(mul2(coef, rr), r0, r1);
       cr = f2(ill0 ? 0.0f : r0, ill1 ? 0.0f : r1);
     } else {
-      dd[0] = d0;
-      dd[1] = d1;
-      dd[2] = d2;
+#pragma unroll
+      for (int e = 0; e < K; ++e) dd[e] = d[e];
       cr = mul2(coef, rr);
     }
-    const F2 q0 = mul2(cr, d0);
-    const F2 t0 = mul2(cr, p12), t1 = mul2(q0, d2), t2 = mul2(q0, d1);  // coef / d_e
-    const F2 u0 = mul2(t0, az0), u1 = mul2(t1, az1), u2 = mul2(t2, az2);
-    z[0] = fma2(t0, i0, z[0]);
-    z[1] = fma2(u0, i0, z[1]);
-    z[2] = fma2(t0, i1, z[2]);
-    z[3] = fma2(u0, i1, z[3]);
-    z[4] = fma2(t1, i1, z[4]);
-    z[5] = fma2(u1, i1, z[5]);
-    z[6] = fma2(t1, i2, z[6]);
-    z[7] = fma2(u1, i2, z[7]);
-    z[8] = fma2(t2, i2, z[8]);
-    z[9] = fma2(u2, i2, z[9]);
-    z[10] = fma2(t2, i3, z[10]);
-    z[11] = fma2(u2, i3, z[11]);
+    if constexpr (K == 3) {
+      const F2 q0 = mul2(cr, d[0]);
+      t[0] = mul2(cr, p23);
+      t[1] = mul2(q0, d[2]);
+      t[2] = mul2(q0, d[1]);
+    } else {
+      const F2 c01 = mul2(cr, p23), c23 = mul2(cr, p01);
+      t[0] = mul2(c01, d[1]);
+      t[1] = mul2(c01, d[0]);
+      t[2] = mul2(c23, d[3]);
+      t[3] = mul2(c23, d[2]);
+    }
+#pragma unroll
+    for (int e = 0; e < K; ++e) {  // t_e = coef / d_e
+      const F2 u = mul2(t[e], az[e]);
+      z[4 * e + 0] = fma2(t[e], ip[e], z[4 * e + 0]);
+      z[4 * e + 1] = fma2(u, ip[e], z[4 * e + 1]);
+      z[4 * e + 2] = fma2(t[e], ip[e + 1], z[4 * e + 2]);
+      z[4 * e + 3] = fma2(u, ip[e + 1], z[4 * e + 3]);
+    }
     return (ill0 ? 1u : 0u) | (ill1 ? 2u : 0u);
   }
   template <bool kUnit, int N>
   __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
                                                   float, F2* z, Screen* mr) {
     // the step's own minima first (short chains), then one min into the run's
-    F2 m[3];
+    F2 m[K];
 #pragma unroll
     for (int u = 0; u < N; ++u) {
-      F2 dd[3];
+      F2 dd[K];
       pair_row2<false>(R, w, f2(zc[u].x, zc[u].y), f2(zc[u].z, zc[u].w), z, dd);
 #pragma unroll
-      for (int e = 0; e < 3; ++e) m[e] = u == 0 ? dd[e] : minnan2(m[e], dd[e]);
+      for (int e = 0; e < K; ++e) m[e] = u == 0 ? dd[e] : minnan2(m[e], dd[e]);
     }
 #pragma unroll
-    for (int e = 0; e < 3; ++e) mr->d[e] = minnan2(mr->d[e], m[e]);
+    for (int e = 0; e < K; ++e) mr->d[e] = minnan2(mr->d[e], m[e]);
   }
   __device__ __forceinline__ static bool ill_run(const Rec& R, const Screen& mr) {
-    const float k[3] = {R.a.w * (1.0f / kIllRatio), R.b.w * (1.0f / kIllRatio),
-                        R.c.w * (1.0f / kIllRatio)};
     bool ill = false;
 #pragma unroll
-    for (int e = 0; e < 3; ++e) {
+    for (int e = 0; e < K; ++e) {
       float lo, hi;
       split(mr.d[e], lo, hi);
-      ill |= !(minnan(lo, hi) > k[e]);
+      ill |= !(minnan(lo, hi) > R.p[e].w * (1.0f / kIllRatio));
     }
     return ill;
   }
@@ -1036,22 +1057,21 @@ struct ExactEdgeBwdTrail {
   // (m = a_P x e: x/y affine in a_z of the edge's first position, z constant)
   __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
                                                    double (*acc)[kBwdThreads]) {
-    double S[kRowAcc];
-#pragma unroll
-    for (int j = 0; j < kRowAcc; ++j) {
-      float lo, hi;
-      split(z[j], lo, hi);
-      S[j] = (double)lo + (double)hi;
-    }
-    const float4 p[4] = {R.a, R.b, R.c, R.u};
     const int t = threadIdx.x;
 #pragma unroll
-    for (int e = 0; e < 3; ++e) {
-      const float ax = p[e].x - w.qx, ay = p[e].y - w.qy;
-      const float ex = p[e + 1].x - p[e].x, ey = p[e + 1].y - p[e].y, ez = p[e + 1].z - p[e].z;
+    for (int e = 0; e < K; ++e) {
+      double s[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float lo, hi;
+        split(z[4 * e + j], lo, hi);
+        s[j] = (double)lo + (double)hi;
+      }
+      const float4 P = R.p[e], Q = R.p[e + 1];
+      const float ax = P.x - w.qx, ay = P.y - w.qy;
+      const float ex = Q.x - P.x, ey = Q.y - P.y, ez = Q.z - P.z;
       const float kx = ay * ez, ky = -(ax * ez), mz = fmaf(ax, ey, -(ay * ex));
       const double dex = (double)ex, dey = (double)ey;
-      const double* s = S + 4 * e;
       acc[6 * e + 0][t] += kx * s[0] - dey * s[1];
       acc[6 * e + 1][t] += ky * s[0] + dex * s[1];
       acc[6 * e + 2][t] += mz * s[0];
@@ -1466,7 +1486,7 @@ size_t exact_pair_bwd_workspace_bytes(int64_t n_faces, int64_t n_count, int num_
       .workspace(n_faces / 2, 1, ExactEdgeBwdPair::kOut);
 }
 // edge trails (ExactEdgeBwdTrail): lattice rows only (the trail records are
-// chosen for row-aligned lattice ranges); out = (n_windows, 18) doubles
+// chosen for row-aligned lattice ranges); out = (n_windows, 2K, 3) doubles
 int launch_exact_trail_bwd_f32(const void* packed, int64_t n_windows, const PointSource& ps,
                                int64_t n_count, const float* coefs, double coef_scale,
                                double* out, void* workspace, size_t ws_bytes, int num_sms,

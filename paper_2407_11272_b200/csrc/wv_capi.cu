@@ -333,6 +333,7 @@ int wv_exact_pair_bwd_points_f32(const void* packed, int64_t n_faces, const floa
                                        sm_count(), as_stream(stream));
 }
 
+int wv_trail_edges(void) { return wv::kTrailK; }
 int wv_edge_trails(const double* vertices, int64_t n_verts, const int64_t* faces,
                    int64_t n_faces, const uint8_t* dead, int64_t* windows, int64_t* n_windows,
                    int64_t* csr_off, int64_t* csr_slots, int64_t* n_slots, int64_t* vrep) {

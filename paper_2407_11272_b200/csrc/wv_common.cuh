@@ -90,6 +90,18 @@ struct __align__(16) ExactGradRecF32 {
 };
 static_assert(sizeof(ExactGradRecF32) == 64, "record size");
 
+// Edge-trail window (wv_trail.cu): K consecutive edges of a trail through
+// the position-welded edge graph, positions p[0..K] (f32-rounded mesh),
+// p[e].w = |p[e+1] - p[e]|^2 (from f64) for e < K, p[K].w = 0.
+#ifndef WV_TRAIL_K
+#define WV_TRAIL_K 4
+#endif
+constexpr int kTrailK = WV_TRAIL_K;
+static_assert(kTrailK == 3 || kTrailK == 4, "trail windows of 3 or 4 edges");
+struct __align__(16) TrailRecF32 {
+  float4 p[kTrailK + 1];
+};
+
 struct __align__(16) ExactGradRecF64 {
   double v[9];
   double w[3];

@@ -17,15 +17,15 @@
 // drops cancelled face edges).  The remaining edges form a multigraph-free
 // graph over positions; Hierholzer's algorithm covers it with trails
 // (p0, p1, p2, ...), consecutive edges sharing a position.  A trail is cut
-// into WINDOWS of three consecutive edges (four positions): one thread of the
-// trail backward owns a window and evaluates 4 corner distances, 3 edge
-// denominators and ONE shared reciprocal per query point, i.e. 2 distances
-// and 1.5 denominators per face of a closed surface (strip pairs: 2 and 2.5).
-// A short last window repeats its own edges (their slots are never read).
+// into WINDOWS of K = kTrailK (4) consecutive edges (K+1 positions): one thread
+// of the trail backward owns a window and evaluates K+1 corner distances, K
+// edge denominators and ONE shared reciprocal per query point, i.e. 1.875
+// distances and 1.5 denominators per face of a closed surface (strip pairs:
+// 2 and 2.5).  A short last window repeats its own edges (never read).
 //
-// Outputs: windows (W x 4 vertex ids, one representative id per position),
-// and a CSR from vertex id to SIGNED slots of the kernel's output
-// (slot = 6 w + 2 e + end, end 0 = the window edge's first position; a
+// Outputs: windows (W x (K+1) vertex ids, one representative id per
+// position), and a CSR from vertex id to SIGNED slots of the kernel's output
+// (slot = 2K w + 2 e + end, end 0 = the window edge's first position; a
 // negative entry -s-1 subtracts slot s), in a fixed order: the gather is
 // deterministic.
 #include <algorithm>
@@ -150,19 +150,27 @@ int edge_trails(const double* verts, int64_t n_verts, const int64_t* faces, int6
     return (it != ekeys.end() && *it == key) ? (int64_t)(it - ekeys.begin()) : -1;
   };
   // seq: the positions of one trail of real edges
+  constexpr int K = kTrailK;
   auto emit_trail = [&]() {
     const int64_t L = (int64_t)seq.size() - 1;  // edges
-    for (int64_t j = 0; j < L; j += 3) {
-      const int64_t r = L - j < 3 ? L - j : 3;  // real edges of this window
-      // pad a short window with its own edges: (p0 p1 p2 p1), (p0 p1 p0 p1)
-      static const int kPad[4][4] = {{0, 0, 0, 0}, {0, 1, 0, 1}, {0, 1, 2, 1}, {0, 1, 2, 3}};
-      int64_t p[4];
-      for (int i = 0; i < 4; ++i) p[i] = seq[(size_t)(j + kPad[r][i])];
-      for (int i = 0; i < 4; ++i) windows[4 * W + i] = rep[(size_t)p[i]];
+    for (int64_t j = 0; j < L; j += K) {
+      const int64_t r = L - j < K ? L - j : K;  // real edges of this window
+      // pad a short window by walking its own edges back and forth:
+      // (p0 p1 p0 p1 ..), (p0 p1 p2 p1 ..), (p0 p1 p2 p3 p2)
+      int64_t p[K + 1];
+      for (int i = 0; i <= K; ++i) {
+        int k = i;
+        if (k > r) {
+          const int b = (int)(k - r) % (2 * (int)r);
+          k = b <= r ? (int)r - b : b - (int)r;
+        }
+        p[i] = seq[(size_t)(j + k)];
+      }
+      for (int i = 0; i <= K; ++i) windows[(K + 1) * W + i] = rep[(size_t)p[i]];
       for (int i = 0; i < r; ++i) {
         const int64_t e = find_edge(p[i], p[i + 1]);
         if (e < 0 || eslot[(size_t)e] >= 0) return false;
-        eslot[(size_t)e] = 3 * W + i;
+        eslot[(size_t)e] = K * W + i;
         efwd[(size_t)e] = p[i] == e_lo(e) ? 1 : 0;
       }
       ++W;
@@ -227,11 +235,11 @@ int edge_trails(const double* verts, int64_t n_verts, const int64_t* faces, int6
   for (const Ent& x : net) {
     while (ekeys[ei] != x.key) ++ei;
     const int64_t e = (int64_t)ei;
-    const int64_t w = eslot[(size_t)e] / 3, k = eslot[(size_t)e] % 3;
+    const int64_t w = eslot[(size_t)e] / K, k = eslot[(size_t)e] % K;
     // the window evaluates its own direction p_k -> p_k+1 (ends 0, 1); the
     // canonical lo -> hi term is that, or minus the reversed ends
     const bool fwd = efwd[(size_t)e] != 0;
-    const int64_t slot = 6 * w + 2 * k + (fwd ? x.end : 1 - x.end);
+    const int64_t slot = 2 * K * w + 2 * k + (fwd ? x.end : 1 - x.end);
     const int32_t sgn = (x.sign > 0 ? 1 : -1) * (fwd ? 1 : -1);
     for (int r = 0; r < std::abs(x.sign); ++r)
       csr_slots[cnt[(size_t)x.vert]++] = sgn > 0 ? slot : -slot - 1;
@@ -241,25 +249,25 @@ int edge_trails(const double* verts, int64_t n_verts, const int64_t* faces, int6
   return kOk;
 }
 
-// Trail records (ExactGradRecF32 reused): a, b, c, u = the window's positions
-// p0..p3 (the f32-rounded mesh), a.w, b.w, c.w = |p1-p0|^2, |p2-p1|^2,
-// |p3-p2|^2 of the rounded positions (f64, rounded once), u.w = 0.
+// Trail records (TrailRecF32): the window's K+1 positions of the f32-rounded
+// mesh, p[e].w = |p[e+1] - p[e]|^2 of the rounded positions (f64, rounded
+// once), p[K].w = 0.
 template <typename V>
 __global__ void pack_trail_kernel(const V* __restrict__ verts, const int64_t* __restrict__ win,
-                                  int64_t n_windows, ExactGradRecF32* __restrict__ recs) {
+                                  int64_t n_windows, TrailRecF32* __restrict__ recs) {
+  constexpr int K = kTrailK;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_windows;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double p[4][3];
-    for (int k = 0; k < 4; ++k)
-      for (int d = 0; d < 3; ++d) p[k][d] = (double)(float)verts[3 * win[4 * i + k] + d];
-    double U[3] = {0.0, 0.0, 0.0};
-    for (int e = 0; e < 3; ++e)
-      for (int d = 0; d < 3; ++d) U[e] += (p[e + 1][d] - p[e][d]) * (p[e + 1][d] - p[e][d]);
-    ExactGradRecF32& r = recs[i];
-    r.a = make_float4((float)p[0][0], (float)p[0][1], (float)p[0][2], (float)U[0]);
-    r.b = make_float4((float)p[1][0], (float)p[1][1], (float)p[1][2], (float)U[1]);
-    r.c = make_float4((float)p[2][0], (float)p[2][1], (float)p[2][2], (float)U[2]);
-    r.u = make_float4((float)p[3][0], (float)p[3][1], (float)p[3][2], 0.0f);
+    double p[K + 1][3];
+    for (int k = 0; k <= K; ++k)
+      for (int d = 0; d < 3; ++d) p[k][d] = (double)(float)verts[3 * win[(K + 1) * i + k] + d];
+    TrailRecF32& r = recs[i];
+    for (int k = 0; k <= K; ++k) {
+      double U = 0.0;
+      if (k < K)
+        for (int d = 0; d < 3; ++d) U += (p[k + 1][d] - p[k][d]) * (p[k + 1][d] - p[k][d]);
+      r.p[k] = make_float4((float)p[k][0], (float)p[k][1], (float)p[k][2], (float)U);
+    }
   }
 }
 
@@ -270,7 +278,7 @@ int launch_pack_trail(const void* verts, int vert_f64, int64_t n_verts, const in
                                     stream);
   if (rc != kOk) return rc;
   if (n_windows <= 0) return kOk;
-  ExactGradRecF32* recs = reinterpret_cast<ExactGradRecF32*>(hdr + 1);
+  TrailRecF32* recs = reinterpret_cast<TrailRecF32*>(hdr + 1);
   int64_t blocks = (n_windows + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   if (vert_f64)

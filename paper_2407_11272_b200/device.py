@@ -53,20 +53,22 @@ def strip_order(vertices: np.ndarray, faces: np.ndarray):
 
 def edge_trails(vertices: np.ndarray, faces: np.ndarray, dead: np.ndarray | None = None):
     """Edge trails of a mesh for the exact backward (wv_edge_trails, host code:
-    no GPU needed): (windows (W,4) int64 vertex ids, CSR offsets (V+1,),
+    no GPU needed): (windows (W,K+1) int64 vertex ids, CSR offsets (V+1,),
     signed CSR slots (S,), representative vertex id per vertex (V,)) -- see
-    include/windvox_b200.h and csrc/wv_trail.cu."""
+    include/windvox_b200.h and csrc/wv_trail.cu; K = wv_trail_edges()."""
     import ctypes
+    lib = L.load_library()
+    K = int(lib.wv_trail_edges())
     v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
     f = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
     F, V = len(f), len(v)
-    win = np.empty((max(1, 3 * F), 4), dtype=np.int64)
+    win = np.empty((max(1, 3 * F), K + 1), dtype=np.int64)
     off = np.empty(V + 1, dtype=np.int64)
     slots = np.empty(max(1, 6 * F), dtype=np.int64)
     vrep = np.empty(max(1, V), dtype=np.int64)
     d = None if dead is None else np.ascontiguousarray(dead, dtype=np.uint8).reshape(-1)
     nw, ns = ctypes.c_int64(0), ctypes.c_int64(0)
-    L.check(L.load_library().wv_edge_trails(
+    L.check(lib.wv_edge_trails(
         v.ctypes.data, V, f.ctypes.data, F, None if d is None else d.ctypes.data,
         win.ctypes.data, ctypes.addressof(nw), off.ctypes.data, slots.ctypes.data,
         ctypes.addressof(ns), vrep.ctypes.data), "wv_edge_trails")
@@ -481,7 +483,7 @@ class DeviceMesh:
 
     def exact_trail_setup(self):
         """Edge trails for the exact f32 backward (wv_exact_trail_bwd_*):
-        (windows (W,4) int64 dev, CSR (off, signed slots) dev, W, (ids, reps)
+        (windows (W,K+1) int64 dev, CSR (off, signed slots) dev, W, (ids, reps)
         dev: vertices that share a representative's position).  Built from
         the positions at setup time; ``set_vertices`` rebuilds it when a move
         splits a weld."""
@@ -515,7 +517,7 @@ class DeviceMesh:
         win, _, W, _ = self.exact_trail_setup()
         lib = L.lib()
         v = self.vertices.contiguous()
-        buf = torch.empty(int(lib.wv_packed_bytes(L.PACK_EXACTGRAD_F32, W)), dtype=torch.uint8,
+        buf = torch.empty(int(lib.wv_packed_bytes(L.PACK_EXACTTRAIL_F32, W)), dtype=torch.uint8,
                           device=v.device)
         L.check(lib.wv_pack_exact_trail(_ptr(v), int(v.dtype == torch.float64), self.num_vertices,
                                         _ptr(win), W, _ptr(buf), _stream()),
@@ -693,7 +695,7 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     """Per-face corner gradients sum_p coef_scale*coefs[p]*dW_p/dv, f64.
     Returns (corner_grad (A,3,3), csr) where the rows are all faces (soft) or
     the active faces of the exact edge form (exact) -- or, for the edge-trail
-    backward, the (2W,3,3) end vectors of the trail windows' edges with a
+    backward, the (2KW,3) end vectors of the trail windows' edges with a
     signed CSR; feed both to ``vertex_grad``.  Exact mode expects coefs == 0
     at flagged points.  ``trails`` / ``pairs``: force (True) or forbid (False)
     those records; None = automatic (large row-aligned lattice ranges of a
@@ -768,15 +770,15 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
 
 def _trail_grad(mesh: DeviceMesh, coefs: torch.Tensor, grid, n0: int, count: int,
                 coef_scale: float):
-    """face_grad over edge trails: (end vectors (2W,3,3) f64, signed CSR)."""
+    """face_grad over edge trails: (end vectors (2KW,3) f64, signed CSR)."""
     lib = L.lib()
     dev = mesh.vertices.device
     packed = mesh.packed_exact_trail()
-    _, csr, W, _ = mesh.exact_trail_setup()
+    win, csr, W, _ = mesh.exact_trail_setup()
     cf = coefs.to(device=dev, dtype=torch.float32).contiguous().reshape(-1)
     if cf.numel() != count:
         raise ValueError(f"coefs has {cf.numel()} entries for {count} query points")
-    out = torch.empty((2 * W, 3, 3), dtype=torch.float64, device=dev)
+    out = torch.empty((2 * (int(win.shape[1]) - 1) * W, 3), dtype=torch.float64, device=dev)
     if W == 0:
         return out, csr
     wsb = int(lib.wv_exact_trail_bwd_workspace_bytes(W, count))

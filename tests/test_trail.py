@@ -29,9 +29,10 @@ def _trails(v, f, dead=None):
 
 
 def _window_terms(v, win, pts, coefs):
-    """f64 end terms of every window edge: (W, 6, 3), slot 2e + end."""
-    out = np.zeros((len(win), 6, 3))
-    for e in range(3):
+    """f64 end terms of every window edge: (W, 2K, 3), slot 2e + end."""
+    K = win.shape[1] - 1
+    out = np.zeros((len(win), 2 * K, 3))
+    for e in range(K):
         P, Q = v[win[:, e]], v[win[:, e + 1]]
         for q, c in zip(pts, coefs):
             a, b = P - q, Q - q
@@ -74,7 +75,7 @@ def test_trails_gather_to_the_exact_gradient(name):
     dead = np.linalg.norm(np.cross(v[f[:, 1]] - v[f[:, 0]], v[f[:, 2]] - v[f[:, 0]]), axis=1) == 0
     win, off, slots, vrep = _trails(v, f, dead)
     # windows walk edges of the welded graph: consecutive positions differ
-    for e in range(3):
+    for e in range(win.shape[1] - 1):
         assert not np.any(np.all(v[win[:, e]] == v[win[:, e + 1]], axis=1))
     # representatives share their vertex's position
     assert np.array_equal(v[vrep], v)
@@ -93,17 +94,18 @@ def test_trails_gather_to_the_exact_gradient(name):
 
 
 def test_trails_cover_each_live_edge_once():
-    """A closed soup: 1.5 edges per face, each in one window, windows of
-    three edges (the trails of a 6-regular position graph are Euler
-    circuits: few padded windows)."""
+    """A closed soup: 1.5 edges per face, each in one window, windows of K
+    edges (the trails of a 6-regular position graph are Euler circuits: few
+    padded windows)."""
     v, f = configs.soup(*configs.torus(0.7, 0.3, 20, 12), seed=2)
     win, off, slots, _ = _trails(v, f)
+    K = win.shape[1] - 1
     E = 3 * len(f) // 2
-    assert len(win) * 3 >= E and len(win) <= E // 3 + 4
+    assert len(win) * K >= E and len(win) <= E // K + 4
     keys = set()
     pos = {tuple(p): i for i, p in enumerate(np.unique(v, axis=0))}
     for w in win:
-        for e in range(3):
+        for e in range(K):
             a, b = pos[tuple(v[w[e]])], pos[tuple(v[w[e + 1]])]
             keys.add((min(a, b), max(a, b)))
     assert len(keys) == E
@@ -134,7 +136,7 @@ def test_trails_reject_bad_indices():
     lib = L.load_library()
     v = np.zeros((3, 3))
     f = np.array([[0, 1, 3]], dtype=np.int64)
-    win = np.empty((3, 4), np.int64)
+    win = np.empty((3, lib.wv_trail_edges() + 1), np.int64)
     off = np.empty(4, np.int64)
     sl = np.empty(6, np.int64)
     nw, ns = ctypes.c_int64(), ctypes.c_int64()
