@@ -68,6 +68,7 @@ KERNELS = {
     ("f64", "fwd", True): "fwd_f64_strip_kernel<GridSrc>",
     ("f64", "fwd", False): "fwd_f64_kernel<ExactF64Pol,GridSrc>",
     ("f64", "bwd", "faces"): "bwd_f64_kernel<ExactBwd64,GridSrc>",
+    ("f64", "bwd", "trails"): "bwd_f64_kernel<ExactTrail64,GridSrc>",
 }
 
 

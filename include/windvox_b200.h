@@ -49,6 +49,7 @@ extern "C" {
 #define WV_PACK_EXACTSTRIP_F32 9 /* wv_pack_exact_strip: exact f32 records in strip order */
 #define WV_PACK_EXACTSTRIP_F64 10 /* wv_pack_exact_strip_f64: f64 parity records in strip order */
 #define WV_PACK_EXACTTRAIL_F32 11 /* wv_pack_exact_trail: edge-trail windows of the exact backward */
+#define WV_PACK_EXACTTRAIL_F64 12 /* wv_pack_exact_trail_f64: their f64 twin */
 
 /* stored value for on-surface (flagged) nodes */
 #define WV_POLICY_RAW 0  /* keep the partial sum: winding_number_batch, winding.py:271-309 */
@@ -243,6 +244,21 @@ int wv_exact_trail_bwd_grid_f32(const void *packed, int64_t n_windows, wv_grid_t
                                 int64_t n0, int64_t count, const float *coefs,
                                 double coef_scale, double *out, void *workspace,
                                 size_t workspace_bytes, void *stream);
+/* f64 twin (the parity path's exact backward over the same trails, any
+ * lattice range or point list): records of kind WV_PACK_EXACTTRAIL_F64 (the
+ * f64 mesh), same output layout and CSR. */
+int wv_pack_exact_trail_f64(const void *vertices, int vert_f64, int64_t n_verts,
+                            const int64_t *windows, int64_t n_windows, void *packed,
+                            void *stream);
+size_t wv_exact_trail_bwd_workspace_bytes_f64(int64_t n_windows, int64_t count);
+int wv_exact_trail_bwd_grid_f64(const void *packed, int64_t n_windows, wv_grid_t grid,
+                                int64_t n0, int64_t count, const double *coefs,
+                                double coef_scale, double *out, void *workspace,
+                                size_t workspace_bytes, void *stream);
+int wv_exact_trail_bwd_points_f64(const void *packed, int64_t n_windows, const double *points,
+                                  int64_t count, const double *coefs, double coef_scale,
+                                  double *out, void *workspace, size_t workspace_bytes,
+                                  void *stream);
 int wv_soft_bwd_grid_f32(const void *packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float *coefs, double coef_scale,
                          double *face_grad, void *workspace, size_t workspace_bytes,

@@ -30,6 +30,7 @@ PACK_EXACTGRAD_F64 = 8
 PACK_EXACTSTRIP_F32 = 9
 PACK_EXACTSTRIP_F64 = 10
 PACK_EXACTTRAIL_F32 = 11
+PACK_EXACTTRAIL_F64 = 12
 POLICY_RAW = 0
 POLICY_HALF = 1
 
@@ -55,6 +56,8 @@ EXPORTED = (
     "wv_face_to_vertex_batch", "wv_pack_exact_strip_f64", "wv_exact_strip_fwd_grid_f64",
     "wv_exact_strip_fwd_points_f64", "wv_trail_edges", "wv_edge_trails", "wv_pack_exact_trail",
     "wv_exact_trail_bwd_workspace_bytes", "wv_exact_trail_bwd_grid_f32",
+    "wv_pack_exact_trail_f64", "wv_exact_trail_bwd_workspace_bytes_f64",
+    "wv_exact_trail_bwd_grid_f64", "wv_exact_trail_bwd_points_f64",
 )
 
 
@@ -146,6 +149,10 @@ def _declare(lib):
         "wv_pack_exact_trail": ([P, I, I64, P, I64, P, P], I),
         "wv_exact_trail_bwd_workspace_bytes": ([I64, I64], SZ),
         "wv_exact_trail_bwd_grid_f32": (bwd_grid, I),
+        "wv_pack_exact_trail_f64": ([P, I, I64, P, I64, P, P], I),
+        "wv_exact_trail_bwd_workspace_bytes_f64": ([I64, I64], SZ),
+        "wv_exact_trail_bwd_grid_f64": (bwd_grid, I),
+        "wv_exact_trail_bwd_points_f64": (bwd_pts, I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

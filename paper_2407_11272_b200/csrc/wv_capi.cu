@@ -370,6 +370,41 @@ int wv_exact_trail_bwd_grid_f32(const void* packed, int64_t n_windows, wv_grid_t
                                         as_stream(stream));
 }
 
+int wv_pack_exact_trail_f64(const void* vertices, int vert_f64, int64_t n_verts,
+                            const int64_t* windows, int64_t n_windows, void* packed,
+                            void* stream) {
+  if (packed == nullptr || n_verts < 0 || n_windows < 0 ||
+      (n_windows > 0 && (windows == nullptr || vertices == nullptr)))
+    return WV_ERR_ARG;
+  return wv::launch_pack_trail_f64(vertices, vert_f64, n_verts, windows, n_windows, packed,
+                                   as_stream(stream));
+}
+size_t wv_exact_trail_bwd_workspace_bytes_f64(int64_t n_windows, int64_t count) {
+  return n_windows > 0 && count > 0
+             ? wv::exact_trail_bwd64_workspace_bytes(n_windows, count, sm_count())
+             : 0;
+}
+int wv_exact_trail_bwd_grid_f64(const void* packed, int64_t n_windows, wv_grid_t grid,
+                                int64_t n0, int64_t count, const double* coefs,
+                                double coef_scale, double* out, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (!bwd_args_ok(packed, coefs, out, n_windows, count) || !grid_ok(grid, n0, count))
+    return WV_ERR_ARG;
+  return wv::launch_exact_trail_bwd_f64(packed, n_windows, grid_src(grid, n0), count, coefs,
+                                        coef_scale, out, workspace, workspace_bytes,
+                                        sm_count(), as_stream(stream));
+}
+int wv_exact_trail_bwd_points_f64(const void* packed, int64_t n_windows, const double* points,
+                                  int64_t count, const double* coefs, double coef_scale,
+                                  double* out, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (!bwd_args_ok(packed, coefs, out, n_windows, count) || (count > 0 && points == nullptr))
+    return WV_ERR_ARG;
+  return wv::launch_exact_trail_bwd_f64(packed, n_windows, list_src(nullptr, points), count,
+                                        coefs, coef_scale, out, workspace, workspace_bytes,
+                                        sm_count(), as_stream(stream));
+}
+
 int wv_soft_bwd_grid_f32(const void* packed, int64_t n_faces, wv_grid_t grid, int64_t n0,
                          int64_t count, const float* coefs, double coef_scale,
                          double* face_grad, void* workspace, size_t workspace_bytes,

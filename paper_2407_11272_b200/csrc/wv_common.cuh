@@ -102,6 +102,11 @@ struct __align__(16) TrailRecF32 {
   float4 p[kTrailK + 1];
 };
 
+// f64 twin of a trail window (the f64 mesh, no rounding)
+struct __align__(16) TrailRecF64 {
+  double p[kTrailK + 1][4];  // x, y, z, 0
+};
+
 struct __align__(16) ExactGradRecF64 {
   double v[9];
   double w[3];

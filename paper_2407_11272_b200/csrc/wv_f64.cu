@@ -358,6 +358,7 @@ constexpr double kEightPi = 8.0 * kPi;
 
 struct ExactBwd64 {
   using Rec = ExactGradRecF64;
+  static constexpr int kOut = 9;
   // edge (Biot-Savart) form of d(Omega)/dv, see ExactEdgeBwd in wv_bwd_f32.cu;
   // coef carries the -1/(4 pi) factor.  Per pair: the three reciprocal corner
   // lengths once (Newton rsqrt), one Newton reciprocal per edge, no branches.
@@ -400,8 +401,38 @@ struct ExactBwd64 {
     edge(c, a, lc, la, ic, ia, coef * R.w[2], g + 6, g + 0);
   }
 };
+// Edge trails (wv_trail.cu; the f32 kernel is ExactEdgeBwdTrail): one thread
+// per window of K edges p0 -> .. -> pK of the f64 mesh; each position's
+// reciprocal length serves both window edges at it, each distinct edge of
+// the mesh is evaluated once (ExactBwd64::edge), and the signed CSR gather
+// distributes the 2K end vectors to the vertex ids.  Per face of a closed
+// surface: 1.5 edges and ~1.9 lengths instead of 3 and 3.
+struct ExactTrail64 {
+  static constexpr int K = kTrailK;
+  using Rec = TrailRecF64;
+  static constexpr int kOut = 6 * K;
+  __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
+                                              double coef, double, double* g) {
+    double a[K + 1][3], l[K + 1], il[K + 1];
+#pragma unroll
+    for (int k = 0; k <= K; ++k) {
+      a[k][0] = R.p[k][0] - qx;
+      a[k][1] = R.p[k][1] - qy;
+      a[k][2] = R.p[k][2] - qz;
+      const double a2 = fma(a[k][0], a[k][0], fma(a[k][1], a[k][1], a[k][2] * a[k][2]));
+      if (!(a2 > 0.0)) return;  // q on a vertex (flagged; its coefficient is 0)
+      il[k] = rsqrt_nr(a2);
+      l[k] = a2 * il[k];
+    }
+#pragma unroll
+    for (int e = 0; e < K; ++e)
+      ExactBwd64::edge(a[e], a[e + 1], l[e], l[e + 1], il[e], il[e + 1], coef, g + 6 * e,
+                       g + 6 * e + 3);
+  }
+};
 struct SoftBwd64 {
   using Rec = SoftGradRecF64;
+  static constexpr int kOut = 9;
   // _kernels.py:198-232, same expression order per pair
   __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
                                               double coef, double eps, double* g) {
@@ -443,7 +474,9 @@ bwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   const int64_t p_begin = (int64_t)blockIdx.y * pts_per_split;
   int64_t p_end = p_begin + pts_per_split;
   if (p_end > n_count) p_end = n_count;
-  double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double g[Pol::kOut];
+#pragma unroll
+  for (int j = 0; j < Pol::kOut; ++j) g[j] = 0.0;
   for (int64_t c0 = p_begin; c0 < p_end; c0 += kBwd64Chunk) {
     const int n = (int)((p_end - c0) < kBwd64Chunk ? (p_end - c0) : kBwd64Chunk);
     __syncthreads();
@@ -461,8 +494,8 @@ bwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     }
   }
   if (live) {
-    double* dst = out + ((int64_t)blockIdx.y * n_faces + f) * 9;
-    for (int j = 0; j < 9; ++j) dst[j] = g[j];
+    double* dst = out + ((int64_t)blockIdx.y * n_faces + f) * Pol::kOut;
+    for (int j = 0; j < Pol::kOut; ++j) dst[j] = g[j];
   }
 }
 
@@ -491,11 +524,17 @@ static void bwd64_plan(int64_t n_faces, int64_t n_count, int num_sms, int64_t* b
   if (*splits < 1) *splits = 1;
 }
 
-size_t bwd64_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+static size_t bwd64_ws(int64_t n_faces, int64_t n_count, int num_sms, int k_out) {
   int64_t bx, pps;
   int s;
   bwd64_plan(n_faces, n_count, num_sms, &bx, &s, &pps);
-  return s > 1 ? (size_t)s * n_faces * 9 * sizeof(double) : 0;
+  return s > 1 ? (size_t)s * n_faces * k_out * sizeof(double) : 0;
+}
+size_t bwd64_workspace_bytes(int64_t n_faces, int64_t n_count, int num_sms) {
+  return bwd64_ws(n_faces, n_count, num_sms, 9);
+}
+size_t exact_trail_bwd64_workspace_bytes(int64_t n_windows, int64_t n_count, int num_sms) {
+  return bwd64_ws(n_windows, n_count, num_sms, ExactTrail64::kOut);
 }
 
 template <class Pol>
@@ -503,9 +542,10 @@ static int launch_bwd64(const void* packed, int64_t n_faces, const PointSource& 
                         int64_t n_count, const double* coefs, double coef_scale,
                         double* face_grad, void* ws, size_t ws_bytes, int num_sms,
                         cudaStream_t stream) {
+  constexpr int KO = Pol::kOut;
   if (n_faces <= 0) return kOk;
   if (n_count <= 0)
-    return cudaMemsetAsync(face_grad, 0, (size_t)n_faces * 9 * sizeof(double), stream) ==
+    return cudaMemsetAsync(face_grad, 0, (size_t)n_faces * KO * sizeof(double), stream) ==
                    cudaSuccess ? kOk : kErrCuda;
   const PackHeader* hdr = static_cast<const PackHeader*>(packed);
   const auto* recs = reinterpret_cast<const typename Pol::Rec*>(hdr + 1);
@@ -514,7 +554,7 @@ static int launch_bwd64(const void* packed, int64_t n_faces, const PointSource& 
   bwd64_plan(n_faces, n_count, num_sms, &bx, &splits, &pps);
   double* dst = face_grad;
   if (splits > 1) {
-    if (ws == nullptr || ws_bytes < (size_t)splits * n_faces * 9 * sizeof(double))
+    if (ws == nullptr || ws_bytes < (size_t)splits * n_faces * KO * sizeof(double))
       return kErrWorkspace;
     dst = static_cast<double*>(ws);
   }
@@ -531,7 +571,7 @@ static int launch_bwd64(const void* packed, int64_t n_faces, const PointSource& 
                                                                        coef_scale, dst); wv::note_launch(); }
   }
   if (splits > 1) {
-    const int64_t n = n_faces * 9;
+    const int64_t n = n_faces * KO;
     int blocks = (int)((n + 255) / 256);
     if (blocks > num_sms * 8) blocks = num_sms * 8;
     { reduce_splits64_kernel<<<blocks, 256, 0, stream>>>(dst, splits, n, face_grad); wv::note_launch(); }
@@ -546,6 +586,14 @@ int launch_exact_bwd_f64(const void* packed, int64_t n_faces, const PointSource&
   return launch_bwd64<ExactBwd64>(packed, n_faces, ps, n_count, coefs,
                                   coef_scale * (-1.0 / (4.0 * kPi)), face_grad,
                                   ws, ws_bytes, num_sms, stream);
+}
+int launch_exact_trail_bwd_f64(const void* packed, int64_t n_windows, const PointSource& ps,
+                               int64_t n_count, const double* coefs, double coef_scale,
+                               double* out, void* ws, size_t ws_bytes, int num_sms,
+                               cudaStream_t stream) {
+  return launch_bwd64<ExactTrail64>(packed, n_windows, ps, n_count, coefs,
+                                    coef_scale * (-1.0 / (4.0 * kPi)), out, ws, ws_bytes,
+                                    num_sms, stream);
 }
 int launch_soft_bwd_f64(const void* packed, int64_t n_faces, const PointSource& ps,
                         int64_t n_count, const double* coefs, double coef_scale,

@@ -196,6 +196,14 @@ int launch_exact_trail_bwd_f32(const void* packed, int64_t n_windows, const Poin
                                double* out, void* workspace, size_t ws_bytes, int num_sms,
                                cudaStream_t stream);
 size_t exact_trail_bwd_workspace_bytes(int64_t n_windows, int64_t n_count, int num_sms);
+int launch_pack_trail_f64(const void* verts, int vert_f64, int64_t n_verts,
+                          const int64_t* windows, int64_t n_windows, void* packed,
+                          cudaStream_t stream);
+int launch_exact_trail_bwd_f64(const void* packed, int64_t n_windows, const PointSource& ps,
+                               int64_t n_count, const double* coefs, double coef_scale,
+                               double* out, void* ws, size_t ws_bytes, int num_sms,
+                               cudaStream_t stream);
+size_t exact_trail_bwd64_workspace_bytes(int64_t n_windows, int64_t n_count, int num_sms);
 // strip-ordered exact forward (wv_strip.cu builds and packs, wv_fwd_f32.cu runs)
 int strip_order(const double* verts, int64_t n_verts, const int64_t* faces, int64_t n_faces,
                 int64_t* perm, int64_t* win, uint8_t* flags);

@@ -327,6 +327,7 @@ size_t packed_bytes(int kind, int64_t n_faces) {
     case 9: rec = sizeof(ExactRecF32); break;  // strip-ordered exact records (wv_strip.cu)
     case 10: rec = sizeof(ExactRecF64); break;  // strip-ordered f64 parity records
     case 11: rec = sizeof(TrailRecF32); break;  // edge-trail windows (wv_trail.cu)
+    case 12: rec = sizeof(TrailRecF64); break;  // f64 edge-trail windows
     default: return 0;
   }
   return sizeof(PackHeader) + rec * (size_t)(n_faces > 0 ? n_faces : 0);

@@ -271,6 +271,42 @@ __global__ void pack_trail_kernel(const V* __restrict__ verts, const int64_t* __
   }
 }
 
+template <typename V>
+__global__ void pack_trail_f64_kernel(const V* __restrict__ verts,
+                                      const int64_t* __restrict__ win, int64_t n_windows,
+                                      TrailRecF64* __restrict__ recs) {
+  constexpr int K = kTrailK;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_windows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k <= K; ++k) {
+      const int64_t v = win[(K + 1) * i + k];
+      for (int d = 0; d < 3; ++d) recs[i].p[k][d] = (double)verts[3 * v + d];
+      recs[i].p[k][3] = 0.0;
+    }
+  }
+}
+
+int launch_pack_trail_f64(const void* verts, int vert_f64, int64_t n_verts,
+                          const int64_t* windows, int64_t n_windows, void* packed,
+                          cudaStream_t stream) {
+  PackHeader* hdr = static_cast<PackHeader*>(packed);
+  const int rc = launch_surface_eps(verts, vert_f64, n_verts, reinterpret_cast<double*>(hdr),
+                                    stream);
+  if (rc != kOk) return rc;
+  if (n_windows <= 0) return kOk;
+  TrailRecF64* recs = reinterpret_cast<TrailRecF64*>(hdr + 1);
+  int64_t blocks = (n_windows + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (vert_f64)
+    pack_trail_f64_kernel<double><<<(unsigned)blocks, 256, 0, stream>>>(
+        static_cast<const double*>(verts), windows, n_windows, recs);
+  else
+    pack_trail_f64_kernel<float><<<(unsigned)blocks, 256, 0, stream>>>(
+        static_cast<const float*>(verts), windows, n_windows, recs);
+  wv::note_launch();
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrLaunch;
+}
+
 int launch_pack_trail(const void* verts, int vert_f64, int64_t n_verts, const int64_t* windows,
                       int64_t n_windows, void* packed, cudaStream_t stream) {
   PackHeader* hdr = static_cast<PackHeader*>(packed);

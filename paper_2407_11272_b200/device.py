@@ -34,6 +34,10 @@ STRIP_MIN_NODES = 1 << 21
 # this fraction of restarting faces (e.g. a random-triangle soup, where no
 # corner position is shared: 100%) the face-ordered kernels are faster
 STRIP_MAX_RESTART = 0.25
+# the f64 exact backward takes the edge trails (no row alignment needed) from
+# this many query points: the host trail builder (~1 us per face, once per
+# DeviceMesh) against ~2x fewer f64 edge evaluations per point
+TRAIL64_MIN_POINTS = 1 << 16
 
 
 def strip_order(vertices: np.ndarray, faces: np.ndarray):
@@ -505,8 +509,8 @@ class DeviceMesh:
             self._exact_trail = ts
         return ts
 
-    def packed_exact_trail(self) -> torch.Tensor:
-        key = "exact_trail_f32"
+    def packed_exact_trail(self, precision: str = "f32") -> torch.Tensor:
+        key = f"exact_trail_{precision}"
         ver = (id(self.vertices), self.vertices._version)
         if ver != self._version:
             self._packs.clear()
@@ -517,11 +521,11 @@ class DeviceMesh:
         win, _, W, _ = self.exact_trail_setup()
         lib = L.lib()
         v = self.vertices.contiguous()
-        buf = torch.empty(int(lib.wv_packed_bytes(L.PACK_EXACTTRAIL_F32, W)), dtype=torch.uint8,
-                          device=v.device)
-        L.check(lib.wv_pack_exact_trail(_ptr(v), int(v.dtype == torch.float64), self.num_vertices,
-                                        _ptr(win), W, _ptr(buf), _stream()),
-                "wv_pack_exact_trail")
+        kind, fn = ((L.PACK_EXACTTRAIL_F32, lib.wv_pack_exact_trail) if precision == "f32"
+                    else (L.PACK_EXACTTRAIL_F64, lib.wv_pack_exact_trail_f64))
+        buf = torch.empty(int(lib.wv_packed_bytes(kind, W)), dtype=torch.uint8, device=v.device)
+        L.check(fn(_ptr(v), int(v.dtype == torch.float64), self.num_vertices, _ptr(win), W,
+                   _ptr(buf), _stream()), "wv_pack_exact_trail")
         self._packs[key] = buf
         return buf
 
@@ -580,6 +584,8 @@ def backward_path(mesh: DeviceMesh, mode: str, precision: str, grid, n0: int, co
     "trails", "pairs", "faces" (exact) or "soft"."""
     if mode != "exact":
         return "soft"
+    if precision == "f64":
+        return "trails" if count >= TRAIL64_MIN_POINTS and mesh.trails_pay() else "faces"
     big = precision == "f32" and count >= STRIP_MIN_NODES and mesh.num_faces > 0
     if big and trail_rows_ok(grid, n0) and mesh.trails_pay():
         return "trails"
@@ -709,13 +715,16 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     else:
         n_pts = _grid_count(grid, n0, count)
     exact32 = mode == "exact" and precision == "f32"
+    exact64 = mode == "exact" and precision == "f64"
     if trails is None:
-        trails = (exact32 and pairs is None and points is None and n_pts >= STRIP_MIN_NODES
-                  and trail_rows_ok(grid, n0) and mesh.trails_pay())
+        trails = pairs is None and (
+            (exact32 and points is None and n_pts >= STRIP_MIN_NODES
+             and trail_rows_ok(grid, n0) and mesh.trails_pay())
+            or (exact64 and n_pts >= TRAIL64_MIN_POINTS and mesh.trails_pay()))
     if trails:
-        if not exact32 or points is not None or not trail_rows_ok(grid, n0):
-            raise ValueError("edge trails exist for the exact f32 backward on lattice rows only")
-        return _trail_grad(mesh, coefs, grid, n0, n_pts, coef_scale)
+        if not (exact64 or (exact32 and points is None and trail_rows_ok(grid, n0))):
+            raise ValueError("edge trails exist for the exact backward (f32: lattice rows only)")
+        return _trail_grad(mesh, coefs, precision, grid, n0, n_pts, points, coef_scale)
     if pairs is None:
         pairs = (exact32 and n_pts >= STRIP_MIN_NODES and mesh.num_faces > 0
                  and mesh.strips_pay())
@@ -768,24 +777,34 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     return out, csr
 
 
-def _trail_grad(mesh: DeviceMesh, coefs: torch.Tensor, grid, n0: int, count: int,
-                coef_scale: float):
+def _trail_grad(mesh: DeviceMesh, coefs: torch.Tensor, precision: str, grid, n0: int,
+                count: int, points, coef_scale: float):
     """face_grad over edge trails: (end vectors (2KW,3) f64, signed CSR)."""
     lib = L.lib()
     dev = mesh.vertices.device
-    packed = mesh.packed_exact_trail()
+    dt = _DT[precision]
+    packed = mesh.packed_exact_trail(precision)
     win, csr, W, _ = mesh.exact_trail_setup()
-    cf = coefs.to(device=dev, dtype=torch.float32).contiguous().reshape(-1)
+    cf = coefs.to(device=dev, dtype=dt).contiguous().reshape(-1)
     if cf.numel() != count:
         raise ValueError(f"coefs has {cf.numel()} entries for {count} query points")
     out = torch.empty((2 * (int(win.shape[1]) - 1) * W, 3), dtype=torch.float64, device=dev)
     if W == 0:
         return out, csr
-    wsb = int(lib.wv_exact_trail_bwd_workspace_bytes(W, count))
+    sfx = "" if precision == "f32" else "_f64"
+    wsb = int(getattr(lib, f"wv_exact_trail_bwd_workspace_bytes{sfx}")(W, count))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
-    L.check(lib.wv_exact_trail_bwd_grid_f32(_ptr(packed), W, L.make_grid(*grid), int(n0), count,
-                                            _ptr(cf), float(coef_scale), _ptr(out), _ptr(ws),
-                                            wsb, _stream()), "wv_exact_trail_bwd_grid_f32")
+    if points is not None:
+        pts, _ = _points_arg(points, dev, dt)
+        name = "wv_exact_trail_bwd_points_f64"
+        rc = lib.wv_exact_trail_bwd_points_f64(_ptr(packed), W, _ptr(pts), count, _ptr(cf),
+                                               float(coef_scale), _ptr(out), _ptr(ws), wsb,
+                                               _stream())
+    else:
+        name = f"wv_exact_trail_bwd_grid_{precision}"
+        rc = getattr(lib, name)(_ptr(packed), W, L.make_grid(*grid), int(n0), count, _ptr(cf),
+                                float(coef_scale), _ptr(out), _ptr(ws), wsb, _stream())
+    L.check(rc, name)
     return out, csr
 
 

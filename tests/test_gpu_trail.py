@@ -140,3 +140,41 @@ def test_trail_backward_c3_full_lattice(cuda_device):
     err = np.abs(a - b).max() / scale
     print("C3 full lattice: trail vs single-face backward, max |dg| / max |g| =", err)
     assert scale > 0 and np.isfinite(b).all() and err <= 1e-4, err
+
+
+@pytest.mark.parametrize("kind", ["soup", "holes", "random"])
+def test_trail_backward_f64(cuda_device, kind):
+    """The f64 parity path over the same trails (ExactTrail64): equal to the
+    f64 single-face backward and to the oracle to f64 rounding (1e-10 of the
+    largest component), on a lattice range and on a point list."""
+    import torch
+    from paper_2407_11272_b200 import configs, device
+    if kind == "holes":
+        v, f = configs.torus_with_holes(30, 20, holes=3, patch=3, seed=1)
+    elif kind == "soup":
+        v, f = configs.soup(*configs.torus(0.7, 0.3, 30, 20), seed=1)
+    else:
+        v, f, _ = random_case(3)
+    s = float(np.abs(v).max())
+    grid = ((-1.1 * s,) * 3, (1.1 * s,) * 3, (12, 10, 17))  # odd rows: no row kernel needed
+    dm = device.DeviceMesh.from_numpy(v, f)
+    p = orc.node_coordinates(*grid)
+    _, fl = orc.winding_number_batch(v, f, p, mode="exact", threads=1)
+    c = np.random.default_rng(4).normal(size=len(p))
+    c[fl] = 0.0
+    ct = torch.from_numpy(c).cuda()
+    out = []
+    for kw in ({"trails": False, "pairs": False}, {"trails": True}):
+        fg = device.face_grad(dm, "exact", "f64", ct, grid=grid, **kw)
+        out.append(device.vertex_grad(dm, fg).cpu().numpy())
+    a, b = out
+    r = orc.exact_grad(v, f, p, c, threads=1)
+    scale = max(np.abs(r).max(), 1e-300)
+    assert np.abs(a - b).max() <= 1e-10 * scale
+    assert np.abs(b - r).max() <= 1e-9 * scale, np.abs(b - r).max() / scale
+    sel = np.random.default_rng(6).choice(len(p), 500, replace=False)
+    fg = device.face_grad(dm, "exact", "f64", ct[sel], points=torch.from_numpy(p[sel]).cuda(),
+                          trails=True)
+    g = device.vertex_grad(dm, fg).cpu().numpy()
+    r2 = orc.exact_grad(v, f, p[sel], c[sel], threads=1)
+    assert np.abs(g - r2).max() <= 1e-9 * max(np.abs(r2).max(), 1e-300)

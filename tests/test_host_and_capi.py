@@ -229,5 +229,6 @@ def test_random_soup_config_and_path_choice():
         # the exact f32 backward: edge trails where corner positions are shared
         assert device.backward_path(m, "exact", "f32", grid, 0, w.n_nodes) == \
             ("trails" if pay else "faces")
-        assert device.backward_path(m, "exact", "f64", grid, 0, w.n_nodes) == "faces"
+        assert device.backward_path(m, "exact", "f64", grid, 0, w.n_nodes) == \
+            ("trails" if pay else "faces")
         assert device.backward_path(m, "soft", "f32", grid, 0, w.n_nodes) == "soft"
