@@ -359,6 +359,8 @@ constexpr double kEightPi = 8.0 * kPi;
 struct ExactBwd64 {
   using Rec = ExactGradRecF64;
   static constexpr int kOut = 9;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kUnroll = 1;
   // edge (Biot-Savart) form of d(Omega)/dv, see ExactEdgeBwd in wv_bwd_f32.cu;
   // coef carries the -1/(4 pi) factor.  Per pair: the three reciprocal corner
   // lengths once (Newton rsqrt), one Newton reciprocal per edge, no branches.
@@ -407,10 +409,18 @@ struct ExactBwd64 {
 // the mesh is evaluated once (ExactBwd64::edge), and the signed CSR gather
 // distributes the 2K end vectors to the vertex ids.  Per face of a closed
 // surface: 1.5 edges and ~1.9 lengths instead of 3 and 3.
+#ifndef WV_TRAIL64_MINB
+#define WV_TRAIL64_MINB 2
+#endif
+#ifndef WV_TRAIL64_UNROLL
+#define WV_TRAIL64_UNROLL 1
+#endif
 struct ExactTrail64 {
   static constexpr int K = kTrailK;
   using Rec = TrailRecF64;
   static constexpr int kOut = 6 * K;
+  static constexpr int kMinBlocks = WV_TRAIL64_MINB;
+  static constexpr int kUnroll = WV_TRAIL64_UNROLL;  // points per loop body (ILP)
   __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
                                               double coef, double, double* g) {
     double a[K + 1][3], l[K + 1], il[K + 1];
@@ -433,6 +443,8 @@ struct ExactTrail64 {
 struct SoftBwd64 {
   using Rec = SoftGradRecF64;
   static constexpr int kOut = 9;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kUnroll = 1;
   // _kernels.py:198-232, same expression order per pair
   __device__ __forceinline__ static void pair(const Rec& R, double qx, double qy, double qz,
                                               double coef, double eps, double* g) {
@@ -462,7 +474,7 @@ struct SoftBwd64 {
 };
 
 template <class Pol, class Src>
-__global__ void __launch_bounds__(kBwd64Threads, 2)
+__global__ void __launch_bounds__(kBwd64Threads, Pol::kMinBlocks)
 bwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __restrict__ recs,
                int64_t n_faces, Src src, const double* __restrict__ coefs, int64_t n_count,
                int64_t pts_per_split, double coef_scale, double* __restrict__ out) {
@@ -486,11 +498,24 @@ bwd_f64_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       chunk[i] = make_double4(x, y, z, coefs[c0 + i] * coef_scale);
     }
     __syncthreads();
+    if constexpr (Pol::kUnroll > 1) {
+      // chunk entries past n hold stale points: their coefficients are read
+      // as 0 (the zero-coefficient skip of _kernels.py:182-184 is per point)
 #pragma unroll 1
-    for (int i = 0; i < n; ++i) {
-      const double4 q = chunk[i];
-      if (q.w == 0.0) continue;  // _kernels.py:182-184
-      Pol::pair(R, q.x, q.y, q.z, q.w, eps, g);
+      for (int i = 0; i < n; i += Pol::kUnroll) {
+#pragma unroll
+        for (int u = 0; u < Pol::kUnroll; ++u) {
+          const double4 q = chunk[i + u < n ? i + u : i];
+          if (i + u < n && q.w != 0.0) Pol::pair(R, q.x, q.y, q.z, q.w, eps, g);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < n; ++i) {
+        const double4 q = chunk[i];
+        if (q.w == 0.0) continue;  // _kernels.py:182-184
+        Pol::pair(R, q.x, q.y, q.z, q.w, eps, g);
+      }
     }
   }
   if (live) {

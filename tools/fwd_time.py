@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--config", default="c3r")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--bwd", action="store_true")
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--path", default="auto", choices=["auto", "trails", "pairs", "faces"],
                     help="backward records (--bwd)")
     a = ap.parse_args()
@@ -27,17 +28,17 @@ def main():
     w = configs.make(a.config)
     grid = (w.lo, w.hi, w.res)
     dm = device.DeviceMesh.from_numpy(w.vertices, w.faces)
-    v, f = device.forward(dm, "exact", "f32", grid=grid)
-    coefs = torch.where(f.bool(), 0.0, 2.0 * (v - (v > 0.5).float()))
+    v, f = device.forward(dm, "exact", a.precision, grid=grid)
+    coefs = torch.where(f.bool(), 0.0, 2.0 * (v - (v > 0.5).to(v.dtype)))
 
     def run():
         dm.invalidate()
         if a.bwd:
             kw = {"auto": {}, "trails": {"trails": True}, "pairs": {"pairs": True},
                   "faces": {"pairs": False}}[a.path]
-            device.face_grad(dm, "exact", "f32", coefs, grid=grid, **kw)
+            device.face_grad(dm, "exact", a.precision, coefs, grid=grid, **kw)
         else:
-            device.forward(dm, "exact", "f32", grid=grid)
+            device.forward(dm, "exact", a.precision, grid=grid)
 
     run()
     torch.cuda.synchronize()
@@ -50,7 +51,7 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     print(json.dumps({"lib": os.environ.get("WV_LIB_PATH", "default"), "config": a.config,
-                      "bwd": a.bwd, "path": a.path, "ms": min(ts), "all": ts}))
+                      "bwd": a.bwd, "path": a.path, "precision": a.precision, "ms": min(ts), "all": ts}))
 
 
 if __name__ == "__main__":
