@@ -13,6 +13,8 @@ path that mirrors the reference's default f64 kernels.
 
 from __future__ import annotations
 
+import hashlib
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -77,6 +79,36 @@ def edge_trails(vertices: np.ndarray, faces: np.ndarray, dead: np.ndarray | None
         win.ctypes.data, ctypes.addressof(nw), off.ctypes.data, slots.ctypes.data,
         ctypes.addressof(ns), vrep.ctypes.data), "wv_edge_trails")
     return win[:nw.value].copy(), off, slots[:ns.value].copy(), vrep[:V].copy()
+
+
+# Host-side plans (strip order, edge trails, corner sharing) depend only on
+# the mesh CONTENT; a caller that rebuilds a DeviceMesh from the same host
+# arrays every step (e.g. an end-to-end loop, one per rank) reuses them.
+# Keyed by a digest of the f64 vertex and int64 face bytes; a few entries.
+_PLANS: OrderedDict = OrderedDict()
+_PLANS_MAX = 8
+
+
+def _digest(*arrays) -> bytes:
+    h = hashlib.sha256()  # SHA extensions: ~1 GB/s on the host
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(f"{a.dtype.str}{a.shape}".encode())
+        h.update(memoryview(a).cast("B"))
+    return h.digest()
+
+
+def _plan(kind: str, key: bytes, build):
+    k = (kind, key)
+    hit = _PLANS.get(k)
+    if hit is None:
+        hit = build()  # (callers treat plan arrays as read-only)
+        _PLANS[k] = hit
+        while len(_PLANS) > _PLANS_MAX:
+            _PLANS.popitem(last=False)
+    else:
+        _PLANS.move_to_end(k)
+    return hit
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -345,7 +377,9 @@ class DeviceMesh:
             vnp = getattr(self, "_verts_np", None)
             if vnp is None:
                 vnp = self.vertices.detach().double().cpu().numpy()
-            perm, win, fl = strip_order(vnp, self.faces_np())
+            fnp = self.faces_np()
+            perm, win, fl = _plan("strip", self._plan_key(vnp),
+                                  lambda: strip_order(vnp, fnp))
             dev = self.vertices.device
             st = tuple(torch.from_numpy(a).to(dev) for a in (perm, win, fl))
             self._strip = st
@@ -359,6 +393,14 @@ class DeviceMesh:
         fl = self._strip_host[2]
         return float(np.count_nonzero(fl & 1)) / max(1, len(fl))
 
+    def _plan_key(self, vnp: np.ndarray) -> bytes:
+        """Digest of (vnp, faces) for the host-plan cache, once per array."""
+        k = getattr(self, "_pkey", None)
+        if k is None or k[0] is not vnp:
+            k = (vnp, _digest(vnp, self.faces_np()))
+            self._pkey = k
+        return k[1]
+
     def shared_corner_fraction(self) -> float:
         """1 - (distinct corner positions) / (3F): ~5/6 for a closed surface
         (welded or un-welded soup alike: the copies are bitwise equal), 0 for
@@ -368,15 +410,20 @@ class DeviceMesh:
         vnp = getattr(self, "_verts_np", None)
         if vnp is None:
             vnp = self.vertices.detach().double().cpu().numpy()
-        bits = np.ascontiguousarray(vnp, dtype=np.float64).view(np.uint64).reshape(-1, 3)
-        with np.errstate(over="ignore"):
-            h = (bits[:, 0] * np.uint64(0x9E3779B97F4A7C15)
-                 ^ bits[:, 1] * np.uint64(0xC2B2AE3D27D4EB4F)
-                 ^ bits[:, 2] * np.uint64(0x165667B19E3779F9))
-        corners = h[self.faces_np().reshape(-1)]
-        if corners.size == 0:
-            return 0.0
-        return 1.0 - np.unique(corners).size / corners.size
+        fnp = self.faces_np()
+
+        def frac():
+            bits = np.ascontiguousarray(vnp, dtype=np.float64).view(np.uint64).reshape(-1, 3)
+            with np.errstate(over="ignore"):
+                h = (bits[:, 0] * np.uint64(0x9E3779B97F4A7C15)
+                     ^ bits[:, 1] * np.uint64(0xC2B2AE3D27D4EB4F)
+                     ^ bits[:, 2] * np.uint64(0x165667B19E3779F9))
+            corners = h[fnp.reshape(-1)]
+            if corners.size == 0:
+                return 0.0
+            return 1.0 - np.unique(corners).size / corners.size
+
+        return _plan("share", self._plan_key(vnp), frac)
 
     def strips_pay(self) -> bool:
         """Whether the strip-ordered kernels beat the face-ordered ones on this
@@ -499,7 +546,8 @@ class DeviceMesh:
             fnp = self.faces_np()
             dead = dead_faces(vnp, fnp)
             self._dead_dev = torch.from_numpy(dead).to(self.vertices.device)
-            win, off, slots, vrep = edge_trails(vnp, fnp, dead)
+            win, off, slots, vrep = _plan("trail", self._plan_key(vnp),
+                                          lambda: edge_trails(vnp, fnp, dead))
             dev = self.vertices.device
             ids = np.flatnonzero(vrep != np.arange(len(vrep))).astype(np.int64)
             ts = (torch.from_numpy(win).to(dev),
