@@ -144,3 +144,28 @@ def test_trails_reject_bad_indices():
                             ctypes.addressof(nw), off.ctypes.data, sl.ctypes.data,
                             ctypes.addressof(ns), None)
     assert rc == 1
+
+
+def test_host_plan_cache_keys_on_content():
+    """The host-plan cache (strip order, trails) is keyed by the mesh bytes:
+    a DeviceMesh rebuilt from equal arrays reuses the plan, a moved vertex
+    gets its own."""
+    import torch
+    from paper_2407_11272_b200 import device
+    _trails(np.zeros((3, 3)), np.zeros((0, 3), np.int64))
+    v, f = configs.soup(*configs.torus(0.7, 0.3, 16, 10), seed=3)
+
+    def mesh(vv):
+        m = device.DeviceMesh(torch.from_numpy(vv), torch.from_numpy(f))
+        m._verts_np, m._faces_np = vv, f
+        return m
+    a, b = mesh(v.copy()), mesh(v.copy())
+    ta, tb = a.exact_trail_setup(), b.exact_trail_setup()
+    assert a._plan_key(a._verts_np) == b._plan_key(b._verts_np)
+    assert torch.equal(ta[0], tb[0]) and torch.equal(ta[1][1], tb[1][1])
+    v2 = v.copy()
+    v2[0, 0] += 1e-3  # splits one weld
+    c = mesh(v2)
+    assert c._plan_key(v2) != a._plan_key(a._verts_np)
+    tc = c.exact_trail_setup()
+    assert tc[2] != ta[2] or not torch.equal(tc[1][1], ta[1][1])
