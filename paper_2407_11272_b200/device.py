@@ -544,10 +544,13 @@ class DeviceMesh:
             if vnp is None:
                 vnp = self.vertices.detach().double().cpu().numpy()
             fnp = self.faces_np()
-            dead = dead_faces(vnp, fnp)
+
+            def build():
+                dead = dead_faces(vnp, fnp)
+                return (*edge_trails(vnp, fnp, dead), dead)
+
+            win, off, slots, vrep, dead = _plan("trail", self._plan_key(vnp), build)
             self._dead_dev = torch.from_numpy(dead).to(self.vertices.device)
-            win, off, slots, vrep = _plan("trail", self._plan_key(vnp),
-                                          lambda: edge_trails(vnp, fnp, dead))
             dev = self.vertices.device
             ids = np.flatnonzero(vrep != np.arange(len(vrep))).astype(np.int64)
             ts = (torch.from_numpy(win).to(dev),
