@@ -410,7 +410,7 @@ struct ExactBwd64 {
 // distributes the 2K end vectors to the vertex ids.  Per face of a closed
 // surface: 1.5 edges and ~1.9 lengths instead of 3 and 3.
 #ifndef WV_TRAIL64_MINB
-#define WV_TRAIL64_MINB 2
+#define WV_TRAIL64_MINB 3  // c3s f64 trail backward: 279 ms (3 CTAs/SM) vs 308 (2); unroll 2: 286-314
 #endif
 #ifndef WV_TRAIL64_UNROLL
 #define WV_TRAIL64_UNROLL 1
