@@ -311,34 +311,6 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         do_rare(Rb, rare_b);
       };
       int f = 0;
-      if constexpr (kRows && Pol::kQuadFaces) {
-        // four faces per angle; a group whose quad fails takes the pairs
-        // (and a pair that fails, its single faces)
-#pragma unroll 1
-        for (; f + 4 <= cnt; f += 4) {
-          const Rec* R4 = tile + f;
-          const typename Pol::Row w4[4] = {Pol::row(R4[0], rx, ry), Pol::row(R4[1], rx, ry),
-                                           Pol::row(R4[2], rx, ry), Pol::row(R4[3], rx, ry)};
-          uint32_t rare[4] = {0u, 0u, 0u, 0u};
-          constexpr int QG = Pol::kQuadGroup;  // point pairs per quad decision
-#pragma unroll
-          for (int g0 = 0; g0 < PP; g0 += QG) {
-            if (Pol::template face_row_quad<QG>(R4, w4, qz + g0, ctx, tacc + g0)) continue;
-#pragma unroll
-            for (int h = 0; h < 4; h += 2) {
-              if (!Pol::template face_row_pair<QG>(R4[h], w4[h], R4[h + 1], w4[h + 1], qz + g0,
-                                                   ctx, tacc + g0)) {
-                rare[h] |= Pol::template face_row<QG>(R4[h], w4[h], qz + g0, ctx, tacc + g0)
-                           << (2 * g0);
-                rare[h + 1] |= Pol::template face_row<QG>(R4[h + 1], w4[h + 1], qz + g0, ctx,
-                                                          tacc + g0) << (2 * g0);
-              }
-            }
-          }
-#pragma unroll
-          for (int h = 0; h < 4; ++h) do_rare(R4[h], rare[h]);
-        }
-      }
 #pragma unroll 1
       for (; f + 2 <= cnt; f += 2) do_pair(tile[f], tile[f + 1]);
       if (f < cnt) do_face(tile[f], R0{});

@@ -338,76 +338,6 @@ struct ExactPol {
     };
     return pair_fast<PP>(Ra, Rb, geo, near, tacc);
   }
-  // ---- four faces per angle (kQuadFaces, lattice rows) -------------------
-  // Two pairs' tan sums (n_i, d_i) combine the same way:
-  //   T = (n1 d2 + n2 d1) / (d1 d2 - n1 n2).
-  // With every beta well conditioned, d1 > 0 and d2 > 0 put each pair's sum
-  // in (-pi/2, pi/2), and D = d1 d2 - n1 n2 > 0 puts the total there too
-  // (its cosine is positive), so atan(T) IS the four faces' sum; then
-  // |T| < 1/8 admits the polynomial.  MUFU 3.5 -> 3.25 per pair on the
-  // random soup (where the face-ordered kernel is bound by the MUFU pipe).
-  // Anything failing takes the pairs (face_row_pair), then single faces.
-#ifndef WV_QUAD_FACES
-#define WV_QUAD_FACES 0
-#endif
-  static constexpr bool kQuadFaces = WV_QUAD_FACES;
-#ifndef WV_QUAD_GROUP
-#define WV_QUAD_GROUP 1
-#endif
-  static constexpr int kQuadGroup = WV_QUAD_GROUP;
-  template <int PP>
-  __device__ __forceinline__ static bool face_row_quad(const Rec* R4, const Row* w4, const F2* qz,
-                                                       const Ctx& ctx, F2* tacc) {
-    float mn = __int_as_float(0x7f800000);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) mn = fminf(mn, fminf(w4[k].a2, fminf(w4[k].b2, w4[k].c2)));
-    const bool near = mn < ctx.eps2;
-    F2 tq[PP], tp[PP];
-    float m = -1.0f;
-#pragma unroll
-    for (int pp = 0; pp < PP; ++pp) {
-      F2 al[4], be[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const Rec& R = R4[k];
-        const Row& w = w4[k];
-        const F2 az = sub2(f2s(R.v0e.z), qz[pp]), bz = sub2(f2s(R.v1.z), qz[pp]);
-        const F2 cz = sub2(f2s(R.v2.z), qz[pp]);
-        al[k] = fma2(f2s(R.n.z), az, f2s(w.alpha));
-        F2 ee;
-        beta_ee(R, fma2(az, az, f2s(w.a2)), fma2(bz, bz, f2s(w.b2)), fma2(cz, cz, f2s(w.c2)),
-                be[k], ee);
-        float e0, e1;
-        split(ee, e0, e1);
-        m = fmaxf(m, fmaxf(e0, e1));
-      }
-      const F2 n1 = fma2(al[0], be[1], mul2(al[1], be[0]));
-      const F2 d1 = fma2(mul2(al[0], al[1]), f2s(-1.0f), mul2(be[0], be[1]));
-      const F2 n2 = fma2(al[2], be[3], mul2(al[3], be[2]));
-      const F2 d2 = fma2(mul2(al[2], al[3]), f2s(-1.0f), mul2(be[2], be[3]));
-      const F2 N = fma2(n1, d2, mul2(n2, d1));
-      const F2 D = fma2(mul2(n1, n2), f2s(-1.0f), mul2(d1, d2));
-      const F2 tt = mul2(N, rcp2(D));
-      const F2 s2 = mul2(tt, tt);
-      float a0, a1, b0, b1, c0, c1, x0, x1;
-      split(add2(s2, f2s(-1.0f / 64.0f)), a0, a1);
-      split(d1, b0, b1);
-      split(d2, c0, c1);
-      split(D, x0, x1);
-      // every test "< 0" (a NaN anywhere fails the max)
-      m = fmaxf(m, fmaxf(fmaxf(a0, a1), fmaxf(fmaxf(-b0, -b1), fmaxf(fmaxf(-c0, -c1),
-                                                                     fmaxf(-x0, -x1)))));
-      tq[pp] = tt;
-      tp[pp] = fma2(fma2(s2, f2s(0.19669890403747559f), f2s(-0.33331409096717834f)), s2,
-                    f2s(1.0f));
-    }
-    if (m < 0.0f && !near) {
-#pragma unroll
-      for (int pp = 0; pp < PP; ++pp) tacc[pp] = fma2(tq[pp], tp[pp], tacc[pp]);
-      return true;
-    }
-    return false;
-  }
   template <int PP>
   __device__ __forceinline__ static bool face_pair(const Rec& Ra, const Rec& Rb, const F2* qx,
                                                    const F2* qy, const F2* qz, const Ctx& ctx,
