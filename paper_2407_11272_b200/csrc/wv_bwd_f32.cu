@@ -84,8 +84,11 @@ __device__ __noinline__ void exact_pair_f64(const ExactGradRecF32& R, double qx,
   }
 }
 
+#ifndef WV_EDGE_PREFETCH
+#define WV_EDGE_PREFETCH 0
+#endif
 struct ExactEdgeBwd {
-  static constexpr bool kPrefetch = false;  // next chunk's coefficients in registers
+  static constexpr bool kPrefetch = WV_EDGE_PREFETCH;  // next chunk's coefficients in registers
   using Rec = ExactGradRecF32;
   static constexpr int kFaces = 1;  // faces per thread (per record)
   static constexpr int kOut = 9;
