@@ -512,8 +512,9 @@ struct ExactStripPol : ExactPol {
         set_s(sA[pp], add2(sA[pp].d, sB[pp].d));
       }
     }
-    constexpr float kL = -16.0f / 7.0f;
-    const float kab = kL * fabsf(R.v1.w), kbc = kL * fabsf(R.v2.w), kca = kL * R.n.w;
+    // the records carry (16/7) h (flags in the sign bits): -|.| folds into
+    // the FFMA2 operands (SASS -|R|.F32), no per-face multiply
+    const float kab = -fabsf(R.v1.w), kbc = -fabsf(R.v2.w), kca = -R.n.w;
     // t/2 = alpha / (2 beta) is what the division gives; the series is taken
     // in (t/2)^2 with its coefficients scaled by powers of 2, so
     // (t/2) (2 p(t^2)) rounds exactly as t p(t^2) does, without doubling alpha
@@ -597,9 +598,8 @@ struct ExactStripPol : ExactPol {
                                                          Slot* s2, Slot* s3, F2* tq, F2* tp) {
     // face a: slots (s0, s1) -> s2; face b: (s1, s2) -> s3 (= s0's storage).
     // Only for pairs that continue their strip (a restart takes strip_fast).
-    constexpr float kL = -16.0f / 7.0f;
-    const float kab_a = kL * fabsf(Ra.v1.w), kbc_a = kL * fabsf(Ra.v2.w), kca_a = kL * Ra.n.w;
-    const float kab_b = kL * fabsf(Rb.v1.w), kbc_b = kL * fabsf(Rb.v2.w), kca_b = kL * Rb.n.w;
+    const float kab_a = -fabsf(Ra.v1.w), kbc_a = -fabsf(Ra.v2.w), kca_a = -Ra.n.w;
+    const float kab_b = -fabsf(Rb.v1.w), kbc_b = -fabsf(Rb.v2.w), kca_b = -Rb.n.w;
     constexpr float kC2 = 32.0f * 0.19669890403747559f, kC1 = 8.0f * -0.33331409096717834f;
     float ms = 0.0f;
     bool cond = true;
@@ -626,8 +626,9 @@ struct ExactStripPol : ExactPol {
   // distances recomputed from the record (the row parts bitwise the carried
   // ones); returns the lanes for the fp64 path
   template <int PP>
-  __device__ __forceinline__ static uint32_t strip_slow(const Rec& R, float qx, float qy,
+  __device__ __forceinline__ static uint32_t strip_slow(const Rec& Rk, float qx, float qy,
                                                         const F2* qz, const Ctx& ctx, F2* tacc) {
+    const Rec R = with_h(Rk);  // the face-ordered tail needs h itself
     Row w = row_c(R, qx, qy);
     row_ab(R, qx, qy, w.a2, w.b2);
     uint32_t rare = 0;
@@ -640,6 +641,21 @@ struct ExactStripPol : ExactPol {
                     fma2(cz, cz, f2s(w.c2)), ctx, tacc[pp]) << (2 * pp);
     }
     return rare;
+  }
+  // strip records carry (16/7) h in the .w fields (flags in the sign bits);
+  // the face-ordered paths (tail2, finish_len) take the record with h
+  __device__ __forceinline__ static Rec with_h(const Rec& Rk) {
+    Rec R = Rk;
+    R.v1.w = fabsf(Rk.v1.w) * (7.0f / 16.0f);
+    R.v2.w = fabsf(Rk.v2.w) * (7.0f / 16.0f);
+    R.n.w = Rk.n.w * (7.0f / 16.0f);
+    return R;
+  }
+  // point lists and unaligned ranges walk strip records face by face
+  template <int PP>
+  __device__ __forceinline__ static uint32_t face(const Rec& Rk, const F2* qx, const F2* qy,
+                                                  const F2* qz, const Ctx& ctx, F2* tacc) {
+    return ExactPol::face<PP>(with_h(Rk), qx, qy, qz, ctx, tacc);
   }
   // the fp64 path needs the face's own orientation (triple product): a
   // reflected window (v2.w < 0) swaps B and C back

@@ -239,7 +239,11 @@ __global__ void pack_strip_kernel(const V* __restrict__ verts, const I* __restri
         restart |= (float)verts[3 * pw[2] + d] != (float)w[1][d];
       }
     }
-    const float hab = (float)half2(0, 1), hbc = (float)half2(1, 2), hca = (float)half2(2, 0);
+    // the strip kernel's beta uses (16/7) h (ExactStripPol::strip_fast), so
+    // the records carry that, rounded once from f64 (its rare tail restores h)
+    constexpr double kL = 16.0 / 7.0;
+    const float hab = (float)(kL * half2(0, 1)), hbc = (float)(kL * half2(1, 2));
+    const float hca = (float)(kL * half2(2, 0));
     ExactRecF32& r = recs[k];
     r.v0e = make_float4((float)w[0][0], (float)w[0][1], (float)w[0][2], epsN);
     // sign bits as flags (set on the bit pattern: a zero length gives -0.0)
