@@ -14,8 +14,9 @@
 // with A, B at the positions of the previous record's B, C (unless the
 // record restarts the strip); N is the face's own normal in its true
 // orientation, so alpha = N.(A - q) keeps the true sign (any corner of the
-// face gives the same alpha).  Flags live in sign bits of the half squared
-// edge lengths (>= 0): v1.w < 0 marks a restart, v2.w < 0 a window that is a
+// face gives the same alpha).  The .w fields carry (16/7) x the half squared
+// edge lengths (>= 0; the strip kernel's beta constants, ExactStripPol), and
+// flags live in their sign bits: v1.w < 0 marks a restart, v2.w < 0 a window that is a
 // reflection of the face's vertex order (the fp64 rare path needs the true
 // order for its triple product).
 #include <algorithm>
