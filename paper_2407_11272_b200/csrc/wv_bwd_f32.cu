@@ -1070,16 +1070,19 @@ struct ExactEdgeBwdTrail {
         split(z[4 * e + j], lo, hi);
         s[j] = (double)lo + (double)hi;
       }
+      // (in f64: exact differences of the f32 coordinates, and an expression
+      // the compiler cannot share with row()'s -- sharing kept the x/y
+      // offsets live through the run and re-derived the row parts every step)
       const float4 P = R.p[e], Q = R.p[e + 1];
-      const float ax = P.x - w.qx, ay = P.y - w.qy;
-      const float ex = Q.x - P.x, ey = Q.y - P.y, ez = Q.z - P.z;
-      const float kx = ay * ez, ky = -(ax * ez), mz = fmaf(ax, ey, -(ay * ex));
-      const double dex = (double)ex, dey = (double)ey;
-      acc[6 * e + 0][t] += kx * s[0] - dey * s[1];
-      acc[6 * e + 1][t] += ky * s[0] + dex * s[1];
+      const double ax = (double)P.x - (double)w.qx, ay = (double)P.y - (double)w.qy;
+      const double ex = (double)Q.x - (double)P.x, ey = (double)Q.y - (double)P.y;
+      const double ez = (double)Q.z - (double)P.z;
+      const double kx = ay * ez, ky = -(ax * ez), mz = ax * ey - ay * ex;
+      acc[6 * e + 0][t] += kx * s[0] - ey * s[1];
+      acc[6 * e + 1][t] += ky * s[0] + ex * s[1];
       acc[6 * e + 2][t] += mz * s[0];
-      acc[6 * e + 3][t] += kx * s[2] - dey * s[3];
-      acc[6 * e + 4][t] += ky * s[2] + dex * s[3];
+      acc[6 * e + 3][t] += kx * s[2] - ey * s[3];
+      acc[6 * e + 4][t] += ky * s[2] + ex * s[3];
       acc[6 * e + 5][t] += mz * s[2];
     }
   }
