@@ -902,26 +902,54 @@ struct ExactEdgeBwdTrail {
   static constexpr int kAcc = 6 * K;
   static constexpr int kRowAcc = 4 * K;  // per edge: sum t/|P|, t a_z/|P|, t/|Q|, t a_z/|Q|
   static constexpr float kIllRatio = ExactEdgeBwd::kIllRatio;
-  __device__ __forceinline__ static void scale(Rec& R, float s) {
-    const float s2 = s * s;
+  // The thread keeps only what every step reads in registers -- the
+  // positions' z and the squared edge lengths, in the power-of-two scaled
+  // frame (launch_bwd's grid_scale) -- and re-reads x / y from the record
+  // (L1) once per row run: with all 20 floats live the compiler re-derived
+  // the row parts of |p - q|^2 in every step to stay inside 128 registers.
+  struct View {
+    float z[K + 1];
+    float u[K];
+    const Rec* g;
+    float gs;
+  };
+  __device__ __forceinline__ static View view(const Rec* g, float gs) {
+    View v;
 #pragma unroll
     for (int k = 0; k <= K; ++k) {
-      R.p[k].x *= s;
-      R.p[k].y *= s;
-      R.p[k].z *= s;
-      R.p[k].w *= s2;
+      const float4 p = __ldg(&g->p[k]);
+      v.z[k] = p.z * gs;
+      if (k < K) v.u[k] = p.w * (gs * gs);
     }
+    v.g = g;
+    v.gs = gs;
+    return v;
   }
-  __device__ __forceinline__ static bool unit_weights(const Rec&) { return true; }
+  __device__ __forceinline__ static float2 xy(const View& V, int k) {
+    const float4 p = __ldg(&V.g->p[k]);
+    return make_float2(p.x * V.gs, p.y * V.gs);
+  }
+  // the full scaled record (rare fp64 path)
+  __device__ __forceinline__ static Rec full(const View& V) {
+    Rec R;
+#pragma unroll
+    for (int k = 0; k <= K; ++k) {
+      const float2 q = xy(V, k);
+      R.p[k] = make_float4(q.x, q.y, V.z[k], k < K ? V.u[k] : 0.0f);
+    }
+    return R;
+  }
+  __device__ __forceinline__ static bool unit_weights(const View&) { return true; }
   struct Row {
     float a2[K + 1];  // x/y parts of |p_k - q|^2
     float qx, qy;
   };
-  __device__ __forceinline__ static Row row(const Rec& R, float qx, float qy) {
+  __device__ __forceinline__ static Row row(const View& V, float qx, float qy) {
     Row w;
 #pragma unroll
     for (int k = 0; k <= K; ++k) {
-      const float dx = R.p[k].x - qx, dy = R.p[k].y - qy;
+      const float2 p = xy(V, k);
+      const float dx = p.x - qx, dy = p.y - qy;
       w.a2[k] = fmaf(dy, dy, dx * dx);
     }
     w.qx = qx;
@@ -949,12 +977,12 @@ struct ExactEdgeBwdTrail {
   // denominators go to dd[K] for the run's screen; kMask = true: ill lanes
   // leave the fp32 sums (bits returned, trail_pair_f64 adds them)
   template <bool kMask>
-  __device__ __forceinline__ static uint32_t pair_row2(const Rec& R, const Row& w, F2 qz, F2 coef,
+  __device__ __forceinline__ static uint32_t pair_row2(const View& R, const Row& w, F2 qz, F2 coef,
                                                        F2* z, F2* dd = nullptr) {
     F2 az[K + 1], ip[K + 1], lp[K + 1];
 #pragma unroll
     for (int k = 0; k <= K; ++k) {
-      az[k] = sub2(f2s(R.p[k].z), qz);
+      az[k] = sub2(f2s(R.z[k]), qz);
       const F2 s2 = fma2(az[k], az[k], f2s(w.a2[k]));
       ip[k] = rsqrt2(s2);
       lp[k] = mul2(s2, ip[k]);
@@ -964,7 +992,7 @@ struct ExactEdgeBwdTrail {
 #pragma unroll
     for (int e = 0; e < K; ++e) {
       const F2 se = add2(lp[e], lp[e + 1]);
-      d[e] = fma2(se, se, f2s(-R.p[e].w));
+      d[e] = fma2(se, se, f2s(-R.u[e]));
     }
     // one reciprocal for the K denominators
     F2 t[K];
@@ -982,7 +1010,7 @@ struct ExactEdgeBwdTrail {
     if constexpr (kMask) {
 #pragma unroll
       for (int e = 0; e < K; ++e) {
-        const float k = R.p[e].w * (1.0f / kIllRatio);
+        const float k = R.u[e] * (1.0f / kIllRatio);
         float lo, hi;
         split(d[e], lo, hi);
         ill0 |= !(lo > k);
@@ -1019,7 +1047,7 @@ struct ExactEdgeBwdTrail {
     return (ill0 ? 1u : 0u) | (ill1 ? 2u : 0u);
   }
   template <bool kUnit, int N>
-  __device__ __forceinline__ static void step_row(const Rec& R, const Row& w, const float4* zc,
+  __device__ __forceinline__ static void step_row(const View& R, const Row& w, const float4* zc,
                                                   float, F2* z, Screen* mr) {
     // the step's own minima first (short chains), then one min into the run's
     F2 m[K];
@@ -1033,32 +1061,33 @@ struct ExactEdgeBwdTrail {
 #pragma unroll
     for (int e = 0; e < K; ++e) mr->d[e] = minnan2(mr->d[e], m[e]);
   }
-  __device__ __forceinline__ static bool ill_run(const Rec& R, const Screen& mr) {
+  __device__ __forceinline__ static bool ill_run(const View& R, const Screen& mr) {
     bool ill = false;
 #pragma unroll
     for (int e = 0; e < K; ++e) {
       float lo, hi;
       split(mr.d[e], lo, hi);
-      ill |= !(minnan(lo, hi) > R.p[e].w * (1.0f / kIllRatio));
+      ill |= !(minnan(lo, hi) > R.u[e] * (1.0f / kIllRatio));
     }
     return ill;
   }
   template <bool kUnit>
-  __device__ __noinline__ static void redo_run(const Rec& R, const Row& w, const float4* zcs,
+  __device__ __noinline__ static void redo_run(const View& R, const Row& w, const float4* zcs,
                                                int j, int e, float, F2* z,
                                                double (*acc)[kBwdThreads]) {
+    const Rec Rf = full(R);
     for (int i = 0; i < kRowAcc; ++i) z[i] = f2(0.0f, 0.0f);
     for (; j < e; ++j) {
       const float4 zc = zcs[j];
       if (zc.z == 0.0f && zc.w == 0.0f) continue;
       const uint32_t ill = pair_row2<true>(R, w, f2(zc.x, zc.y), f2(zc.z, zc.w), z);
-      if (ill & 1u) trail_pair_f64(R, w.qx, w.qy, zc.x, zc.z, acc);
-      if (ill & 2u) trail_pair_f64(R, w.qx, w.qy, zc.y, zc.w, acc);
+      if (ill & 1u) trail_pair_f64(Rf, w.qx, w.qy, zc.x, zc.z, acc);
+      if (ill & 2u) trail_pair_f64(Rf, w.qx, w.qy, zc.y, zc.w, acc);
     }
   }
   // the run's sums -> sum_q m s per (edge, end) into the fp64 accumulators
   // (m = a_P x e: x/y affine in a_z of the edge's first position, z constant)
-  __device__ __forceinline__ static void flush_row(const Rec& R, const Row& w, const F2* z,
+  __device__ __forceinline__ static void flush_row(const View& R, const Row& w, const F2* z,
                                                    double (*acc)[kBwdThreads]) {
     const int t = threadIdx.x;
 #pragma unroll
@@ -1070,13 +1099,11 @@ struct ExactEdgeBwdTrail {
         split(z[4 * e + j], lo, hi);
         s[j] = (double)lo + (double)hi;
       }
-      // (in f64: exact differences of the f32 coordinates, and an expression
-      // the compiler cannot share with row()'s -- sharing kept the x/y
-      // offsets live through the run and re-derived the row parts every step)
-      const float4 P = R.p[e], Q = R.p[e + 1];
+      // (the moments in f64 from the f32 coordinates, exact differences)
+      const float2 P = xy(R, e), Q = xy(R, e + 1);
       const double ax = (double)P.x - (double)w.qx, ay = (double)P.y - (double)w.qy;
       const double ex = (double)Q.x - (double)P.x, ey = (double)Q.y - (double)P.y;
-      const double ez = (double)Q.z - (double)P.z;
+      const double ez = (double)R.z[e + 1] - (double)R.z[e];
       const double kx = ay * ez, ky = -(ax * ez), mz = ax * ey - ay * ex;
       acc[6 * e + 0][t] += kx * s[0] - ey * s[1];
       acc[6 * e + 1][t] += ky * s[0] + ex * s[1];
@@ -1086,7 +1113,7 @@ struct ExactEdgeBwdTrail {
       acc[6 * e + 5][t] += mz * s[2];
     }
   }
-  __device__ __forceinline__ static void finish(const Rec&, const double* acc, double* out) {
+  __device__ __forceinline__ static void finish(const View&, const double* acc, double* out) {
     for (int j = 0; j < kOut; ++j) out[j] = acc[j];
   }
 };
@@ -1123,6 +1150,26 @@ __device__ __forceinline__ void chunk_loop(const typename Pol::Rec& R, const Poi
 // Row mode: the chunk is cut at k-row boundaries (warp-uniform), each run of
 // pairs shares the row's x/y, and the per-face row constants are computed
 // once per run.  Needs rz and the range start even (pairs never straddle).
+// the thread's register copy of its record: Pol::View when the policy
+// defines one (a partial copy; the rest is re-read from global memory where
+// needed), else the scaled record itself
+template <class Pol, class = void>
+struct RecOf {
+  using T = typename Pol::Rec;
+  __device__ __forceinline__ static T load(const typename Pol::Rec* recs, int64_t f, float gs) {
+    T R = recs[f];
+    if (gs != 1.0f) Pol::scale(R, gs);
+    return R;
+  }
+};
+template <class Pol>
+struct RecOf<Pol, std::void_t<typename Pol::View>> {
+  using T = typename Pol::View;
+  __device__ __forceinline__ static T load(const typename Pol::Rec* recs, int64_t f, float gs) {
+    return Pol::view(recs + f, gs);
+  }
+};
+
 // the row loop's screen state: Pol::Screen when the policy defines one, else
 // one F2 (a running max, 0 = clean)
 template <class Pol, class = void>
@@ -1137,7 +1184,7 @@ struct ScreenOf<Pol, std::void_t<typename Pol::Screen>> {
 };
 
 template <class Pol, bool kUnit>
-__device__ __forceinline__ void chunk_rows(const typename Pol::Rec& R, const PointChunk& ch,
+__device__ __forceinline__ void chunk_rows(const typename RecOf<Pol>::T& R, const PointChunk& ch,
                                            int n_pairs, int64_t flat0, int64_t rz, float eps2,
                                            bool dense, double (*acc)[kBwdThreads]) {
   int j = 0;
@@ -1202,11 +1249,10 @@ bwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   coefs += (int64_t)blockIdx.z * n_count;
   const int64_t f = (int64_t)blockIdx.x * kBwdThreads + threadIdx.x;
   const bool live = f < n_faces;
-  typename Pol::Rec R = recs[live ? f : 0];
+  const typename RecOf<Pol>::T R = RecOf<Pol>::load(recs, live ? f : 0, gscale);
   // power-of-two geometry scale (row mode of the exact backward, see
   // launch_bwd): exact in floating point, so the arithmetic is the unscaled
   // one; the corner sums are scaled back on the way out
-  if (gscale != 1.0f) Pol::scale(R, gscale);
   const float eps = hdr->eps_f32;
   const float eps2 = eps * eps;
   const int64_t p_begin = (int64_t)blockIdx.y * pts_per_split;
