@@ -39,6 +39,14 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   // touched once per tile (and by rare pairs), and keeping them out of the
   // register file leaves the 128-register budget to the pair arithmetic
   __shared__ double accs[P][NC];
+  // warp rows (RowSrcW, strip policies): per tile, lane i computes the row
+  // terms of faces i, i+32, ... for the warp's k-row; every lane reads them
+  // back (a broadcast LDS.64 per face instead of 6 FP32 ops per face)
+  constexpr bool kTab = [] {
+    if constexpr (Src::kRows) return Src::kWarpRow && Pol::kStrip;
+    else return false;
+  }();
+  __shared__ float2 rtab[kTab ? CW : 1][kTab ? TILE : 1];
   // batched launches: blockIdx.z selects the mesh (its packed records lie
   // pack_stride bytes apart; its outputs n_count apart)
   hdr = reinterpret_cast<const PackHeader*>(reinterpret_cast<const char*>(hdr) +
@@ -142,6 +150,31 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
     using R2 = std::integral_constant<int, 2>;
     if constexpr (Pol::kStrip && kRows) {
       static_assert(PP <= Pol::kGroup, "strip faces are decided for all point pairs at once");
+      [[maybe_unused]] const int wrp = tid >> 5;
+      if constexpr (kTab) {
+        __syncwarp();  // the previous tile's terms are consumed
+#pragma unroll
+        for (int k = 0; k < TILE / 32; ++k) {
+          const int fi = (tid & 31) + 32 * k;
+          if (fi < cnt) {
+            const typename Pol::Row w = Pol::row_c(tile[fi], rx, ry);
+            rtab[wrp][fi] = make_float2(w.c2, w.alpha);
+          }
+        }
+        __syncwarp();
+      }
+      // the row terms of face R (its C corner): the warp's table or computed
+      auto row_c = [&](const Rec& R) {
+        if constexpr (kTab) {
+          const float2 v = rtab[wrp][&R - tile];
+          typename Pol::Row w;
+          w.c2 = v.x;
+          w.alpha = v.y;
+          return w;
+        } else {
+          return Pol::row_c(R, rx, ry);
+        }
+      };
       // one strip face's common-path terms; the slots rotate by kRot
       // may_restart: false when the caller has checked that R continues its
       // strip (then the block has no restart branch)
@@ -151,7 +184,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
             decltype(may_restart)::value && __float_as_int(R.v1.w) < 0;  // uniform per face
         // the row parts of |A - q|^2, |B - q|^2 are the previous faces'
         // |C - q|^2 row parts (ring of 3, like the distance slots)
-        typename Pol::Row w = Pol::row_c(R, rx, ry);
+        typename Pol::Row w = row_c(R);
         if (restart) Pol::row_ab(R, rx, ry, rrow[kRot], rrow[(kRot + 1) % 3]);
         w.a2 = rrow[kRot];
         w.b2 = rrow[(kRot + 1) % 3];
@@ -178,7 +211,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       auto row_of = [&](const Rec& R, auto rot, auto may_restart, bool& restart) {
         constexpr int kRot = decltype(rot)::value;
         restart = decltype(may_restart)::value && __float_as_int(R.v1.w) < 0;
-        typename Pol::Row w = Pol::row_c(R, rx, ry);
+        typename Pol::Row w = row_c(R);
         if (restart) Pol::row_ab(R, rx, ry, rrow[kRot], rrow[(kRot + 1) % 3]);
         w.a2 = rrow[kRot];
         w.b2 = rrow[(kRot + 1) % 3];
@@ -396,7 +429,19 @@ int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, i
   }
   dim3 grid((unsigned)pl.blocks_x, (unsigned)pl.splits, (unsigned)bt.n);
   const unsigned threads = Pol::kThreads;
-  if (rows) {
+  // every warp's 32 P nodes in one k-row: row length, start and count are
+  // multiples of them
+  constexpr int64_t kWarpNodes = 32 * Pol::kP;
+  const bool warp_rows = rows && ps.grid.res[2] % kWarpNodes == 0 &&
+                         ps.n0 % kWarpNodes == 0 && n_count % kWarpNodes == 0;
+  if (rows && warp_rows && Pol::kStrip) {
+    if constexpr (Pol::kStrip) {
+      RowSrcW src{{{ps.grid, ps.n0}}};
+      fwd_f32_kernel<Pol, RowSrcW><<<grid, threads, 0, stream>>>(
+          hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
+      wv::note_launch();
+    }
+  } else if (rows) {
     RowSrc src{{ps.grid, ps.n0}};
     { fwd_f32_kernel<Pol, RowSrc><<<grid, threads, 0, stream>>>(
         hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o); wv::note_launch(); }

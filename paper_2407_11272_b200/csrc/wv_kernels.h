@@ -57,6 +57,13 @@ struct GridSrc {
 // identical coordinates to GridSrc, different thread -> node mapping.
 struct RowSrc : GridSrc {
   static constexpr bool kRows = true;
+  static constexpr bool kWarpRow = false;
+};
+// Row mode where every warp's 32 P consecutive nodes lie in ONE k-row (the
+// row length and the range start and count are multiples of them): the strip
+// forward then computes each face's row terms once per warp (wv_fwd.cuh).
+struct RowSrcW : RowSrc {
+  static constexpr bool kWarpRow = true;
 };
 // Row mode needs every run of `run` nodes to stay inside one k-row.
 inline bool row_aligned(const GridDesc& g, int64_t n0, int64_t count, int run) {
