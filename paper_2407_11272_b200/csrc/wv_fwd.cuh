@@ -42,11 +42,20 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
   // warp rows (RowSrcW, strip policies): per tile, lane i computes the row
   // terms of faces i, i+32, ... for the warp's k-row; every lane reads them
   // back (a broadcast LDS.64 per face instead of 6 FP32 ops per face)
+  // (face-ordered pairs: all four row terms of each face the same way)
   constexpr bool kTab = [] {
     if constexpr (Src::kRows) return Src::kWarpRow && Pol::kStrip;
     else return false;
   }();
+  constexpr bool kTabF = [] {
+    if constexpr (Src::kRows) return Src::kWarpRow && !Pol::kStrip && Pol::kPairFaces;
+    else return false;
+  }();
   __shared__ float2 rtab[kTab ? CW : 1][kTab ? TILE : 1];
+  // (half a tile at a time: the whole-tile table would pass the 48 KB of
+  // static shared memory next to the 4-stage ring)
+  constexpr int kHalf = TILE / 2;
+  __shared__ typename Pol::Row rtabf[kTabF ? CW : 1][kTabF ? kHalf : 1];
   // batched launches: blockIdx.z selects the mesh (its packed records lie
   // pack_stride bytes apart; its outputs n_count apart)
   hdr = reinterpret_cast<const PackHeader*>(reinterpret_cast<const char*>(hdr) +
@@ -103,6 +112,23 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
 #pragma unroll
     for (int pp = 0; pp < PP; ++pp) tacc[pp] = f2(0.0f, 0.0f);
 
+    [[maybe_unused]] const int wrpf = tid >> 5;
+    [[maybe_unused]] int tab0 = 0;  // first face of the table's half tile
+    [[maybe_unused]] auto fill_half = [&](int h0) {
+      __syncwarp();  // the previous half's terms are consumed
+#pragma unroll
+      for (int k = 0; k < kHalf / 32; ++k) {
+        const int fi = h0 + (tid & 31) + 32 * k;
+        if (fi < cnt) rtabf[wrpf][fi - h0] = Pol::row(tile[fi], rx, ry);
+      }
+      tab0 = h0;
+      __syncwarp();
+    };
+    // the row terms of a face: the warp's table (warp rows) or computed
+    auto row_f = [&](const Rec& R) {
+      if constexpr (kTabF) return rtabf[wrpf][(&R - tile) - tab0];
+      else return Pol::row(R, rx, ry);
+    };
     // lanes of one face that the fp32 paths left to the fp64 path
     auto do_rare = [&](const Rec& R, uint32_t rare) {
       if (rare != 0u) {
@@ -130,7 +156,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         // shared by all of a thread's points, the temporaries by one group
         rare = 0;
         {
-          const typename Pol::Row w = Pol::row(R, rx, ry);
+          const typename Pol::Row w = row_f(R);
 #pragma unroll
           for (int g0 = 0; g0 < PP; g0 += 4)
             rare |= Pol::template face_row<(PP < 4 ? PP : 4)>(R, w, qz + g0, ctx, tacc + g0)
@@ -321,7 +347,7 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
       auto do_pair = [&](const Rec& Ra, const Rec& Rb) {
         uint32_t rare_a = 0, rare_b = 0;
         if constexpr (kRows) {
-          const typename Pol::Row wa = Pol::row(Ra, rx, ry), wb = Pol::row(Rb, rx, ry);
+          const typename Pol::Row wa = row_f(Ra), wb = row_f(Rb);
 #pragma unroll
           for (int g0 = 0; g0 < PP; g0 += G) {
             if (!Pol::template face_row_pair<G>(Ra, wa, Rb, wb, qz + g0, ctx, tacc + g0)) {
@@ -343,10 +369,23 @@ fwd_f32_kernel(const PackHeader* __restrict__ hdr, const typename Pol::Rec* __re
         do_rare(Ra, rare_a);
         do_rare(Rb, rare_b);
       };
-      int f = 0;
+      if constexpr (kTabF) {
+        static_assert(kHalf % 2 == 0, "pairs never straddle the halves");
 #pragma unroll 1
-      for (; f + 2 <= cnt; f += 2) do_pair(tile[f], tile[f + 1]);
-      if (f < cnt) do_face(tile[f], R0{});
+        for (int h0 = 0; h0 < cnt; h0 += kHalf) {
+          fill_half(h0);
+          const int he = cnt < h0 + kHalf ? cnt : h0 + kHalf;
+          int f = h0;
+#pragma unroll 1
+          for (; f + 2 <= he; f += 2) do_pair(tile[f], tile[f + 1]);
+          if (f < he) do_face(tile[f], R0{});
+        }
+      } else {
+        int f = 0;
+#pragma unroll 1
+        for (; f + 2 <= cnt; f += 2) do_pair(tile[f], tile[f + 1]);
+        if (f < cnt) do_face(tile[f], R0{});
+      }
     } else {
 #pragma unroll 1
       for (int f = 0; f < cnt; ++f) do_face(tile[f], R0{});
@@ -434,8 +473,9 @@ int launch_fwd_f32(const void* packed, int64_t n_faces, const PointSource& ps, i
   constexpr int64_t kWarpNodes = 32 * Pol::kP;
   const bool warp_rows = rows && ps.grid.res[2] % kWarpNodes == 0 &&
                          ps.n0 % kWarpNodes == 0 && n_count % kWarpNodes == 0;
-  if (rows && warp_rows && Pol::kStrip) {
-    if constexpr (Pol::kStrip) {
+  constexpr bool kWarpRowPol = Pol::kStrip || (Pol::kPairFaces && std::is_same_v<typename Pol::Rec, ExactRecF32>);
+  if (rows && warp_rows && kWarpRowPol) {
+    if constexpr (kWarpRowPol) {
       RowSrcW src{{{ps.grid, ps.n0}}};
       fwd_f32_kernel<Pol, RowSrcW><<<grid, threads, 0, stream>>>(
           hdr, recs, bt.pack_stride, n_faces, src, n_count, pl.tiles_per_split, o);
