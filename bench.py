@@ -72,6 +72,15 @@ KERNELS = {
 }
 
 
+def fwd_kernel(prec: str, strip: bool, grid, n0: int, cnt: int) -> str:
+    """The forward kernel a lattice range launches: the warp-row variant
+    (RowSrcW) when every warp's 256 nodes lie in one k-row (wv_fwd.cuh)."""
+    k = KERNELS[(prec, "fwd", strip)]
+    if prec == "f32" and int(grid[2][2]) % 256 == 0 and n0 % 256 == 0 and cnt % 256 == 0:
+        k = k.replace(",RowSrc>", ",RowSrcW>")
+    return k
+
+
 def exec_mix(kernel: str, workload: str):
     """Executed work per pair of ``kernel`` from profiles/exec_mix.json: the
     entry for this workload, else the kernel's first entry (None if absent)."""
@@ -80,6 +89,8 @@ def exec_mix(kernel: str, workload: str):
     except (OSError, ValueError, KeyError):
         return None
     hits = [e for e in ents if e["kernel"] == kernel]
+    if not hits and ",RowSrcW>" in kernel:  # the row-kernel capture, if the warp-row one is absent
+        hits = [e for e in ents if e["kernel"] == kernel.replace(",RowSrcW>", ",RowSrc>")]
     exact = [e for e in hits if e["workload"] == workload]
     return (exact or hits or [None])[0]
 
@@ -517,7 +528,7 @@ def run_ours(args):
     active = int(dmesh.exact_grad_setup()[0].shape[0])
     fwd_strip, _ = device.lattice_paths(dmesh, "exact", prec, grid, n0, cnt)
     bpath = device.backward_path(dmesh, "exact", prec, grid, n0, cnt)
-    kf = KERNELS[(prec, "fwd", fwd_strip)]
+    kf = fwd_kernel(prec, fwd_strip, grid, n0, cnt)
     kb = KERNELS[(prec, "bwd", bpath)]
 
     meas = measured_peaks() if rank == 0 else {}
@@ -952,7 +963,7 @@ def run_c5(args):
         clocks = clk.summary()
         clk_mhz = clocks.get("sm_mhz") or 1965.0
         fwd_strip, _ = device.lattice_paths(dmesh, "exact", "f32", grid, n0, cnt)
-        kf = KERNELS[("f32", "fwd", fwd_strip)]
+        kf = fwd_kernel("f32", fwd_strip, grid, n0, cnt)
         rf = roofline(kf, w.name, cnt * w.n_faces, ms_step, PINNED["exact_fwd"], "f32", clk_mhz,
                       "fp32 (FMA + XU pipes)")
         cpu = None
