@@ -40,3 +40,24 @@ def test_warp_rows_match_lane_rows_bitwise(cuda_device, strip):
     ref, rf = orc.winding_number_batch(r32(v), f, p32, mode="exact", threads=1)
     assert np.array_equal(rf, fa.cpu().numpy().astype(bool))
     assert np.abs(a - ref)[~rf].max() <= 1e-5
+
+
+def test_f64_strip_grid_equals_points_bitwise(cuda_device):
+    """The f64 strip forward on a lattice range equals the same kernel on
+    the same nodes given as a point list BIT FOR BIT, flags included (the
+    node expression is the reference's, winding.py:118-140) -- on a welded
+    soup and a random mesh with on-surface nodes."""
+    import torch
+    from paper_2407_11272_b200 import _lib as L, configs, device
+    from test_gpu_fuzz import random_case
+    cases = [configs.soup(*configs.torus(0.7, 0.3, 30, 20), seed=3), random_case(5)[:2]]
+    for v, f in cases:
+        s = float(np.abs(v).max())
+        grid = ((-1.1 * s,) * 3, (1.1 * s,) * 3, (6, 5, 24))
+        dm = device.DeviceMesh.from_numpy(v, f)
+        a, fa = device.forward(dm, "exact", "f64", grid=grid, policy=L.POLICY_RAW, strip=True)
+        pts = torch.from_numpy(orc.node_coordinates(*grid)).cuda()
+        b, fb = device.forward(dm, "exact", "f64", points=pts, policy=L.POLICY_RAW, strip=True)
+        assert np.array_equal(fa.cpu().numpy(), fb.cpu().numpy())
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
