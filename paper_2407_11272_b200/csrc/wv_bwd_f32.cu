@@ -32,7 +32,10 @@
 namespace wv {
 
 constexpr int kBwdThreads = 128;   // faces per CTA
-constexpr int kBwdChunk = 256;     // query points per shared-memory chunk
+#ifndef WV_BWD_CHUNK
+#define WV_BWD_CHUNK 256
+#endif
+constexpr int kBwdChunk = WV_BWD_CHUNK;  // query points per shared-memory chunk
 constexpr int kBwdMinBlocks = 5;  // CTAs per SM (launch bounds and split plan)
 constexpr int kRowStep = 4;       // point pairs per basic block in the row loop
 constexpr int kAxisMax = 1024;    // lattice axes up to this length use node tables
