@@ -522,6 +522,18 @@ class DeviceMesh:
         self._packs[key] = buf
         return buf
 
+    def abs_max(self) -> float:
+        """Largest |vertex coordinate| (setup-time positions, cached: the
+        trail-scale screen it feeds has a 1024x margin)."""
+        am = getattr(self, "_abs_max", None)
+        if am is None:
+            vnp = getattr(self, "_verts_np", None)
+            if vnp is None:
+                vnp = self.vertices.detach().double().cpu().numpy()
+            am = float(np.abs(vnp).max()) if vnp.size else 0.0
+            self._abs_max = am
+        return am
+
     def trails_pay(self) -> bool:
         """Whether the edge-trail backward beats the face kernels: corner
         positions must be shared (a closed surface, welded or a soup); a
@@ -638,7 +650,7 @@ def backward_path(mesh: DeviceMesh, mode: str, precision: str, grid, n0: int, co
     if precision == "f64":
         return "trails" if count >= TRAIL64_MIN_POINTS and mesh.trails_pay() else "faces"
     big = precision == "f32" and count >= STRIP_MIN_NODES and mesh.num_faces > 0
-    if big and trail_rows_ok(grid, n0) and mesh.trails_pay():
+    if big and trail_rows_ok(grid, n0) and mesh.trails_pay() and trail_scale_ok(mesh, grid):
         return "trails"
     if big and mesh.strips_pay():
         return "pairs"
@@ -746,6 +758,18 @@ def trail_rows_ok(grid, n0: int) -> bool:
     return rz >= 16 and rz % 2 == 0 and int(n0) % 2 == 0
 
 
+# The f32 trail kernel shares ONE reciprocal among four edge denominators
+# (~|x|^8 in the power-of-two frame where the lattice's largest coordinate is
+# in [1, 2)); meshes reaching beyond this many lattice extents keep the
+# face kernels (3-fold products), so the product stays far inside f32 range.
+TRAIL_MAX_MESH_EXTENT = 1024.0
+
+
+def trail_scale_ok(mesh: "DeviceMesh", grid) -> bool:
+    ext = max(max(abs(float(x)) for x in grid[0]), max(abs(float(x)) for x in grid[1]))
+    return ext > 0.0 and mesh.abs_max() <= TRAIL_MAX_MESH_EXTENT * ext
+
+
 def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, *, grid=None,
               n0: int = 0, count: int | None = None, points=None, coef_scale: float = 1.0,
               pairs: bool | None = None, trails: bool | None = None):
@@ -770,7 +794,7 @@ def face_grad(mesh: DeviceMesh, mode: str, precision: str, coefs: torch.Tensor, 
     if trails is None:
         trails = pairs is None and (
             (exact32 and points is None and n_pts >= STRIP_MIN_NODES
-             and trail_rows_ok(grid, n0) and mesh.trails_pay())
+             and trail_rows_ok(grid, n0) and mesh.trails_pay() and trail_scale_ok(mesh, grid))
             or (exact64 and n_pts >= TRAIL64_MIN_POINTS and mesh.trails_pay()))
     if trails:
         if not (exact64 or (exact32 and points is None and trail_rows_ok(grid, n0))):

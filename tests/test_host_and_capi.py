@@ -232,3 +232,10 @@ def test_random_soup_config_and_path_choice():
         assert device.backward_path(m, "exact", "f64", grid, 0, w.n_nodes) == \
             ("trails" if pay else "faces")
         assert device.backward_path(m, "soft", "f32", grid, 0, w.n_nodes) == "soft"
+    # a mesh reaching far beyond the lattice keeps the face kernels (the trail
+    # kernel's four-fold denominator product must stay inside f32 range)
+    w = configs.make("c3")
+    m = device.DeviceMesh(torch.from_numpy(w.vertices), torch.from_numpy(w.faces))
+    m._verts_np, m._faces_np = w.vertices, w.faces
+    small = ((-1e-4,) * 3, (1e-4,) * 3, w.res)
+    assert device.backward_path(m, "exact", "f32", small, 0, w.n_nodes) == "pairs"
